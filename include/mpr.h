@@ -1,0 +1,184 @@
+/*
+ * mpr.h — C-ABI of libmpr.so, the B200 (sm_100a) LE-MPR gap filler.
+ *
+ * Method: Lach & Zukovic, "Fast gap-filling of massive data by local-equilibrium
+ * conditional simulations on GPU", arXiv 2212.01317. The library runs
+ * the paper's SV-MPR hot path (the north star's "LE-MPR"): data -> spin transform
+ * (PAPER.md:85), block sample energies and energy-matched block temperatures with
+ * the median fallback (Eq.(2)), SST smoothing
+ * (PAPER.md:124), conditional checkerboard Metropolis over the gap sites with the
+ * samples frozen, and the back-transformed conditional mean
+ * (PAPER.md:95). MPR (uniform T) is l_b >= max(Lx, Ly); BST is n_s = 0.
+ * Every floating-point step that feeds a decision follows docs/ARITH.md.
+ *
+ * Conventions shared by every call:
+ *  - Grids are row-major, Ly rows x Lx columns, element (r, c) at index r*Lx + c.
+ *  - mask[i] != 0 marks a known sample (the set G_S of PAPER.md:80); mask[i] == 0 a
+ *    gap (G_P). grid[i] at a gap is never read (it may be NaN).
+ *  - Host pointers are borrowed for the duration of the call only; the library
+ *    copies in and out and never frees caller memory. Device pointers ("_device"
+ *    variants) must be device memory of ctx's device, valid until the call returns
+ *    on the host (all work is stream-ordered on the context stream and the calls
+ *    synchronise that stream before returning unless stated otherwise).
+ *  - Call order: mpr_init -> mpr_set_data -> mpr_estimate_local_params ->
+ *    mpr_simulate (or mpr_simulate_range, any number of times) -> mpr_predict.
+ *    Re-calling an earlier stage invalidates the later ones; out-of-order calls
+ *    return MPR_ERR_STATE.
+ *  - Every call returns a status; on failure mpr_last_error(ctx) holds one line.
+ *  - A context is single-owner (not thread-safe); distinct contexts are independent.
+ */
+#ifndef MPR_H_
+#define MPR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mpr_ctx mpr_ctx;
+
+typedef enum {
+  MPR_OK = 0,
+  MPR_ERR_INVALID_ARG = 1,      /* bad size, parameter, table or non-finite sample   */
+  MPR_ERR_STATE = 2,            /* call out of order                                 */
+  MPR_ERR_TOO_FEW_SAMPLES = 3,  /* fewer than 2 known sites                          */
+  MPR_ERR_NO_SAMPLE_BONDS = 4,  /* no block has a sample-sample bond  */
+  MPR_ERR_CUDA = 5,             /* a CUDA runtime error; message in mpr_last_error   */
+  MPR_ERR_OOM = 6               /* device allocation failed                          */
+} mpr_status;
+
+typedef enum { MPR_INIT_BLOCK_MEAN = 0, MPR_INIT_RANDOM = 1 } mpr_init_mode;
+
+typedef struct {
+  int device;        /* CUDA device ordinal                                           */
+  void *stream;      /* cudaStream_t to run on (e.g. torch's current stream); NULL =>
+                        the library creates its own non-blocking stream                */
+  float J;           /* coupling J > 0 of Eq.(1); default 1           */
+  float q;           /* modification parameter, 0 < q <= 1/2; default .5 */
+  int l_b;           /* block side (l_b = 32 in Table 2); >= 2            */
+  int r_s;           /* smoothing radius (unstated; R8); >= 0   */
+  int n_s;           /* smoothing passes (n_s = 5); 0 => BST              */
+  int init;          /* mpr_init_mode                                   */
+  int n_avg;         /* sweeps averaged at the end of each realization (>= 1)          */
+  const float *calib_T;  /* calibration table T_k, strictly increasing, 0 < T <= 1e4   */
+  const float *calib_e;  /* e_k = e(T_k), strictly increasing (host pointers, copied)  */
+  int calib_n;           /* K >= 2                                                     */
+  int64_t max_batch;     /* max realizations simulated concurrently (0 => automatic)  */
+} mpr_config;
+
+/* Fill *cfg with the defaults above (calibration pointers NULL: the caller must set
+ * them; the Python binding loads the shipped table). */
+void mpr_config_default(mpr_config *cfg);
+
+/* Create a context on cfg->device. Validates cfg (INVALID_ARG) and copies the table.
+ * Ownership of *out passes to the caller; release with mpr_destroy. */
+mpr_status mpr_init(const mpr_config *cfg, mpr_ctx **out);
+
+/* Release every device and host resource of ctx (NULL is a no-op). */
+void mpr_destroy(mpr_ctx *ctx);
+
+/* One-line description of the last failure on ctx ("" if none). Owned by ctx. */
+const char *mpr_last_error(const mpr_ctx *ctx);
+
+/* Stage a problem: grid (float32, Lx*Ly) and mask (uint8, Lx*Ly), host memory.
+ * Computes z_min/z_max over the samples and the spin angles phi = 2pi(z - z_min)/
+ * (z_max - z_min) at the samples (ARITH §D), and builds the gap-site
+ * index. Errors: Lx < 2 or Ly < 2 or Lx*Ly >= 2^31 or a non-finite sample ->
+ * INVALID_ARG; fewer than 2 samples -> TOO_FEW_SAMPLES. z_max == z_min is not an
+ * error: the DEGENERATE_RANGE flag is set, simulate is a no-op and predict fills
+ * the gaps with z_min. */
+mpr_status mpr_set_data(mpr_ctx *ctx, const float *grid, const uint8_t *mask, int64_t Lx, int64_t Ly);
+
+/* Same as mpr_set_data with device pointers (no host<->device copy). */
+mpr_status mpr_set_data_device(mpr_ctx *ctx, const float *grid_dev, const uint8_t *mask_dev,
+                               int64_t Lx, int64_t Ly);
+
+/* Local parameter field: block sample energies e_b (Eq.(2) per
+ * block; a bond belongs to the block of its left/top end), block temperatures by
+ * energy matching (table inversion), the lower-median fallback for blocks without
+ * sample bonds, expansion to sites and n_s smoothing passes of radius r_s.
+ * T_out (nullable, host, Lx*Ly floats) receives the per-site temperature field.
+ * Errors: NO_SAMPLE_BONDS when no block has a sample-sample bond. */
+mpr_status mpr_estimate_local_params(mpr_ctx *ctx, float *T_out);
+
+/* Conditional simulation (ARITH §G-H): realizations
+ * m = 0..M-1 (global ids), each initialised (BLOCK_MEAN or RANDOM) and swept
+ * `sweeps` times (colour A = (r+c) even, then B) with the Philox stream keyed by
+ * `seed`; the last n_avg sweeps of every realization are accumulated for the
+ * conditional mean. Replaces any previous accumulation. Errors: M < 1, sweeps < 1,
+ * n_avg > sweeps -> INVALID_ARG. */
+mpr_status mpr_simulate(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed);
+
+/* Multi-rank building block (realization sharding): simulate global realization
+ * ids [m_begin, m_end) of an M-realization run and ADD them to the accumulator
+ * (reset it first with mpr_reset_accumulator). The result of mpr_predict after all
+ * ranks' accumulators are summed (mpr_accumulator_device + an all-reduce) equals
+ * the single-call mpr_simulate(M) up to fp64 summation order. */
+mpr_status mpr_reset_accumulator(mpr_ctx *ctx);
+mpr_status mpr_simulate_range(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed,
+                              int64_t m_begin, int64_t m_end);
+
+/* Device view of the per-gap-site accumulator (double, *n entries, gap-site order)
+ * so an external collective (NCCL all-reduce) can sum it in place across ranks. The
+ * pointer stays owned by ctx and valid until the next set_data/destroy. */
+mpr_status mpr_accumulator_device(mpr_ctx *ctx, double **acc_dev, int64_t *n);
+
+/* Predictions (ARITH §I): known sites return the input bitwise, gaps
+ * z_min + (z_max - z_min) * mean_phi / 2pi. out: host, Lx*Ly floats, caller-owned. */
+mpr_status mpr_predict(mpr_ctx *ctx, float *out);
+mpr_status mpr_predict_device(mpr_ctx *ctx, float *out_dev);
+
+/* ---- diagnostics / test hooks -------------------------------------------- */
+typedef struct {
+  int64_t Lx, Ly, n_samples, n_gaps, n_gaps_a;  /* n_gaps_a: colour-A gap sites      */
+  float z_min, z_max;
+  int degenerate_range;                          /* z_max == z_min                  */
+  int64_t n_blocks, n_blocks_fallback;           /* blocks given the median         */
+  float median_T;
+  int64_t M, sweeps;                             /* last simulate call              */
+  int64_t batch;                                 /* realizations per launch batch   */
+  int64_t kernel_launches;                       /* kernels launched by the last
+                                                    simulate call                   */
+  int64_t total_launches;                        /* kernels launched since mpr_init */
+  int64_t sweep_launches;                        /* half-sweep kernels timed        */
+  double sweep_ms;                               /* device time of those launches
+                                                    (CUDA events on the context
+                                                    stream; needs kernel timing)    */
+  int64_t last_m_base, last_batch;               /* realizations [last_m_base,
+                                                    last_m_base + last_batch) are in
+                                                    the state buffer (MPR_BUF_STATE)*/
+} mpr_info;
+mpr_status mpr_get_info(mpr_ctx *ctx, mpr_info *info);
+
+/* Buffers for tests: */
+typedef enum {
+  MPR_BUF_PHI_KNOWN = 0,  /* float, Lx*Ly: angles at samples, 0 at gaps          */
+  MPR_BUF_T = 1,          /* float, Lx*Ly: temperature field                      */
+  MPR_BUF_BLOCK_T = 2,    /* float, n_blocks: block temperatures after fallback   */
+  MPR_BUF_BLOCK_STATS = 3,/* int64, 4*n_blocks: SB, NB, SP, NK (ARITH §E)         */
+  MPR_BUF_STATE = 4,      /* float, Lx*Ly per realization: dense angles of the
+                             realizations of the LAST simulate batch (index arg)  */
+  MPR_BUF_ACC = 5,        /* double, Lx*Ly: accumulator scattered to sites (0 at
+                             samples)                                             */
+  MPR_BUF_ENERGY = 6      /* double, M*sweeps: whole-grid specific energy after
+                             each sweep (only if mpr_set_energy_trace(ctx, 1))    */
+} mpr_buffer;
+mpr_status mpr_debug_get(mpr_ctx *ctx, mpr_buffer which, int64_t index, void *host_out);
+
+/* Enable (1) / disable (0) the fused whole-grid energy trace (ARITH §J). */
+mpr_status mpr_set_energy_trace(mpr_ctx *ctx, int enable);
+
+/* Enable (1) / disable (0) CUDA-event timing of the half-sweep kernels: events are
+ * recorded on the context stream around each batch's sweep loop and summed into
+ * mpr_info.sweep_ms / sweep_launches (reset by enabling again). */
+mpr_status mpr_set_kernel_timing(mpr_ctx *ctx, int enable);
+
+/* Library version string. */
+const char *mpr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPR_H_ */

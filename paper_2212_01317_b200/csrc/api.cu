@@ -1,0 +1,648 @@
+// api.cu — the C-ABI of libmpr.so (include/mpr.h): context state machine, device
+// memory ownership, stage orchestration and the realization-batch loop of the
+// conditional simulation. All arithmetic happens in the kernels of params.cu and
+// sweep.cu; this file only allocates, launches and copies.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstddef>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+#include "mpr.h"
+
+using namespace mpr;
+
+namespace {
+
+// Grow-only device buffer.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t b) {
+    if (b <= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (b == 0) b = 16;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+enum Stage { ST_INIT = 0, ST_DATA = 1, ST_PARAMS = 2, ST_SIM = 3 };
+
+}  // namespace
+
+struct mpr_ctx {
+  mpr_config cfg{};
+  std::vector<float> calT, cale;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int stage = ST_INIT;
+  std::string err;
+  int sweep_grid = 0;
+  // problem
+  int64_t Lx = 0, Ly = 0, n = 0;
+  int64_t P = 0, PA = 0, n_known = 0;
+  float zmin = 0, zmax = 0;
+  int degenerate = 0;
+  int64_t nbx = 0, nby = 0, nblocks = 0;
+  int64_t n_fallback = 0;
+  float median_T = 0;
+  double sum_SB = 0;
+  // simulation bookkeeping
+  int64_t M_total = 0, sweeps = 0, batch = 0, last_m_base = 0, last_R = 0;
+  int64_t launches = 0, total_launches = 0;
+  int timing = 0;
+  int64_t sweep_launches = 0;
+  double sweep_ms = 0.0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int energy_enabled = 0;
+  int64_t energy_M = 0, energy_S = 0;
+  // device memory
+  DBuf z, mask, phiK, scal, calTd, caled, rowcnt, rowoff, gid, rec, bstats, Tb, T, T2, G, A, acc,
+      energy, out, tmp;
+  DevScalars* hsc = nullptr;  // pinned host mirror of the device scalars
+};
+
+namespace {
+
+mpr_status fail(mpr_ctx* c, mpr_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+mpr_status cuda_fail(mpr_ctx* c, cudaError_t e, const char* where) {
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return fail(c, MPR_ERR_OOM, std::string(where) + ": out of device memory");
+  }
+  return fail(c, MPR_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr, where)                                 \
+  do {                                                  \
+    cudaError_t e_ = (expr);                            \
+    if (e_ != cudaSuccess) return cuda_fail(c, e_, where); \
+  } while (0)
+
+mpr_status check_launch(mpr_ctx* c, const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(c, e, where);
+  return MPR_OK;
+}
+
+#define CKL(where)                              \
+  do {                                          \
+    mpr_status s_ = check_launch(c, where);     \
+    if (s_ != MPR_OK) return s_;                \
+    ++c->total_launches;                        \
+  } while (0)
+
+mpr_status validate_cfg(const mpr_config* cfg, std::string& why) {
+  if (!cfg) { why = "cfg is NULL"; return MPR_ERR_INVALID_ARG; }
+  if (!(cfg->J > 0.0f) || !std::isfinite(cfg->J)) { why = "J must be finite and > 0"; return MPR_ERR_INVALID_ARG; }
+  if (!(cfg->q > 0.0f && cfg->q <= 0.5f)) { why = "q must be in (0, 1/2]"; return MPR_ERR_INVALID_ARG; }
+  if (cfg->l_b < 2) { why = "l_b must be >= 2"; return MPR_ERR_INVALID_ARG; }
+  if (cfg->r_s < 0 || cfg->r_s > 16) { why = "r_s must be in [0, 16]"; return MPR_ERR_INVALID_ARG; }
+  if (cfg->n_s < 0) { why = "n_s must be >= 0"; return MPR_ERR_INVALID_ARG; }
+  if (cfg->init != MPR_INIT_BLOCK_MEAN && cfg->init != MPR_INIT_RANDOM) { why = "init must be BLOCK_MEAN or RANDOM"; return MPR_ERR_INVALID_ARG; }
+  if (cfg->n_avg < 1) { why = "n_avg must be >= 1"; return MPR_ERR_INVALID_ARG; }
+  if (cfg->max_batch < 0) { why = "max_batch must be >= 0"; return MPR_ERR_INVALID_ARG; }
+  if (!cfg->calib_T || !cfg->calib_e || cfg->calib_n < 2 || cfg->calib_n > 256) {
+    why = "calibration table must have 2..256 points";
+    return MPR_ERR_INVALID_ARG;
+  }
+  for (int k = 0; k < cfg->calib_n; ++k) {
+    const float T = cfg->calib_T[k], e = cfg->calib_e[k];
+    if (!std::isfinite(T) || !std::isfinite(e) || !(T > 0.0f) || T > 1e4f) {
+      why = "calibration table: T must be finite, in (0, 1e4]";
+      return MPR_ERR_INVALID_ARG;
+    }
+    if (k > 0 && !(T > cfg->calib_T[k - 1] && e > cfg->calib_e[k - 1])) {
+      why = "calibration table: T and e must be strictly increasing";
+      return MPR_ERR_INVALID_ARG;
+    }
+  }
+  return MPR_OK;
+}
+
+void set_scalars_init(DevScalars* h) {
+  std::memset(h, 0, sizeof(*h));
+  h->zmin_key = 0x7fffffff;
+  h->zmax_key = static_cast<int>(0x80000000u);
+}
+
+// Inverse of the ordered-int key of device_math.cuh (host side).
+float key_to_float(int k) {
+  const int b = k >= 0 ? k : (k ^ 0x7fffffff);
+  float f;
+  std::memcpy(&f, &b, sizeof f);
+  return f;
+}
+
+mpr_status stage_data(mpr_ctx* c) {
+  cudaStream_t st = c->stream;
+  const int64_t n = c->n;
+  set_scalars_init(c->hsc);
+  CK(cudaMemcpyAsync(c->scal.p, c->hsc, sizeof(DevScalars), cudaMemcpyHostToDevice, st), "scalars upload");
+  launch_minmax_count(c->z.as<float>(), c->mask.as<uint8_t>(), c->Lx, c->Ly, c->scal.as<DevScalars>(), st);
+  CKL("minmax_count");
+  CK(cudaMemcpyAsync(c->hsc, c->scal.p, sizeof(DevScalars), cudaMemcpyDeviceToHost, st), "scalars download");
+  CK(cudaStreamSynchronize(st), "minmax_count sync");
+  if (c->hsc->bad_sample) return fail(c, MPR_ERR_INVALID_ARG, "non-finite value at a known sample");
+  c->n_known = static_cast<int64_t>(c->hsc->n_known);
+  if (c->n_known < 2) return fail(c, MPR_ERR_TOO_FEW_SAMPLES, "fewer than 2 known samples");
+  c->PA = static_cast<int64_t>(c->hsc->n_gap[0]);
+  c->P = c->PA + static_cast<int64_t>(c->hsc->n_gap[1]);
+  c->zmin = key_to_float(c->hsc->zmin_key) + 0.0f;
+  c->zmax = key_to_float(c->hsc->zmax_key) + 0.0f;
+  c->degenerate = (c->zmin == c->zmax);
+  CK(c->phiK.ensure(sizeof(float) * n), "alloc phi");
+  launch_transform(c->z.as<float>(), c->mask.as<uint8_t>(), n, c->scal.as<DevScalars>(), c->phiK.as<float>(), st);
+  CKL("transform");
+  CK(c->gid.ensure(sizeof(int32_t) * n), "alloc gid");
+  CK(c->rec.ensure(sizeof(GapRec) * std::max<int64_t>(c->P, 1)), "alloc records");
+  CK(c->rowcnt.ensure(sizeof(int) * 2 * c->Ly), "alloc rowcnt");
+  CK(c->rowoff.ensure(sizeof(int) * 2 * c->Ly), "alloc rowoff");
+  launch_gap_index(c->mask.as<uint8_t>(), c->Lx, c->Ly, c->PA, c->rowcnt.as<int>(), c->rowoff.as<int>(),
+                   c->gid.as<int32_t>(), c->rec.as<GapRec>(), st);
+  CKL("gap_index");
+  c->total_launches += 2;  // row counts, scan, compaction
+  CK(cudaStreamSynchronize(st), "set_data sync");
+  c->stage = ST_DATA;
+  c->M_total = 0;
+  return MPR_OK;
+}
+
+mpr_status check_dims(mpr_ctx* c, int64_t Lx, int64_t Ly) {
+  if (Lx < 2 || Ly < 2) return fail(c, MPR_ERR_INVALID_ARG, "Lx and Ly must be >= 2");
+  if (Lx * Ly >= (int64_t(1) << 31)) return fail(c, MPR_ERR_INVALID_ARG, "Lx*Ly must be < 2^31");
+  return MPR_OK;
+}
+
+mpr_status alloc_inputs(mpr_ctx* c, int64_t Lx, int64_t Ly) {
+  c->Lx = Lx;
+  c->Ly = Ly;
+  c->n = Lx * Ly;
+  c->stage = ST_INIT;
+  CK(c->z.ensure(sizeof(float) * c->n), "alloc z");
+  CK(c->mask.ensure(c->n), "alloc mask");
+  return MPR_OK;
+}
+
+int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
+  int64_t R = M_span + (M_span & 1);
+  if (R > 1024) R = 1024;
+  if (c->cfg.max_batch > 0) {
+    int64_t mb = c->cfg.max_batch + (c->cfg.max_batch & 1);
+    R = std::min(R, std::max<int64_t>(mb, 2));
+  }
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  const double per_r = 4.0 * static_cast<double>(std::max<int64_t>(c->P, 1)) * (c->cfg.n_avg > 1 ? 2.0 : 1.0);
+  const double budget = 0.6 * static_cast<double>(fr + c->G.bytes + c->A.bytes);
+  int64_t cap = static_cast<int64_t>(budget / per_r);
+  cap -= cap & 1;
+  if (cap < 2) cap = 2;
+  return std::min(R, cap);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mpr_version(void) { return "libmpr 0.1 (sm_100a, LE-MPR / SV-MPR arXiv 2212.01317)"; }
+
+void mpr_config_default(mpr_config* cfg) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->device = 0;
+  cfg->stream = nullptr;
+  cfg->J = 1.0f;
+  cfg->q = 0.5f;
+  cfg->l_b = 32;
+  cfg->r_s = 2;
+  cfg->n_s = 5;
+  cfg->init = MPR_INIT_BLOCK_MEAN;
+  cfg->n_avg = 1;
+  cfg->max_batch = 0;
+}
+
+mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
+  if (!out) return MPR_ERR_INVALID_ARG;
+  *out = nullptr;
+  std::string why;
+  mpr_status s = validate_cfg(cfg, why);
+  if (s != MPR_OK) {
+    std::fprintf(stderr, "mpr_init: %s\n", why.c_str());
+    return s;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    std::fprintf(stderr, "mpr_init: no CUDA device\n");
+    return MPR_ERR_CUDA;
+  }
+  if (cfg->device < 0 || cfg->device >= ndev) return MPR_ERR_INVALID_ARG;
+  mpr_ctx* c = new mpr_ctx();
+  c->cfg = *cfg;
+  c->device = cfg->device;
+  c->calT.assign(cfg->calib_T, cfg->calib_T + cfg->calib_n);
+  c->cale.assign(cfg->calib_e, cfg->calib_e + cfg->calib_n);
+  c->cfg.calib_T = c->calT.data();
+  c->cfg.calib_e = c->cale.data();
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e == cudaSuccess) {
+    if (cfg->stream) {
+      c->stream = static_cast<cudaStream_t>(cfg->stream);
+    } else {
+      e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+      c->own_stream = true;
+    }
+  }
+  if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c->hsc), sizeof(DevScalars));
+  if (e == cudaSuccess) e = c->scal.ensure(sizeof(DevScalars));
+  if (e == cudaSuccess) e = c->calTd.ensure(sizeof(float) * c->calT.size());
+  if (e == cudaSuccess) e = c->caled.ensure(sizeof(float) * c->cale.size());
+  if (e == cudaSuccess)
+    e = cudaMemcpy(c->calTd.p, c->calT.data(), sizeof(float) * c->calT.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(c->caled.p, c->cale.data(), sizeof(float) * c->cale.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    std::fprintf(stderr, "mpr_init: %s\n", cudaGetErrorString(e));
+    mpr_destroy(c);
+    return e == cudaErrorMemoryAllocation ? MPR_ERR_OOM : MPR_ERR_CUDA;
+  }
+  c->sweep_grid = sweep_grid_size(c->device);
+  *out = c;
+  return MPR_OK;
+}
+
+void mpr_destroy(mpr_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  DBuf* bufs[] = {&c->z, &c->mask, &c->phiK, &c->scal, &c->calTd, &c->caled, &c->rowcnt, &c->rowoff,
+                  &c->gid, &c->rec, &c->bstats, &c->Tb, &c->T, &c->T2, &c->G, &c->A, &c->acc,
+                  &c->energy, &c->out, &c->tmp};
+  for (DBuf* b : bufs) b->release();
+  if (c->hsc) cudaFreeHost(c->hsc);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* mpr_last_error(const mpr_ctx* c) { return c ? c->err.c_str() : "NULL context"; }
+
+mpr_status mpr_set_data(mpr_ctx* c, const float* grid, const uint8_t* mask, int64_t Lx, int64_t Ly) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (!grid || !mask) return fail(c, MPR_ERR_INVALID_ARG, "grid and mask must be non-NULL");
+  mpr_status s = check_dims(c, Lx, Ly);
+  if (s != MPR_OK) return s;
+  CK(cudaSetDevice(c->device), "set device");
+  s = alloc_inputs(c, Lx, Ly);
+  if (s != MPR_OK) return s;
+  CK(cudaMemcpyAsync(c->z.p, grid, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream), "H2D grid");
+  CK(cudaMemcpyAsync(c->mask.p, mask, c->n, cudaMemcpyHostToDevice, c->stream), "H2D mask");
+  return stage_data(c);
+}
+
+mpr_status mpr_set_data_device(mpr_ctx* c, const float* grid, const uint8_t* mask, int64_t Lx, int64_t Ly) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (!grid || !mask) return fail(c, MPR_ERR_INVALID_ARG, "grid and mask must be non-NULL");
+  mpr_status s = check_dims(c, Lx, Ly);
+  if (s != MPR_OK) return s;
+  CK(cudaSetDevice(c->device), "set device");
+  s = alloc_inputs(c, Lx, Ly);
+  if (s != MPR_OK) return s;
+  CK(cudaMemcpyAsync(c->z.p, grid, sizeof(float) * c->n, cudaMemcpyDeviceToDevice, c->stream), "D2D grid");
+  CK(cudaMemcpyAsync(c->mask.p, mask, c->n, cudaMemcpyDeviceToDevice, c->stream), "D2D mask");
+  return stage_data(c);
+}
+
+mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (c->stage < ST_DATA) return fail(c, MPR_ERR_STATE, "estimate_local_params before set_data");
+  CK(cudaSetDevice(c->device), "set device");
+  cudaStream_t st = c->stream;
+  const int lb = c->cfg.l_b;
+  c->nbx = (c->Lx + lb - 1) / lb;
+  c->nby = (c->Ly + lb - 1) / lb;
+  c->nblocks = c->nbx * c->nby;
+  CK(c->bstats.ensure(sizeof(long long) * 4 * c->nblocks), "alloc block stats");
+  CK(c->Tb.ensure(sizeof(float) * c->nblocks), "alloc Tb");
+  CK(c->T.ensure(sizeof(float) * c->n), "alloc T");
+  if (c->cfg.n_s > 0) CK(c->T2.ensure(sizeof(float) * c->n), "alloc T2");
+  long long* SB = c->bstats.as<long long>();
+  long long* NB = SB + c->nblocks;
+  long long* SP = NB + c->nblocks;
+  long long* NK = SP + c->nblocks;
+  DevScalars* dsc = c->scal.as<DevScalars>();
+  // reset the parameter-stage scalars (n_avail .. median_T)
+  const size_t off = offsetof(DevScalars, n_avail);
+  CK(cudaMemsetAsync(reinterpret_cast<char*>(dsc) + off, 0, sizeof(DevScalars) - off, st), "reset scalars");
+  launch_block_stats(c->phiK.as<float>(), c->mask.as<uint8_t>(), c->Lx, c->Ly, lb, c->cfg.q, SB, NB, SP, NK,
+                     c->nblocks, st);
+  CKL("block_stats");
+  launch_block_T(SB, NB, SP, NK, c->nblocks, c->calTd.as<float>(), c->caled.as<float>(),
+                 static_cast<int>(c->calT.size()), c->Tb.as<float>(), dsc, st);
+  CKL("block_T");
+  launch_median_fill(c->Tb.as<float>(), NB, c->nblocks, dsc, st);
+  CKL("median_fill");
+  launch_expand(c->Tb.as<float>(), c->Lx, c->Ly, lb, c->T.as<float>(), st);
+  CKL("expand");
+  for (int k = 0; k < c->cfg.n_s; ++k) {
+    launch_smooth(c->T.as<float>(), c->T2.as<float>(), c->Lx, c->Ly, c->cfg.r_s, st);
+    CKL("smooth");
+    std::swap(c->T, c->T2);
+  }
+  launch_build_records(c->gid.as<int32_t>(), c->mask.as<uint8_t>(), c->phiK.as<float>(), c->T.as<float>(), SP,
+                       NK, dsc, c->Lx, c->Ly, lb, c->P, c->rec.as<GapRec>(), st);
+  CKL("build_records");
+  CK(cudaMemcpyAsync(c->hsc, c->scal.p, sizeof(DevScalars), cudaMemcpyDeviceToHost, st), "scalars download");
+  if (T_out) CK(cudaMemcpyAsync(T_out, c->T.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, st), "D2H T");
+  CK(cudaStreamSynchronize(st), "estimate_local_params sync");
+  c->n_fallback = static_cast<int64_t>(c->hsc->n_fallback);
+  c->median_T = c->hsc->median_T;
+  c->sum_SB = static_cast<double>(c->hsc->sum_SB) * 0x1p-32;
+  if (c->hsc->n_avail == 0 && !c->degenerate)
+    return fail(c, MPR_ERR_NO_SAMPLE_BONDS, "no block has a sample-sample bond (PAPER.md:108)");
+  c->stage = ST_PARAMS;
+  c->M_total = 0;
+  return MPR_OK;
+}
+
+mpr_status mpr_set_energy_trace(mpr_ctx* c, int enable) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  c->energy_enabled = enable ? 1 : 0;
+  return MPR_OK;
+}
+
+mpr_status mpr_set_kernel_timing(mpr_ctx* c, int enable) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  c->timing = enable ? 1 : 0;
+  c->sweep_ms = 0.0;
+  c->sweep_launches = 0;
+  return MPR_OK;
+}
+
+mpr_status mpr_reset_accumulator(mpr_ctx* c) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "reset_accumulator before estimate_local_params");
+  CK(cudaSetDevice(c->device), "set device");
+  CK(c->acc.ensure(sizeof(double) * std::max<int64_t>(c->P, 1)), "alloc acc");
+  CK(cudaMemsetAsync(c->acc.p, 0, sizeof(double) * std::max<int64_t>(c->P, 1), c->stream), "zero acc");
+  c->M_total = 0;
+  c->energy_M = 0;
+  c->stage = ST_PARAMS;
+  return MPR_OK;
+}
+
+mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed, int64_t m_begin,
+                              int64_t m_end) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "simulate before estimate_local_params");
+  if (M < 1 || sweeps < 1) return fail(c, MPR_ERR_INVALID_ARG, "M and sweeps must be >= 1");
+  if (c->cfg.n_avg > sweeps) return fail(c, MPR_ERR_INVALID_ARG, "n_avg must be <= sweeps");
+  if (m_begin < 0 || m_end > M || m_begin > m_end) return fail(c, MPR_ERR_INVALID_ARG, "bad realization range");
+  if (M >= (int64_t(1) << 32)) return fail(c, MPR_ERR_INVALID_ARG, "M too large");
+  if (!c->acc.p) {
+    mpr_status s = mpr_reset_accumulator(c);
+    if (s != MPR_OK) return s;
+  }
+  CK(cudaSetDevice(c->device), "set device");
+  cudaStream_t st = c->stream;
+  c->M_total = M;
+  c->sweeps = sweeps;
+  c->launches = 0;
+  const uint32_t k0 = static_cast<uint32_t>(seed & 0xffffffffu), k1 = static_cast<uint32_t>(seed >> 32);
+  if (c->energy_enabled) {
+    if (c->energy_M != M || c->energy_S != sweeps) {
+      CK(c->energy.ensure(sizeof(double) * M * sweeps), "alloc energy");
+      CK(cudaMemsetAsync(c->energy.p, 0, sizeof(double) * M * sweeps, st), "zero energy");
+      c->energy_M = M;
+      c->energy_S = sweeps;
+    }
+  }
+  if (c->degenerate || c->P == 0 || m_begin == m_end) {
+    c->stage = ST_SIM;
+    return MPR_OK;
+  }
+  const int64_t mb0 = m_begin & ~int64_t(1);
+  const int64_t R = choose_batch(c, m_end - mb0);
+  c->batch = R;
+  const bool avg = c->cfg.n_avg > 1;
+  CK(c->G.ensure(sizeof(float) * c->P * R), "alloc state");
+  if (avg) CK(c->A.ensure(sizeof(float) * c->P * R), "alloc accumulator state");
+  for (int64_t mb = mb0; mb < m_end; mb += R) {
+    const int64_t span = std::min<int64_t>(R, m_end - mb);
+    const int Rb = static_cast<int>(span + (span & 1));
+    const int npairs = Rb / 2;
+    const uint32_t pair_base = static_cast<uint32_t>(mb / 2);
+    const int r_lo = static_cast<int>(std::max<int64_t>(m_begin - mb, 0));
+    const int r_hi = static_cast<int>(std::min<int64_t>(m_end - mb, Rb));
+    if (c->timing && !c->ev0) {
+      CK(cudaEventCreate(&c->ev0), "event");
+      CK(cudaEventCreate(&c->ev1), "event");
+    }
+    launch_init_states(c->rec.as<GapRec>(), c->G.as<float>(), avg ? c->A.as<float>() : nullptr, c->P, Rb,
+                       npairs, pair_base, c->cfg.init == MPR_INIT_RANDOM, k0, k1, st);
+    CKL("init_states");
+    ++c->launches;
+    SweepArgs a{};
+    a.rec = c->rec.as<GapRec>();
+    a.G = c->G.as<float>();
+    a.A = avg ? c->A.as<float>() : nullptr;
+    a.R = Rb;
+    a.npairs = npairs;
+    a.pair_base = pair_base;
+    a.k0 = k0;
+    a.k1 = k1;
+    a.q = c->cfg.q;
+    a.J = c->cfg.J;
+    a.r_valid_lo = r_lo;
+    a.r_valid_hi = r_hi;
+    a.energy_stride = sweeps;
+    int64_t nsweep_launch = 0;
+    if (c->timing) CK(cudaEventRecord(c->ev0, st), "event record");
+    for (int32_t s = 1; s <= sweeps; ++s) {
+      a.sweep = static_cast<uint32_t>(s);
+      a.accumulate = avg && (s > sweeps - c->cfg.n_avg);
+      a.energy = c->energy_enabled ? c->energy.as<double>() + mb * sweeps + (s - 1) : nullptr;
+      for (int colour = 0; colour < 2; ++colour) {
+        a.is_b = colour;
+        a.g_begin = colour ? c->PA : 0;
+        a.g_count = colour ? c->P - c->PA : c->PA;
+        if (a.g_count > 0) {
+          launch_sweep_half(a, c->sweep_grid, st);
+          CKL("sweep_half");
+          ++c->launches;
+          ++nsweep_launch;
+        }
+      }
+    }
+    if (c->timing) {
+      CK(cudaEventRecord(c->ev1, st), "event record");
+      CK(cudaEventSynchronize(c->ev1), "event sync");
+      float ms = 0.0f;
+      CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event elapsed");
+      c->sweep_ms += ms;
+      c->sweep_launches += nsweep_launch;
+    }
+    launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), c->P, Rb, r_lo, r_hi, c->acc.as<double>(), st);
+    CKL("acc_reduce");
+    ++c->launches;
+    c->last_m_base = mb;
+    c->last_R = Rb;
+  }
+  CK(cudaStreamSynchronize(st), "simulate sync");
+  c->stage = ST_SIM;
+  return MPR_OK;
+}
+
+mpr_status mpr_simulate(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed) {
+  mpr_status s = mpr_reset_accumulator(c);
+  if (s != MPR_OK) return s;
+  return mpr_simulate_range(c, M, sweeps, seed, 0, M);
+}
+
+mpr_status mpr_accumulator_device(mpr_ctx* c, double** acc_dev, int64_t* n) {
+  if (!c || !acc_dev || !n) return MPR_ERR_INVALID_ARG;
+  if (c->stage < ST_PARAMS || !c->acc.p) return fail(c, MPR_ERR_STATE, "no accumulator yet");
+  *acc_dev = c->acc.as<double>();
+  *n = c->P;
+  return MPR_OK;
+}
+
+static mpr_status predict_impl(mpr_ctx* c, float* out_dev) {
+  if (c->stage < ST_SIM || c->M_total < 1) return fail(c, MPR_ERR_STATE, "predict before simulate");
+  const double denom = static_cast<double>(c->M_total * static_cast<int64_t>(c->cfg.n_avg));
+  launch_predict(c->z.as<float>(), c->mask.as<uint8_t>(), c->gid.as<int32_t>(), c->acc.as<double>(), c->n, denom,
+                 c->scal.as<DevScalars>(), c->degenerate, out_dev, c->stream);
+  CKL("predict");
+  return MPR_OK;
+}
+
+mpr_status mpr_predict(mpr_ctx* c, float* out) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (!out) return fail(c, MPR_ERR_INVALID_ARG, "out is NULL");
+  CK(cudaSetDevice(c->device), "set device");
+  CK(c->out.ensure(sizeof(float) * c->n), "alloc out");
+  mpr_status s = predict_impl(c, c->out.as<float>());
+  if (s != MPR_OK) return s;
+  CK(cudaMemcpyAsync(out, c->out.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, c->stream), "D2H out");
+  CK(cudaStreamSynchronize(c->stream), "predict sync");
+  return MPR_OK;
+}
+
+mpr_status mpr_predict_device(mpr_ctx* c, float* out_dev) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (!out_dev) return fail(c, MPR_ERR_INVALID_ARG, "out is NULL");
+  CK(cudaSetDevice(c->device), "set device");
+  mpr_status s = predict_impl(c, out_dev);
+  if (s != MPR_OK) return s;
+  CK(cudaStreamSynchronize(c->stream), "predict sync");
+  return MPR_OK;
+}
+
+mpr_status mpr_get_info(mpr_ctx* c, mpr_info* info) {
+  if (!c || !info) return MPR_ERR_INVALID_ARG;
+  std::memset(info, 0, sizeof(*info));
+  info->Lx = c->Lx;
+  info->Ly = c->Ly;
+  info->n_samples = c->n_known;
+  info->n_gaps = c->P;
+  info->n_gaps_a = c->PA;
+  info->z_min = c->zmin;
+  info->z_max = c->zmax;
+  info->degenerate_range = c->degenerate;
+  info->n_blocks = c->nblocks;
+  info->n_blocks_fallback = c->n_fallback;
+  info->median_T = c->median_T;
+  info->M = c->M_total;
+  info->sweeps = c->sweeps;
+  info->batch = c->batch;
+  info->kernel_launches = c->launches;
+  info->total_launches = c->total_launches;
+  info->sweep_launches = c->sweep_launches;
+  info->sweep_ms = c->sweep_ms;
+  info->last_m_base = c->last_m_base;
+  info->last_batch = c->last_R;
+  return MPR_OK;
+}
+
+mpr_status mpr_debug_get(mpr_ctx* c, mpr_buffer which, int64_t index, void* host_out) {
+  if (!c || !host_out) return MPR_ERR_INVALID_ARG;
+  CK(cudaSetDevice(c->device), "set device");
+  cudaStream_t st = c->stream;
+  switch (which) {
+    case MPR_BUF_PHI_KNOWN:
+      if (c->stage < ST_DATA) return fail(c, MPR_ERR_STATE, "no data");
+      CK(cudaMemcpyAsync(host_out, c->phiK.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, st), "D2H");
+      break;
+    case MPR_BUF_T:
+      if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "no parameters");
+      CK(cudaMemcpyAsync(host_out, c->T.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, st), "D2H");
+      break;
+    case MPR_BUF_BLOCK_T:
+      if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "no parameters");
+      CK(cudaMemcpyAsync(host_out, c->Tb.p, sizeof(float) * c->nblocks, cudaMemcpyDeviceToHost, st), "D2H");
+      break;
+    case MPR_BUF_BLOCK_STATS:
+      if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "no parameters");
+      CK(cudaMemcpyAsync(host_out, c->bstats.p, sizeof(long long) * 4 * c->nblocks, cudaMemcpyDeviceToHost, st),
+         "D2H");
+      break;
+    case MPR_BUF_STATE: {
+      if (c->stage < ST_SIM || !c->G.p || c->last_R == 0) return fail(c, MPR_ERR_STATE, "no state");
+      const int64_t r = index - c->last_m_base;
+      if (r < 0 || r >= c->last_R) return fail(c, MPR_ERR_INVALID_ARG, "realization not in the last batch");
+      CK(c->tmp.ensure(sizeof(double) * c->n), "alloc tmp");
+      launch_scatter_state(c->phiK.as<float>(), c->gid.as<int32_t>(), c->G.as<float>(), c->last_R, r, c->n,
+                           c->tmp.as<float>(), st);
+      CKL("scatter_state");
+      CK(cudaMemcpyAsync(host_out, c->tmp.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, st), "D2H");
+      break;
+    }
+    case MPR_BUF_ACC:
+      if (c->stage < ST_PARAMS || !c->acc.p) return fail(c, MPR_ERR_STATE, "no accumulator");
+      CK(c->tmp.ensure(sizeof(double) * c->n), "alloc tmp");
+      launch_scatter_acc(c->gid.as<int32_t>(), c->acc.as<double>(), c->n, c->tmp.as<double>(), st);
+      CKL("scatter_acc");
+      CK(cudaMemcpyAsync(host_out, c->tmp.p, sizeof(double) * c->n, cudaMemcpyDeviceToHost, st), "D2H");
+      break;
+    case MPR_BUF_ENERGY: {
+      if (!c->energy_enabled || c->energy_M == 0) return fail(c, MPR_ERR_STATE, "energy trace not enabled");
+      const int64_t cnt = c->energy_M * c->energy_S;
+      CK(cudaMemcpyAsync(host_out, c->energy.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st), "D2H");
+      CK(cudaStreamSynchronize(st), "debug sync");
+      // e = -(sum over known-known bonds + fused sums) / N_bonds  (ARITH §J)
+      const double nb = static_cast<double>(2 * c->Lx * c->Ly - c->Lx - c->Ly);
+      double* e = static_cast<double*>(host_out);
+      for (int64_t k = 0; k < cnt; ++k) e[k] = -(c->sum_SB + e[k]) / nb;
+      return MPR_OK;
+    }
+    default:
+      return fail(c, MPR_ERR_INVALID_ARG, "unknown buffer");
+  }
+  CK(cudaStreamSynchronize(st), "debug sync");
+  return MPR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// device_math.cuh — sm_100a device implementations of the docs/ARITH.md primitives
+// (Philox4x32-10, cos_spec, exp_spec, fixed-point conversions). Written from the
+// text of docs/ARITH.md; shares no code with oracle/. Every floating-point operation
+// that feeds a decision is an explicit round-to-nearest intrinsic, so nvcc can
+// neither contract nor reorder it.
+#pragma once
+#include <cstdint>
+
+namespace mpr {
+
+constexpr float kTwoPiF = 0x1.921fb6p+2f;  // ARITH notation TWO_PI_F
+
+// ARITH §A — Philox4x32-10. The 32x32->64 products are single IMAD.WIDE.U32.
+struct Words4 {
+  uint32_t w0, w1, w2, w3;
+};
+
+__device__ __forceinline__ Words4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int round = 0; round < 10; ++round) {
+    const uint64_t p0 = static_cast<uint64_t>(0xD2511F53u) * c0;
+    const uint64_t p1 = static_cast<uint64_t>(0xCD9E8D57u) * c2;
+    const uint32_t hi0 = static_cast<uint32_t>(p0 >> 32), lo0 = static_cast<uint32_t>(p0);
+    const uint32_t hi1 = static_cast<uint32_t>(p1 >> 32), lo1 = static_cast<uint32_t>(p1);
+    c0 = hi1 ^ c1 ^ k0;
+    c1 = lo1;
+    c2 = hi0 ^ c3 ^ k1;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return Words4{c0, c1, c2, c3};
+}
+
+// u(w) = (w >> 8) * 2^-24, exact.
+__device__ __forceinline__ float u24(uint32_t w) {
+  return __fmul_rn(__uint2float_rn(w >> 8), 0x1p-24f);
+}
+
+// ARITH §B — cos_spec(x) = P(x*x).
+__device__ __forceinline__ float cos_spec(float x) {
+  const float t = __fmul_rn(x, x);
+  float p = 0x1.e0c79cp-30f;
+  p = __fmaf_rn(p, t, -0x1.2392p-22f);
+  p = __fmaf_rn(p, t, 0x1.9fb7a2p-16f);
+  p = __fmaf_rn(p, t, -0x1.6c12aep-10f);
+  p = __fmaf_rn(p, t, 0x1.555536p-5f);
+  p = __fmaf_rn(p, t, -0.5f);
+  p = __fmaf_rn(p, t, 1.0f);
+  return p;
+}
+
+// cos_spec(0.5 * d) evaluated as P'(d*d) with coefficients c_k * 4^-k: bit-identical
+// to cos_spec(__fmul_rn(0.5f, d)) (ARITH §B "implementation latitude").
+__device__ __forceinline__ float cos_half_spec(float d) {
+  const float t = __fmul_rn(d, d);
+  float p = 0x1.e0c79cp-42f;                // c6 * 4^-6
+  p = __fmaf_rn(p, t, -0x1.2392p-32f);      // c5 * 4^-5
+  p = __fmaf_rn(p, t, 0x1.9fb7a2p-24f);     // c4 * 4^-4
+  p = __fmaf_rn(p, t, -0x1.6c12aep-16f);    // c3 * 4^-3
+  p = __fmaf_rn(p, t, 0x1.555536p-9f);      // c2 * 4^-2
+  p = __fmaf_rn(p, t, -0.125f);             // c1 * 4^-1
+  p = __fmaf_rn(p, t, 1.0f);                // c0
+  return p;
+}
+
+// ARITH §C — exp_spec(x), x <= 0.
+__device__ __forceinline__ float exp_spec(float x) {
+  const float n = rintf(__fmul_rn(x, 0x1.715476p+0f));
+  float f = __fmaf_rn(-n, 0x1.62e430p-1f, x);
+  f = __fmaf_rn(-n, -0x1.05c610p-29f, f);
+  float p = 0x1.6ac2a0p-10f;
+  p = __fmaf_rn(p, f, 0x1.126e38p-7f);
+  p = __fmaf_rn(p, f, 0x1.555890p-5f);
+  p = __fmaf_rn(p, f, 0x1.555408p-3f);
+  p = __fmaf_rn(p, f, 0x1.fffffap-2f);
+  p = __fmaf_rn(p, f, 1.0f);
+  p = __fmaf_rn(p, f, 1.0f);
+  const int ni = static_cast<int>(n);
+  const float scale = __int_as_float((ni + 127) << 23);
+  const float r = __fmul_rn(p, scale);
+  return x < -80.0f ? 0.0f : r;
+}
+
+// Order-preserving key of a float for integer atomicMin/atomicMax.
+__device__ __forceinline__ int float_to_ordered(float f) {
+  const int b = __float_as_int(f);
+  return b >= 0 ? b : (b ^ 0x7fffffff);
+}
+__device__ __host__ __forceinline__ float ordered_to_float(int k) {
+  const int b = k >= 0 ? k : (k ^ 0x7fffffff);
+#ifdef __CUDA_ARCH__
+  return __int_as_float(b);
+#else
+  float f;
+  __builtin_memcpy(&f, &b, 4);
+  return f;
+#endif
+}
+
+}  // namespace mpr

@@ -1,0 +1,104 @@
+// internal.cuh — context layout and kernel launchers of libmpr.so (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "mpr.h"
+
+namespace mpr {
+
+// Per-gap-site record, 32 bytes (one sector), read once per half-sweep per launch
+// item and shared by all realizations of the batch.
+//   site  : global row-major site index i = r*Lx + c (Philox counter x, ARITH §A)
+//   beta  : 1/T_i (ARITH §F)
+//   flags : 2 bits per neighbour k in (N, S, W, E): 0 none (outside the grid),
+//           1 known (nb[k] holds the float bits of the frozen angle), 2 gap (nb[k]
+//           holds the neighbour's gap id)
+//   init  : BLOCK_MEAN initial angle (ARITH §G)
+struct __align__(16) GapRec {
+  uint32_t site;
+  float beta;
+  uint32_t flags;
+  float init;
+  int32_t nb[4];
+};
+static_assert(sizeof(GapRec) == 32, "GapRec must be one 32-byte sector");
+
+enum NbType : uint32_t { NB_NONE = 0, NB_KNOWN = 1, NB_GAP = 2 };
+
+// Device scalars written by the parameter kernels (one cudaMalloc).
+struct DevScalars {
+  int zmin_key, zmax_key;        // ordered-int keys (device_math.cuh)
+  int bad_sample;                // non-finite known value seen
+  int pad0;
+  unsigned long long n_known;    // samples
+  unsigned long long n_gap[2];   // gaps by colour (0 = A: (r+c) even)
+  unsigned long long n_avail;    // blocks with >= 1 sample bond
+  unsigned long long n_fallback; // blocks given the median
+  long long sum_SB;              // sum over blocks of SB (known-known bond cos, 2^32)
+  long long sum_SP;              // sum of llrint(phi*2^28) over samples
+  long long sum_NK;              // samples (again, as int64 for the global mean)
+  float median_T;
+  float pad1;
+};
+
+// ---- launchers (params.cu) ----
+void launch_minmax_count(const float* z, const uint8_t* mask, int64_t Lx, int64_t Ly,
+                         DevScalars* sc, cudaStream_t st);
+void launch_transform(const float* z, const uint8_t* mask, int64_t n, const DevScalars* sc,
+                      float* phiK, cudaStream_t st);
+void launch_gap_index(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t PA, int* rowcnt,
+                      int* rowoff, int32_t* gid, GapRec* rec, cudaStream_t st);
+void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int64_t Ly, int lb,
+                        float q, long long* SB, long long* NB, long long* SP, long long* NK,
+                        int64_t nblocks, cudaStream_t st);
+void launch_block_T(const long long* SB, const long long* NB, const long long* SP,
+                    const long long* NK, int64_t nblocks, const float* calT, const float* cale,
+                    int K, float* Tb, DevScalars* sc, cudaStream_t st);
+void launch_median_fill(float* Tb, const long long* NB, int64_t nblocks, DevScalars* sc,
+                        cudaStream_t st);
+void launch_expand(const float* Tb, int64_t Lx, int64_t Ly, int lb, float* T, cudaStream_t st);
+void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int rs, cudaStream_t st);
+void launch_build_records(const int32_t* gid, const uint8_t* mask, const float* phiK,
+                          const float* T, const long long* SP, const long long* NK,
+                          const DevScalars* sc, int64_t Lx, int64_t Ly, int lb, int64_t P,
+                          GapRec* rec, cudaStream_t st);
+void launch_predict(const float* z, const uint8_t* mask, const int32_t* gid, const double* acc,
+                    int64_t n, double denom, const DevScalars* sc, int degenerate, float* out,
+                    cudaStream_t st);
+void launch_scatter_state(const float* phiK, const int32_t* gid, const float* G, int64_t R,
+                          int64_t r, int64_t n, float* out, cudaStream_t st);
+void launch_scatter_acc(const int32_t* gid, const double* acc, int64_t n, double* out,
+                        cudaStream_t st);
+
+// ---- launchers (sweep.cu) ----
+struct SweepArgs {
+  const GapRec* rec;
+  float* G;          // state, [P][R] floats (gap-site major, realization minor)
+  float* A;          // accumulator of the last n_avg sweeps, same layout (nullable)
+  int64_t g_begin;   // first gap id of this colour
+  int64_t g_count;   // gap sites of this colour
+  int R;             // realization stride of the batch (even)
+  int npairs;        // realization pairs in the batch
+  uint32_t pair_base;// global pair index of pair 0 (= m_base / 2)
+  uint32_t sweep;    // 1-based sweep index s
+  uint32_t k0, k1;   // Philox key
+  float q, J;
+  int is_b;          // colour B half-sweep
+  int accumulate;    // add the new state to A
+  double* energy;    // nullable: per-realization bond sums for this sweep, stride S
+  int64_t energy_stride;
+  int r_valid_lo, r_valid_hi;  // realizations [lo, hi) of the batch contribute energy
+};
+int sweep_grid_size(int device);
+void launch_sweep_half(const SweepArgs& a, int grid, cudaStream_t st);
+void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,
+                        uint32_t pair_base, int random_init, uint32_t k0, uint32_t k1,
+                        cudaStream_t st);
+void launch_acc_reduce(const float* X, int64_t P, int R, int r_lo, int r_hi, double* acc,
+                       cudaStream_t st);
+
+}  // namespace mpr

@@ -1,0 +1,645 @@
+// params.cu — parameter-stage kernels of the LE-MPR hot path (a1-a5, a11 of SURVEY §8(a)).
+//
+//  k_minmax_count   a1  sample min/max + counts          (ARITH §D)
+//  k_transform      a2  data -> spin angles at samples   (ARITH §D)
+//  k_row_* / scan   gap-site index (colour, row-major) used by the sweep layout
+//  k_block_stats    a3  block sample-bond sums, exact fixed point (ARITH §E-F)
+//  k_block_T        a4  energy matching by table inversion (ARITH §F)
+//  k_median_fill    a4  lower-median fallback, radix select
+//  k_expand/k_smooth a5 BST step field and SST window smoothing
+//  k_build_records      per-gap records: neighbours, beta = 1/T, BLOCK_MEAN init (ARITH §G)
+//  k_predict        a11 back-transform of the conditional mean (ARITH §I)
+//
+// All of these are HBM-bound streaming/stencil kernels that run once per problem;
+// the hot loop is in sweep.cu.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_math.cuh"
+#include "internal.cuh"
+
+namespace mpr {
+
+namespace {
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_sum_ull(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ----------------------------------------------------------------- a1: min/max
+// 16 sites per thread per iteration: 4 x LDG.128 of z + 1 x LDG.128 of the mask.
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_minmax_count(const float* __restrict__ z,
+                                                      const uint8_t* __restrict__ mask,
+                                                      int64_t Lx, int64_t n, DevScalars* sc) {
+  int kmin = 0x7fffffff, kmax = static_cast<int>(0x80000000u);
+  unsigned long long nk = 0, ng0 = 0, ng1 = 0;
+  int bad = 0;
+  const int64_t nchunks = (n + 15) / 16;
+  for (int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ch < nchunks;
+       ch += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = ch * 16;
+    float zv[16];
+    uint8_t mv[16];
+    if (VEC && i0 + 16 <= n) {
+      const float4* z4 = reinterpret_cast<const float4*>(z + i0);
+      const uint4 m4 = *reinterpret_cast<const uint4*>(mask + i0);
+      const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+      for (int k = 0; k < 16; ++k) mv[k] = static_cast<uint8_t>(mw[k >> 2] >> (8 * (k & 3)));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        // z at gaps is never used: load all 4 (the bytes are in range), select below.
+        const float4 v = __ldg(z4 + k);
+        zv[4 * k] = v.x; zv[4 * k + 1] = v.y; zv[4 * k + 2] = v.z; zv[4 * k + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int64_t i = i0 + k;
+        mv[k] = i < n ? mask[i] : 1;  // out of range: treated below via i < n
+        zv[k] = (i < n && mv[k]) ? z[i] : 0.0f;
+      }
+    }
+    int64_t r = i0 / Lx, c = i0 - r * Lx;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const bool in = (i0 + k) < n;
+      if (in) {
+        if (mv[k]) {
+          const float v = zv[k];
+          if (!isfinite(v)) bad = 1;
+          const int key = float_to_ordered(v);
+          kmin = min(kmin, key);
+          kmax = max(kmax, key);
+          ++nk;
+        } else if (((r + c) & 1) == 0) {
+          ++ng0;
+        } else {
+          ++ng1;
+        }
+      }
+      if (++c == Lx) { c = 0; ++r; }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  nk = warp_sum_ull(nk);
+  ng0 = warp_sum_ull(ng0);
+  ng1 = warp_sum_ull(ng1);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&sc->zmin_key, kmin);
+    atomicMax(&sc->zmax_key, kmax);
+    if (bad) atomicOr(&sc->bad_sample, 1);
+    atomicAdd(&sc->n_known, nk);
+    atomicAdd(&sc->n_gap[0], ng0);
+    atomicAdd(&sc->n_gap[1], ng1);
+  }
+}
+
+__device__ __forceinline__ void range_params(const DevScalars* sc, float* zmin, float* zmax,
+                                             float* s) {
+  // ARITH §D: canonicalise -0 to +0, then s = TWO_PI_F / (z_max - z_min).
+  *zmin = __fadd_rn(ordered_to_float(sc->zmin_key), 0.0f);
+  *zmax = __fadd_rn(ordered_to_float(sc->zmax_key), 0.0f);
+  *s = (*zmax == *zmin) ? 0.0f : __fdiv_rn(kTwoPiF, __fsub_rn(*zmax, *zmin));
+}
+
+// ----------------------------------------------------------------- a2: transform
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_transform(const float* __restrict__ z,
+                                                   const uint8_t* __restrict__ mask, int64_t n,
+                                                   const DevScalars* __restrict__ sc,
+                                                   float* __restrict__ phi) {
+  float zmin, zmax, s;
+  range_params(sc, &zmin, &zmax, &s);
+  const int64_t nch = (n + 3) / 4;
+  for (int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ch < nch;
+       ch += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i0 = ch * 4;
+    if (VEC && i0 + 4 <= n) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(z + i0));
+      const uint32_t m = *reinterpret_cast<const uint32_t*>(mask + i0);
+      const float zz[4] = {v.x, v.y, v.z, v.w};
+      float o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool known = (m >> (8 * k)) & 0xffu;
+        const float p = fminf(__fmul_rn(__fsub_rn(zz[k], zmin), s), kTwoPiF);
+        o[k] = known ? p : 0.0f;
+      }
+      *reinterpret_cast<float4*>(phi + i0) = make_float4(o[0], o[1], o[2], o[3]);
+    } else {
+      for (int64_t i = i0; i < n && i < i0 + 4; ++i)
+        phi[i] = mask[i] ? fminf(__fmul_rn(__fsub_rn(z[i], zmin), s), kTwoPiF) : 0.0f;
+    }
+  }
+}
+
+// ------------------------------------------------------------ gap-site index
+// Gap ids: colour A ((r+c) even) first, then colour B; row-major within a colour.
+__global__ void __launch_bounds__(256) k_row_counts(const uint8_t* __restrict__ mask, int64_t Lx,
+                                                    int64_t Ly, int* __restrict__ rowcnt) {
+  const int64_t r = blockIdx.x;
+  int cnt[2] = {0, 0};
+  for (int64_t c = threadIdx.x; c < Lx; c += blockDim.x)
+    if (!mask[r * Lx + c]) ++cnt[(r + c) & 1];
+  __shared__ int s[2][8];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    int v = cnt[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) s[k][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    int v = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += s[threadIdx.x][w];
+    rowcnt[threadIdx.x * Ly + r] = v;
+  }
+}
+
+// Exclusive scan of m ints (single CTA, 1024 threads, chunked with carry).
+__global__ void __launch_bounds__(1024) k_scan_excl(const int* __restrict__ in, int64_t m,
+                                                    int* __restrict__ out) {
+  __shared__ int warp_tot[32];
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t base = 0; base < m; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const int v = i < m ? in[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int t = warp_tot[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      warp_tot[lane] = t;  // inclusive
+    }
+    __syncthreads();
+    const int wbase = wid ? warp_tot[wid - 1] : 0;
+    if (i < m) out[i] = static_cast<int>(carry) + wbase + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_tot[31];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_row_compact(const uint8_t* __restrict__ mask, int64_t Lx,
+                                                     int64_t Ly, const int* __restrict__ rowoff,
+                                                     int32_t* __restrict__ gid,
+                                                     GapRec* __restrict__ rec) {
+  const int64_t r = blockIdx.x;
+  __shared__ int wcnt[2][8];
+  __shared__ int base[2];
+  if (threadIdx.x < 2) base[threadIdx.x] = rowoff[threadIdx.x * Ly + r];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < Lx; c0 += blockDim.x) {
+    const int64_t c = c0 + threadIdx.x;
+    const int64_t i = r * Lx + c;
+    const bool in = c < Lx;
+    const bool gap = in && !mask[i];
+    const int col = static_cast<int>((r + c) & 1);
+    const unsigned b0 = __ballot_sync(0xffffffffu, gap && col == 0);
+    const unsigned b1 = __ballot_sync(0xffffffffu, gap && col == 1);
+    if (lane == 0) { wcnt[0][wid] = __popc(b0); wcnt[1][wid] = __popc(b1); }
+    __syncthreads();
+    int pre = 0;
+    for (int w = 0; w < wid; ++w) pre += wcnt[col][w];
+    const unsigned below = (1u << lane) - 1u;
+    const int rank = pre + __popc((col ? b1 : b0) & below);
+    if (in) {
+      if (gap) {
+        const int g = base[col] + rank;
+        gid[i] = g;
+        rec[g].site = static_cast<uint32_t>(i);
+      } else {
+        gid[i] = -1;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+      int t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wcnt[threadIdx.x][w];
+      base[threadIdx.x] += t;
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------- a3: block bond statistics
+constexpr int kTile = 32;            // 32 x 32 sites per CTA
+constexpr int kMaxSlots = 17 * 17;   // blocks a tile can touch when l_b >= 2
+
+__global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ phi,
+                                                     const uint8_t* __restrict__ mask, int64_t Lx,
+                                                     int64_t Ly, int lb, float q,
+                                                     long long* __restrict__ SB,
+                                                     long long* __restrict__ NB,
+                                                     long long* __restrict__ SP,
+                                                     long long* __restrict__ NK) {
+  __shared__ long long sSB[kMaxSlots], sNB[kMaxSlots], sSP[kMaxSlots], sNK[kMaxSlots];
+  const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (int64_t)blockIdx.y * kTile;
+  const int64_t nbx = (Lx + lb - 1) / lb;
+  const int64_t bc0 = c0 / lb, br0 = r0 / lb;
+  const int64_t cl = min(c0 + kTile, Lx) - 1, rl = min(r0 + kTile, Ly) - 1;
+  const int nbc = static_cast<int>(cl / lb - bc0 + 1), nbr = static_cast<int>(rl / lb - br0 + 1);
+  const int nslots = nbc * nbr;
+  for (int t = threadIdx.x; t < nslots; t += blockDim.x) { sSB[t] = 0; sNB[t] = 0; sSP[t] = 0; sNK[t] = 0; }
+  __syncthreads();
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int k = 0; k < kTile / 8; ++k) {
+    const int64_t r = r0 + ty + 8 * k, c = c0 + tx;
+    long long vsb = 0, vnb = 0, vsp = 0, vnk = 0;
+    int slot = 0;
+    const bool in = r < Ly && c < Lx;
+    if (in) {
+      slot = static_cast<int>((r / lb - br0) * nbc + (c / lb - bc0));
+      const int64_t i = r * Lx + c;
+      if (mask[i]) {
+        const float pi = phi[i];
+        vsp = __float2ll_rn(__fmul_rn(pi, 0x1p28f));
+        vnk = 1;
+        if (c + 1 < Lx && mask[i + 1]) {
+          const float b = cos_spec(__fmul_rn(q, __fsub_rn(pi, phi[i + 1])));
+          vsb += __float2ll_rn(__fmul_rn(b, 0x1p32f));
+          vnb += 1;
+        }
+        if (r + 1 < Ly && mask[i + Lx]) {
+          const float b = cos_spec(__fmul_rn(q, __fsub_rn(pi, phi[i + Lx])));
+          vsb += __float2ll_rn(__fmul_rn(b, 0x1p32f));
+          vnb += 1;
+        }
+      }
+    }
+    const int slot0 = __shfl_sync(0xffffffffu, slot, 0);
+    if (!in) slot = slot0;
+    if (__all_sync(0xffffffffu, slot == slot0)) {
+      vsb = warp_sum_ll(vsb); vnb = warp_sum_ll(vnb); vsp = warp_sum_ll(vsp); vnk = warp_sum_ll(vnk);
+      if (tx == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&sSB[slot0]), static_cast<unsigned long long>(vsb));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&sNB[slot0]), static_cast<unsigned long long>(vnb));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&sSP[slot0]), static_cast<unsigned long long>(vsp));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&sNK[slot0]), static_cast<unsigned long long>(vnk));
+      }
+    } else if (in) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sSB[slot]), static_cast<unsigned long long>(vsb));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sNB[slot]), static_cast<unsigned long long>(vnb));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sSP[slot]), static_cast<unsigned long long>(vsp));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sNK[slot]), static_cast<unsigned long long>(vnk));
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nslots; t += blockDim.x) {
+    const int64_t b = (br0 + t / nbc) * nbx + (bc0 + t % nbc);
+    if (sSB[t]) atomicAdd(reinterpret_cast<unsigned long long*>(&SB[b]), static_cast<unsigned long long>(sSB[t]));
+    if (sNB[t]) atomicAdd(reinterpret_cast<unsigned long long*>(&NB[b]), static_cast<unsigned long long>(sNB[t]));
+    if (sSP[t]) atomicAdd(reinterpret_cast<unsigned long long*>(&SP[b]), static_cast<unsigned long long>(sSP[t]));
+    if (sNK[t]) atomicAdd(reinterpret_cast<unsigned long long*>(&NK[b]), static_cast<unsigned long long>(sNK[t]));
+  }
+}
+
+// ------------------------------------------------- a4: e_b -> T_b (table inversion)
+__global__ void __launch_bounds__(256) k_block_T(const long long* __restrict__ SB,
+                                                 const long long* __restrict__ NB,
+                                                 const long long* __restrict__ SP,
+                                                 const long long* __restrict__ NK, int64_t nblocks,
+                                                 const float* __restrict__ calT,
+                                                 const float* __restrict__ cale, int K,
+                                                 float* __restrict__ Tb, DevScalars* sc) {
+  __shared__ float sT[256], se[256];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) { sT[k] = calT[k]; se[k] = cale[k]; }
+  __syncthreads();
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long avail = 0;
+  long long sb = 0, sp = 0, nk = 0;
+  if (b < nblocks) {
+    const long long nbv = NB[b];
+    sb = SB[b]; sp = SP[b]; nk = NK[b];
+    float T = -1.0f;  // marker: no sample bond in this block
+    if (nbv > 0) {
+      const double a = -__ll2double_rn(sb) * 0x1p-32;
+      const float e = __double2float_rn(__ddiv_rn(a, __ll2double_rn(nbv)));
+      if (e <= se[0]) {
+        T = sT[0];
+      } else if (e >= se[K - 1]) {
+        T = sT[K - 1];
+      } else {
+        int k = 0;
+        for (int j = 1; j < K; ++j)
+          if (se[j] <= e) k = j;
+        const float w = __fdiv_rn(__fsub_rn(e, se[k]), __fsub_rn(se[k + 1], se[k]));
+        T = __fadd_rn(sT[k], __fmul_rn(w, __fsub_rn(sT[k + 1], sT[k])));
+      }
+      avail = 1;
+    }
+    Tb[b] = T;
+  }
+  avail = warp_sum_ull(avail);
+  sb = warp_sum_ll(sb); sp = warp_sum_ll(sp); nk = warp_sum_ll(nk);
+  if ((threadIdx.x & 31) == 0) {
+    if (avail) atomicAdd(&sc->n_avail, avail);
+    if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(&sc->sum_SB), static_cast<unsigned long long>(sb));
+    if (sp) atomicAdd(reinterpret_cast<unsigned long long*>(&sc->sum_SP), static_cast<unsigned long long>(sp));
+    if (nk) atomicAdd(reinterpret_cast<unsigned long long*>(&sc->sum_NK), static_cast<unsigned long long>(nk));
+  }
+}
+
+// ------------------------------------------- a4: lower median + fallback (1 CTA)
+// Radix select (4 passes of 8 bits) on the bit patterns of the positive available T_b.
+__global__ void __launch_bounds__(1024) k_median_fill(float* __restrict__ Tb,
+                                                      const long long* __restrict__ NB,
+                                                      int64_t nblocks, DevScalars* sc) {
+  __shared__ unsigned hist[256];
+  __shared__ unsigned prefix, pmask;
+  __shared__ unsigned long long rank;
+  const unsigned long long n = sc->n_avail;
+  if (n == 0) return;
+  if (threadIdx.x == 0) { prefix = 0; pmask = 0; rank = (n - 1) / 2; }
+  __syncthreads();
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) hist[t] = 0;
+    __syncthreads();
+    const unsigned pf = prefix, pm = pmask;
+    for (int64_t b = threadIdx.x; b < nblocks; b += blockDim.x) {
+      const float v = Tb[b];
+      if (v > 0.0f) {
+        const unsigned bits = __float_as_uint(v);
+        if ((bits & pm) == pf) atomicAdd(&hist[(bits >> shift) & 255u], 1u);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long cum = 0;
+      unsigned bin = 0;
+      for (; bin < 256; ++bin) {
+        if (cum + hist[bin] > rank) break;
+        cum += hist[bin];
+      }
+      rank -= cum;
+      prefix |= bin << shift;
+      pmask |= 255u << shift;
+    }
+    __syncthreads();
+  }
+  const float med = __uint_as_float(prefix);
+  unsigned long long nf = 0;
+  for (int64_t b = threadIdx.x; b < nblocks; b += blockDim.x)
+    if (NB[b] == 0) { Tb[b] = med; ++nf; }
+  nf = warp_sum_ull(nf);
+  if ((threadIdx.x & 31) == 0 && nf) atomicAdd(&sc->n_fallback, nf);
+  if (threadIdx.x == 0) sc->median_T = med;
+}
+
+// ---------------------------------------------------- a5: expand + SST smoothing
+__global__ void __launch_bounds__(256) k_expand(const float* __restrict__ Tb, int64_t Lx,
+                                                int64_t Ly, int lb, float* __restrict__ T) {
+  const int64_t n = Lx * Ly, nbx = (Lx + lb - 1) / lb;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / Lx, c = i - r * Lx;
+    T[i] = Tb[(r / lb) * nbx + c / lb];
+  }
+}
+
+// One SST pass: clipped (2rs+1)^2 window mean with exact int64 window sums (ARITH §F).
+// 32x32 output tile per CTA; the (32+2rs)^2 input tile is converted once to fixed point
+// in shared memory, summed horizontally, then vertically.
+__global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
+                                                float* __restrict__ Tout, int64_t Lx, int64_t Ly,
+                                                int rs) {
+  extern __shared__ long long smem[];
+  const int W = kTile + 2 * rs;
+  long long* Q = smem;             // W x W
+  long long* H = smem + W * W;     // W x kTile
+  const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (int64_t)blockIdx.y * kTile;
+  for (int t = threadIdx.x; t < W * W; t += blockDim.x) {
+    const int y = t / W, x = t - y * W;
+    const int64_t r = r0 - rs + y, c = c0 - rs + x;
+    Q[t] = (r >= 0 && r < Ly && c >= 0 && c < Lx) ? __float2ll_rn(__fmul_rn(Tin[r * Lx + c], 0x1p40f)) : 0;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < W * kTile; t += blockDim.x) {
+    const int y = t / kTile, x = t - y * kTile;
+    long long s = 0;
+    for (int d = 0; d <= 2 * rs; ++d) s += Q[y * W + x + d];
+    H[t] = s;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kTile * kTile; t += blockDim.x) {
+    const int y = t / kTile, x = t - y * kTile;
+    const int64_t r = r0 + y, c = c0 + x;
+    if (r >= Ly || c >= Lx) continue;
+    long long s = 0;
+    for (int d = 0; d <= 2 * rs; ++d) s += H[(y + d) * kTile + x];
+    const int64_t ra = r - rs > 0 ? r - rs : 0, rb = r + rs < Ly - 1 ? r + rs : Ly - 1;
+    const int64_t ca = c - rs > 0 ? c - rs : 0, cb = c + rs < Lx - 1 ? c + rs : Lx - 1;
+    const double cnt = static_cast<double>((rb - ra + 1) * (cb - ca + 1));
+    Tout[r * Lx + c] = __double2float_rn(__ddiv_rn(__ll2double_rn(s) * 0x1p-40, cnt));
+  }
+}
+
+// -------------------------------------------------- per-gap records (sweep input)
+__global__ void __launch_bounds__(256) k_build_records(
+    const int32_t* __restrict__ gid, const uint8_t* __restrict__ mask,
+    const float* __restrict__ phi, const float* __restrict__ T, const long long* __restrict__ SP,
+    const long long* __restrict__ NK, const DevScalars* __restrict__ sc, int64_t Lx, int64_t Ly,
+    int lb, int64_t P, GapRec* __restrict__ rec) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= P) return;
+  GapRec R = rec[g];
+  const int64_t i = R.site, r = i / Lx, c = i - r * Lx;
+  const int64_t nr[4] = {r - 1, r + 1, r, r};
+  const int64_t nc[4] = {c, c, c - 1, c + 1};
+  uint32_t flags = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    int32_t v = 0;
+    uint32_t ty = NB_NONE;
+    if (nr[k] >= 0 && nr[k] < Ly && nc[k] >= 0 && nc[k] < Lx) {
+      const int64_t j = nr[k] * Lx + nc[k];
+      if (mask[j]) { ty = NB_KNOWN; v = __float_as_int(phi[j]); }
+      else         { ty = NB_GAP;   v = gid[j]; }
+    }
+    flags |= ty << (2 * k);
+    R.nb[k] = v;
+  }
+  R.flags = flags;
+  R.beta = __fdiv_rn(1.0f, T[i]);
+  const int64_t nbx = (Lx + lb - 1) / lb;
+  const int64_t b = (r / lb) * nbx + c / lb;
+  const long long nk = NK[b];
+  R.init = nk ? __double2float_rn(__ddiv_rn(__ll2double_rn(SP[b]) * 0x1p-28, __ll2double_rn(nk)))
+              : __double2float_rn(__ddiv_rn(__ll2double_rn(sc->sum_SP) * 0x1p-28,
+                                            __ll2double_rn(sc->sum_NK)));
+  rec[g] = R;
+}
+
+// ------------------------------------------------------------- a11: predict
+__global__ void __launch_bounds__(256) k_predict(const float* __restrict__ z,
+                                                 const uint8_t* __restrict__ mask,
+                                                 const int32_t* __restrict__ gid,
+                                                 const double* __restrict__ acc, int64_t n,
+                                                 double denom, const DevScalars* __restrict__ sc,
+                                                 int degenerate, float* __restrict__ out) {
+  float zmin, zmax, s;
+  range_params(sc, &zmin, &zmax, &s);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (mask[i]) { out[i] = z[i]; continue; }
+    if (degenerate) { out[i] = zmin; continue; }
+    const double mean = __ddiv_rn(acc[gid[i]], denom);
+    const double dz = __dsub_rn(static_cast<double>(zmax), static_cast<double>(zmin));
+    const double v = __dadd_rn(static_cast<double>(zmin),
+                               __dmul_rn(dz, __ddiv_rn(mean, static_cast<double>(kTwoPiF))));
+    out[i] = __double2float_rn(v);
+  }
+}
+
+__global__ void k_scatter_state(const float* __restrict__ phiK, const int32_t* __restrict__ gid,
+                                const float* __restrict__ G, int64_t R, int64_t rr, int64_t n,
+                                float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t g = gid[i];
+    out[i] = g < 0 ? phiK[i] : G[static_cast<int64_t>(g) * R + rr];
+  }
+}
+
+__global__ void k_scatter_acc(const int32_t* __restrict__ gid, const double* __restrict__ acc,
+                              int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t g = gid[i];
+    out[i] = g < 0 ? 0.0 : acc[g];
+  }
+}
+
+inline int grid_for(int64_t work, int threads, int cap = 148 * 16) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<int>(g);
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+void launch_minmax_count(const float* z, const uint8_t* mask, int64_t Lx, int64_t Ly,
+                         DevScalars* sc, cudaStream_t st) {
+  const int64_t n = Lx * Ly;
+  const int g = grid_for((n + 15) / 16, 256);
+  if (aligned16(z) && aligned16(mask))
+    k_minmax_count<true><<<g, 256, 0, st>>>(z, mask, Lx, n, sc);
+  else
+    k_minmax_count<false><<<g, 256, 0, st>>>(z, mask, Lx, n, sc);
+}
+
+void launch_transform(const float* z, const uint8_t* mask, int64_t n, const DevScalars* sc,
+                      float* phiK, cudaStream_t st) {
+  const int g = grid_for((n + 3) / 4, 256);
+  if (aligned16(z) && aligned16(phiK) && (reinterpret_cast<uintptr_t>(mask) & 3u) == 0)
+    k_transform<true><<<g, 256, 0, st>>>(z, mask, n, sc, phiK);
+  else
+    k_transform<false><<<g, 256, 0, st>>>(z, mask, n, sc, phiK);
+}
+
+void launch_gap_index(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t /*PA*/, int* rowcnt,
+                      int* rowoff, int32_t* gid, GapRec* rec, cudaStream_t st) {
+  k_row_counts<<<static_cast<unsigned>(Ly), 256, 0, st>>>(mask, Lx, Ly, rowcnt);
+  k_scan_excl<<<1, 1024, 0, st>>>(rowcnt, 2 * Ly, rowoff);
+  k_row_compact<<<static_cast<unsigned>(Ly), 256, 0, st>>>(mask, Lx, Ly, rowoff, gid, rec);
+}
+
+void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int64_t Ly, int lb,
+                        float q, long long* SB, long long* NB, long long* SP, long long* NK,
+                        int64_t nblocks, cudaStream_t st) {
+  cudaMemsetAsync(SB, 0, sizeof(long long) * nblocks, st);
+  cudaMemsetAsync(NB, 0, sizeof(long long) * nblocks, st);
+  cudaMemsetAsync(SP, 0, sizeof(long long) * nblocks, st);
+  cudaMemsetAsync(NK, 0, sizeof(long long) * nblocks, st);
+  dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((Ly + kTile - 1) / kTile));
+  k_block_stats<<<grid, 256, 0, st>>>(phiK, mask, Lx, Ly, lb, q, SB, NB, SP, NK);
+}
+
+void launch_block_T(const long long* SB, const long long* NB, const long long* SP,
+                    const long long* NK, int64_t nblocks, const float* calT, const float* cale,
+                    int K, float* Tb, DevScalars* sc, cudaStream_t st) {
+  k_block_T<<<static_cast<unsigned>((nblocks + 255) / 256), 256, 0, st>>>(SB, NB, SP, NK, nblocks,
+                                                                          calT, cale, K, Tb, sc);
+}
+
+void launch_median_fill(float* Tb, const long long* NB, int64_t nblocks, DevScalars* sc,
+                        cudaStream_t st) {
+  k_median_fill<<<1, 1024, 0, st>>>(Tb, NB, nblocks, sc);
+}
+
+void launch_expand(const float* Tb, int64_t Lx, int64_t Ly, int lb, float* T, cudaStream_t st) {
+  k_expand<<<grid_for(Lx * Ly, 256), 256, 0, st>>>(Tb, Lx, Ly, lb, T);
+}
+
+void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int rs,
+                   cudaStream_t st) {
+  const int W = kTile + 2 * rs;
+  const size_t smem = sizeof(long long) * (static_cast<size_t>(W) * W + static_cast<size_t>(W) * kTile);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_smooth, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((Ly + kTile - 1) / kTile));
+  k_smooth<<<grid, 256, smem, st>>>(Tin, Tout, Lx, Ly, rs);
+}
+
+void launch_build_records(const int32_t* gid, const uint8_t* mask, const float* phiK,
+                          const float* T, const long long* SP, const long long* NK,
+                          const DevScalars* sc, int64_t Lx, int64_t Ly, int lb, int64_t P,
+                          GapRec* rec, cudaStream_t st) {
+  if (P == 0) return;
+  k_build_records<<<static_cast<unsigned>((P + 255) / 256), 256, 0, st>>>(gid, mask, phiK, T, SP, NK,
+                                                                         sc, Lx, Ly, lb, P, rec);
+}
+
+void launch_predict(const float* z, const uint8_t* mask, const int32_t* gid, const double* acc,
+                    int64_t n, double denom, const DevScalars* sc, int degenerate, float* out,
+                    cudaStream_t st) {
+  k_predict<<<grid_for(n, 256), 256, 0, st>>>(z, mask, gid, acc, n, denom, sc, degenerate, out);
+}
+
+void launch_scatter_state(const float* phiK, const int32_t* gid, const float* G, int64_t R,
+                          int64_t r, int64_t n, float* out, cudaStream_t st) {
+  k_scatter_state<<<grid_for(n, 256), 256, 0, st>>>(phiK, gid, G, R, r, n, out);
+}
+
+void launch_scatter_acc(const int32_t* gid, const double* acc, int64_t n, double* out,
+                        cudaStream_t st) {
+  k_scatter_acc<<<grid_for(n, 256), 256, 0, st>>>(gid, acc, n, out);
+}
+
+}  // namespace mpr

@@ -1,0 +1,216 @@
+// sweep.cu — the hot loop of the LE-MPR conditional simulation.
+//
+// One launch = one colour half-sweep ("the updating algorithm can be
+// applied to all the spins on the same sub-grid in parallel") over ALL realizations
+// of a batch. Layout: the state G is gap-site major and
+// realization minor, G[g][r], so
+//   * only gap sites are stored and updated (samples are frozen, and
+//     shared by all realizations: their angles live in the 32-byte GapRec of each
+//     gap neighbour);
+//   * one work item = (gap site g, realization pair j): a float2 of the state, one
+//     Philox4x32-10 call whose four words serve both realizations (ARITH §A), eight
+//     cos_spec evaluations per realization (ARITH §B, H) and one exp_spec;
+//   * consecutive lanes take consecutive items, so the self and neighbour float2
+//     accesses of a warp are contiguous runs of G (coalesced), and every lane of a
+//     warp does useful work whatever the gap pattern (no idle lanes on frozen sites).
+// The whole-grid energy (a8) and the last-n_avg accumulation (a9) are fused into the
+// epilogue; the energy of each bond is the value of the branch the Metropolis step
+// already chose, so the diagnostic costs no extra cos evaluation.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_math.cuh"
+#include "internal.cuh"
+
+namespace mpr {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxPairs = 512;  // batch <= 1024 realizations
+
+template <bool QHALF>
+__device__ __forceinline__ float cosq(float d, float q) {
+  if (QHALF) return cos_half_spec(d);
+  return cos_spec(__fmul_rn(q, d));
+}
+
+// ARITH §H for one realization. Returns the new angle; `sel` selects the bonds whose
+// chosen-branch cos is added to *e_sel (energy epilogue).
+template <bool QHALF, bool ENERGY>
+__device__ __forceinline__ float metropolis(float cur, const float (&nbv)[4], uint32_t flags,
+                                            uint32_t sel, float beta, float q, float J,
+                                            uint32_t wa, uint32_t wb, bool& accepted,
+                                            float& e_sel) {
+  const float prop = __fmul_rn(u24(wa), kTwoPiF);
+  float s_cur = 0.0f, s_new = 0.0f, ec = 0.0f, en = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool has = ((flags >> (2 * k)) & 3u) != 0u;
+    float cc = cosq<QHALF>(__fsub_rn(cur, nbv[k]), q);
+    float cn = cosq<QHALF>(__fsub_rn(prop, nbv[k]), q);
+    cc = has ? cc : 0.0f;
+    cn = has ? cn : 0.0f;
+    s_cur = __fadd_rn(s_cur, cc);
+    s_new = __fadd_rn(s_new, cn);
+    if (ENERGY) {
+      const bool s = (sel >> k) & 1u;
+      ec += s ? cc : 0.0f;
+      en += s ? cn : 0.0f;
+    }
+  }
+  const float dE = __fmul_rn(J, __fsub_rn(s_cur, s_new));
+  const float x = -__fmul_rn(dE, beta);
+  accepted = (dE <= 0.0f) || (u24(wb) < exp_spec(x));
+  if (ENERGY) e_sel += accepted ? en : ec;
+  return accepted ? prop : cur;
+}
+
+template <bool QHALF, bool ENERGY>
+__global__ void __launch_bounds__(kThreads) k_sweep_half(const SweepArgs a) {
+  const int tid = blockIdx.x * kThreads + threadIdx.x;
+  const int total = gridDim.x * kThreads;
+  const int npairs = a.npairs;
+  const int active = (total / npairs) * npairs;
+  const int j = tid % npairs;
+  const int64_t gstride = active / npairs;
+  const int64_t R = a.R;
+  float e0 = 0.0f, e1 = 0.0f;
+  if (tid < active) {
+    const uint32_t pair = a.pair_base + static_cast<uint32_t>(j);
+    for (int64_t g = tid / npairs; g < a.g_count; g += gstride) {
+      const int64_t gg = a.g_begin + g;
+      const GapRec rec = a.rec[gg];
+      float2* selfp = reinterpret_cast<float2*>(a.G + gg * R + 2 * j);
+      const float2 cur = *selfp;
+      float nv0[4], nv1[4];
+      uint32_t sel = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
+        if (ty == NB_GAP) {
+          const float2 v = *reinterpret_cast<const float2*>(a.G + static_cast<int64_t>(rec.nb[k]) * R + 2 * j);
+          nv0[k] = v.x;
+          nv1[k] = v.y;
+        } else {
+          const float f = __int_as_float(rec.nb[k]);
+          nv0[k] = f;
+          nv1[k] = f;
+        }
+        if (ENERGY) sel |= (a.is_b ? (ty != NB_NONE) : (ty == NB_KNOWN)) ? (1u << k) : 0u;
+      }
+      const Words4 w = philox4x32_10(rec.site, a.sweep, pair, 2u, a.k0, a.k1);
+      bool acc0, acc1;
+      const float n0 = metropolis<QHALF, ENERGY>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J,
+                                                 w.w0, w.w1, acc0, e0);
+      const float n1 = metropolis<QHALF, ENERGY>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J,
+                                                 w.w2, w.w3, acc1, e1);
+      if (acc0 || acc1) *selfp = make_float2(n0, n1);
+      if (a.accumulate) {
+        float2* ap = reinterpret_cast<float2*>(a.A + gg * R + 2 * j);
+        float2 av = *ap;
+        av.x = __fadd_rn(av.x, n0);
+        av.y = __fadd_rn(av.y, n1);
+        *ap = av;
+      }
+    }
+  }
+  if (ENERGY) {
+    __shared__ double es[2 * kMaxPairs];
+    for (int t = threadIdx.x; t < 2 * npairs; t += kThreads) es[t] = 0.0;
+    __syncthreads();
+    if (tid < active && (e0 != 0.0f || e1 != 0.0f)) {
+      atomicAdd(&es[2 * j], static_cast<double>(e0));
+      atomicAdd(&es[2 * j + 1], static_cast<double>(e1));
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 2 * npairs; t += kThreads)
+      if (t >= a.r_valid_lo && t < a.r_valid_hi && es[t] != 0.0)
+        atomicAdd(a.energy + static_cast<int64_t>(t) * a.energy_stride, es[t]);
+  }
+}
+
+// a6: initial states of a batch (ARITH §G).
+__global__ void __launch_bounds__(256) k_init_states(const GapRec* __restrict__ rec,
+                                                     float* __restrict__ G, float* __restrict__ A,
+                                                     int64_t P, int R, int npairs,
+                                                     uint32_t pair_base, int random_init,
+                                                     uint32_t k0, uint32_t k1) {
+  const int64_t items = P * npairs;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < items;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = t / npairs;
+    const int j = static_cast<int>(t - g * npairs);
+    float2 v;
+    if (random_init) {
+      const Words4 w = philox4x32_10(rec[g].site, 0u, pair_base + static_cast<uint32_t>(j), 1u, k0, k1);
+      v = make_float2(__fmul_rn(u24(w.w0), kTwoPiF), __fmul_rn(u24(w.w2), kTwoPiF));
+    } else {
+      const float f = rec[g].init;
+      v = make_float2(f, f);
+    }
+    *reinterpret_cast<float2*>(G + g * R + 2 * j) = v;
+    if (A) *reinterpret_cast<float2*>(A + g * R + 2 * j) = make_float2(0.0f, 0.0f);
+  }
+}
+
+// a9 (realization sum): acc[g] += sum_{r in [r_lo, r_hi)} X[g][r], fp64, r ascending —
+// the same summation order as the oracle (ARITH §I).
+__global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X, int64_t P, int R,
+                                                    int r_lo, int r_hi, double* __restrict__ acc) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < P;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    double s = acc[g];
+    const float* x = X + g * R;
+    for (int r = r_lo; r < r_hi; ++r) s = __dadd_rn(s, static_cast<double>(x[r]));
+    acc[g] = s;
+  }
+}
+
+}  // namespace
+
+int sweep_grid_size(int device) {
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep_half<true, false>, kThreads, 0);
+  if (per < 1) per = 1;
+  return sms * per;
+}
+
+void launch_sweep_half(const SweepArgs& a, int grid, cudaStream_t st) {
+  const int64_t items = a.g_count * a.npairs;
+  int64_t g = (items + kThreads - 1) / kThreads;
+  if (g > grid) g = grid;
+  const int64_t need = (a.npairs + kThreads - 1) / kThreads;  // active threads >= npairs
+  if (g < need) g = need;
+  if (g < 1) g = 1;
+  const bool qhalf = (a.q == 0.5f);
+  const bool energy = (a.energy != nullptr);
+  const dim3 gr(static_cast<unsigned>(g));
+  if (qhalf && !energy) k_sweep_half<true, false><<<gr, kThreads, 0, st>>>(a);
+  else if (qhalf && energy) k_sweep_half<true, true><<<gr, kThreads, 0, st>>>(a);
+  else if (!qhalf && !energy) k_sweep_half<false, false><<<gr, kThreads, 0, st>>>(a);
+  else k_sweep_half<false, true><<<gr, kThreads, 0, st>>>(a);
+}
+
+void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,
+                        uint32_t pair_base, int random_init, uint32_t k0, uint32_t k1,
+                        cudaStream_t st) {
+  const int64_t items = P * npairs;
+  int64_t g = (items + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  if (g < 1) g = 1;
+  k_init_states<<<static_cast<unsigned>(g), 256, 0, st>>>(rec, G, A, P, R, npairs, pair_base,
+                                                          random_init, k0, k1);
+}
+
+void launch_acc_reduce(const float* X, int64_t P, int R, int r_lo, int r_hi, double* acc,
+                       cudaStream_t st) {
+  int64_t g = (P + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  if (g < 1) g = 1;
+  k_acc_reduce<<<static_cast<unsigned>(g), 256, 0, st>>>(X, P, R, r_lo, r_hi, acc);
+}
+
+}  // namespace mpr

@@ -1,0 +1,208 @@
+"""GPU (libmpr.so, sm_100a) vs CPU oracle parity, through the C-ABI.
+
+Bars (BASELINE.json north star):
+- spin transform, masks, block statistics, temperature field: bit-exact;
+- Markov-chain states after k sweeps: bit-exact (shared Philox stream, docs/ARITH.md);
+- predictions: within 1e-3 of the data range (bit-exact when n_avg = 1 on one GPU);
+- MAE / RMSE / MARE: within 1e-4 relative; energy trace: within 1e-5 relative.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from inputs.synth import make_problem
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2212_01317_b200 import _build
+    _build.build()
+    import paper_2212_01317_b200 as P
+    P.load_library()
+    return P
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint32 if a.dtype == np.float32 else np.uint64)
+
+
+def assert_bitwise(a, b, what):
+    a = np.ascontiguousarray(a); b = np.ascontiguousarray(b)
+    assert a.shape == b.shape, what
+    diff = np.flatnonzero(bits(a).ravel() != bits(b).ravel())
+    assert diff.size == 0, f"{what}: {diff.size} mismatches, first at {np.unravel_index(diff[0], a.shape)}: " \
+                           f"gpu={a.ravel()[diff[0]]!r} oracle={b.ravel()[diff[0]]!r}"
+
+
+def gpu_run(P, z, mask, cfg, calib, M, S, seed, energy=False):
+    m = P.LeMpr(cfg, calib)
+    m.set_data(z, mask)
+    m.set_energy_trace(energy)
+    T = m.estimate_local_params(want_T=True)
+    m.simulate(M, S, seed)
+    out = dict(T=T, pred=m.predict(), info=m.info(), phiK=m.debug(P.binding.MPR_BUF_PHI_KNOWN),
+               Tb=m.debug(P.binding.MPR_BUF_BLOCK_T), stats=m.debug(P.binding.MPR_BUF_BLOCK_STATS),
+               acc=m.debug(P.binding.MPR_BUF_ACC))
+    inf = out["info"]
+    lo, hi = inf["last_m_base"], min(inf["last_m_base"] + inf["last_batch"], M)
+    out["states"] = {r: m.debug(P.binding.MPR_BUF_STATE, r) for r in range(lo, hi)}
+    if energy:
+        out["energy"] = m.debug(P.binding.MPR_BUF_ENERGY)
+    m.close()
+    return out
+
+
+def ocfg(cfg):
+    return O.OracleConfig(q=cfg.q, J=cfg.J, lb=cfg.l_b, rs=cfg.r_s, ns=cfg.n_s, init=cfg.init, n_avg=cfg.n_avg)
+
+
+def compare(P, z, mask, truth, cfg, calib, M, S, seed, energy=False, exact_pred=True):
+    g = gpu_run(P, z, mask, cfg, calib, M, S, seed, energy=energy)
+    Tk, ek = calib
+    o = O.fill(z, mask, ocfg(cfg), Tk, ek, M, S, seed, energy=energy, states=True)
+    p = o["params"]
+    assert_bitwise(g["phiK"], p.phi0, "phi at samples")
+    assert g["info"]["z_min"] == p.zmin and g["info"]["z_max"] == p.zmax
+    nb = p.Tb.size
+    assert np.array_equal(g["stats"][2], p.SP.ravel()) and np.array_equal(g["stats"][3], p.NK.ravel())
+    assert_bitwise(g["Tb"], p.Tb.ravel(), "block temperatures")
+    assert_bitwise(g["T"], p.T, "temperature field")
+    for r, st in g["states"].items():
+        assert_bitwise(st, o["sim"]["phi"][r], f"state of realization {r}")
+    rng = p.zmax - p.zmin
+    gaps = mask == 0
+    if exact_pred:
+        assert_bitwise(g["acc"][gaps], o["sim"]["acc"][gaps], "accumulator")
+        assert_bitwise(g["pred"], o["pred"], "predictions")
+    else:
+        assert np.max(np.abs(g["pred"][gaps] - o["pred"][gaps])) <= 1e-3 * rng
+        assert_bitwise(g["pred"][~gaps], z[~gaps], "samples returned bitwise")
+    sg, so = O.score(g["pred"], truth, mask), O.score(o["pred"], truth, mask)
+    for k in ("mae", "rmse", "mare"):
+        assert abs(sg[k] - so[k]) <= 1e-4 * abs(so[k]) + 1e-12, k
+    if energy:
+        assert np.max(np.abs(g["energy"] / o["sim"]["energy"] - 1)) < 1e-5
+    return g, o
+
+
+def test_c1_config_bit_exact(P, calib):
+    """BASELINE config 1: 64x64 Matern, 50% random gaps, M = 10, S = 30, SST defaults."""
+    truth, z, mask = make_problem(64, 0.5)
+    compare(P, z, mask, truth, P.Config(), calib, 10, 30, 20221202, energy=True)
+
+
+def test_ragged_odd_m_random_init(P, calib):
+    """Sizes that divide nothing (67 x 45), l_b = 8, r_s = 3, n_s = 2, odd M, RANDOM init."""
+    truth, z, mask = make_problem(45, 0.4, Lx=67, corr_len=8.0)
+    cfg = P.Config(l_b=8, r_s=3, n_s=2, init="random")
+    compare(P, z, mask, truth, cfg, calib, 7, 12, 99)
+
+
+def test_generic_q_and_J(P, calib):
+    """q != 1/2 and J != 1 take the generic (non-specialised) cos path; still bit-exact."""
+    truth, z, mask = make_problem(40, 0.6, Lx=36, corr_len=5.0)
+    compare(P, z, mask, truth, P.Config(q=0.3, J=2.0, l_b=16, n_s=1, r_s=1), calib, 4, 10, 5)
+
+
+def test_n_avg_tolerance(P, calib):
+    """Averaging the last 5 sweeps: states bit-exact, predictions within 1e-3 of the range."""
+    truth, z, mask = make_problem(48, 0.5, corr_len=6.0)
+    compare(P, z, mask, truth, P.Config(n_avg=5), calib, 6, 15, 3, exact_pred=False)
+
+
+def test_batched_realizations(P, calib):
+    """max_batch = 4 forces 3 launch batches for M = 10 (pairs of the Philox stream split)."""
+    truth, z, mask = make_problem(32, 0.5, corr_len=5.0)
+    compare(P, z, mask, truth, P.Config(max_batch=4, l_b=8), calib, 10, 8, 17)
+
+
+def test_cloud_gaps_bst_and_mpr_modes(P, calib):
+    """Clustered gaps (70%), BST (n_s = 0) and uniform MPR (l_b >= L) special cases."""
+    truth, z, mask = make_problem(96, 0.7, gaps="cloud", corr_len=10.0)
+    compare(P, z, mask, truth, P.Config(n_s=0), calib, 4, 10, 1)
+    compare(P, z, mask, truth, P.Config(l_b=128, n_s=0), calib, 4, 10, 2)
+
+
+def test_small_blocks_many_fallbacks(P, calib):
+    """l_b = 2 at 90% missing: most blocks have no sample bond and take the lower median."""
+    truth, z, mask = make_problem(50, 0.9, corr_len=4.0)
+    g, o = compare(P, z, mask, truth, P.Config(l_b=2, n_s=1, r_s=1), calib, 2, 6, 8)
+    assert g["info"]["n_blocks_fallback"] > 0
+
+
+def test_sharded_ranges_equal_single_call(P, calib):
+    """simulate_range over [0,4) then [4,10) == simulate(10) bit for bit (global realization ids)."""
+    truth, z, mask = make_problem(40, 0.5, corr_len=6.0)
+    cfg = P.Config(l_b=8)
+    ref = gpu_run(P, z, mask, cfg, calib, 10, 8, 77)
+    m = P.LeMpr(cfg, calib)
+    m.set_data(z, mask); m.estimate_local_params(); m.reset_accumulator()
+    m.simulate_range(10, 8, 77, 0, 4)
+    m.simulate_range(10, 8, 77, 4, 10)
+    assert_bitwise(m.predict(), ref["pred"], "predictions of the sharded run")
+    m.close()
+
+
+def test_degenerate_no_gap_and_errors(P, calib):
+    Tk, ek = calib
+    z = np.full((8, 8), 3.25, np.float32); mask = np.ones((8, 8), np.uint8); mask[2, 3] = 0; z[2, 3] = np.nan
+    m = P.LeMpr(P.Config(), calib)
+    m.set_data(z, mask); m.estimate_local_params(); m.simulate(4, 5, 1)
+    out = m.predict()
+    assert out[2, 3] == np.float32(3.25) and m.info()["degenerate_range"] == 1
+    # no gaps: predictions are the input, bitwise
+    truth, _, _ = make_problem(16, 0.5)
+    m.set_data(truth, np.ones((16, 16), np.uint8)); m.estimate_local_params(); m.simulate(2, 3, 1)
+    assert_bitwise(m.predict(), truth, "P = 0 returns the input")
+    # too few samples
+    mask = np.zeros((8, 8), np.uint8); mask[0, 0] = 1
+    with pytest.raises(P.MprError) as e:
+        m.set_data(np.zeros((8, 8), np.float32), mask)
+    assert e.value.status == P.binding.MPR_ERR_TOO_FEW_SAMPLES
+    # no sample bonds: samples only on colour A
+    mask = (np.add.outer(np.arange(8), np.arange(8)) % 2 == 0).astype(np.uint8)
+    m.set_data(np.arange(64, dtype=np.float32).reshape(8, 8), mask)
+    with pytest.raises(P.MprError) as e:
+        m.estimate_local_params()
+    assert e.value.status == P.binding.MPR_ERR_NO_SAMPLE_BONDS
+    # out of order
+    m2 = P.LeMpr(P.Config(), calib)
+    with pytest.raises(P.MprError) as e:
+        m2.simulate(1, 1, 1)
+    assert e.value.status == P.binding.MPR_ERR_STATE
+    # non-finite sample
+    bad = np.ones((4, 4), np.float32); bad[1, 1] = np.inf
+    with pytest.raises(P.MprError) as e:
+        m2.set_data(bad, np.ones((4, 4), np.uint8))
+    assert e.value.status == P.binding.MPR_ERR_INVALID_ARG
+    m.close(); m2.close()
+
+
+@pytest.mark.slow
+def test_c2_full_size_sampled(P, calib):
+    """BASELINE config 2 at full size (1024^2, p = 0.33, M = 100, S = 30) in the launch
+    configuration bench.py times: the whole parameter stage bit-exact, and realizations
+    0, 57, 99 (sampled; each one is a 1e7-update oracle run) bit-exact."""
+    Tk, ek = calib
+    truth, z, mask = make_problem(1024, 0.33, nu=0.5)
+    cfg = P.Config()
+    m = P.LeMpr(cfg, calib)
+    m.set_data(z, mask)
+    T = m.estimate_local_params(want_T=True)
+    m.simulate(100, 30, 20221202)
+    pred = m.predict()
+    p = O.parameters(z, mask, ocfg(cfg), Tk, ek)
+    assert_bitwise(T, p.T, "temperature field (1024^2)")
+    for r in (0, 57, 99):
+        st = m.debug(P.binding.MPR_BUF_STATE, r)
+        o = O.simulate(p, mask, ocfg(cfg), 100, 30, 20221202, m_begin=r, m_end=r + 1, states=True)
+        assert_bitwise(st, o["phi"][0], f"realization {r} at 1024^2")
+    gaps = mask == 0
+    assert_bitwise(pred[~gaps], z[~gaps], "samples")
+    assert pred[gaps].min() >= p.zmin and pred[gaps].max() <= p.zmax
+    m.close()
