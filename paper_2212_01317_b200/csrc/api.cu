@@ -8,6 +8,7 @@
 #include <cstddef>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -55,6 +56,7 @@ struct mpr_ctx {
   int stage = ST_INIT;
   std::string err;
   int sweep_grid = 0;
+  int sweep_variant = 0;  // kernel variant (MPR_SWEEP_VARIANT, tuning only)
   // problem
   int64_t Lx = 0, Ly = 0, n = 0;
   int64_t P = 0, PA = 0, n_known = 0;
@@ -217,6 +219,8 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
   const double per_r = 4.0 * static_cast<double>(std::max<int64_t>(c->P, 1)) * (c->cfg.n_avg > 1 ? 2.0 : 1.0);
   const double budget = 0.6 * static_cast<double>(fr + c->G.bytes + c->A.bytes);
   int64_t cap = static_cast<int64_t>(budget / per_r);
+  // the sweep kernel indexes the state with 32-bit element offsets: P * R < 2^31
+  cap = std::min<int64_t>(cap, ((int64_t(1) << 31) - 1) / std::max<int64_t>(c->P, 1));
   cap -= cap & 1;
   if (cap < 2) cap = 2;
   return std::min(R, cap);
@@ -288,7 +292,8 @@ mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
     mpr_destroy(c);
     return e == cudaErrorMemoryAllocation ? MPR_ERR_OOM : MPR_ERR_CUDA;
   }
-  c->sweep_grid = sweep_grid_size(c->device);
+  if (const char* v = std::getenv("MPR_SWEEP_VARIANT")) c->sweep_variant = std::atoi(v);
+  c->sweep_grid = sweep_grid_size(c->device, c->sweep_variant);
   *out = c;
   return MPR_OK;
 }
@@ -490,7 +495,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
         a.g_begin = colour ? c->PA : 0;
         a.g_count = colour ? c->P - c->PA : c->PA;
         if (a.g_count > 0) {
-          launch_sweep_half(a, c->sweep_grid, st);
+          launch_sweep_half(a, c->sweep_grid, c->sweep_variant, st);
           CKL("sweep_half");
           ++c->launches;
           ++nsweep_launch;

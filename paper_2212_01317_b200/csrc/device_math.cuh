@@ -65,7 +65,34 @@ __device__ __forceinline__ float cos_half_spec(float d) {
   return p;
 }
 
-// ARITH §C — exp_spec(x), x <= 0.
+// phi' = u(w) * TWO_PI_F computed as one multiply: (w>>8) * (TWO_PI_F * 2^-24). The
+// 2^-24 scaling is exact, so the single rounding is the one of ARITH §H.
+__device__ __forceinline__ float proposal_angle(uint32_t w) {
+  return __fmul_rn(__uint2float_rn(w >> 8), 0x1.921fb6p-22f);
+}
+
+// ARITH §C — exp_spec(x), x <= 0. rint() is done with the 1.5*2^23 magic constant:
+// for |v| < 2^22, (v + 1.5*2^23) rounds v to the nearest integer (ties to even) in
+// round-to-nearest mode, so n equals rintf(v) bit for bit; the integer n is read
+// from the low mantissa bits. No XU (FRND/F2I) instructions.
+__device__ __forceinline__ float exp_spec_fast(float x) {
+  const float v = __fmul_rn(x, 0x1.715476p+0f);
+  const float tm = __fadd_rn(v, 12582912.0f);
+  const float n = __fsub_rn(tm, 12582912.0f);
+  const int ni = __float_as_int(tm) - 0x4b400000;
+  float f = __fmaf_rn(-n, 0x1.62e430p-1f, x);
+  f = __fmaf_rn(-n, -0x1.05c610p-29f, f);
+  float p = 0x1.6ac2a0p-10f;
+  p = __fmaf_rn(p, f, 0x1.126e38p-7f);
+  p = __fmaf_rn(p, f, 0x1.555890p-5f);
+  p = __fmaf_rn(p, f, 0x1.555408p-3f);
+  p = __fmaf_rn(p, f, 0x1.fffffap-2f);
+  p = __fmaf_rn(p, f, 1.0f);
+  p = __fmaf_rn(p, f, 1.0f);
+  const float r = __fmul_rn(p, __int_as_float((ni + 127) << 23));
+  return x < -80.0f ? 0.0f : r;
+}
+
 __device__ __forceinline__ float exp_spec(float x) {
   const float n = rintf(__fmul_rn(x, 0x1.715476p+0f));
   float f = __fmaf_rn(-n, 0x1.62e430p-1f, x);

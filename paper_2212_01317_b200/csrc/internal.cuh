@@ -93,8 +93,8 @@ struct SweepArgs {
   int64_t energy_stride;
   int r_valid_lo, r_valid_hi;  // realizations [lo, hi) of the batch contribute energy
 };
-int sweep_grid_size(int device);
-void launch_sweep_half(const SweepArgs& a, int grid, cudaStream_t st);
+int sweep_grid_size(int device, int variant);
+void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st);
 void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,
                         uint32_t pair_base, int random_init, uint32_t k0, uint32_t k1,
                         cudaStream_t st);

@@ -36,24 +36,33 @@ __device__ __forceinline__ float cosq(float d, float q) {
   return cos_spec(__fmul_rn(q, d));
 }
 
-// ARITH §H for one realization. Returns the new angle; `sel` selects the bonds whose
+// ARITH §H for one realization. FULL: all four neighbours exist (interior site), so
+// the sums need no masking and start from the first term (+0 + c == c exactly, since
+// cos_spec never returns -0). Returns the new angle; `sel` selects the bonds whose
 // chosen-branch cos is added to *e_sel (energy epilogue).
-template <bool QHALF, bool ENERGY>
+template <bool QHALF, bool ENERGY, bool FULL>
 __device__ __forceinline__ float metropolis(float cur, const float (&nbv)[4], uint32_t flags,
                                             uint32_t sel, float beta, float q, float J,
                                             uint32_t wa, uint32_t wb, bool& accepted,
                                             float& e_sel) {
-  const float prop = __fmul_rn(u24(wa), kTwoPiF);
+  const float prop = proposal_angle(wa);
   float s_cur = 0.0f, s_new = 0.0f, ec = 0.0f, en = 0.0f;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const bool has = ((flags >> (2 * k)) & 3u) != 0u;
     float cc = cosq<QHALF>(__fsub_rn(cur, nbv[k]), q);
     float cn = cosq<QHALF>(__fsub_rn(prop, nbv[k]), q);
-    cc = has ? cc : 0.0f;
-    cn = has ? cn : 0.0f;
-    s_cur = __fadd_rn(s_cur, cc);
-    s_new = __fadd_rn(s_new, cn);
+    if (!FULL) {
+      const bool has = ((flags >> (2 * k)) & 3u) != 0u;
+      cc = has ? cc : 0.0f;
+      cn = has ? cn : 0.0f;
+    }
+    if (FULL && k == 0) {
+      s_cur = cc;
+      s_new = cn;
+    } else {
+      s_cur = __fadd_rn(s_cur, cc);
+      s_new = __fadd_rn(s_new, cn);
+    }
     if (ENERGY) {
       const bool s = (sel >> k) & 1u;
       ec += s ? cc : 0.0f;
@@ -62,35 +71,44 @@ __device__ __forceinline__ float metropolis(float cur, const float (&nbv)[4], ui
   }
   const float dE = __fmul_rn(J, __fsub_rn(s_cur, s_new));
   const float x = -__fmul_rn(dE, beta);
-  accepted = (dE <= 0.0f) || (u24(wb) < exp_spec(x));
+  accepted = (dE <= 0.0f) || (u24(wb) < exp_spec_fast(x));
   if (ENERGY) e_sel += accepted ? en : ec;
   return accepted ? prop : cur;
 }
 
-template <bool QHALF, bool ENERGY>
-__global__ void __launch_bounds__(kThreads) k_sweep_half(const SweepArgs a) {
+// Every neighbour present: each 2-bit field of flags is non-zero.
+__device__ __forceinline__ bool all_present(uint32_t f) {
+  return ((f | (f >> 1)) & 0x55u) == 0x55u;
+}
+
+template <bool QHALF, bool ENERGY, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_sweep_half(const SweepArgs a) {
   const int tid = blockIdx.x * kThreads + threadIdx.x;
   const int total = gridDim.x * kThreads;
   const int npairs = a.npairs;
   const int active = (total / npairs) * npairs;
   const int j = tid % npairs;
-  const int64_t gstride = active / npairs;
-  const int64_t R = a.R;
+  const uint32_t gstride = static_cast<uint32_t>(active / npairs);
+  // 32-bit element offsets: the host caps the batch so that P * R < 2^31
+  const uint32_t R = static_cast<uint32_t>(a.R);
+  const uint32_t j2 = 2u * static_cast<uint32_t>(j);
+  const uint32_t gcount = static_cast<uint32_t>(a.g_count);
+  const uint32_t gbegin = static_cast<uint32_t>(a.g_begin);
   float e0 = 0.0f, e1 = 0.0f;
   if (tid < active) {
     const uint32_t pair = a.pair_base + static_cast<uint32_t>(j);
-    for (int64_t g = tid / npairs; g < a.g_count; g += gstride) {
-      const int64_t gg = a.g_begin + g;
+    for (uint32_t g = static_cast<uint32_t>(tid / npairs); g < gcount; g += gstride) {
+      const uint32_t gg = gbegin + g;
       const GapRec rec = a.rec[gg];
-      float2* selfp = reinterpret_cast<float2*>(a.G + gg * R + 2 * j);
-      const float2 cur = *selfp;
+      const uint32_t self_off = gg * R + j2;
+      const float2 cur = *reinterpret_cast<const float2*>(a.G + self_off);
       float nv0[4], nv1[4];
       uint32_t sel = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
         if (ty == NB_GAP) {
-          const float2 v = *reinterpret_cast<const float2*>(a.G + static_cast<int64_t>(rec.nb[k]) * R + 2 * j);
+          const float2 v = *reinterpret_cast<const float2*>(a.G + (static_cast<uint32_t>(rec.nb[k]) * R + j2));
           nv0[k] = v.x;
           nv1[k] = v.y;
         } else {
@@ -102,13 +120,17 @@ __global__ void __launch_bounds__(kThreads) k_sweep_half(const SweepArgs a) {
       }
       const Words4 w = philox4x32_10(rec.site, a.sweep, pair, 2u, a.k0, a.k1);
       bool acc0, acc1;
-      const float n0 = metropolis<QHALF, ENERGY>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J,
-                                                 w.w0, w.w1, acc0, e0);
-      const float n1 = metropolis<QHALF, ENERGY>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J,
-                                                 w.w2, w.w3, acc1, e1);
-      if (acc0 || acc1) *selfp = make_float2(n0, n1);
+      float n0, n1;
+      if (all_present(rec.flags)) {
+        n0 = metropolis<QHALF, ENERGY, true>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
+        n1 = metropolis<QHALF, ENERGY, true>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
+      } else {
+        n0 = metropolis<QHALF, ENERGY, false>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
+        n1 = metropolis<QHALF, ENERGY, false>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
+      }
+      if (acc0 || acc1) *reinterpret_cast<float2*>(a.G + self_off) = make_float2(n0, n1);
       if (a.accumulate) {
-        float2* ap = reinterpret_cast<float2*>(a.A + gg * R + 2 * j);
+        float2* ap = reinterpret_cast<float2*>(a.A + self_off);
         float2 av = *ap;
         av.x = __fadd_rn(av.x, n0);
         av.y = __fadd_rn(av.y, n1);
@@ -145,7 +167,7 @@ __global__ void __launch_bounds__(256) k_init_states(const GapRec* __restrict__ 
     float2 v;
     if (random_init) {
       const Words4 w = philox4x32_10(rec[g].site, 0u, pair_base + static_cast<uint32_t>(j), 1u, k0, k1);
-      v = make_float2(__fmul_rn(u24(w.w0), kTwoPiF), __fmul_rn(u24(w.w2), kTwoPiF));
+      v = make_float2(proposal_angle(w.w0), proposal_angle(w.w2));
     } else {
       const float f = rec[g].init;
       v = make_float2(f, f);
@@ -170,15 +192,31 @@ __global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X,
 
 }  // namespace
 
-int sweep_grid_size(int device) {
+// Kernel variants (tuning knob, MPR_SWEEP_VARIANT): register cap via min blocks per SM.
+template <bool Q, bool E>
+static void* sweep_kernel_ptr(int variant) {
+  switch (variant) {
+    case 1: return reinterpret_cast<void*>(k_sweep_half<Q, E, 5>);
+    case 2: return reinterpret_cast<void*>(k_sweep_half<Q, E, 6>);
+    case 3: return reinterpret_cast<void*>(k_sweep_half<Q, E, 8>);
+    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1>);
+  }
+}
+
+static void* sweep_kernel(bool qhalf, bool energy, int variant) {
+  if (qhalf) return energy ? sweep_kernel_ptr<true, true>(variant) : sweep_kernel_ptr<true, false>(variant);
+  return energy ? sweep_kernel_ptr<false, true>(variant) : sweep_kernel_ptr<false, false>(variant);
+}
+
+int sweep_grid_size(int device, int variant) {
   int sms = 0, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep_half<true, false>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, variant), kThreads, 0);
   if (per < 1) per = 1;
   return sms * per;
 }
 
-void launch_sweep_half(const SweepArgs& a, int grid, cudaStream_t st) {
+void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st) {
   const int64_t items = a.g_count * a.npairs;
   int64_t g = (items + kThreads - 1) / kThreads;
   if (g > grid) g = grid;
@@ -187,11 +225,9 @@ void launch_sweep_half(const SweepArgs& a, int grid, cudaStream_t st) {
   if (g < 1) g = 1;
   const bool qhalf = (a.q == 0.5f);
   const bool energy = (a.energy != nullptr);
-  const dim3 gr(static_cast<unsigned>(g));
-  if (qhalf && !energy) k_sweep_half<true, false><<<gr, kThreads, 0, st>>>(a);
-  else if (qhalf && energy) k_sweep_half<true, true><<<gr, kThreads, 0, st>>>(a);
-  else if (!qhalf && !energy) k_sweep_half<false, false><<<gr, kThreads, 0, st>>>(a);
-  else k_sweep_half<false, true><<<gr, kThreads, 0, st>>>(a);
+  void* fn = sweep_kernel(qhalf, energy, variant);
+  void* args[] = {const_cast<SweepArgs*>(&a)};
+  cudaLaunchKernel(fn, dim3(static_cast<unsigned>(g)), dim3(kThreads), args, 0, st);
 }
 
 void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,

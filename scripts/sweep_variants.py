@@ -1,0 +1,51 @@
+#!/usr/bin/env python3
+"""Time the half-sweep kernel variants (MPR_SWEEP_VARIANT) on one config; check they agree bitwise."""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from inputs.synth import CONFIGS, make_problem  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--variants", default="0,1,2,3,4")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--M", type=int, default=None)
+    a = ap.parse_args()
+    import paper_2212_01317_b200 as P
+    c = CONFIGS[a.config]
+    M = a.M or c["M"]
+    truth, z, mask = make_problem(c["L"], c["p"], gaps=c["gaps"], nu=c["nu"])
+    Pg = int((mask == 0).sum())
+    calib = P.load_calibration()
+    ref = None
+    for v in [int(x) for x in a.variants.split(",")]:
+        os.environ["MPR_SWEEP_VARIANT"] = str(v)
+        m = P.LeMpr(P.Config(), calib)
+        m.set_data(z, mask)
+        m.estimate_local_params()
+        m.simulate(M, c["sweeps"], 1)  # warm-up
+        m.set_kernel_timing(True)
+        for _ in range(a.reps):
+            m.simulate(M, c["sweeps"], 1)
+        inf = m.info()
+        pred = m.predict()
+        if ref is None:
+            ref = pred
+        same = bool(np.array_equal(pred.view(np.uint32), ref.view(np.uint32)))
+        per = inf["sweep_ms"] / inf["sweep_launches"]
+        ups = Pg * M / 2 / (per / 1e3)
+        print(json.dumps({"variant": v, "config": a.config, "M": M, "ms_per_halfsweep": per,
+                          "updates_per_s": ups, "bitwise_equal_to_first": same}), flush=True)
+        m.close()
+
+
+if __name__ == "__main__":
+    main()
