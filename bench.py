@@ -32,6 +32,10 @@ sys.path.insert(0, ROOT)
 from inputs.synth import CONFIGS, SEED_SIM, make_problem  # noqa: E402
 
 METRIC = "gap-site spin updates/sec (LE-MPR conditional simulation, whole fill)"
+# FP32 lane-ops the arithmetic contract fixes per gap-site update (8 cos_spec
+# of 8 ops, 8 sums, dE/beta 3, exp_spec 12, 4 conversions = 93) + half a Philox4x32-10
+# call (10 rounds x 2 IMAD.WIDE + 2 LOP3 = 40 per pair) = 113.
+ALG_OPS_PER_UPDATE = 113
 UNIT = "updates/s"
 
 
@@ -78,7 +82,7 @@ def algorithmic_bytes_per_update(p, n_avg=1, S=30, b_T=4):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 20 ms during the timed regions."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -92,7 +96,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -188,8 +192,9 @@ def run_mpr(args):
     calib = Pk.load_calibration()
     cfg = Pk.Config(device=local)
     eng = Pk.LeMpr(cfg, calib, stream=stream.cuda_stream)
-    M_glob = M * ws
-    m0, m1 = rank * M, (rank + 1) * M
+    from paper_2212_01317_b200.sharding import allreduce_accumulator, shard_range
+    M_glob = M * ws  # weak scaling: M realizations per rank
+    m0, m1 = shard_range(M_glob, ws, rank)
 
     # device-resident inputs (the "value" leg) and pinned host buffers (the e2e leg)
     z_dev = torch.from_numpy(np.nan_to_num(z, nan=0.0)).to(dev)
@@ -200,19 +205,9 @@ def run_mpr(args):
     out_pin = torch.empty((Ly, Lx), dtype=torch.float32).pin_memory()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    acc_view = None
-
     def allreduce_acc():
-        nonlocal acc_view
-        if ws == 1:
-            return
-        ptr, cnt = eng.simulate_device_acc()
-
-        class _CAI:
-            __cuda_array_interface__ = {"shape": (cnt,), "typestr": "<f8", "data": (ptr, False), "version": 3,
-                                        "stream": None}
-        acc_view = torch.as_tensor(_CAI(), device=dev)
-        dist.all_reduce(acc_view, op=dist.ReduceOp.SUM)
+        if ws > 1:
+            allreduce_accumulator(eng.accumulator_tensor())
 
     def step_device():
         eng.set_data_device(z_dev.data_ptr(), m_dev.data_ptr(), Lx, Ly)
@@ -257,7 +252,6 @@ def run_mpr(args):
         e1.synchronize()
         total_ms += e0.elapsed_time(e1)
     barrier()
-    ck = clocks.stop() if clocks else None
     info = eng.info()
     launches = info["total_launches"] - launches0
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -269,15 +263,19 @@ def run_mpr(args):
 
     # dominant kernel: the half-sweep (CUDA events on the library's stream around the sweep loops)
     sweep_ms, sweep_n = info["sweep_ms"], info["sweep_launches"]
-    sweep_updates = P * S * M * args.steps
+    sweep_updates = P * S * (m1 - m0) * args.steps
+    sweep_s = sweep_ms / 1000.0
     b_upd = algorithmic_bytes_per_update(c["p"])
-    achieved = b_upd * sweep_updates / (sweep_ms / 1000.0) / 1e9 if sweep_ms > 0 else None
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_achieved = b_upd * sweep_updates / sweep_s / 1e9 if sweep_s > 0 else None
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # Gop/s: SMs x FP32 lanes x max SM clock
+    alu_achieved = ALG_OPS_PER_UPDATE * sweep_updates / sweep_s / 1e9 if sweep_s > 0 else None
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "sweep_traffic.json")))
@@ -302,6 +300,7 @@ def run_mpr(args):
         e2e = {"value": updates_per_step * args.steps / wall, "unit": UNIT,
                "h2d_bytes_per_step": int(n * 4 + n * 1), "d2h_bytes_per_step": int(n * 4),
                "fill_time_ms": 1000 * wall / args.steps}
+    ck = clocks.stop() if clocks else None
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -313,15 +312,21 @@ def run_mpr(args):
                            "l2": "flushed between timed steps (256 MiB write, outside the events)"},
                 "fill_time_ms": total_ms / args.steps,
                 "gpu_launches": int(launches),
-                "roofline": {"bound": "hbm", "kernel": "k_sweep_half", "achieved": achieved, "peak": peak,
-                             "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+                "roofline": {"bound": "alu", "kernel": "k_sweep_half", "achieved": alu_achieved,
+                             "peak": alu_peak, "unit": "Gop/s",
+                             "frac": (alu_achieved / alu_peak) if alu_achieved else None,
                              "traffic": traffic,
-                             "algorithmic_bytes_per_update": b_upd,
+                             "algorithmic_ops_per_update": ALG_OPS_PER_UPDATE,
+                             "peak_derivation": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (max SM clock)",
                              "sweep_launches_timed": sweep_n, "sweep_ms_per_launch": sweep_ms / max(sweep_n, 1),
-                             "sweep_share_of_step": sweep_ms / max(total_ms * ws / ws, 1e-9),
-                             "frac_of_8TBps": (achieved / 8000.0) if achieved else None,
-                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
-                             else "fallback 6650 GB/s (B200_PROFILING.md)"},
+                             "sweep_share_of_step": sweep_ms / max(total_ms, 1e-9),
+                             "sweep_updates_per_s": sweep_updates / sweep_s if sweep_s > 0 else None,
+                             "hbm_view": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                                          "frac": (hbm_achieved / hbm_peak) if hbm_achieved else None,
+                                          "frac_of_8TBps": (hbm_achieved / 8000.0) if hbm_achieved else None,
+                                          "algorithmic_bytes_per_update": b_upd,
+                                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+                                          if "hbm_gbs" in peaks else "fallback 6650 GB/s (B200_PROFILING.md)"}},
                 "clocks": ck}
         if e2e:
             line["e2e"] = e2e

@@ -297,6 +297,17 @@ class LeMpr:
         """(device pointer, count) of the fp64 per-gap accumulator, for an external all-reduce."""
         return mpr_accumulator_device(self.ctx)
 
+    def accumulator_tensor(self):
+        """Zero-copy torch view (cuda, float64) of the per-gap accumulator owned by the
+        context, via __cuda_array_interface__ (valid until the next set_data/close)."""
+        import torch
+        ptr, n = mpr_accumulator_device(self.ctx)
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (max(n, 1),), "typestr": "<f8", "data": (ptr, False),
+                                        "version": 3, "stream": None}
+        return torch.as_tensor(_View(), device=torch.device("cuda", self.cfg.device))
+
     def predict_device(self, out_ptr):
         mpr_predict_device(self.ctx, out_ptr)
 

@@ -56,7 +56,7 @@ struct mpr_ctx {
   int stage = ST_INIT;
   std::string err;
   int sweep_grid = 0;
-  int sweep_variant = 0;  // kernel variant (MPR_SWEEP_VARIANT, tuning only)
+  int sweep_variant = 2;  // kernel variant (MPR_SWEEP_VARIANT, tuning only)
   // problem
   int64_t Lx = 0, Ly = 0, n = 0;
   int64_t P = 0, PA = 0, n_known = 0;
@@ -68,6 +68,7 @@ struct mpr_ctx {
   double sum_SB = 0;
   // simulation bookkeeping
   int64_t M_total = 0, sweeps = 0, batch = 0, last_m_base = 0, last_R = 0;
+  int64_t batch_key_P = -1, batch_key_R = -1, batch_cached = 0;
   int64_t launches = 0, total_launches = 0;
   int timing = 0;
   int64_t sweep_launches = 0;
@@ -214,6 +215,8 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
     int64_t mb = c->cfg.max_batch + (c->cfg.max_batch & 1);
     R = std::min(R, std::max<int64_t>(mb, 2));
   }
+  // cudaMemGetInfo is slow (driver round trip): reuse the last answer for the same shape
+  if (c->batch_key_P == c->P && c->batch_key_R == R && c->batch_cached > 0) return c->batch_cached;
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
   const double per_r = 4.0 * static_cast<double>(std::max<int64_t>(c->P, 1)) * (c->cfg.n_avg > 1 ? 2.0 : 1.0);
@@ -223,7 +226,10 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
   cap = std::min<int64_t>(cap, ((int64_t(1) << 31) - 1) / std::max<int64_t>(c->P, 1));
   cap -= cap & 1;
   if (cap < 2) cap = 2;
-  return std::min(R, cap);
+  c->batch_key_P = c->P;
+  c->batch_key_R = R;
+  c->batch_cached = std::min(R, cap);
+  return c->batch_cached;
 }
 
 }  // namespace

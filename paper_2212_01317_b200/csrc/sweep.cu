@@ -81,29 +81,106 @@ __device__ __forceinline__ bool all_present(uint32_t f) {
   return ((f | (f >> 1)) & 0x55u) == 0x55u;
 }
 
-template <bool QHALF, bool ENERGY, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_sweep_half(const SweepArgs a) {
+// One work item (gap site, realization pair) once its record and the states it reads
+// are in registers: Philox, two Metropolis updates, store, fused epilogues.
+template <bool QHALF, bool ENERGY>
+__device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& rec, float2 cur,
+                                             const float (&nv0)[4], const float (&nv1)[4],
+                                             uint32_t self_off, uint32_t pair, float& e0, float& e1) {
+  uint32_t sel = 0;
+  if (ENERGY) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
+      sel |= (a.is_b ? (ty != NB_NONE) : (ty == NB_KNOWN)) ? (1u << k) : 0u;
+    }
+  }
+  const Words4 w = philox4x32_10(rec.site, a.sweep, pair, 2u, a.k0, a.k1);
+  bool acc0, acc1;
+  float n0, n1;
+  if (all_present(rec.flags)) {
+    n0 = metropolis<QHALF, ENERGY, true>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
+    n1 = metropolis<QHALF, ENERGY, true>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
+  } else {
+    n0 = metropolis<QHALF, ENERGY, false>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
+    n1 = metropolis<QHALF, ENERGY, false>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
+  }
+  if (acc0 || acc1) *reinterpret_cast<float2*>(a.G + self_off) = make_float2(n0, n1);
+  if (a.accumulate) {
+    float2* ap = reinterpret_cast<float2*>(a.A + self_off);
+    float2 av = *ap;
+    av.x = __fadd_rn(av.x, n0);
+    av.y = __fadd_rn(av.y, n1);
+    *ap = av;
+  }
+}
+
+// a8: per-realization bond sums of this CTA -> global (fp64 atomics, one per realization).
+__device__ __forceinline__ void energy_epilogue(const SweepArgs& a, int npairs, bool active, int j, float e0,
+                                                float e1) {
+  __shared__ double es[2 * kMaxPairs];
+  for (int t = threadIdx.x; t < 2 * npairs; t += kThreads) es[t] = 0.0;
+  __syncthreads();
+  if (active && (e0 != 0.0f || e1 != 0.0f)) {
+    atomicAdd(&es[2 * j], static_cast<double>(e0));
+    atomicAdd(&es[2 * j + 1], static_cast<double>(e1));
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 2 * npairs; t += kThreads)
+    if (t >= a.r_valid_lo && t < a.r_valid_hi && es[t] != 0.0)
+      atomicAdd(a.energy + static_cast<int64_t>(t) * a.energy_stride, es[t]);
+}
+
+// Work split: thread tid owns realization pair j = tid % npairs and gap sites
+// g = tid / npairs + k * gstride; consecutive lanes -> consecutive (g, j) items.
+struct Split {
+  int j;
+  bool active;
+  uint32_t g0, gstride;
+};
+__device__ __forceinline__ Split split_work(int npairs) {
   const int tid = blockIdx.x * kThreads + threadIdx.x;
   const int total = gridDim.x * kThreads;
-  const int npairs = a.npairs;
   const int active = (total / npairs) * npairs;
-  const int j = tid % npairs;
-  const uint32_t gstride = static_cast<uint32_t>(active / npairs);
+  Split s;
+  s.j = tid % npairs;
+  s.active = tid < active;
+  s.g0 = static_cast<uint32_t>(tid / npairs);
+  s.gstride = static_cast<uint32_t>(active / npairs);
+  return s;
+}
+
+// Direct-load variant: record, own state and neighbour states loaded from global memory
+// at the start of each item (PF: register-free prefetch of the next item).
+template <bool QHALF, bool ENERGY, int MINB, int PF>
+__global__ void __launch_bounds__(kThreads, MINB) k_sweep_half(const SweepArgs a) {
+  const Split sp = split_work(a.npairs);
   // 32-bit element offsets: the host caps the batch so that P * R < 2^31
   const uint32_t R = static_cast<uint32_t>(a.R);
-  const uint32_t j2 = 2u * static_cast<uint32_t>(j);
+  const uint32_t j2 = 2u * static_cast<uint32_t>(sp.j);
   const uint32_t gcount = static_cast<uint32_t>(a.g_count);
   const uint32_t gbegin = static_cast<uint32_t>(a.g_begin);
   float e0 = 0.0f, e1 = 0.0f;
-  if (tid < active) {
-    const uint32_t pair = a.pair_base + static_cast<uint32_t>(j);
-    for (uint32_t g = static_cast<uint32_t>(tid / npairs); g < gcount; g += gstride) {
+  if (sp.active) {
+    const uint32_t pair = a.pair_base + static_cast<uint32_t>(sp.j);
+    for (uint32_t g = sp.g0; g < gcount; g += sp.gstride) {
       const uint32_t gg = gbegin + g;
       const GapRec rec = a.rec[gg];
       const uint32_t self_off = gg * R + j2;
       const float2 cur = *reinterpret_cast<const float2*>(a.G + self_off);
+      if (PF) {
+        const uint32_t gn = gg + sp.gstride;
+        if (gn < gbegin + gcount) {
+          if (PF == 1) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.rec + gn));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.G + (gn * R + j2)));
+          } else {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rec + gn));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.G + (gn * R + j2)));
+          }
+        }
+      }
       float nv0[4], nv1[4];
-      uint32_t sel = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
@@ -116,41 +193,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sweep_half(const SweepArgs a
           nv0[k] = f;
           nv1[k] = f;
         }
-        if (ENERGY) sel |= (a.is_b ? (ty != NB_NONE) : (ty == NB_KNOWN)) ? (1u << k) : 0u;
       }
-      const Words4 w = philox4x32_10(rec.site, a.sweep, pair, 2u, a.k0, a.k1);
-      bool acc0, acc1;
-      float n0, n1;
-      if (all_present(rec.flags)) {
-        n0 = metropolis<QHALF, ENERGY, true>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
-        n1 = metropolis<QHALF, ENERGY, true>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
-      } else {
-        n0 = metropolis<QHALF, ENERGY, false>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
-        n1 = metropolis<QHALF, ENERGY, false>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
-      }
-      if (acc0 || acc1) *reinterpret_cast<float2*>(a.G + self_off) = make_float2(n0, n1);
-      if (a.accumulate) {
-        float2* ap = reinterpret_cast<float2*>(a.A + self_off);
-        float2 av = *ap;
-        av.x = __fadd_rn(av.x, n0);
-        av.y = __fadd_rn(av.y, n1);
-        *ap = av;
-      }
+      process_item<QHALF, ENERGY>(a, rec, cur, nv0, nv1, self_off, pair, e0, e1);
     }
   }
-  if (ENERGY) {
-    __shared__ double es[2 * kMaxPairs];
-    for (int t = threadIdx.x; t < 2 * npairs; t += kThreads) es[t] = 0.0;
-    __syncthreads();
-    if (tid < active && (e0 != 0.0f || e1 != 0.0f)) {
-      atomicAdd(&es[2 * j], static_cast<double>(e0));
-      atomicAdd(&es[2 * j + 1], static_cast<double>(e1));
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < 2 * npairs; t += kThreads)
-      if (t >= a.r_valid_lo && t < a.r_valid_hi && es[t] != 0.0)
-        atomicAdd(a.energy + static_cast<int64_t>(t) * a.energy_stride, es[t]);
-  }
+  if (ENERGY) energy_epilogue(a, a.npairs, sp.active, sp.j, e0, e1);
 }
 
 // a6: initial states of a batch (ARITH §G).
@@ -196,12 +243,16 @@ __global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X,
 template <bool Q, bool E>
 static void* sweep_kernel_ptr(int variant) {
   switch (variant) {
-    case 1: return reinterpret_cast<void*>(k_sweep_half<Q, E, 5>);
-    case 2: return reinterpret_cast<void*>(k_sweep_half<Q, E, 6>);
-    case 3: return reinterpret_cast<void*>(k_sweep_half<Q, E, 8>);
-    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1>);
+    case 1: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 1>);
+    case 2: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2>);
+    case 3: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 1>);
+    case 4: return reinterpret_cast<void*>(k_sweep_half<Q, E, 2, 0>);
+
+    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 0>);
   }
 }
+
+static size_t sweep_smem(int) { return 0; }
 
 static void* sweep_kernel(bool qhalf, bool energy, int variant) {
   if (qhalf) return energy ? sweep_kernel_ptr<true, true>(variant) : sweep_kernel_ptr<true, false>(variant);
@@ -211,7 +262,8 @@ static void* sweep_kernel(bool qhalf, bool energy, int variant) {
 int sweep_grid_size(int device, int variant) {
   int sms = 0, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, variant), kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, variant), kThreads,
+                                                sweep_smem(variant));
   if (per < 1) per = 1;
   return sms * per;
 }
@@ -227,7 +279,7 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   const bool energy = (a.energy != nullptr);
   void* fn = sweep_kernel(qhalf, energy, variant);
   void* args[] = {const_cast<SweepArgs*>(&a)};
-  cudaLaunchKernel(fn, dim3(static_cast<unsigned>(g)), dim3(kThreads), args, 0, st);
+  cudaLaunchKernel(fn, dim3(static_cast<unsigned>(g)), dim3(kThreads), args, sweep_smem(variant), st);
 }
 
 void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,

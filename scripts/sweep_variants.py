@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--variants", default="0,1,2,3,4")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--M", type=int, default=None)
+    ap.add_argument("--max-batch", default="0", help="comma list of max_batch values to try")
     a = ap.parse_args()
     import paper_2212_01317_b200 as P
     c = CONFIGS[a.config]
@@ -26,9 +27,10 @@ def main():
     Pg = int((mask == 0).sum())
     calib = P.load_calibration()
     ref = None
-    for v in [int(x) for x in a.variants.split(",")]:
+    runs = [(int(v), int(b)) for v in a.variants.split(",") for b in a.max_batch.split(",")]
+    for v, mb in runs:
         os.environ["MPR_SWEEP_VARIANT"] = str(v)
-        m = P.LeMpr(P.Config(), calib)
+        m = P.LeMpr(P.Config(max_batch=mb), calib)
         m.set_data(z, mask)
         m.estimate_local_params()
         m.simulate(M, c["sweeps"], 1)  # warm-up
@@ -42,7 +44,10 @@ def main():
         same = bool(np.array_equal(pred.view(np.uint32), ref.view(np.uint32)))
         per = inf["sweep_ms"] / inf["sweep_launches"]
         ups = Pg * M / 2 / (per / 1e3)
-        print(json.dumps({"variant": v, "config": a.config, "M": M, "ms_per_halfsweep": per,
+        per = inf["sweep_ms"] / a.reps / (2 * c["sweeps"])  # per half-sweep of the whole M
+        ups = Pg * M / 2 / (per / 1e3)
+        print(json.dumps({"variant": v, "max_batch": mb, "batch": inf["batch"], "config": a.config, "M": M,
+                          "ms_per_halfsweep_allM": per,
                           "updates_per_s": ups, "bitwise_equal_to_first": same}), flush=True)
         m.close()
 

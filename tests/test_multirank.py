@@ -1,0 +1,95 @@
+"""Multi-rank (realization sharding) host logic on CPU: world_size-2 gloo process group.
+
+The product's sharding driver (paper_2212_01317_b200/sharding.py) is run with an
+oracle-backed engine injected by the test (the product never imports oracle/): each rank
+simulates its shard of global realization ids, the accumulators are all-reduced over
+gloo, and the predictions must equal the single-process fill up to fp64 reassociation.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2212_01317_b200.sharding import distributed_fill, shard_range
+
+
+@pytest.mark.parametrize("M,world", [(10, 2), (7, 2), (1, 2), (100, 8), (3, 4), (0, 3)])
+def test_shard_range_covers_exactly_once(M, world):
+    ranges = [shard_range(M, world, r) for r in range(world)]
+    ids = [m for a, b in ranges for m in range(a, b)]
+    assert ids == list(range(M))
+    for a, b in ranges:
+        assert a % 2 == 0  # pair-aligned starts (Philox pairs, ARITH §A)
+    sizes = [b - a for a, b in ranges]
+    assert max(sizes) - min(sizes) <= 2
+
+
+class OracleEngine:
+    """CPU stand-in with the Engine interface, backed by oracle/ (test-only)."""
+
+    def __init__(self, calib, cfg):
+        import oracle as O
+        self.O, self.calib, self.cfg = O, calib, cfg
+
+    def set_data(self, grid, mask):
+        self.z, self.mask = grid, mask
+
+    def estimate_local_params(self, want_T=False):
+        self.p = self.O.parameters(self.z, self.mask, self.cfg, *self.calib)
+
+    def reset_accumulator(self):
+        self.acc = torch.zeros(self.z.size, dtype=torch.float64)
+        self.M = 0
+
+    def simulate_range(self, M, sweeps, seed, m0, m1):
+        self.M = M
+        if m1 > m0:
+            r = self.O.simulate(self.p, self.mask, self.cfg, M, sweeps, seed, m_begin=m0, m_end=m1)
+            self.acc += torch.from_numpy(r["acc"].ravel())
+
+    def accumulator_tensor(self):
+        return self.acc
+
+    def predict(self):
+        acc = self.acc.numpy().reshape(self.z.shape)
+        return self.O.predict(np.nan_to_num(self.z), self.mask, acc, self.M, self.cfg.n_avg,
+                              self.p.zmin, self.p.zmax, 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle as O
+    from inputs.synth import make_problem
+    from tests.conftest import read_calibration
+    truth, z, mask = make_problem(24, 0.5, corr_len=5.0)
+    eng = OracleEngine(read_calibration(), O.OracleConfig(lb=8, rs=1, ns=2))
+    pred = distributed_fill(eng, z, mask, M=7, sweeps=6, seed=31)
+    out[rank] = pred
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_equals_single_process(calib):
+    import oracle as O
+    from inputs.synth import make_problem
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
+    truth, z, mask = make_problem(24, 0.5, corr_len=5.0)
+    ref = O.fill(z, mask, O.OracleConfig(lb=8, rs=1, ns=2), *calib, M=7, S=6, seed=31)["pred"]
+    for r in range(2):
+        assert np.max(np.abs(out[r] - ref)) <= 1e-6 * (np.nanmax(z) - np.nanmin(z))
+    assert np.array_equal(out[0], out[1])
