@@ -125,6 +125,31 @@ mpr_status mpr_simulate_range(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t 
  * pointer stays owned by ctx and valid until the next set_data/destroy. */
 mpr_status mpr_accumulator_device(mpr_ctx *ctx, double **acc_dev, int64_t *n);
 
+/* Row-slab decomposition (for grids split over GPUs by rows). Every
+ * rank holds the whole problem (set_data + estimate_local_params are deterministic and
+ * bit-exact, so each rank computes them itself) but updates only the gap sites of its
+ * rows [row_begin, row_end). After each half-sweep the caller exchanges halo rows:
+ * the colour-c states of the first and last own rows go to the neighbouring ranks,
+ * whose ghost rows (row_begin-1, row_end) are overwritten in place through
+ * mpr_slab_row_states. Because random numbers are keyed by global (site, sweep,
+ * realization), the chains are bit-identical to a single-GPU mpr_simulate.
+ *   mpr_slab_begin     : realizations [m_begin, m_end) (one batch, <= 1024), init of
+ *                        every gap (a pure function of the ids: ghosts need no exchange)
+ *   mpr_slab_half_sweep: sweep s (1-based), colour 0 = A ((r+c) even), 1 = B; own rows
+ *   mpr_slab_row_states: device view of the colour-c gap states of one row: *count
+ *                        floats, gap-site major, realization minor (send or receive in
+ *                        place); valid until slab_end
+ *   mpr_slab_end       : adds the own rows' realizations to the accumulator (others
+ *                        stay 0, so an all-reduce of the accumulators completes it)
+ * Not supported in slab mode: the energy trace (INVALID_ARG). Launches are stream
+ * ordered; mpr_sync waits for the context stream. */
+mpr_status mpr_slab_begin(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed, int64_t m_begin,
+                          int64_t m_end, int64_t row_begin, int64_t row_end);
+mpr_status mpr_slab_half_sweep(mpr_ctx *ctx, int32_t sweep, int colour);
+mpr_status mpr_slab_row_states(mpr_ctx *ctx, int64_t row, int colour, float **dev_ptr, int64_t *count);
+mpr_status mpr_slab_end(mpr_ctx *ctx);
+mpr_status mpr_sync(mpr_ctx *ctx);
+
 /* Predictions (ARITH §I): known sites return the input bitwise, gaps
  * z_min + (z_max - z_min) * mean_phi / 2pi. out: host, Lx*Ly floats, caller-owned. */
 mpr_status mpr_predict(mpr_ctx *ctx, float *out);

@@ -371,6 +371,23 @@ int64_t oracle_sweep(float *phi, const uint8_t *mask, const float *beta, int Lx,
     return acc;
 }
 
+/* One colour half of sweep `sweep` restricted to rows [r0, r1) (a row slab of the
+ * checkerboard update): the gap sites of that colour in those rows, in row-major
+ * order. Returns #accepted. */
+int64_t oracle_half_sweep_rows(float *phi, const uint8_t *mask, const float *beta, int Lx, int Ly,
+                               float q, float J, uint32_t sweep, int64_t m, uint64_t seed,
+                               int colour, int r0, int r1)
+{
+    int64_t acc = 0;
+    for (int r = r0; r < r1; ++r)
+        for (int c = 0; c < Lx; ++c) {
+            int64_t i = (int64_t)r * Lx + c;
+            if (((r + c) & 1) != colour || mask[i]) continue;
+            acc += update_site(phi, Lx, Ly, r, c, beta[i], q, J, sweep, m, seed);
+        }
+    return acc;
+}
+
 /* Sweeps s_begin..s_end-1 of realization m on a given beta field; adds phi after
  * every sweep to sum_phi (fp64, per site) and returns #accepted. Used by the
  * quadrature / brute-force pins of the Metropolis step. */

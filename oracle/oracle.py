@@ -88,6 +88,9 @@ def _declare(L):
     L.oracle_run_chain.argtypes = [_f32p, _u8p, _f32p, C.c_int, C.c_int, C.c_float, C.c_float, C.c_uint32,
                                    C.c_uint32, C.c_int64, C.c_uint64, C.c_void_p]
     L.oracle_run_chain.restype = C.c_int64
+    L.oracle_half_sweep_rows.argtypes = [_f32p, _u8p, _f32p, C.c_int, C.c_int, C.c_float, C.c_float, C.c_uint32,
+                                         C.c_int64, C.c_uint64, C.c_int, C.c_int, C.c_int]
+    L.oracle_half_sweep_rows.restype = C.c_int64
     L.oracle_parameters.argtypes = [_f32p, _u8p, C.c_int, C.c_int, C.POINTER(_Cfg), _f32p, _f32p,
                                     C.c_int, _f32p, _f32p, _f32p, C.POINTER(C.c_float),
                                     C.POINTER(C.c_float), _i64p, _i64p, C.c_void_p]
@@ -235,6 +238,15 @@ def run_chain(phi, mask, beta, s_begin, s_end, m=0, seed=1, q=0.5, J=1.0):
     n = lib().oracle_run_chain(phi.ravel(), mask.ravel(), beta.ravel(), phi.shape[1], phi.shape[0], float(q),
                                float(J), int(s_begin), int(s_end), int(m), int(seed), sp.ctypes.data)
     return sp, n
+
+
+def half_sweep_rows(phi, mask, beta, sweep, m, seed, colour, r0, r1, q=0.5, J=1.0) -> int:
+    """Colour half of one checkerboard sweep over rows [r0, r1) only (row slab), in place."""
+    assert phi.dtype == np.float32 and phi.flags.c_contiguous
+    mask = np.ascontiguousarray(mask, np.uint8); beta = np.ascontiguousarray(beta, np.float32)
+    return lib().oracle_half_sweep_rows(phi.ravel(), mask.ravel(), beta.ravel(), phi.shape[1], phi.shape[0],
+                                        float(q), float(J), int(sweep), int(m), int(seed), int(colour), int(r0),
+                                        int(r1))
 
 
 def unconditional_energy(L, T, q=0.5, init="ordered", n_eq=200, n_meas=200, seed=1, m=0,

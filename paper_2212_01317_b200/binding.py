@@ -27,7 +27,8 @@ MPR_INIT_BLOCK_MEAN, MPR_INIT_RANDOM = 0, 1
 EXPORTED = ["mpr_config_default", "mpr_init", "mpr_destroy", "mpr_last_error", "mpr_set_data",
             "mpr_set_data_device", "mpr_estimate_local_params", "mpr_simulate", "mpr_reset_accumulator",
             "mpr_simulate_range", "mpr_accumulator_device", "mpr_predict", "mpr_predict_device",
-            "mpr_get_info", "mpr_debug_get", "mpr_set_energy_trace", "mpr_set_kernel_timing", "mpr_version"]
+            "mpr_get_info", "mpr_debug_get", "mpr_set_energy_trace", "mpr_set_kernel_timing", "mpr_version",
+            "mpr_slab_begin", "mpr_slab_half_sweep", "mpr_slab_row_states", "mpr_slab_end", "mpr_sync"]
 
 
 class MprError(RuntimeError):
@@ -82,6 +83,12 @@ def load_library(path: str = LIB_PATH):
     L.mpr_debug_get.argtypes = [vp, C.c_int, i64, vp]; L.mpr_debug_get.restype = C.c_int
     L.mpr_set_energy_trace.argtypes = [vp, C.c_int]; L.mpr_set_energy_trace.restype = C.c_int
     L.mpr_set_kernel_timing.argtypes = [vp, C.c_int]; L.mpr_set_kernel_timing.restype = C.c_int
+    L.mpr_slab_begin.argtypes = [vp, i64, i32, u64, i64, i64, i64, i64]; L.mpr_slab_begin.restype = C.c_int
+    L.mpr_slab_half_sweep.argtypes = [vp, i32, C.c_int]; L.mpr_slab_half_sweep.restype = C.c_int
+    L.mpr_slab_row_states.argtypes = [vp, i64, C.c_int, C.POINTER(vp), C.POINTER(i64)]
+    L.mpr_slab_row_states.restype = C.c_int
+    L.mpr_slab_end.argtypes = [vp]; L.mpr_slab_end.restype = C.c_int
+    L.mpr_sync.argtypes = [vp]; L.mpr_sync.restype = C.c_int
     L.mpr_version.argtypes = []; L.mpr_version.restype = C.c_char_p
     _lib = L
     return L
@@ -179,6 +186,28 @@ def mpr_set_energy_trace(ctx, enable: bool) -> None:
 
 def mpr_set_kernel_timing(ctx, enable: bool) -> None:
     _check(ctx, load_library().mpr_set_kernel_timing(ctx, 1 if enable else 0))
+
+
+def mpr_slab_begin(ctx, M, sweeps, seed, m_begin, m_end, row_begin, row_end) -> None:
+    _check(ctx, load_library().mpr_slab_begin(ctx, M, sweeps, seed, m_begin, m_end, row_begin, row_end))
+
+
+def mpr_slab_half_sweep(ctx, sweep, colour) -> None:
+    _check(ctx, load_library().mpr_slab_half_sweep(ctx, sweep, colour))
+
+
+def mpr_slab_row_states(ctx, row, colour):
+    p, n = C.c_void_p(), C.c_int64()
+    _check(ctx, load_library().mpr_slab_row_states(ctx, row, colour, C.byref(p), C.byref(n)))
+    return p.value, n.value
+
+
+def mpr_slab_end(ctx) -> None:
+    _check(ctx, load_library().mpr_slab_end(ctx))
+
+
+def mpr_sync(ctx) -> None:
+    _check(ctx, load_library().mpr_sync(ctx))
 
 
 def mpr_version() -> str:
@@ -297,19 +326,47 @@ class LeMpr:
         """(device pointer, count) of the fp64 per-gap accumulator, for an external all-reduce."""
         return mpr_accumulator_device(self.ctx)
 
-    def accumulator_tensor(self):
-        """Zero-copy torch view (cuda, float64) of the per-gap accumulator owned by the
-        context, via __cuda_array_interface__ (valid until the next set_data/close)."""
+    def _device_view(self, ptr, n, typestr):
         import torch
-        ptr, n = mpr_accumulator_device(self.ctx)
 
         class _View:
-            __cuda_array_interface__ = {"shape": (max(n, 1),), "typestr": "<f8", "data": (ptr, False),
+            __cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
                                         "version": 3, "stream": None}
         return torch.as_tensor(_View(), device=torch.device("cuda", self.cfg.device))
 
+    def accumulator_tensor(self):
+        """Zero-copy torch view (cuda, float64) of the per-gap accumulator owned by the
+        context, via __cuda_array_interface__ (valid until the next set_data/close)."""
+        ptr, n = mpr_accumulator_device(self.ctx)
+        return self._device_view(ptr, max(n, 1), "<f8")
+
     def predict_device(self, out_ptr):
         mpr_predict_device(self.ctx, out_ptr)
+
+    # ---- row-slab mode (include/mpr.h mpr_slab_*) ----
+    def slab_begin(self, M, sweeps, seed, m_begin, m_end, row_begin, row_end):
+        mpr_slab_begin(self.ctx, M, sweeps, seed, m_begin, m_end, row_begin, row_end)
+
+    def slab_half_sweep(self, sweep, colour):
+        mpr_slab_half_sweep(self.ctx, sweep, colour)
+
+    def row_view(self, row, colour):
+        """Zero-copy (cuda, float32) view of the colour-`colour` gap states of `row`; the
+        halo exchange sends from / receives into it in place."""
+        ptr, n = mpr_slab_row_states(self.ctx, row, colour)
+        if n == 0:
+            import torch
+            return torch.empty(0, dtype=torch.float32, device=torch.device("cuda", self.cfg.device))
+        return self._device_view(ptr, n, "<f4")
+
+    def commit_row(self, row, colour, tensor):
+        """Received halo rows land in place (row_view is zero-copy): nothing to do."""
+
+    def slab_end(self):
+        mpr_slab_end(self.ctx)
+
+    def sync(self):
+        mpr_sync(self.ctx)
 
 
 def fill(grid, mask, M=100, sweeps=30, seed=20221202, cfg: Config | None = None, calib=None):

@@ -56,7 +56,7 @@ struct mpr_ctx {
   int stage = ST_INIT;
   std::string err;
   int sweep_grid = 0;
-  int sweep_variant = 2;  // kernel variant (MPR_SWEEP_VARIANT, tuning only)
+  int sweep_variant = 5;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
   // problem
   int64_t Lx = 0, Ly = 0, n = 0;
   int64_t P = 0, PA = 0, n_known = 0;
@@ -76,6 +76,12 @@ struct mpr_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int energy_enabled = 0;
   int64_t energy_M = 0, energy_S = 0;
+  // row-slab mode (mpr_slab_*)
+  int slab_active = 0;
+  int64_t slab_row0 = 0, slab_row1 = 0, slab_m0 = 0, slab_m1 = 0, slab_mb = 0;
+  int slab_R = 0, slab_S = 0;
+  uint32_t slab_k0 = 0, slab_k1 = 0;
+  std::vector<int> rowoff_h;  // host copy of the gap-id row offsets (2*Ly)
   // device memory
   DBuf z, mask, phiK, scal, calTd, caled, rowcnt, rowoff, gid, rec, bstats, Tb, T, T2, G, A, acc,
       energy, out, tmp;
@@ -516,7 +522,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
       c->sweep_ms += ms;
       c->sweep_launches += nsweep_launch;
     }
-    launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), c->P, Rb, r_lo, r_hi, c->acc.as<double>(), st);
+    launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), 0, c->P, Rb, r_lo, r_hi, c->acc.as<double>(), st);
     CKL("acc_reduce");
     ++c->launches;
     c->last_m_base = mb;
@@ -531,6 +537,135 @@ mpr_status mpr_simulate(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed) {
   mpr_status s = mpr_reset_accumulator(c);
   if (s != MPR_OK) return s;
   return mpr_simulate_range(c, M, sweeps, seed, 0, M);
+}
+
+// ---- row-slab decomposition ------------------------------------
+namespace {
+// First gap id of colour `col` in row r (r == Ly: end of the colour range).
+int64_t gap_row_offset(const mpr_ctx* c, int col, int64_t r) {
+  if (r >= c->Ly) return col == 0 ? c->PA : c->P;
+  return c->rowoff_h[static_cast<size_t>(col * c->Ly + r)];
+}
+}  // namespace
+
+mpr_status mpr_slab_begin(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed, int64_t m_begin, int64_t m_end,
+                          int64_t row_begin, int64_t row_end) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "slab_begin before estimate_local_params");
+  if (M < 1 || sweeps < 1 || c->cfg.n_avg > sweeps) return fail(c, MPR_ERR_INVALID_ARG, "bad M / sweeps / n_avg");
+  if (m_begin < 0 || m_end > M || m_begin >= m_end) return fail(c, MPR_ERR_INVALID_ARG, "bad realization range");
+  if (row_begin < 0 || row_end > c->Ly || row_begin >= row_end) return fail(c, MPR_ERR_INVALID_ARG, "bad row range");
+  if (c->energy_enabled) return fail(c, MPR_ERR_INVALID_ARG, "energy trace is not supported in slab mode");
+  if (!c->acc.p) {
+    mpr_status s = mpr_reset_accumulator(c);
+    if (s != MPR_OK) return s;
+  }
+  CK(cudaSetDevice(c->device), "set device");
+  cudaStream_t st = c->stream;
+  c->rowoff_h.resize(static_cast<size_t>(2 * c->Ly));
+  CK(cudaMemcpyAsync(c->rowoff_h.data(), c->rowoff.p, sizeof(int) * 2 * c->Ly, cudaMemcpyDeviceToHost, st),
+     "D2H row offsets");
+  CK(cudaStreamSynchronize(st), "slab sync");
+  const int64_t mb = m_begin & ~int64_t(1);
+  const int64_t span = m_end - mb;
+  const int Rb = static_cast<int>(span + (span & 1));
+  if (Rb > 1024 || static_cast<int64_t>(Rb) * std::max<int64_t>(c->P, 1) >= (int64_t(1) << 31))
+    return fail(c, MPR_ERR_INVALID_ARG, "slab mode runs its realizations as one batch: range too large");
+  const bool avg = c->cfg.n_avg > 1;
+  CK(c->G.ensure(sizeof(float) * std::max<int64_t>(c->P, 1) * Rb), "alloc state");
+  if (avg) CK(c->A.ensure(sizeof(float) * std::max<int64_t>(c->P, 1) * Rb), "alloc accumulator state");
+  c->M_total = M;
+  c->sweeps = sweeps;
+  c->slab_active = 1;
+  c->slab_row0 = row_begin;
+  c->slab_row1 = row_end;
+  c->slab_m0 = m_begin;
+  c->slab_m1 = m_end;
+  c->slab_mb = mb;
+  c->slab_R = Rb;
+  c->slab_S = sweeps;
+  c->slab_k0 = static_cast<uint32_t>(seed & 0xffffffffu);
+  c->slab_k1 = static_cast<uint32_t>(seed >> 32);
+  c->batch = Rb;
+  c->last_m_base = mb;
+  c->last_R = Rb;
+  if (c->degenerate || c->P == 0) return MPR_OK;
+  // every gap (own rows and ghost rows alike) gets its initial state: the init is a pure
+  // function of the global ids, so ghost rows need no exchange before the first sweep
+  launch_init_states(c->rec.as<GapRec>(), c->G.as<float>(), avg ? c->A.as<float>() : nullptr, c->P, Rb, Rb / 2,
+                     static_cast<uint32_t>(mb / 2), c->cfg.init == MPR_INIT_RANDOM, c->slab_k0, c->slab_k1, st);
+  CKL("init_states");
+  return MPR_OK;
+}
+
+mpr_status mpr_slab_half_sweep(mpr_ctx* c, int32_t sweep, int colour) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_half_sweep outside slab_begin/slab_end");
+  if (sweep < 1 || sweep > c->slab_S || (colour != 0 && colour != 1))
+    return fail(c, MPR_ERR_INVALID_ARG, "bad sweep or colour");
+  if (c->degenerate || c->P == 0) return MPR_OK;
+  CK(cudaSetDevice(c->device), "set device");
+  const int64_t g0 = gap_row_offset(c, colour, c->slab_row0);
+  const int64_t g1 = gap_row_offset(c, colour, c->slab_row1);
+  if (g1 <= g0) return MPR_OK;
+  const bool avg = c->cfg.n_avg > 1;
+  SweepArgs a{};
+  a.rec = c->rec.as<GapRec>();
+  a.G = c->G.as<float>();
+  a.A = avg ? c->A.as<float>() : nullptr;
+  a.g_begin = g0;
+  a.g_count = g1 - g0;
+  a.R = c->slab_R;
+  a.npairs = c->slab_R / 2;
+  a.pair_base = static_cast<uint32_t>(c->slab_mb / 2);
+  a.sweep = static_cast<uint32_t>(sweep);
+  a.k0 = c->slab_k0;
+  a.k1 = c->slab_k1;
+  a.q = c->cfg.q;
+  a.J = c->cfg.J;
+  a.is_b = colour;
+  a.accumulate = avg && (sweep > c->slab_S - c->cfg.n_avg);
+  a.energy = nullptr;
+  launch_sweep_half(a, c->sweep_grid, c->sweep_variant, c->stream);
+  CKL("sweep_half");
+  return MPR_OK;
+}
+
+mpr_status mpr_slab_row_states(mpr_ctx* c, int64_t row, int colour, float** dev_ptr, int64_t* count) {
+  if (!c || !dev_ptr || !count) return MPR_ERR_INVALID_ARG;
+  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_row_states outside slab_begin/slab_end");
+  if (row < 0 || row >= c->Ly || (colour != 0 && colour != 1)) return fail(c, MPR_ERR_INVALID_ARG, "bad row/colour");
+  const int64_t g0 = gap_row_offset(c, colour, row), g1 = gap_row_offset(c, colour, row + 1);
+  *dev_ptr = c->G.as<float>() + g0 * c->slab_R;
+  *count = (g1 - g0) * c->slab_R;
+  return MPR_OK;
+}
+
+mpr_status mpr_slab_end(mpr_ctx* c) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_end without slab_begin");
+  CK(cudaSetDevice(c->device), "set device");
+  c->slab_active = 0;
+  if (!(c->degenerate || c->P == 0)) {
+    const bool avg = c->cfg.n_avg > 1;
+    const int r_lo = static_cast<int>(c->slab_m0 - c->slab_mb), r_hi = static_cast<int>(c->slab_m1 - c->slab_mb);
+    for (int col = 0; col < 2; ++col) {
+      const int64_t g0 = gap_row_offset(c, col, c->slab_row0), g1 = gap_row_offset(c, col, c->slab_row1);
+      launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), g0, g1 - g0, c->slab_R, r_lo, r_hi,
+                        c->acc.as<double>(), c->stream);
+      CKL("acc_reduce");
+    }
+  }
+  CK(cudaStreamSynchronize(c->stream), "slab_end sync");
+  c->stage = ST_SIM;
+  return MPR_OK;
+}
+
+mpr_status mpr_sync(mpr_ctx* c) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  CK(cudaSetDevice(c->device), "set device");
+  CK(cudaStreamSynchronize(c->stream), "sync");
+  return MPR_OK;
 }
 
 mpr_status mpr_accumulator_device(mpr_ctx* c, double** acc_dev, int64_t* n) {

@@ -98,7 +98,7 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
 void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,
                         uint32_t pair_base, int random_init, uint32_t k0, uint32_t k1,
                         cudaStream_t st);
-void launch_acc_reduce(const float* X, int64_t P, int R, int r_lo, int r_hi, double* acc,
-                       cudaStream_t st);
+void launch_acc_reduce(const float* X, int64_t g_begin, int64_t g_count, int R, int r_lo, int r_hi,
+                       double* acc, cudaStream_t st);
 
 }  // namespace mpr

@@ -27,7 +27,6 @@ namespace mpr {
 
 namespace {
 
-constexpr int kThreads = 256;
 constexpr int kMaxPairs = 512;  // batch <= 1024 realizations
 
 template <bool QHALF>
@@ -40,7 +39,7 @@ __device__ __forceinline__ float cosq(float d, float q) {
 // the sums need no masking and start from the first term (+0 + c == c exactly, since
 // cos_spec never returns -0). Returns the new angle; `sel` selects the bonds whose
 // chosen-branch cos is added to *e_sel (energy epilogue).
-template <bool QHALF, bool ENERGY, bool FULL>
+template <bool QHALF, bool ENERGY, bool FULL, bool BFEXP>
 __device__ __forceinline__ float metropolis(float cur, const float (&nbv)[4], uint32_t flags,
                                             uint32_t sel, float beta, float q, float J,
                                             uint32_t wa, uint32_t wb, bool& accepted,
@@ -71,7 +70,12 @@ __device__ __forceinline__ float metropolis(float cur, const float (&nbv)[4], ui
   }
   const float dE = __fmul_rn(J, __fsub_rn(s_cur, s_new));
   const float x = -__fmul_rn(dE, beta);
-  accepted = (dE <= 0.0f) || (u24(wb) < exp_spec_fast(x));
+  if (BFEXP) {  // branch-free: exp evaluated by every lane (no divergence around it)
+    const float e = exp_spec_fast(x);
+    accepted = (dE <= 0.0f) | (u24(wb) < e);
+  } else {
+    accepted = (dE <= 0.0f) || (u24(wb) < exp_spec_fast(x));
+  }
   if (ENERGY) e_sel += accepted ? en : ec;
   return accepted ? prop : cur;
 }
@@ -83,7 +87,7 @@ __device__ __forceinline__ bool all_present(uint32_t f) {
 
 // One work item (gap site, realization pair) once its record and the states it reads
 // are in registers: Philox, two Metropolis updates, store, fused epilogues.
-template <bool QHALF, bool ENERGY>
+template <bool QHALF, bool ENERGY, bool BFEXP>
 __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& rec, float2 cur,
                                              const float (&nv0)[4], const float (&nv1)[4],
                                              uint32_t self_off, uint32_t pair, float& e0, float& e1) {
@@ -99,11 +103,11 @@ __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& r
   bool acc0, acc1;
   float n0, n1;
   if (all_present(rec.flags)) {
-    n0 = metropolis<QHALF, ENERGY, true>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
-    n1 = metropolis<QHALF, ENERGY, true>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
+    n0 = metropolis<QHALF, ENERGY, true, BFEXP>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
+    n1 = metropolis<QHALF, ENERGY, true, BFEXP>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
   } else {
-    n0 = metropolis<QHALF, ENERGY, false>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
-    n1 = metropolis<QHALF, ENERGY, false>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
+    n0 = metropolis<QHALF, ENERGY, false, BFEXP>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
+    n1 = metropolis<QHALF, ENERGY, false, BFEXP>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
   }
   if (acc0 || acc1) *reinterpret_cast<float2*>(a.G + self_off) = make_float2(n0, n1);
   if (a.accumulate) {
@@ -119,14 +123,14 @@ __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& r
 __device__ __forceinline__ void energy_epilogue(const SweepArgs& a, int npairs, bool active, int j, float e0,
                                                 float e1) {
   __shared__ double es[2 * kMaxPairs];
-  for (int t = threadIdx.x; t < 2 * npairs; t += kThreads) es[t] = 0.0;
+  for (int t = threadIdx.x; t < 2 * npairs; t += blockDim.x) es[t] = 0.0;
   __syncthreads();
   if (active && (e0 != 0.0f || e1 != 0.0f)) {
     atomicAdd(&es[2 * j], static_cast<double>(e0));
     atomicAdd(&es[2 * j + 1], static_cast<double>(e1));
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < 2 * npairs; t += kThreads)
+  for (int t = threadIdx.x; t < 2 * npairs; t += blockDim.x)
     if (t >= a.r_valid_lo && t < a.r_valid_hi && es[t] != 0.0)
       atomicAdd(a.energy + static_cast<int64_t>(t) * a.energy_stride, es[t]);
 }
@@ -139,8 +143,8 @@ struct Split {
   uint32_t g0, gstride;
 };
 __device__ __forceinline__ Split split_work(int npairs) {
-  const int tid = blockIdx.x * kThreads + threadIdx.x;
-  const int total = gridDim.x * kThreads;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int total = gridDim.x * blockDim.x;
   const int active = (total / npairs) * npairs;
   Split s;
   s.j = tid % npairs;
@@ -152,8 +156,8 @@ __device__ __forceinline__ Split split_work(int npairs) {
 
 // Direct-load variant: record, own state and neighbour states loaded from global memory
 // at the start of each item (PF: register-free prefetch of the next item).
-template <bool QHALF, bool ENERGY, int MINB, int PF>
-__global__ void __launch_bounds__(kThreads, MINB) k_sweep_half(const SweepArgs a) {
+template <bool QHALF, bool ENERGY, int MINB, int PF, int NT, bool BFEXP>
+__global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   const Split sp = split_work(a.npairs);
   // 32-bit element offsets: the host caps the batch so that P * R < 2^31
   const uint32_t R = static_cast<uint32_t>(a.R);
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_sweep_half(const SweepArgs a
           nv1[k] = f;
         }
       }
-      process_item<QHALF, ENERGY>(a, rec, cur, nv0, nv1, self_off, pair, e0, e1);
+      process_item<QHALF, ENERGY, BFEXP>(a, rec, cur, nv0, nv1, self_off, pair, e0, e1);
     }
   }
   if (ENERGY) energy_epilogue(a, a.npairs, sp.active, sp.j, e0, e1);
@@ -226,9 +230,10 @@ __global__ void __launch_bounds__(256) k_init_states(const GapRec* __restrict__ 
 
 // a9 (realization sum): acc[g] += sum_{r in [r_lo, r_hi)} X[g][r], fp64, r ascending —
 // the same summation order as the oracle (ARITH §I).
-__global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X, int64_t P, int R,
-                                                    int r_lo, int r_hi, double* __restrict__ acc) {
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < P;
+__global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X, int64_t g_begin,
+                                                    int64_t g_end, int R, int r_lo, int r_hi,
+                                                    double* __restrict__ acc) {
+  for (int64_t g = g_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < g_end;
        g += (int64_t)gridDim.x * blockDim.x) {
     double s = acc[g];
     const float* x = X + g * R;
@@ -243,14 +248,18 @@ __global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X,
 template <bool Q, bool E>
 static void* sweep_kernel_ptr(int variant) {
   switch (variant) {
-    case 1: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 1>);
-    case 2: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2>);
-    case 3: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 1>);
-    case 4: return reinterpret_cast<void*>(k_sweep_half<Q, E, 2, 0>);
-
-    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 0>);
+    case 0: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 0, 256, false>);
+    case 1: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 1, 256, false>);
+    case 3: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 1, 256, false>);
+    case 4: return reinterpret_cast<void*>(k_sweep_half<Q, E, 2, 0, 256, false>);
+    case 2: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, false>);
+    case 6: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 128, false>);
+    case 7: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 128, true>);
+    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true>);  // 5
   }
 }
+
+static int sweep_threads(int variant) { return (variant == 6 || variant == 7) ? 128 : 256; }
 
 static size_t sweep_smem(int) { return 0; }
 
@@ -262,24 +271,25 @@ static void* sweep_kernel(bool qhalf, bool energy, int variant) {
 int sweep_grid_size(int device, int variant) {
   int sms = 0, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, variant), kThreads,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, variant), sweep_threads(variant),
                                                 sweep_smem(variant));
   if (per < 1) per = 1;
   return sms * per;
 }
 
 void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st) {
+  const int nt = sweep_threads(variant);
   const int64_t items = a.g_count * a.npairs;
-  int64_t g = (items + kThreads - 1) / kThreads;
+  int64_t g = (items + nt - 1) / nt;
   if (g > grid) g = grid;
-  const int64_t need = (a.npairs + kThreads - 1) / kThreads;  // active threads >= npairs
+  const int64_t need = (a.npairs + nt - 1) / nt;  // active threads >= npairs
   if (g < need) g = need;
   if (g < 1) g = 1;
   const bool qhalf = (a.q == 0.5f);
   const bool energy = (a.energy != nullptr);
   void* fn = sweep_kernel(qhalf, energy, variant);
   void* args[] = {const_cast<SweepArgs*>(&a)};
-  cudaLaunchKernel(fn, dim3(static_cast<unsigned>(g)), dim3(kThreads), args, sweep_smem(variant), st);
+  cudaLaunchKernel(fn, dim3(static_cast<unsigned>(g)), dim3(nt), args, sweep_smem(variant), st);
 }
 
 void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,
@@ -293,12 +303,13 @@ void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R,
                                                           random_init, k0, k1);
 }
 
-void launch_acc_reduce(const float* X, int64_t P, int R, int r_lo, int r_hi, double* acc,
-                       cudaStream_t st) {
-  int64_t g = (P + 255) / 256;
+void launch_acc_reduce(const float* X, int64_t g_begin, int64_t g_count, int R, int r_lo, int r_hi,
+                       double* acc, cudaStream_t st) {
+  if (g_count <= 0) return;
+  int64_t g = (g_count + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
   if (g < 1) g = 1;
-  k_acc_reduce<<<static_cast<unsigned>(g), 256, 0, st>>>(X, P, R, r_lo, r_hi, acc);
+  k_acc_reduce<<<static_cast<unsigned>(g), 256, 0, st>>>(X, g_begin, g_begin + g_count, R, r_lo, r_hi, acc);
 }
 
 }  // namespace mpr

@@ -47,6 +47,62 @@ def allreduce_accumulator(acc: torch.Tensor, group=None) -> None:
         dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
 
 
+def row_range(Ly: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous rows [r0, r1) of a row slab; sizes differ by at most one row."""
+    if Ly < world or world < 1 or not 0 <= rank < world:
+        raise ValueError("need at least one row per rank")
+    return rank * Ly // world, (rank + 1) * Ly // world
+
+
+def exchange_halo(engine, colour: int, r0: int, r1: int, rank: int, world: int, group=None) -> None:
+    """After the colour-`colour` half-sweep: send the colour's gap states of the first and
+    last own rows to the neighbouring slabs, receive theirs into the ghost rows (one row
+    per side). Row sizes are global facts, so both ends agree on them."""
+    ops, recvs = [], []
+    peer = lambda r: r if group is None else dist.get_global_rank(group, r)  # noqa: E731
+    if rank > 0:
+        snd, rcv = engine.row_view(r0, colour), engine.row_view(r0 - 1, colour)
+        if snd.numel():
+            ops.append(dist.P2POp(dist.isend, snd, peer(rank - 1), group))
+        if rcv.numel():
+            ops.append(dist.P2POp(dist.irecv, rcv, peer(rank - 1), group))
+            recvs.append((r0 - 1, rcv))
+    if rank < world - 1:
+        snd, rcv = engine.row_view(r1 - 1, colour), engine.row_view(r1, colour)
+        if snd.numel():
+            ops.append(dist.P2POp(dist.isend, snd, peer(rank + 1), group))
+        if rcv.numel():
+            ops.append(dist.P2POp(dist.irecv, rcv, peer(rank + 1), group))
+            recvs.append((r1, rcv))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for row, t in recvs:
+        engine.commit_row(row, colour, t)
+
+
+def distributed_fill_slabs(engine, grid, mask, M: int, sweeps: int, seed: int, group=None):
+    """SPMD gap fill with the grid split into row slabs (one per rank) and a one-row halo
+    exchange per colour half-sweep; every rank runs all M realizations on its rows. The
+    chains are bit-identical to the single-GPU run (global Philox counters)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    Ly = grid.shape[0]
+    r0, r1 = row_range(Ly, world, rank)
+    engine.set_data(grid, mask)
+    engine.estimate_local_params()
+    engine.reset_accumulator()
+    engine.slab_begin(M, sweeps, seed, 0, M, r0, r1)
+    for s in range(1, sweeps + 1):
+        for colour in (0, 1):
+            engine.slab_half_sweep(s, colour)
+            if world > 1:
+                exchange_halo(engine, colour, r0, r1, rank, world, group)
+    engine.slab_end()
+    allreduce_accumulator(engine.accumulator_tensor(), group)
+    return engine.predict()
+
+
 def distributed_fill(engine: Engine, grid, mask, M: int, sweeps: int, seed: int, group=None):
     """SPMD gap fill: every rank calls this with the same arguments; returns the
     predictions (identical on every rank)."""

@@ -206,3 +206,47 @@ def test_c2_full_size_sampled(P, calib):
     assert_bitwise(pred[~gaps], z[~gaps], "samples")
     assert pred[gaps].min() >= p.zmin and pred[gaps].max() <= p.zmax
     m.close()
+
+
+def _emulated_slabs(P, z, mask, cfg, calib, M, S, seed, world):
+    """Row slabs of `world` contexts on one GPU; halo rows exchanged by device copies through
+    the same zero-copy row views the NCCL path sends from and receives into."""
+    import torch
+    from paper_2212_01317_b200.sharding import row_range
+    Ly = z.shape[0]
+    engs = [P.LeMpr(cfg, calib) for _ in range(world)]
+    ranges = [row_range(Ly, world, w) for w in range(world)]
+    for e, (r0, r1) in zip(engs, ranges):
+        e.set_data(z, mask); e.estimate_local_params(); e.reset_accumulator()
+        e.slab_begin(M, S, seed, 0, M, r0, r1)
+    for s in range(1, S + 1):
+        for colour in (0, 1):
+            for e in engs:
+                e.slab_half_sweep(s, colour)
+            for e in engs:
+                e.sync()
+            for w in range(world - 1):  # boundary between slab w and w+1
+                r = ranges[w][1]
+                engs[w + 1].row_view(r - 1, colour).copy_(engs[w].row_view(r - 1, colour))  # w's last row
+                engs[w].row_view(r, colour).copy_(engs[w + 1].row_view(r, colour))          # w+1's first row
+            torch.cuda.synchronize()
+    for e in engs:
+        e.slab_end()
+    total = sum(e.accumulator_tensor().clone() for e in engs)
+    engs[0].accumulator_tensor().copy_(total)
+    torch.cuda.synchronize()
+    pred = engs[0].predict()
+    for e in engs:
+        e.close()
+    return pred
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_slabs_emulated_bit_exact(P, calib, world):
+    """Row-slab mode: slabs with one-row halo exchanges reproduce the
+    single-context predictions bit for bit (and therefore the oracle's)."""
+    truth, z, mask = make_problem(61, 0.5, Lx=52, corr_len=6.0)
+    cfg = P.Config(l_b=8, n_s=2, r_s=1)
+    ref = gpu_run(P, z, mask, cfg, calib, 6, 10, 123)["pred"]
+    got = _emulated_slabs(P, z, mask, cfg, calib, 6, 10, 123, world)
+    assert_bitwise(got, ref, f"row slabs x{world}")

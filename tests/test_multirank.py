@@ -93,3 +93,77 @@ def test_gloo_world2_equals_single_process(calib):
     for r in range(2):
         assert np.max(np.abs(out[r] - ref)) <= 1e-6 * (np.nanmax(z) - np.nanmin(z))
     assert np.array_equal(out[0], out[1])
+
+
+# ------------------------------------------------------------------ row slabs
+class OracleSlabEngine(OracleEngine):
+    """Row-slab interface on top of the oracle: dense per-realization states, own rows
+    updated by oracle.half_sweep_rows, halo rows exchanged through row_view/commit_row."""
+
+    def slab_begin(self, M, sweeps, seed, m0, m1, r0, r1):
+        self.M, self.S, self.seed, self.m0, self.m1, self.r0, self.r1 = M, sweeps, seed, m0, m1, r0, r1
+        self.phi = np.stack([self.O.init_angles(self.p.phi0, self.mask, self.cfg.lb, self.p.SP, self.p.NK,
+                                                0 if self.cfg.init == "block_mean" else 1, m, seed)
+                             for m in range(m0, m1)])
+
+    def slab_half_sweep(self, s, colour):
+        for k, m in enumerate(range(self.m0, self.m1)):
+            ph = np.ascontiguousarray(self.phi[k])
+            self.O.half_sweep_rows(ph, self.mask, self.p.beta, s, m, self.seed, colour, self.r0, self.r1,
+                                   q=self.cfg.q, J=self.cfg.J)
+            self.phi[k] = ph
+
+    def _cols(self, row, colour):
+        Lx = self.mask.shape[1]
+        return [c for c in range(Lx) if ((row + c) & 1) == colour and not self.mask[row, c]]
+
+    def row_view(self, row, colour):
+        cols = self._cols(row, colour)
+        return torch.from_numpy(np.ascontiguousarray(self.phi[:, row, cols].T.ravel()))
+
+    def commit_row(self, row, colour, t):
+        cols = self._cols(row, colour)
+        self.phi[:, row, cols] = t.numpy().reshape(len(cols), -1).T
+
+    def slab_end(self):
+        rows = slice(self.r0, self.r1)
+        gaps = np.zeros(self.mask.shape, bool)
+        gaps[rows] = self.mask[rows] == 0
+        acc = np.zeros(self.mask.shape)
+        for k in range(self.phi.shape[0]):  # realization order, as the oracle accumulates
+            acc[gaps] += self.phi[k][gaps].astype(np.float64)
+        self.acc += torch.from_numpy(acc.ravel())
+
+
+def _slab_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle as O
+    from inputs.synth import make_problem
+    from paper_2212_01317_b200.sharding import distributed_fill_slabs
+    from tests.conftest import read_calibration
+    truth, z, mask = make_problem(21, 0.6, Lx=18, corr_len=5.0)
+    eng = OracleSlabEngine(read_calibration(), O.OracleConfig(lb=8, rs=1, ns=2))
+    out[rank] = distributed_fill_slabs(eng, z, mask, M=3, sweeps=5, seed=41)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_row_slabs_bit_exact(calib, world):
+    """Row-slab decomposition with one-row halos per colour half-sweep reproduces the
+    single-process chains bit for bit (global Philox counters)."""
+    import oracle as O
+    from inputs.synth import make_problem
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_slab_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    truth, z, mask = make_problem(21, 0.6, Lx=18, corr_len=5.0)
+    ref = O.fill(z, mask, O.OracleConfig(lb=8, rs=1, ns=2), *calib, M=3, S=5, seed=41)["pred"]
+    for r in range(world):
+        assert np.array_equal(out[r].view(np.uint32), ref.view(np.uint32))
+
+
+def test_row_range():
+    from paper_2212_01317_b200.sharding import row_range
+    rr = [row_range(10, 3, r) for r in range(3)]
+    assert rr == [(0, 3), (3, 6), (6, 10)]
