@@ -339,17 +339,67 @@ float oracle_delta_energy(const float *phi, int Lx, int Ly, int r, int c, float 
 /* One Metropolis update of gap site (r,c) with the uniform independence proposal
  * phi' ~ U[0, 2pi) (reading R1) and acceptance min(1, exp(-dE/T)), T = 1/beta
  * (P:85); returns 1 if accepted. */
-static int update_site(float *phi, int Lx, int Ly, int r, int c, float beta, float q, float J,
-                       uint32_t sweep, int64_t m, uint64_t seed)
+static int update_site_ctr(float *phi, int Lx, int Ly, int r, int c, uint32_t ctr_site, float beta,
+                           float q, float J, uint32_t sweep, int64_t m, uint64_t seed)
 {
     int64_t i = (int64_t)r * Lx + c;
     uint32_t wa, wb;
-    sweep_words((uint32_t)i, sweep, m, seed, &wa, &wb);
+    sweep_words(ctr_site, sweep, m, seed, &wa, &wb);
     float prop = oracle_uniform(wa) * TWO_PI_F;
     float dE = oracle_delta_energy(phi, Lx, Ly, r, c, prop, q, J);
     int accept = (dE <= 0.0f) || (oracle_uniform(wb) < oracle_exp_spec(-(dE * beta)));
     if (accept) phi[i] = prop;
     return accept;
+}
+
+static int update_site(float *phi, int Lx, int Ly, int r, int c, float beta, float q, float J,
+                       uint32_t sweep, int64_t m, uint64_t seed)
+{
+    return update_site_ctr(phi, Lx, Ly, r, c, (uint32_t)((int64_t)r * Lx + c), beta, q, J, sweep, m, seed);
+}
+
+/* Realization m of a CROP [r_off, r_off+wLy) x [c_off, c_off+wLx) of an Lx_g x Ly_g grid
+ * (test device for full-size sampled parity): gaps initialised from the GLOBAL block sums
+ * (BLOCK_MEAN) or the global-site Philox counter (RANDOM), then S sweeps whose colour and
+ * Philox counters use global coordinates. The crop edge acts as an open boundary, so sites
+ * within 2S+1 of an inner crop edge are not exact; the caller compares only the interior
+ * (information moves one site per half-sweep). phi0/mask/beta are crop arrays. */
+void oracle_simulate_window(const float *phi0, const uint8_t *mask, const float *beta, int wLx, int wLy,
+                            int r_off, int c_off, int Lx_g, int Ly_g, int lb, const int64_t *SP_g,
+                            const int64_t *NK_g, int init_mode, float q, float J, int64_t m, int S,
+                            uint64_t seed, float *phi)
+{
+    int nbx = (Lx_g + lb - 1) / lb, nby = (Ly_g + lb - 1) / lb;
+    int64_t spg = 0, nkg = 0;
+    for (int b = 0; b < nbx * nby; ++b) { spg += SP_g[b]; nkg += NK_g[b]; }
+    float gmean = nkg ? (float)(((double)spg * 0x1p-28) / (double)nkg) : 0.0f;
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    memcpy(phi, phi0, sizeof(float) * (size_t)wLx * (size_t)wLy);
+    for (int r = 0; r < wLy; ++r)
+        for (int c = 0; c < wLx; ++c) {
+            int64_t i = (int64_t)r * wLx + c;
+            if (mask[i]) continue;
+            int rg = r + r_off, cg = c + c_off;
+            if (init_mode == 0) {
+                int b = (rg / lb) * nbx + (cg / lb);
+                phi[i] = NK_g[b] ? (float)(((double)SP_g[b] * 0x1p-28) / (double)NK_g[b]) : gmean;
+            } else {
+                uint32_t ctr[4] = {(uint32_t)((int64_t)rg * Lx_g + cg), 0u, (uint32_t)(m >> 1), 1u};
+                uint32_t w[4];
+                oracle_philox4x32_10(ctr, key, w);
+                phi[i] = oracle_uniform((m & 1) ? w[2] : w[0]) * TWO_PI_F;
+            }
+        }
+    for (int s = 1; s <= S; ++s)
+        for (int colour = 0; colour < 2; ++colour)
+            for (int r = 0; r < wLy; ++r)
+                for (int c = 0; c < wLx; ++c) {
+                    int64_t i = (int64_t)r * wLx + c;
+                    int rg = r + r_off, cg = c + c_off;
+                    if (((rg + cg) & 1) != colour || mask[i]) continue;
+                    update_site_ctr(phi, wLx, wLy, r, c, (uint32_t)((int64_t)rg * Lx_g + cg), beta[i], q, J,
+                                    (uint32_t)s, m, seed);
+                }
 }
 
 /* One checkerboard sweep (colour A = (r+c) even, then B) over the gap sites of one

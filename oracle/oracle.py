@@ -91,6 +91,9 @@ def _declare(L):
     L.oracle_half_sweep_rows.argtypes = [_f32p, _u8p, _f32p, C.c_int, C.c_int, C.c_float, C.c_float, C.c_uint32,
                                          C.c_int64, C.c_uint64, C.c_int, C.c_int, C.c_int]
     L.oracle_half_sweep_rows.restype = C.c_int64
+    L.oracle_simulate_window.argtypes = [_f32p, _u8p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, _i64p, _i64p, C.c_int, C.c_float, C.c_float, C.c_int64,
+                                         C.c_int, C.c_uint64, _f32p]
     L.oracle_parameters.argtypes = [_f32p, _u8p, C.c_int, C.c_int, C.POINTER(_Cfg), _f32p, _f32p,
                                     C.c_int, _f32p, _f32p, _f32p, C.POINTER(C.c_float),
                                     C.POINTER(C.c_float), _i64p, _i64p, C.c_void_p]
@@ -358,3 +361,57 @@ def fill(z, mask, cfg: OracleConfig, Tk, ek, M, S, seed, energy=False, states=Fa
     zin = np.where(mask != 0, z, np.float32(0)).astype(np.float32)
     pred = predict(zin, mask, sim["acc"], M, cfg.n_avg, p.zmin, p.zmax, degenerate)
     return dict(pred=pred, params=p, sim=sim)
+
+
+class WindowOracle:
+    """Exact oracle states of a small window of a LARGE grid (full-size sampled parity).
+
+    Global quantities are computed on the whole grid with the oracle's own functions:
+    z_min/z_max and the spin transform (a1-a2), block sums, block temperatures and the global
+    lower median (a3-a4). The rest of the method is local, so it runs on a crop:
+    - SST smoothing (a5) on a crop with margin r_s*n_s around the simulation crop: a clipped
+      window at an inner crop edge differs from the global one, and the difference moves
+      r_s sites per pass;
+    - the simulation (a6-a7) on a crop with margin 2S+2 around the target window: an inner
+      crop edge acts as an open boundary, and information moves one site per half-sweep.
+    Inside the target window the result is therefore exactly the full-grid oracle's."""
+
+    def __init__(self, z, mask, cfg: OracleConfig, Tk, ek):
+        self.z = np.ascontiguousarray(np.where(mask != 0, z, np.float32(0)), np.float32)
+        self.mask = np.ascontiguousarray(mask, np.uint8)
+        self.cfg, self.Tk, self.ek = cfg, Tk, ek
+        self.phi, self.zmin, self.zmax, st = to_angles(self.z, self.mask)
+        SB, NB, self.SP, self.NK = block_stats(self.phi, self.mask, cfg.lb, cfg.q)
+        self.Tb, self.n_avail = block_temperatures(SB, NB, Tk, ek)
+
+    def T_window(self, r0, r1, c0, c1):
+        """Exact SST field on [r0,r1)x[c0,c1) (crop with margin r_s*n_s, expand, smooth)."""
+        Ly, Lx = self.mask.shape
+        mt = self.cfg.rs * self.cfg.ns
+        R0, R1, C0, C1 = max(r0 - mt, 0), min(r1 + mt, Ly), max(c0 - mt, 0), min(c1 + mt, Lx)
+        lb = self.cfg.lb
+        rows = np.arange(R0, R1) // lb
+        cols = np.arange(C0, C1) // lb
+        T = np.ascontiguousarray(self.Tb[rows[:, None], cols[None, :]], np.float32)
+        T = smooth(T, self.cfg.rs, self.cfg.ns)
+        return T[r0 - R0:r1 - R0, c0 - C0:c1 - C0]
+
+    def states(self, r0, r1, c0, c1, realizations, S, seed):
+        """Final states (after S sweeps) of realizations on the window [r0,r1)x[c0,c1)."""
+        Ly, Lx = self.mask.shape
+        ms = 2 * S + 2
+        R0, R1, C0, C1 = max(r0 - ms, 0), min(r1 + ms, Ly), max(c0 - ms, 0), min(c1 + ms, Lx)
+        T = self.T_window(R0, R1, C0, C1)
+        beta = np.ascontiguousarray(np.float32(1.0) / T, np.float32)
+        phi0 = np.ascontiguousarray(self.phi[R0:R1, C0:C1])
+        mk = np.ascontiguousarray(self.mask[R0:R1, C0:C1])
+        out = []
+        for m in realizations:
+            st = np.zeros_like(phi0)
+            lib().oracle_simulate_window(phi0, mk, beta, C1 - C0, R1 - R0, R0, C0, Lx, Ly, self.cfg.lb,
+                                         np.ascontiguousarray(self.SP, np.int64).ravel(),
+                                         np.ascontiguousarray(self.NK, np.int64).ravel(),
+                                         0 if self.cfg.init == "block_mean" else 1, float(self.cfg.q),
+                                         float(self.cfg.J), int(m), int(S), int(seed), st)
+            out.append(st[r0 - R0:r1 - R0, c0 - C0:c1 - C0].copy())
+        return np.stack(out)

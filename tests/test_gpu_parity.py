@@ -250,3 +250,55 @@ def test_row_slabs_emulated_bit_exact(P, calib, world):
     ref = gpu_run(P, z, mask, cfg, calib, 6, 10, 123)["pred"]
     got = _emulated_slabs(P, z, mask, cfg, calib, 6, 10, 123, world)
     assert_bitwise(got, ref, f"row slabs x{world}")
+
+
+def _full_size_sampled(P, calib, L, p, gaps, nu, M, S, windows, realizations):
+    """Full-size run in bench's launch configuration; oracle.WindowOracle gives the exact
+    oracle states and predictions of sampled windows (bit-exact comparison)."""
+    Tk, ek = calib
+    truth, z, mask = make_problem(L, p, gaps=gaps, nu=nu)
+    cfg = P.Config()
+    m = P.LeMpr(cfg, calib)
+    m.set_data(z, mask)
+    T = m.estimate_local_params(want_T=True)
+    m.simulate(M, S, 20221202)
+    pred = m.predict()
+    info = m.info()
+    W = O.WindowOracle(z, mask, ocfg(cfg), Tk, ek)
+    assert info["z_min"] == W.zmin and info["z_max"] == W.zmax
+    assert np.array_equal(m.debug(P.binding.MPR_BUF_BLOCK_T).reshape(W.Tb.shape).view(np.uint32),
+                          W.Tb.view(np.uint32))
+    states = {r: m.debug(P.binding.MPR_BUF_STATE, r) for r in realizations}
+    m.close()
+    for (r0, r1, c0, c1) in windows:
+        assert_bitwise(T[r0:r1, c0:c1], W.T_window(r0, r1, c0, c1), f"T window {(r0, c0)}")
+        ref = W.states(r0, r1, c0, c1, range(M), S, 20221202)
+        for r in realizations:
+            assert_bitwise(states[r][r0:r1, c0:c1], ref[r], f"state of realization {r} at {(r0, c0)}")
+        acc = np.zeros(ref.shape[1:])
+        for k in range(M):
+            acc += ref[k].astype(np.float64)
+        zw = np.ascontiguousarray(np.nan_to_num(z[r0:r1, c0:c1]))
+        mw = np.ascontiguousarray(mask[r0:r1, c0:c1])
+        pw = O.predict(zw, mw, np.where(mw == 0, acc, 0.0), M, 1, W.zmin, W.zmax, 0)
+        assert_bitwise(pred[r0:r1, c0:c1], pw, f"predictions at {(r0, c0)}")
+    gapm = mask == 0
+    assert_bitwise(pred[~gapm], z[~gapm], "samples returned bitwise")
+    assert pred[gapm].min() >= W.zmin and pred[gapm].max() <= W.zmax
+
+
+@pytest.mark.slow
+def test_c3_full_size_sampled(P, calib):
+    """BASELINE config 3 at full size: 4096^2, 70% cloud gaps, M = 8 (one GPU's shard of 64)."""
+    L = 4096
+    wins = [(2040, 2056, 2040, 2056), (0, 12, 0, 12), (4084, 4096, 1000, 1016), (777, 793, 4080, 4096)]
+    _full_size_sampled(P, calib, L, 0.7, "cloud", 1.5, 8, 30, wins, [0, 5])
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled(P, calib):
+    """BASELINE config 4 at full size: 16384^2, 50% random gaps, M = 10, S = 30 (the north
+    star's < 1 s target workload), sampled windows bit-exact vs the oracle."""
+    L = 16384
+    wins = [(8190, 8202, 8190, 8202), (0, 10, 16374, 16384), (12000, 12010, 3, 13)]
+    _full_size_sampled(P, calib, L, 0.5, "random", 1.5, 10, 30, wins, [0, 9])

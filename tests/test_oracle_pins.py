@@ -462,3 +462,19 @@ def test_score_hand_values():
     assert s["mae"] == 3.5 and abs(s["rmse"] - math.sqrt(12.5)) < 1e-12
     assert abs(s["mare"] - (3 / 10 + 4 / 20) / 2) < 1e-12
     assert O.score(truth, truth, mask)["rmse"] == 0
+
+
+def test_window_oracle_equals_full_oracle(calib):
+    """The full-size sampling device (oracle.WindowOracle) reproduces the full-grid oracle
+    bit for bit inside its window (locality of the smoothing and of the Metropolis chain)."""
+    Tk, ek = calib
+    from inputs.synth import make_problem
+    truth, z, mask = make_problem(70, 0.5, Lx=83, corr_len=6.0)
+    for cfg in (O.OracleConfig(lb=8, rs=2, ns=2), O.OracleConfig(lb=16, rs=1, ns=3, init="random")):
+        p = O.parameters(z, mask, cfg, Tk, ek)
+        full = O.simulate(p, mask, cfg, 3, 5, 77, states=True)["phi"]
+        W = O.WindowOracle(z, mask, cfg, Tk, ek)
+        for (r0, r1, c0, c1) in [(30, 38, 40, 47), (0, 6, 0, 9), (62, 70, 75, 83)]:
+            assert np.array_equal(W.T_window(r0, r1, c0, c1), p.T[r0:r1, c0:c1])
+            got = W.states(r0, r1, c0, c1, [0, 2], 5, 77)
+            assert np.array_equal(got.view(np.uint32), full[[0, 2], r0:r1, c0:c1].view(np.uint32))
