@@ -45,6 +45,25 @@ struct DBuf {
 
 enum Stage { ST_INIT = 0, ST_DATA = 1, ST_PARAMS = 2, ST_SIM = 3 };
 
+// Everything a realization batch's launch sequence depends on (CUDA graph cache key).
+struct BatchKey {
+  int64_t P, PA;
+  int Rb;
+  uint32_t pair_base;
+  int32_t sweeps;
+  uint32_t k0, k1;
+  int n_avg, init, r_lo, r_hi, timing, variant;
+  float q, J;
+  void *G, *A, *rec, *acc;
+  double* energy;
+};
+
+struct GraphEntry {
+  BatchKey key{};
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+};
+
 }  // namespace
 
 struct mpr_ctx {
@@ -74,6 +93,10 @@ struct mpr_ctx {
   int64_t sweep_launches = 0;
   double sweep_ms = 0.0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // CUDA graphs of the per-batch launch sequence (replayed when the key repeats)
+  int use_graphs = 1;
+  std::vector<GraphEntry> graphs = std::vector<GraphEntry>(8);
+  size_t graph_next = 0;
   int energy_enabled = 0;
   int64_t energy_M = 0, energy_S = 0;
   // row-slab mode (mpr_slab_*)
@@ -305,6 +328,7 @@ mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
     return e == cudaErrorMemoryAllocation ? MPR_ERR_OOM : MPR_ERR_CUDA;
   }
   if (const char* v = std::getenv("MPR_SWEEP_VARIANT")) c->sweep_variant = std::atoi(v);
+  if (const char* v = std::getenv("MPR_NO_GRAPHS")) c->use_graphs = std::atoi(v) ? 0 : 1;
   c->sweep_grid = sweep_grid_size(c->device, c->sweep_variant);
   *out = c;
   return MPR_OK;
@@ -319,6 +343,8 @@ void mpr_destroy(mpr_ctx* c) {
                   &c->energy, &c->out, &c->tmp};
   for (DBuf* b : bufs) b->release();
   if (c->hsc) cudaFreeHost(c->hsc);
+  for (auto& e : c->graphs)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -431,6 +457,55 @@ mpr_status mpr_reset_accumulator(mpr_ctx* c) {
   return MPR_OK;
 }
 
+// One realization batch: init, 2*S half-sweeps (bracketed by the timing events), and the
+// realization sum into the accumulator. Issued directly or captured into a CUDA graph.
+static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep) {
+  cudaStream_t st = c->stream;
+  const bool avg = k.n_avg > 1;
+  const int npairs = k.Rb / 2;
+  launch_init_states(c->rec.as<GapRec>(), c->G.as<float>(), avg ? c->A.as<float>() : nullptr, k.P, k.Rb, npairs,
+                     k.pair_base, k.init == MPR_INIT_RANDOM, k.k0, k.k1, st);
+  CKL("init_states");
+  ++c->launches;
+  SweepArgs a{};
+  a.rec = c->rec.as<GapRec>();
+  a.G = c->G.as<float>();
+  a.A = avg ? c->A.as<float>() : nullptr;
+  a.R = k.Rb;
+  a.npairs = npairs;
+  a.pair_base = k.pair_base;
+  a.k0 = k.k0;
+  a.k1 = k.k1;
+  a.q = k.q;
+  a.J = k.J;
+  a.r_valid_lo = k.r_lo;
+  a.r_valid_hi = k.r_hi;
+  a.energy_stride = k.sweeps;
+  *nsweep = 0;
+  if (k.timing) CK(cudaEventRecord(c->ev0, st), "event record");
+  for (int32_t s = 1; s <= k.sweeps; ++s) {
+    a.sweep = static_cast<uint32_t>(s);
+    a.accumulate = avg && (s > k.sweeps - k.n_avg);
+    a.energy = k.energy ? k.energy + (s - 1) : nullptr;
+    for (int colour = 0; colour < 2; ++colour) {
+      a.is_b = colour;
+      a.g_begin = colour ? k.PA : 0;
+      a.g_count = colour ? k.P - k.PA : k.PA;
+      if (a.g_count > 0) {
+        launch_sweep_half(a, c->sweep_grid, k.variant, st);
+        CKL("sweep_half");
+        ++c->launches;
+        ++*nsweep;
+      }
+    }
+  }
+  if (k.timing) CK(cudaEventRecord(c->ev1, st), "event record");
+  launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), 0, k.P, k.Rb, k.r_lo, k.r_hi, c->acc.as<double>(), st);
+  CKL("acc_reduce");
+  ++c->launches;
+  return MPR_OK;
+}
+
 mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed, int64_t m_begin,
                               int64_t m_end) {
   if (!c) return MPR_ERR_INVALID_ARG;
@@ -470,7 +545,6 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
   for (int64_t mb = mb0; mb < m_end; mb += R) {
     const int64_t span = std::min<int64_t>(R, m_end - mb);
     const int Rb = static_cast<int>(span + (span & 1));
-    const int npairs = Rb / 2;
     const uint32_t pair_base = static_cast<uint32_t>(mb / 2);
     const int r_lo = static_cast<int>(std::max<int64_t>(m_begin - mb, 0));
     const int r_hi = static_cast<int>(std::min<int64_t>(m_end - mb, Rb));
@@ -478,53 +552,50 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
       CK(cudaEventCreate(&c->ev0), "event");
       CK(cudaEventCreate(&c->ev1), "event");
     }
-    launch_init_states(c->rec.as<GapRec>(), c->G.as<float>(), avg ? c->A.as<float>() : nullptr, c->P, Rb,
-                       npairs, pair_base, c->cfg.init == MPR_INIT_RANDOM, k0, k1, st);
-    CKL("init_states");
-    ++c->launches;
-    SweepArgs a{};
-    a.rec = c->rec.as<GapRec>();
-    a.G = c->G.as<float>();
-    a.A = avg ? c->A.as<float>() : nullptr;
-    a.R = Rb;
-    a.npairs = npairs;
-    a.pair_base = pair_base;
-    a.k0 = k0;
-    a.k1 = k1;
-    a.q = c->cfg.q;
-    a.J = c->cfg.J;
-    a.r_valid_lo = r_lo;
-    a.r_valid_hi = r_hi;
-    a.energy_stride = sweeps;
+    BatchKey key{};
+    key.P = c->P; key.PA = c->PA; key.Rb = Rb; key.pair_base = pair_base; key.sweeps = sweeps;
+    key.k0 = k0; key.k1 = k1; key.n_avg = c->cfg.n_avg; key.init = c->cfg.init; key.r_lo = r_lo; key.r_hi = r_hi;
+    key.timing = c->timing; key.variant = c->sweep_variant; key.q = c->cfg.q; key.J = c->cfg.J;
+    key.G = c->G.p; key.A = c->A.p; key.rec = c->rec.p; key.acc = c->acc.p;
+    key.energy = c->energy_enabled ? c->energy.as<double>() + mb * sweeps : nullptr;
     int64_t nsweep_launch = 0;
-    if (c->timing) CK(cudaEventRecord(c->ev0, st), "event record");
-    for (int32_t s = 1; s <= sweeps; ++s) {
-      a.sweep = static_cast<uint32_t>(s);
-      a.accumulate = avg && (s > sweeps - c->cfg.n_avg);
-      a.energy = c->energy_enabled ? c->energy.as<double>() + mb * sweeps + (s - 1) : nullptr;
-      for (int colour = 0; colour < 2; ++colour) {
-        a.is_b = colour;
-        a.g_begin = colour ? c->PA : 0;
-        a.g_count = colour ? c->P - c->PA : c->PA;
-        if (a.g_count > 0) {
-          launch_sweep_half(a, c->sweep_grid, c->sweep_variant, st);
-          CKL("sweep_half");
-          ++c->launches;
-          ++nsweep_launch;
-        }
+    if (c->use_graphs) {
+      cudaGraphExec_t exec = nullptr;
+      for (auto& e : c->graphs)
+        if (e.exec && std::memcmp(&e.key, &key, sizeof key) == 0) exec = e.exec;
+      if (!exec) {
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        mpr_status sb = issue_batch(c, key, &nsweep_launch);
+        cudaGraph_t graph = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(st, &graph);
+        if (sb != MPR_OK) { if (graph) cudaGraphDestroy(graph); return sb; }
+        CK(ce, "end capture");
+        ce = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CK(ce, "graph instantiate");
+        GraphEntry& slot = c->graphs[c->graph_next++ % c->graphs.size()];
+        if (slot.exec) cudaGraphExecDestroy(slot.exec);
+        std::memcpy(&slot.key, &key, sizeof key);  // bytewise (padding included) for memcmp
+        slot.exec = exec;
+        slot.launches = nsweep_launch;
+      } else {
+        for (auto& e : c->graphs)
+          if (e.exec == exec) nsweep_launch = e.launches;
       }
+      CK(cudaGraphLaunch(exec, st), "graph launch");
+      c->launches += nsweep_launch + 2;
+      c->total_launches += nsweep_launch + 2;
+    } else {
+      mpr_status sb = issue_batch(c, key, &nsweep_launch);
+      if (sb != MPR_OK) return sb;
     }
     if (c->timing) {
-      CK(cudaEventRecord(c->ev1, st), "event record");
       CK(cudaEventSynchronize(c->ev1), "event sync");
       float ms = 0.0f;
       CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event elapsed");
       c->sweep_ms += ms;
       c->sweep_launches += nsweep_launch;
     }
-    launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), 0, c->P, Rb, r_lo, r_hi, c->acc.as<double>(), st);
-    CKL("acc_reduce");
-    ++c->launches;
     c->last_m_base = mb;
     c->last_R = Rb;
   }
