@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--ref-sample-realizations", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--decomp", default="realizations", choices=["realizations", "rows"],
+                    help="multi-GPU split: realization shards (weak scaling, default) or row slabs "
+                         "with one-row halos (strong scaling)")
     return ap.parse_args()
 
 
@@ -82,7 +85,7 @@ def algorithmic_bytes_per_update(p, n_avg=1, S=30, b_T=4):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 20 ms during the timed regions."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms during the timed regions."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -96,7 +99,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -192,9 +195,15 @@ def run_mpr(args):
     calib = Pk.load_calibration()
     cfg = Pk.Config(device=local)
     eng = Pk.LeMpr(cfg, calib, stream=stream.cuda_stream)
-    from paper_2212_01317_b200.sharding import allreduce_accumulator, shard_range
-    M_glob = M * ws  # weak scaling: M realizations per rank
-    m0, m1 = shard_range(M_glob, ws, rank)
+    from paper_2212_01317_b200.sharding import allreduce_accumulator, exchange_halo, row_range, shard_range
+    rows = args.decomp == "rows"
+    if rows:  # strong scaling: the whole M on every rank, the grid split into row slabs
+        M_glob = M
+        m0, m1 = 0, M
+        r0, r1 = row_range(Ly, ws, rank)
+    else:     # weak scaling: M realizations per rank
+        M_glob = M * ws
+        m0, m1 = shard_range(M_glob, ws, rank)
 
     # device-resident inputs (the "value" leg) and pinned host buffers (the e2e leg)
     z_dev = torch.from_numpy(np.nan_to_num(z, nan=0.0)).to(dev)
@@ -209,11 +218,23 @@ def run_mpr(args):
         if ws > 1:
             allreduce_accumulator(eng.accumulator_tensor())
 
+    def simulate():
+        if not rows:
+            eng.simulate_range(M_glob, S, SEED_SIM, m0, m1)
+            return
+        eng.slab_begin(M_glob, S, SEED_SIM, 0, M_glob, r0, r1)
+        for s in range(1, S + 1):
+            for colour in (0, 1):
+                eng.slab_half_sweep(s, colour)
+                if ws > 1:
+                    exchange_halo(eng, colour, r0, r1, rank, ws)
+        eng.slab_end()
+
     def step_device():
         eng.set_data_device(z_dev.data_ptr(), m_dev.data_ptr(), Lx, Ly)
         eng.estimate_local_params()
         eng.reset_accumulator()
-        eng.simulate_range(M_glob, S, SEED_SIM, m0, m1)
+        simulate()
         allreduce_acc()
         eng.predict_device(out_dev.data_ptr())
 
@@ -222,7 +243,7 @@ def run_mpr(args):
         eng.shape = (Ly, Lx)
         eng.estimate_local_params()
         eng.reset_accumulator()
-        eng.simulate_range(M_glob, S, SEED_SIM, m0, m1)
+        simulate()
         allreduce_acc()
         Pk.binding._check(eng.ctx, Pk.load_library().mpr_predict(eng.ctx, out_pin.data_ptr()))
 
@@ -263,7 +284,8 @@ def run_mpr(args):
 
     # dominant kernel: the half-sweep (CUDA events on the library's stream around the sweep loops)
     sweep_ms, sweep_n = info["sweep_ms"], info["sweep_launches"]
-    sweep_updates = P * S * (m1 - m0) * args.steps
+    P_loc = int((mask[r0:r1] == 0).sum()) if rows else P
+    sweep_updates = P_loc * S * (m1 - m0) * args.steps
     sweep_s = sweep_ms / 1000.0
     b_upd = algorithmic_bytes_per_update(c["p"])
     peaks = {}
@@ -305,10 +327,10 @@ def run_mpr(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "scaling": "strong" if rows else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": desc, "L": c["L"], "p": c["p"], "gaps": c["gaps"], "gap_sites": P,
                            "M_per_rank": M, "M_total": M_glob, "sweeps": S,
-                           "updates_per_step": updates_per_step, "parallelism": f"realizations x{ws}",
+                           "updates_per_step": updates_per_step, "parallelism": f"row slabs x{ws}" if rows else f"realizations x{ws}",
                            "l2": "flushed between timed steps (256 MiB write, outside the events)"},
                 "fill_time_ms": total_ms / args.steps,
                 "gpu_launches": int(launches),

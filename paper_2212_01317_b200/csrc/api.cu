@@ -459,7 +459,9 @@ mpr_status mpr_reset_accumulator(mpr_ctx* c) {
 
 // One realization batch: init, 2*S half-sweeps (bracketed by the timing events), and the
 // realization sum into the accumulator. Issued directly or captured into a CUDA graph.
-static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep) {
+static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bool capturing) {
+  // inside a stream capture the timing events must be external record nodes
+  const unsigned ev_flags = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
   cudaStream_t st = c->stream;
   const bool avg = k.n_avg > 1;
   const int npairs = k.Rb / 2;
@@ -482,7 +484,7 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep) {
   a.r_valid_hi = k.r_hi;
   a.energy_stride = k.sweeps;
   *nsweep = 0;
-  if (k.timing) CK(cudaEventRecord(c->ev0, st), "event record");
+  if (k.timing) CK(cudaEventRecordWithFlags(c->ev0, st, ev_flags), "event record");
   for (int32_t s = 1; s <= k.sweeps; ++s) {
     a.sweep = static_cast<uint32_t>(s);
     a.accumulate = avg && (s > k.sweeps - k.n_avg);
@@ -499,7 +501,7 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep) {
       }
     }
   }
-  if (k.timing) CK(cudaEventRecord(c->ev1, st), "event record");
+  if (k.timing) CK(cudaEventRecordWithFlags(c->ev1, st, ev_flags), "event record");
   launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), 0, k.P, k.Rb, k.r_lo, k.r_hi, c->acc.as<double>(), st);
   CKL("acc_reduce");
   ++c->launches;
@@ -565,7 +567,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
         if (e.exec && std::memcmp(&e.key, &key, sizeof key) == 0) exec = e.exec;
       if (!exec) {
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
-        mpr_status sb = issue_batch(c, key, &nsweep_launch);
+        mpr_status sb = issue_batch(c, key, &nsweep_launch, true);
         cudaGraph_t graph = nullptr;
         cudaError_t ce = cudaStreamEndCapture(st, &graph);
         if (sb != MPR_OK) { if (graph) cudaGraphDestroy(graph); return sb; }
@@ -586,7 +588,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
       c->launches += nsweep_launch + 2;
       c->total_launches += nsweep_launch + 2;
     } else {
-      mpr_status sb = issue_batch(c, key, &nsweep_launch);
+      mpr_status sb = issue_batch(c, key, &nsweep_launch, false);
       if (sb != MPR_OK) return sb;
     }
     if (c->timing) {
