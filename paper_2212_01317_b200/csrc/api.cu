@@ -567,7 +567,10 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
         if (e.exec && std::memcmp(&e.key, &key, sizeof key) == 0) exec = e.exec;
       if (!exec) {
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        const int64_t l0 = c->launches, t0 = c->total_launches;  // capture launches nothing
         mpr_status sb = issue_batch(c, key, &nsweep_launch, true);
+        c->launches = l0;
+        c->total_launches = t0;
         cudaGraph_t graph = nullptr;
         cudaError_t ce = cudaStreamEndCapture(st, &graph);
         if (sb != MPR_OK) { if (graph) cudaGraphDestroy(graph); return sb; }
