@@ -490,6 +490,9 @@ int oracle_parameters(const float *z, const uint8_t *mask, int Lx, int Ly, const
     return rc;
 }
 
+int64_t oracle_grid_energy_fx(const float *phi, int Lx, int Ly, float q);
+double oracle_energy_from_fx(int64_t E_fx, int Lx, int Ly);
+
 /* Realizations m in [m_begin, m_end): init, S sweeps, accumulate the last n_avg
  * (P:95 conditional mean). acc (fp64, length Lx*Ly) is added to; energy
  * (nullable, (m_end-m_begin)*S) receives the whole-grid specific energy after each
@@ -510,13 +513,102 @@ void oracle_simulate(const float *phi0, const uint8_t *mask, const float *beta, 
             if (s > S - cfg->n_avg)
                 for (int64_t i = 0; i < n; ++i)
                     if (!mask[i]) acc[i] += (double)phi[i];
-            if (energy)
-                energy[(m - m_begin) * S + (s - 1)] = oracle_grid_specific_energy(phi, Lx, Ly, cfg->q);
+            if (energy)  /* ARITH §J fixed-point definition (pinned against the fp64 one) */
+                energy[(m - m_begin) * S + (s - 1)] =
+                    oracle_energy_from_fx(oracle_grid_energy_fx(phi, Lx, Ly, cfg->q), Lx, Ly);
         }
         if (phi_out) memcpy(phi_out + (m - m_begin) * n, phi, sizeof(float) * (size_t)n);
     }
     if (accepted) *accepted = nacc;
     free(phi);
+}
+
+/* Whole-grid bond sum in fixed point (ARITH §J): sum over all bonds of
+ * llrint(cos_spec(q(phi_i - phi_j)) * 2^32), every unordered bond once. */
+int64_t oracle_grid_energy_fx(const float *phi, int Lx, int Ly, float q)
+{
+    int64_t sum = 0;
+    for (int r = 0; r < Ly; ++r)
+        for (int c = 0; c < Lx; ++c) {
+            int64_t i = (int64_t)r * Lx + c;
+            if (c + 1 < Lx) sum += llrintf(oracle_cos_spec(q * (phi[i] - phi[i + 1])) * 0x1p32f);
+            if (r + 1 < Ly) sum += llrintf(oracle_cos_spec(q * (phi[i] - phi[i + Lx])) * 0x1p32f);
+        }
+    return sum;
+}
+
+/* e = (-(double)E_fx * 2^-32) / N_bonds (ARITH §J). */
+double oracle_energy_from_fx(int64_t E_fx, int Lx, int Ly)
+{
+    double nb = (double)(2 * (int64_t)Lx * Ly - Lx - Ly);
+    return (-(double)E_fx * 0x1p-32) / nb;
+}
+
+/* Equilibrium test of ARITH §K on y[0 .. n_fit-1] (the last n_fit energies): least-squares
+ * slope b against t = 0..n_fit-1, residual scale, tau = 2 sigma / n_fit; 1 iff b >= -tau. */
+int oracle_equilibrium_test(const double *y, int n_fit)
+{
+    double xbar = (double)(n_fit - 1) / 2.0;
+    double sy = 0.0;
+    for (int t = 0; t < n_fit; ++t) sy = sy + y[t];
+    double ybar = sy / (double)n_fit;
+    double sxx = 0.0, sxy = 0.0;
+    for (int t = 0; t < n_fit; ++t) {
+        double dx = (double)t - xbar;
+        sxx = sxx + dx * dx;
+        sxy = sxy + dx * (y[t] - ybar);
+    }
+    double b = sxy / sxx;
+    double a = ybar - b * xbar;
+    double sse = 0.0;
+    for (int t = 0; t < n_fit; ++t) {
+        double res = y[t] - a - b * (double)t;
+        sse = sse + res * res;
+    }
+    double tau = 2.0 * sqrt(sse / (double)(n_fit - 2)) / (double)n_fit;
+    return b >= -tau;
+}
+
+/* Adaptive protocol (row f1; ARITH §K): realization m sweeps until the energy
+ * trace passes the equilibrium test at a check sweep (s = n_fit + k n_f), then runs
+ * n_avg more sweeps accumulating each; capped at S_max. acc (fp64, Lx*Ly) is added to;
+ * s_eq[m - m_begin] receives the equilibrium sweep (negated if forced by the cap);
+ * energy (nullable, (m_end-m_begin)*S_max) the per-sweep energies (0 after the stop). */
+void oracle_simulate_adaptive(const float *phi0, const uint8_t *mask, const float *beta, int Lx, int Ly,
+                              const oracle_cfg *cfg, const int64_t *SP, const int64_t *NK,
+                              int64_t m_begin, int64_t m_end, int n_fit, int n_f, int S_max, uint64_t seed,
+                              double *acc, int32_t *s_eq, double *energy, float *phi_out)
+{
+    int64_t n = (int64_t)Lx * Ly;
+    float *phi = (float *)malloc(sizeof(float) * (size_t)n);
+    double *e = (double *)malloc(sizeof(double) * (size_t)(S_max + 1));
+    for (int64_t m = m_begin; m < m_end; ++m) {
+        memcpy(phi, phi0, sizeof(float) * (size_t)n);
+        oracle_init(phi, mask, Lx, Ly, cfg->lb, SP, NK, cfg->init_mode, m, seed);
+        int eq = 0, stop = S_max;
+        for (int s = 1; s <= stop; ++s) {
+            oracle_sweep(phi, mask, beta, Lx, Ly, cfg->q, cfg->J, (uint32_t)s, m, seed, 0);
+            e[s] = oracle_energy_from_fx(oracle_grid_energy_fx(phi, Lx, Ly, cfg->q), Lx, Ly);
+            if (energy) energy[(m - m_begin) * S_max + (s - 1)] = e[s];
+            if (eq) {
+                for (int64_t i = 0; i < n; ++i)
+                    if (!mask[i]) acc[i] += (double)phi[i];
+                continue;
+            }
+            int check = s >= n_fit + n_f && (s - n_fit) % n_f == 0 && s + cfg->n_avg <= S_max;
+            if (check && oracle_equilibrium_test(&e[s - n_fit + 1], n_fit)) {
+                eq = s;
+                stop = s + cfg->n_avg;
+            } else if (s == S_max - cfg->n_avg) {
+                eq = -s;  /* forced by the cap */
+                stop = S_max;
+            }
+        }
+        s_eq[m - m_begin] = eq;
+        if (phi_out) memcpy(phi_out + (m - m_begin) * n, phi, sizeof(float) * (size_t)n);
+    }
+    free(phi);
+    free(e);
 }
 
 /* Back-transform of the conditional mean, P:95 (ARITH §I). */

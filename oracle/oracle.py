@@ -108,6 +108,16 @@ def _declare(L):
     L.oracle_unconditional_energy.restype = C.c_double
     L.oracle_score.argtypes = [_f32p, _f32p, _u8p, C.c_int64, C.POINTER(C.c_double),
                                C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    L.oracle_grid_energy_fx.argtypes = [_f32p, C.c_int, C.c_int, C.c_float]
+    L.oracle_grid_energy_fx.restype = C.c_int64
+    L.oracle_energy_from_fx.argtypes = [C.c_int64, C.c_int, C.c_int]
+    L.oracle_energy_from_fx.restype = C.c_double
+    L.oracle_equilibrium_test.argtypes = [_f64p, C.c_int]
+    L.oracle_equilibrium_test.restype = C.c_int
+    L.oracle_simulate_adaptive.argtypes = [_f32p, _u8p, _f32p, C.c_int, C.c_int, C.POINTER(_Cfg), _i64p, _i64p,
+                                           C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_uint64, _f64p,
+                                           np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"), C.c_void_p,
+                                           C.c_void_p]
 
 
 # ------------------------------------------------------------------ primitives
@@ -270,6 +280,43 @@ def score(pred, truth, mask):
     lib().oracle_score(pred.ravel(), truth.ravel(), mask.ravel(), pred.size, C.byref(a), C.byref(b),
                        C.byref(c), C.byref(n))
     return dict(mae=a.value, rmse=b.value, mare=c.value, mare_excluded=n.value)
+
+
+def grid_energy_fx(phi, q=0.5) -> int:
+    """Fixed-point whole-grid bond sum E_fx (ARITH §J)."""
+    phi = np.ascontiguousarray(phi, np.float32)
+    return lib().oracle_grid_energy_fx(phi.ravel(), phi.shape[1], phi.shape[0], float(q))
+
+
+def energy_from_fx(E_fx, Lx, Ly) -> float:
+    return lib().oracle_energy_from_fx(int(E_fx), int(Lx), int(Ly))
+
+
+def equilibrium_test(y) -> bool:
+    """ARITH §K slope test on the last n_fit energies."""
+    y = np.ascontiguousarray(y, np.float64)
+    return bool(lib().oracle_equilibrium_test(y, len(y)))
+
+
+def simulate_adaptive(params, mask, cfg, M, seed, n_fit=20, n_f=5, S_max=500, m_begin=0, m_end=None,
+                      energy=False, states=False):
+    """Row f1 protocol (ARITH §K) for realizations [m_begin, m_end): returns
+    dict(acc, s_eq (negative = forced by the cap), energy, phi)."""
+    m_end = M if m_end is None else m_end
+    mask = np.ascontiguousarray(mask, np.uint8)
+    Ly, Lx = mask.shape
+    R = m_end - m_begin
+    acc = np.zeros(Lx * Ly, np.float64)
+    s_eq = np.zeros(R, np.int32)
+    en = np.zeros(R * S_max, np.float64) if energy else None
+    ph = np.zeros(R * Lx * Ly, np.float32) if states else None
+    c = _Cfg(cfg.q, cfg.J, cfg.lb, cfg.rs, cfg.ns, 0 if cfg.init == "block_mean" else 1, cfg.n_avg)
+    lib().oracle_simulate_adaptive(params.phi0.ravel(), mask.ravel(), params.beta.ravel(), Lx, Ly, C.byref(c),
+                                   params.SP.ravel(), params.NK.ravel(), int(m_begin), int(m_end), int(n_fit),
+                                   int(n_f), int(S_max), int(seed), acc, s_eq,
+                                   en.ctypes.data if energy else None, ph.ctypes.data if states else None)
+    return dict(acc=acc.reshape(Ly, Lx), s_eq=s_eq, energy=None if en is None else en.reshape(R, S_max),
+                phi=None if ph is None else ph.reshape(R, Ly, Lx))
 
 
 # ------------------------------------------------------------------ pipeline

@@ -15,6 +15,7 @@ FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-ffp-contract=off",  # host-side decision arithmetic (ARITH §K) unfused
     "-prec-div=true", "-ftz=false", "-prec-sqrt=true",
     "-Xptxas", "-v",
 ]

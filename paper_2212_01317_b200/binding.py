@@ -28,7 +28,8 @@ EXPORTED = ["mpr_config_default", "mpr_init", "mpr_destroy", "mpr_last_error", "
             "mpr_set_data_device", "mpr_estimate_local_params", "mpr_simulate", "mpr_reset_accumulator",
             "mpr_simulate_range", "mpr_accumulator_device", "mpr_predict", "mpr_predict_device",
             "mpr_get_info", "mpr_debug_get", "mpr_set_energy_trace", "mpr_set_kernel_timing", "mpr_version",
-            "mpr_slab_begin", "mpr_slab_half_sweep", "mpr_slab_row_states", "mpr_slab_end", "mpr_sync"]
+            "mpr_slab_begin", "mpr_slab_half_sweep", "mpr_slab_row_states", "mpr_slab_end", "mpr_sync",
+            "mpr_simulate_adaptive"]
 
 
 class MprError(RuntimeError):
@@ -89,6 +90,8 @@ def load_library(path: str = LIB_PATH):
     L.mpr_slab_row_states.restype = C.c_int
     L.mpr_slab_end.argtypes = [vp]; L.mpr_slab_end.restype = C.c_int
     L.mpr_sync.argtypes = [vp]; L.mpr_sync.restype = C.c_int
+    L.mpr_simulate_adaptive.argtypes = [vp, i64, u64, i32, i32, i32, vp]
+    L.mpr_simulate_adaptive.restype = C.c_int
     L.mpr_version.argtypes = []; L.mpr_version.restype = C.c_char_p
     _lib = L
     return L
@@ -210,6 +213,14 @@ def mpr_sync(ctx) -> None:
     _check(ctx, load_library().mpr_sync(ctx))
 
 
+def mpr_simulate_adaptive(ctx, M, seed, n_fit=20, n_f=5, max_sweeps=500) -> np.ndarray:
+    """Adaptive equilibration (ARITH §K); returns s_eq per realization
+    (negative = forced by max_sweeps)."""
+    s_eq = np.zeros(M, np.int32)
+    _check(ctx, load_library().mpr_simulate_adaptive(ctx, M, seed, n_fit, n_f, max_sweeps, s_eq.ctypes.data))
+    return s_eq
+
+
 def mpr_version() -> str:
     return load_library().mpr_version().decode()
 
@@ -289,6 +300,9 @@ class LeMpr:
 
     def simulate_range(self, M, sweeps, seed, m_begin, m_end):
         mpr_simulate_range(self.ctx, M, sweeps, seed, m_begin, m_end)
+
+    def simulate_adaptive(self, M, seed, n_fit=20, n_f=5, max_sweeps=500):
+        return mpr_simulate_adaptive(self.ctx, M, seed, n_fit, n_f, max_sweeps)
 
     def reset_accumulator(self):
         mpr_reset_accumulator(self.ctx)

@@ -55,7 +55,7 @@ struct BatchKey {
   int n_avg, init, r_lo, r_hi, timing, variant;
   float q, J;
   void *G, *A, *rec, *acc;
-  double* energy;
+  long long* energy;
 };
 
 struct GraphEntry {
@@ -84,7 +84,7 @@ struct mpr_ctx {
   int64_t nbx = 0, nby = 0, nblocks = 0;
   int64_t n_fallback = 0;
   float median_T = 0;
-  double sum_SB = 0;
+  long long sum_SB_fx = 0;  // fixed-point bond sum of the known-known bonds (ARITH §J)
   // simulation bookkeeping
   int64_t M_total = 0, sweeps = 0, batch = 0, last_m_base = 0, last_R = 0;
   int64_t batch_key_P = -1, batch_key_R = -1, batch_cached = 0;
@@ -107,7 +107,7 @@ struct mpr_ctx {
   std::vector<int> rowoff_h;  // host copy of the gap-id row offsets (2*Ly)
   // device memory
   DBuf z, mask, phiK, scal, calTd, caled, rowcnt, rowoff, gid, rec, bstats, Tb, T, T2, G, A, acc,
-      energy, out, tmp;
+      energy, out, tmp, win;
   DevScalars* hsc = nullptr;  // pinned host mirror of the device scalars
 };
 
@@ -185,6 +185,35 @@ float key_to_float(int k) {
   float f;
   std::memcpy(&f, &b, sizeof f);
   return f;
+}
+
+// e = (-(double)E_fx * 2^-32) / N_bonds  (ARITH §J)
+double energy_from_fx(const mpr_ctx* c, long long E_fx) {
+  const double nb = static_cast<double>(2 * c->Lx * c->Ly - c->Lx - c->Ly);
+  return (-static_cast<double>(E_fx) * 0x1p-32) / nb;
+}
+
+// ARITH §K slope test on y[0 .. n_fit-1], every operation in the written order.
+bool equilibrium_reached(const double* y, int n_fit) {
+  const double xbar = static_cast<double>(n_fit - 1) / 2.0;
+  double sy = 0.0;
+  for (int t = 0; t < n_fit; ++t) sy = sy + y[t];
+  const double ybar = sy / static_cast<double>(n_fit);
+  double sxx = 0.0, sxy = 0.0;
+  for (int t = 0; t < n_fit; ++t) {
+    const double dx = static_cast<double>(t) - xbar;
+    sxx = sxx + dx * dx;
+    sxy = sxy + dx * (y[t] - ybar);
+  }
+  const double b = sxy / sxx;
+  const double a = ybar - b * xbar;
+  double sse = 0.0;
+  for (int t = 0; t < n_fit; ++t) {
+    const double res = y[t] - a - b * static_cast<double>(t);
+    sse = sse + res * res;
+  }
+  const double tau = 2.0 * std::sqrt(sse / static_cast<double>(n_fit - 2)) / static_cast<double>(n_fit);
+  return b >= -tau;
 }
 
 mpr_status stage_data(mpr_ctx* c) {
@@ -340,7 +369,7 @@ void mpr_destroy(mpr_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   DBuf* bufs[] = {&c->z, &c->mask, &c->phiK, &c->scal, &c->calTd, &c->caled, &c->rowcnt, &c->rowoff,
                   &c->gid, &c->rec, &c->bstats, &c->Tb, &c->T, &c->T2, &c->G, &c->A, &c->acc,
-                  &c->energy, &c->out, &c->tmp};
+                  &c->energy, &c->out, &c->tmp, &c->win};
   for (DBuf* b : bufs) b->release();
   if (c->hsc) cudaFreeHost(c->hsc);
   for (auto& e : c->graphs)
@@ -423,7 +452,7 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   CK(cudaStreamSynchronize(st), "estimate_local_params sync");
   c->n_fallback = static_cast<int64_t>(c->hsc->n_fallback);
   c->median_T = c->hsc->median_T;
-  c->sum_SB = static_cast<double>(c->hsc->sum_SB) * 0x1p-32;
+  c->sum_SB_fx = c->hsc->sum_SB;
   if (c->hsc->n_avail == 0 && !c->degenerate)
     return fail(c, MPR_ERR_NO_SAMPLE_BONDS, "no block has a sample-sample bond (PAPER.md:108)");
   c->stage = ST_PARAMS;
@@ -528,8 +557,8 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
   const uint32_t k0 = static_cast<uint32_t>(seed & 0xffffffffu), k1 = static_cast<uint32_t>(seed >> 32);
   if (c->energy_enabled) {
     if (c->energy_M != M || c->energy_S != sweeps) {
-      CK(c->energy.ensure(sizeof(double) * M * sweeps), "alloc energy");
-      CK(cudaMemsetAsync(c->energy.p, 0, sizeof(double) * M * sweeps, st), "zero energy");
+      CK(c->energy.ensure(sizeof(long long) * M * sweeps), "alloc energy");
+      CK(cudaMemsetAsync(c->energy.p, 0, sizeof(long long) * M * sweeps, st), "zero energy");
       c->energy_M = M;
       c->energy_S = sweeps;
     }
@@ -559,7 +588,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
     key.k0 = k0; key.k1 = k1; key.n_avg = c->cfg.n_avg; key.init = c->cfg.init; key.r_lo = r_lo; key.r_hi = r_hi;
     key.timing = c->timing; key.variant = c->sweep_variant; key.q = c->cfg.q; key.J = c->cfg.J;
     key.G = c->G.p; key.A = c->A.p; key.rec = c->rec.p; key.acc = c->acc.p;
-    key.energy = c->energy_enabled ? c->energy.as<double>() + mb * sweeps : nullptr;
+    key.energy = c->energy_enabled ? c->energy.as<long long>() + mb * sweeps : nullptr;
     int64_t nsweep_launch = 0;
     if (c->use_graphs) {
       cudaGraphExec_t exec = nullptr;
@@ -613,6 +642,128 @@ mpr_status mpr_simulate(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed) {
   mpr_status s = mpr_reset_accumulator(c);
   if (s != MPR_OK) return s;
   return mpr_simulate_range(c, M, sweeps, seed, 0, M);
+}
+
+// Row f1 (ARITH §K): every realization sweeps until its energy trace passes
+// the slope test at a check sweep, then averages n_avg more sweeps. The sweeps run on the
+// device for the whole batch; at check sweeps the host reads the fixed-point energies,
+// decides, and uploads the per-realization accumulation windows.
+mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n_fit, int32_t n_f,
+                                 int32_t max_sweeps, int32_t* s_eq_out) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "simulate before estimate_local_params");
+  const int n_avg = c->cfg.n_avg;
+  if (M < 1 || n_fit < 3 || n_f < 1 || max_sweeps < n_avg + 1 || M >= (int64_t(1) << 32))
+    return fail(c, MPR_ERR_INVALID_ARG, "need M >= 1, n_fit >= 3, n_f >= 1, max_sweeps > n_avg");
+  mpr_status st0 = mpr_reset_accumulator(c);
+  if (st0 != MPR_OK) return st0;
+  CK(cudaSetDevice(c->device), "set device");
+  cudaStream_t st = c->stream;
+  c->M_total = M;
+  c->sweeps = max_sweeps;
+  c->launches = 0;
+  if (c->degenerate || c->P == 0) {
+    if (s_eq_out)
+      for (int64_t m = 0; m < M; ++m) s_eq_out[m] = 0;
+    c->stage = ST_SIM;
+    return MPR_OK;
+  }
+  const uint32_t k0 = static_cast<uint32_t>(seed & 0xffffffffu), k1 = static_cast<uint32_t>(seed >> 32);
+  const int64_t R = choose_batch(c, M);
+  CK(c->G.ensure(sizeof(float) * c->P * R), "alloc state");
+  CK(c->A.ensure(sizeof(float) * c->P * R), "alloc accumulator state");
+  CK(c->energy.ensure(sizeof(long long) * R * max_sweeps), "alloc energy");
+  CK(c->win.ensure(sizeof(int) * 2 * R), "alloc windows");
+  std::vector<long long> fx(static_cast<size_t>(R * max_sweeps));
+  std::vector<int> win(static_cast<size_t>(2 * R));
+  std::vector<double> y(static_cast<size_t>(n_fit));
+  for (int64_t mb = 0; mb < M; mb += R) {
+    const int64_t span = std::min<int64_t>(R, M - mb);
+    const int Rb = static_cast<int>(span + (span & 1));
+    const int r_hi = static_cast<int>(span);
+    // windows: (lo, hi] accumulates; hi = INT_MAX while undecided; the pad realization
+    // (odd M) is "done" from the start
+    for (int r = 0; r < Rb; ++r) {
+      win[r] = r < r_hi ? INT32_MAX : 0;
+      win[Rb + r] = r < r_hi ? INT32_MAX : 0;
+    }
+    std::vector<int> eq(static_cast<size_t>(Rb), 0);
+    CK(cudaMemcpyAsync(c->win.p, win.data(), sizeof(int) * 2 * Rb, cudaMemcpyHostToDevice, st), "H2D windows");
+    CK(cudaMemsetAsync(c->energy.p, 0, sizeof(long long) * Rb * max_sweeps, st), "zero energy");
+    launch_init_states(c->rec.as<GapRec>(), c->G.as<float>(), c->A.as<float>(), c->P, Rb, Rb / 2,
+                       static_cast<uint32_t>(mb / 2), c->cfg.init == MPR_INIT_RANDOM, k0, k1, st);
+    CKL("init_states");
+    ++c->launches;
+    SweepArgs a{};
+    a.rec = c->rec.as<GapRec>();
+    a.G = c->G.as<float>();
+    a.A = c->A.as<float>();
+    a.R = Rb;
+    a.npairs = Rb / 2;
+    a.pair_base = static_cast<uint32_t>(mb / 2);
+    a.k0 = k0;
+    a.k1 = k1;
+    a.q = c->cfg.q;
+    a.J = c->cfg.J;
+    a.win_lo = c->win.as<int>();
+    a.win_hi = c->win.as<int>() + Rb;
+    a.energy_stride = max_sweeps;
+    a.r_valid_lo = 0;
+    a.r_valid_hi = r_hi;
+    int pending = r_hi;
+    for (int32_t s = 1; s <= max_sweeps; ++s) {
+      // stop once every realization has passed the end of its averaging window
+      int stop_all = 0;
+      for (int r = 0; r < r_hi; ++r) stop_all = std::max(stop_all, win[Rb + r] == INT32_MAX ? max_sweeps : win[Rb + r]);
+      if (pending == 0 && s > stop_all) break;
+      a.sweep = static_cast<uint32_t>(s);
+      a.energy = c->energy.as<long long>() + (s - 1);
+      for (int colour = 0; colour < 2; ++colour) {
+        a.is_b = colour;
+        a.g_begin = colour ? c->PA : 0;
+        a.g_count = colour ? c->P - c->PA : c->PA;
+        if (a.g_count > 0) {
+          launch_sweep_half(a, c->sweep_grid, c->sweep_variant, st);
+          CKL("sweep_half");
+          ++c->launches;
+        }
+      }
+      const bool check = s >= n_fit + n_f && (s - n_fit) % n_f == 0 && s + n_avg <= max_sweeps;
+      const bool forced = s == max_sweeps - n_avg;
+      if (pending > 0 && (check || forced)) {
+        CK(cudaMemcpyAsync(fx.data(), c->energy.p, sizeof(long long) * Rb * max_sweeps, cudaMemcpyDeviceToHost, st),
+           "D2H energy");
+        CK(cudaStreamSynchronize(st), "check sync");
+        for (int r = 0; r < r_hi; ++r) {
+          if (eq[r] != 0) continue;
+          bool ok = false;
+          if (check) {
+            for (int t = 0; t < n_fit; ++t)
+              y[t] = energy_from_fx(c, c->sum_SB_fx + fx[static_cast<size_t>(r) * max_sweeps + (s - n_fit + t)]);
+            ok = equilibrium_reached(y.data(), n_fit);
+          }
+          if (ok || forced) {
+            eq[r] = ok ? s : -s;
+            win[r] = s;
+            win[Rb + r] = s + n_avg;
+            --pending;
+          }
+        }
+        CK(cudaMemcpyAsync(c->win.p, win.data(), sizeof(int) * 2 * Rb, cudaMemcpyHostToDevice, st), "H2D windows");
+      }
+    }
+    launch_acc_reduce(c->A.as<float>(), 0, c->P, Rb, 0, r_hi, c->acc.as<double>(), st);
+    CKL("acc_reduce");
+    ++c->launches;
+    CK(cudaStreamSynchronize(st), "adaptive sync");
+    if (s_eq_out)
+      for (int r = 0; r < r_hi; ++r) s_eq_out[mb + r] = eq[static_cast<size_t>(r)];
+    c->last_m_base = mb;
+    c->last_R = Rb;
+  }
+  c->batch = R;
+  c->stage = ST_SIM;
+  return MPR_OK;
 }
 
 // ---- row-slab decomposition ------------------------------------
@@ -852,12 +1003,12 @@ mpr_status mpr_debug_get(mpr_ctx* c, mpr_buffer which, int64_t index, void* host
     case MPR_BUF_ENERGY: {
       if (!c->energy_enabled || c->energy_M == 0) return fail(c, MPR_ERR_STATE, "energy trace not enabled");
       const int64_t cnt = c->energy_M * c->energy_S;
-      CK(cudaMemcpyAsync(host_out, c->energy.p, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st), "D2H");
+      // the int64 fixed-point sums have the size of the doubles they become: copy in place
+      CK(cudaMemcpyAsync(host_out, c->energy.p, sizeof(long long) * cnt, cudaMemcpyDeviceToHost, st), "D2H");
       CK(cudaStreamSynchronize(st), "debug sync");
-      // e = -(sum over known-known bonds + fused sums) / N_bonds  (ARITH §J)
-      const double nb = static_cast<double>(2 * c->Lx * c->Ly - c->Lx - c->Ly);
+      long long* fx = static_cast<long long*>(host_out);
       double* e = static_cast<double*>(host_out);
-      for (int64_t k = 0; k < cnt; ++k) e[k] = -(c->sum_SB + e[k]) / nb;
+      for (int64_t k = 0; k < cnt; ++k) e[k] = energy_from_fx(c, c->sum_SB_fx + fx[k]);
       return MPR_OK;
     }
     default:

@@ -88,8 +88,11 @@ struct SweepArgs {
   uint32_t k0, k1;   // Philox key
   float q, J;
   int is_b;          // colour B half-sweep
-  int accumulate;    // add the new state to A
-  double* energy;    // nullable: per-realization bond sums for this sweep, stride S
+  int accumulate;    // add the new state to A (fixed window)
+  const int* win_lo; // nullable: adaptive protocol, realization r accumulates at sweeps
+  const int* win_hi; //           win_lo[r] < s <= win_hi[r] and stops after win_hi[r]
+  long long* energy; // nullable: per-realization fixed-point bond sums (ARITH §J) for
+                     // this sweep, stride energy_stride
   int64_t energy_stride;
   int r_valid_lo, r_valid_hi;  // realizations [lo, hi) of the batch contribute energy
 };

@@ -43,9 +43,10 @@ template <bool QHALF, bool ENERGY, bool FULL, bool BFEXP>
 __device__ __forceinline__ float metropolis(float cur, const float (&nbv)[4], uint32_t flags,
                                             uint32_t sel, float beta, float q, float J,
                                             uint32_t wa, uint32_t wb, bool& accepted,
-                                            float& e_sel) {
+                                            long long& e_sel) {
   const float prop = proposal_angle(wa);
-  float s_cur = 0.0f, s_new = 0.0f, ec = 0.0f, en = 0.0f;
+  float s_cur = 0.0f, s_new = 0.0f;
+  long long ec = 0, en = 0;  // ARITH §J fixed-point bond sums of the selected bonds
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     float cc = cosq<QHALF>(__fsub_rn(cur, nbv[k]), q);
@@ -62,10 +63,9 @@ __device__ __forceinline__ float metropolis(float cur, const float (&nbv)[4], ui
       s_cur = __fadd_rn(s_cur, cc);
       s_new = __fadd_rn(s_new, cn);
     }
-    if (ENERGY) {
-      const bool s = (sel >> k) & 1u;
-      ec += s ? cc : 0.0f;
-      en += s ? cn : 0.0f;
+    if (ENERGY && ((sel >> k) & 1u)) {
+      ec += __float2ll_rn(__fmul_rn(cc, 0x1p32f));
+      en += __float2ll_rn(__fmul_rn(cn, 0x1p32f));
     }
   }
   const float dE = __fmul_rn(J, __fsub_rn(s_cur, s_new));
@@ -90,7 +90,8 @@ __device__ __forceinline__ bool all_present(uint32_t f) {
 template <bool QHALF, bool ENERGY, bool BFEXP>
 __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& rec, float2 cur,
                                              const float (&nv0)[4], const float (&nv1)[4],
-                                             uint32_t self_off, uint32_t pair, float& e0, float& e1) {
+                                             uint32_t self_off, uint32_t pair, long long& e0, long long& e1,
+                                             bool accum0, bool accum1) {
   uint32_t sel = 0;
   if (ENERGY) {
 #pragma unroll
@@ -110,29 +111,43 @@ __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& r
     n1 = metropolis<QHALF, ENERGY, false, BFEXP>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
   }
   if (acc0 || acc1) *reinterpret_cast<float2*>(a.G + self_off) = make_float2(n0, n1);
-  if (a.accumulate) {
+  if (accum0 || accum1) {
     float2* ap = reinterpret_cast<float2*>(a.A + self_off);
     float2 av = *ap;
-    av.x = __fadd_rn(av.x, n0);
-    av.y = __fadd_rn(av.y, n1);
+    if (accum0) av.x = __fadd_rn(av.x, n0);
+    if (accum1) av.y = __fadd_rn(av.y, n1);
     *ap = av;
   }
 }
 
-// a8: per-realization bond sums of this CTA -> global (fp64 atomics, one per realization).
-__device__ __forceinline__ void energy_epilogue(const SweepArgs& a, int npairs, bool active, int j, float e0,
-                                                float e1) {
-  __shared__ double es[2 * kMaxPairs];
-  for (int t = threadIdx.x; t < 2 * npairs; t += blockDim.x) es[t] = 0.0;
+// Accumulation flags of the realization pair j for this sweep: the fixed window of the
+// last n_avg sweeps, or (adaptive protocol, ARITH §K) each realization's own window
+// (win_lo, win_hi].
+__device__ __forceinline__ void accum_flags(const SweepArgs& a, int j, bool& f0, bool& f1) {
+  if (a.win_lo) {
+    const int s = static_cast<int>(a.sweep);
+    f0 = a.win_lo[2 * j] < s && s <= a.win_hi[2 * j];
+    f1 = a.win_lo[2 * j + 1] < s && s <= a.win_hi[2 * j + 1];
+  } else {
+    f0 = f1 = a.accumulate != 0;
+  }
+}
+
+// a8: per-realization fixed-point bond sums of this CTA -> global int64 atomics, one per
+// realization (exact, so the result does not depend on the order: ARITH §J).
+__device__ __forceinline__ void energy_epilogue(const SweepArgs& a, int npairs, bool active, int j, long long e0,
+                                                long long e1) {
+  __shared__ unsigned long long es[2 * kMaxPairs];
+  for (int t = threadIdx.x; t < 2 * npairs; t += blockDim.x) es[t] = 0ull;
   __syncthreads();
-  if (active && (e0 != 0.0f || e1 != 0.0f)) {
-    atomicAdd(&es[2 * j], static_cast<double>(e0));
-    atomicAdd(&es[2 * j + 1], static_cast<double>(e1));
+  if (active && (e0 != 0 || e1 != 0)) {
+    atomicAdd(&es[2 * j], static_cast<unsigned long long>(e0));
+    atomicAdd(&es[2 * j + 1], static_cast<unsigned long long>(e1));
   }
   __syncthreads();
   for (int t = threadIdx.x; t < 2 * npairs; t += blockDim.x)
-    if (t >= a.r_valid_lo && t < a.r_valid_hi && es[t] != 0.0)
-      atomicAdd(a.energy + static_cast<int64_t>(t) * a.energy_stride, es[t]);
+    if (t >= a.r_valid_lo && t < a.r_valid_hi && es[t] != 0ull)
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.energy + static_cast<int64_t>(t) * a.energy_stride), es[t]);
 }
 
 // Work split: thread tid owns realization pair j = tid % npairs and gap sites
@@ -164,8 +179,15 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   const uint32_t j2 = 2u * static_cast<uint32_t>(sp.j);
   const uint32_t gcount = static_cast<uint32_t>(a.g_count);
   const uint32_t gbegin = static_cast<uint32_t>(a.g_begin);
-  float e0 = 0.0f, e1 = 0.0f;
-  if (sp.active) {
+  long long e0 = 0, e1 = 0;
+  bool accum0 = false, accum1 = false;
+  bool live = sp.active;
+  if (live) {
+    accum_flags(a, sp.j, accum0, accum1);
+    // adaptive protocol: a pair whose two realizations have finished is frozen
+    if (a.win_hi) live = static_cast<int>(a.sweep) <= max(a.win_hi[2 * sp.j], a.win_hi[2 * sp.j + 1]);
+  }
+  if (live) {
     const uint32_t pair = a.pair_base + static_cast<uint32_t>(sp.j);
     for (uint32_t g = sp.g0; g < gcount; g += sp.gstride) {
       const uint32_t gg = gbegin + g;
@@ -198,10 +220,10 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
           nv1[k] = f;
         }
       }
-      process_item<QHALF, ENERGY, BFEXP>(a, rec, cur, nv0, nv1, self_off, pair, e0, e1);
+      process_item<QHALF, ENERGY, BFEXP>(a, rec, cur, nv0, nv1, self_off, pair, e0, e1, accum0, accum1);
     }
   }
-  if (ENERGY) energy_epilogue(a, a.npairs, sp.active, sp.j, e0, e1);
+  if (ENERGY) energy_epilogue(a, a.npairs, sp.active && live, sp.j, e0, e1);
 }
 
 // a6: initial states of a batch (ARITH §G).

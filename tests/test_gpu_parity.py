@@ -86,7 +86,7 @@ def compare(P, z, mask, truth, cfg, calib, M, S, seed, energy=False, exact_pred=
     for k in ("mae", "rmse", "mare"):
         assert abs(sg[k] - so[k]) <= 1e-4 * abs(so[k]) + 1e-12, k
     if energy:
-        assert np.max(np.abs(g["energy"] / o["sim"]["energy"] - 1)) < 1e-5
+        assert_bitwise(g["energy"], o["sim"]["energy"], "energy trace (ARITH §J fixed point)")
     return g, o
 
 
@@ -302,3 +302,39 @@ def test_c4_full_size_sampled(P, calib):
     L = 16384
     wins = [(8190, 8202, 8190, 8202), (0, 10, 16374, 16384), (12000, 12010, 3, 13)]
     _full_size_sampled(P, calib, L, 0.5, "random", 1.5, 10, 30, wins, [0, 9])
+
+
+@pytest.mark.parametrize("init,n_avg", [("block_mean", 1), ("random", 1), ("block_mean", 3)])
+def test_adaptive_equilibration_matches_oracle(P, calib, init, n_avg):
+    """Row f1 (ARITH §K): the per-realization equilibrium sweeps agree exactly
+    with the oracle (exact fixed-point energies + the same fp64 slope test), and so do the
+    predictions (bit-exact for n_avg = 1, within 1e-3 of the range otherwise)."""
+    Tk, ek = calib
+    truth, z, mask = make_problem(48, 0.5, corr_len=6.0)
+    cfg = P.Config(init=init, n_avg=n_avg)
+    m = P.LeMpr(cfg, calib)
+    m.set_data(z, mask)
+    m.estimate_local_params()
+    s_eq = m.simulate_adaptive(6, 11, n_fit=20, n_f=5, max_sweeps=120)
+    pred = m.predict()
+    m.close()
+    oc = ocfg(cfg)
+    p = O.parameters(z, mask, oc, Tk, ek)
+    r = O.simulate_adaptive(p, mask, oc, 6, 11, n_fit=20, n_f=5, S_max=120)
+    assert s_eq.tolist() == r["s_eq"].tolist()
+    ref = O.predict(np.nan_to_num(z), mask, r["acc"], 6, n_avg, p.zmin, p.zmax, 0)
+    if n_avg == 1:
+        assert_bitwise(pred, ref, "adaptive predictions")
+    else:
+        assert np.max(np.abs(pred - ref)) <= 1e-3 * (p.zmax - p.zmin)
+
+
+def test_adaptive_forced_cap(P, calib):
+    """A cap too short for any check sweep forces s_eq = max_sweeps - n_avg (negated)."""
+    truth, z, mask = make_problem(32, 0.5, corr_len=5.0)
+    m = P.LeMpr(P.Config(), calib)
+    m.set_data(z, mask)
+    m.estimate_local_params()
+    s_eq = m.simulate_adaptive(3, 5, n_fit=20, n_f=5, max_sweeps=12)
+    assert s_eq.tolist() == [-11, -11, -11]
+    m.close()

@@ -478,3 +478,60 @@ def test_window_oracle_equals_full_oracle(calib):
             assert np.array_equal(W.T_window(r0, r1, c0, c1), p.T[r0:r1, c0:c1])
             got = W.states(r0, r1, c0, c1, [0, 2], 5, 77)
             assert np.array_equal(got.view(np.uint32), full[[0, 2], r0:r1, c0:c1].view(np.uint32))
+
+
+# --------------------------------------------------- ARITH §J/§K (row f1) pins
+def test_fixed_point_energy_equals_libm_definition():
+    """E_fx (ARITH §J) reproduces the fp64/libm whole-grid energy to cos_spec accuracy."""
+    rng = np.random.default_rng(9)
+    for L in (17, 64):
+        phi = (rng.random((L, L + 3)) * 2 * np.pi).astype(np.float32)
+        e_fx = O.energy_from_fx(O.grid_energy_fx(phi), L + 3, L)
+        assert abs(e_fx - O.grid_specific_energy(phi)) < 4e-7
+    phi = np.full((9, 9), 2.0, np.float32)
+    assert O.energy_from_fx(O.grid_energy_fx(phi), 9, 9) == -1.0
+
+
+def test_equilibrium_test_against_numpy_fit():
+    """The ARITH §K slope test decides like an independent numpy least-squares fit
+    (np.polyfit) wherever the decision is not within rounding of the threshold."""
+    rng = np.random.default_rng(3)
+    assert O.equilibrium_test(np.full(20, -0.93))
+    assert not O.equilibrium_test(-0.9 - 1e-3 * np.arange(20))
+    assert O.equilibrium_test(-0.9 + 1e-3 * np.arange(20))
+    agree = 0
+    for _ in range(400):
+        slope = rng.normal(0, 2e-4)
+        y = -0.95 + slope * np.arange(20) + rng.normal(0, 1e-3, 20)
+        b, a = np.polyfit(np.arange(20), y, 1)
+        tau = 2 * np.sqrt(np.sum((y - a - b * np.arange(20)) ** 2) / 18) / 20
+        if abs(b + tau) < 1e-9:
+            continue
+        assert O.equilibrium_test(y) == (b >= -tau)
+        agree += 1
+    assert agree > 390
+
+
+def test_adaptive_protocol_invariants(calib):
+    """Equilibrium is declared only at check sweeps n_fit + k n_f (first at 25) or at
+    the cap; each realization averages exactly n_avg sweeps (predictions in range); the
+    per-block-average start is not slower than the random start on average."""
+    Tk, ek = calib
+    from inputs.synth import make_problem
+    truth, z, mask = make_problem(40, 0.5, corr_len=6.0)
+    res = {}
+    for init in ("block_mean", "random"):
+        cfg = O.OracleConfig(init=init, n_avg=2)
+        p = O.parameters(z, mask, cfg, Tk, ek)
+        r = O.simulate_adaptive(p, mask, cfg, 6, 21, n_fit=20, n_f=5, S_max=200, energy=True)
+        for s in r["s_eq"]:
+            assert s > 0 and s >= 25 and (s - 20) % 5 == 0
+        pred = O.predict(np.nan_to_num(z), mask, r["acc"], 6, 2, p.zmin, p.zmax, 0)
+        assert pred[mask == 0].min() >= p.zmin and pred[mask == 0].max() <= p.zmax
+        assert np.all(r["energy"][:, 0] > r["energy"][:, 20])  # relaxation toward equilibrium
+        res[init] = r["s_eq"].mean()
+    assert res["block_mean"] <= res["random"]
+    cfg = O.OracleConfig(n_avg=3)
+    p = O.parameters(z, mask, cfg, Tk, ek)
+    r = O.simulate_adaptive(p, mask, cfg, 2, 21, n_fit=20, n_f=5, S_max=15)
+    assert r["s_eq"].tolist() == [-12, -12]
