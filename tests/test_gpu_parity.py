@@ -338,3 +338,18 @@ def test_adaptive_forced_cap(P, calib):
     s_eq = m.simulate_adaptive(3, 5, n_fit=20, n_f=5, max_sweeps=12)
     assert s_eq.tolist() == [-11, -11, -11]
     m.close()
+
+
+@pytest.mark.slow
+def test_sv_mpr_beats_mpr_on_heterogeneous_field(P):
+    """Row f4 (fig:err-p; SPEC acceptance #1): on a field with domains of
+    very different variability, block/site-specific temperatures (BST, SST) predict better
+    than one global temperature (MPR) — paired over random thinnings."""
+    import sys
+    sys.path.insert(0, "scripts")
+    from validate_methods import run
+    rows = run(L=256, K=4, M=10, S=30, ps=(0.85,))
+    r = rows[0]
+    for name in ("BST", "SST"):
+        assert r[f"ratio_AAE_{name}"] < 0.9 and r[f"ratio_RASE_{name}"] < 1.0
+        assert r[f"win_rate_RASE_{name}"] == 1.0
