@@ -123,6 +123,19 @@ mpr_status mpr_simulate(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed);
 mpr_status mpr_simulate_adaptive(mpr_ctx *ctx, int64_t M, uint64_t seed, int32_t n_fit, int32_t n_f,
                                  int32_t max_sweeps, int32_t *s_eq_out);
 
+/* Calibration curve e(T) on the GPU (row f2; the T <-> e relation the energy matching of
+ * PAPER.md:90 inverts, construction deferred to [mz-dth18]; reading R2):
+ * for each of the K increasing temperatures T (host), `reps` replicas of an open L x L
+ * lattice, every site free, start ordered (phi = pi) and run n_eq + n_meas checkerboard
+ * sweeps of symmetric local moves phi' = phi + min(2pi, 3 sqrt T)(2u - 1) (rejected outside
+ * [0, 2pi]; Philox counter (site, sweep, replica, tag 3)); e_raw[k] = mean over replicas
+ * of the mean whole-grid energy (ARITH §J) over the measurement sweeps; e_out (host, K
+ * floats) = its pool-adjacent-violators fit rounded to fp32 and made strictly increasing
+ * (ties split by one ulp) — usable directly as mpr_config.calib_e. e_raw_out nullable.
+ * Uses ctx's device and stream; does not touch the context's problem state. */
+mpr_status mpr_build_calibration(mpr_ctx *ctx, const float *T, int32_t K, int32_t L, float q, int32_t n_eq,
+                                 int32_t n_meas, int32_t reps, uint64_t seed, float *e_out, double *e_raw_out);
+
 /* Multi-rank building block (realization sharding): simulate global realization
  * ids [m_begin, m_end) of an M-realization run and ADD them to the accumulator
  * (reset it first with mpr_reset_accumulator). The result of mpr_predict after all

@@ -665,7 +665,7 @@ double oracle_unconditional_energy(int L, float T, float q, int init_mode, int n
     for (int s = 1; s <= n_eq + n_meas; ++s) {
         if (step > 0.0f) local_sweep(phi, L, 1.0f / T, q, step, (uint32_t)s, m, seed);
         else oracle_sweep(phi, mask, beta, L, L, q, 1.0f, (uint32_t)s, m, seed, 0);
-        double e = oracle_grid_specific_energy(phi, L, L, q);
+        double e = oracle_energy_from_fx(oracle_grid_energy_fx(phi, L, L, q), L, L);  /* ARITH §J */
         if (trace) trace[s - 1] = e;
         if (s > n_eq) sum += e;
     }

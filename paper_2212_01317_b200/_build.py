@@ -8,7 +8,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmpr.so")
-SOURCES = ["api.cu", "params.cu", "sweep.cu"]
+SOURCES = ["api.cu", "params.cu", "sweep.cu", "calib.cu"]
 HEADERS = ["device_math.cuh", "internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -29,7 +29,7 @@ EXPORTED = ["mpr_config_default", "mpr_init", "mpr_destroy", "mpr_last_error", "
             "mpr_simulate_range", "mpr_accumulator_device", "mpr_predict", "mpr_predict_device",
             "mpr_get_info", "mpr_debug_get", "mpr_set_energy_trace", "mpr_set_kernel_timing", "mpr_version",
             "mpr_slab_begin", "mpr_slab_half_sweep", "mpr_slab_row_states", "mpr_slab_end", "mpr_sync",
-            "mpr_simulate_adaptive"]
+            "mpr_simulate_adaptive", "mpr_build_calibration"]
 
 
 class MprError(RuntimeError):
@@ -92,6 +92,8 @@ def load_library(path: str = LIB_PATH):
     L.mpr_sync.argtypes = [vp]; L.mpr_sync.restype = C.c_int
     L.mpr_simulate_adaptive.argtypes = [vp, i64, u64, i32, i32, i32, vp]
     L.mpr_simulate_adaptive.restype = C.c_int
+    L.mpr_build_calibration.argtypes = [vp, vp, i32, i32, C.c_float, i32, i32, i32, u64, vp, vp]
+    L.mpr_build_calibration.restype = C.c_int
     L.mpr_version.argtypes = []; L.mpr_version.restype = C.c_char_p
     _lib = L
     return L
@@ -211,6 +213,16 @@ def mpr_slab_end(ctx) -> None:
 
 def mpr_sync(ctx) -> None:
     _check(ctx, load_library().mpr_sync(ctx))
+
+
+def mpr_build_calibration(ctx, T, L=128, q=0.5, n_eq=400, n_meas=800, reps=2, seed=20221202):
+    """Row f2: e(T) table on the GPU (defaults = scripts/make_calibration.py). Returns (e, e_raw)."""
+    T = np.ascontiguousarray(T, np.float32)
+    e = np.zeros(len(T), np.float32)
+    raw = np.zeros(len(T), np.float64)
+    _check(ctx, load_library().mpr_build_calibration(ctx, T.ctypes.data, len(T), L, q, n_eq, n_meas, reps, seed,
+                                                     e.ctypes.data, raw.ctypes.data))
+    return e, raw
 
 
 def mpr_simulate_adaptive(ctx, M, seed, n_fit=20, n_f=5, max_sweeps=500) -> np.ndarray:

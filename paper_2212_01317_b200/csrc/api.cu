@@ -895,6 +895,63 @@ mpr_status mpr_sync(mpr_ctx* c) {
   return MPR_OK;
 }
 
+mpr_status mpr_build_calibration(mpr_ctx* c, const float* T, int32_t K, int32_t L, float q, int32_t n_eq,
+                                 int32_t n_meas, int32_t reps, uint64_t seed, float* e_out, double* e_raw_out) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (!T || !e_out || K < 2 || L < 2 || n_eq < 0 || n_meas < 1 || reps < 1 || !(q > 0.0f && q <= 0.5f))
+    return fail(c, MPR_ERR_INVALID_ARG, "bad calibration arguments");
+  for (int k = 0; k < K; ++k)
+    if (!(T[k] > 0.0f) || !std::isfinite(T[k]) || (k > 0 && !(T[k] > T[k - 1])))
+      return fail(c, MPR_ERR_INVALID_ARG, "calibration temperatures must be positive and increasing");
+  CK(cudaSetDevice(c->device), "set device");
+  const int nlat = K * reps, S = n_eq + n_meas;
+  std::vector<long long> fx(static_cast<size_t>(nlat) * S);
+  CK(run_calibration(T, K, L, q, n_eq, n_meas, reps, seed, fx.data(), c->stream), "calibration sweeps");
+  // mean energy of each lattice over the measurement sweeps, then over replicas (fp64,
+  // in sweep / replica order)
+  const double nb = static_cast<double>(2 * static_cast<int64_t>(L) * L - L - L);
+  std::vector<double> raw(static_cast<size_t>(K));
+  for (int k = 0; k < K; ++k) {
+    double rsum = 0.0;
+    for (int r = 0; r < reps; ++r) {
+      double sum = 0.0;
+      for (int s = n_eq + 1; s <= S; ++s) {
+        const long long E = fx[static_cast<size_t>(s - 1) * nlat + k * reps + r];
+        sum = sum + (-static_cast<double>(E) * 0x1p-32) / nb;
+      }
+      rsum = rsum + sum / static_cast<double>(n_meas);
+    }
+    raw[k] = rsum / static_cast<double>(reps);
+  }
+  // pool adjacent violators (non-decreasing), then strictly increasing in fp32
+  std::vector<double> val, wt;
+  std::vector<int> len;
+  for (int k = 0; k < K; ++k) {
+    val.push_back(raw[k]);
+    wt.push_back(1.0);
+    len.push_back(1);
+    while (val.size() > 1 && val[val.size() - 2] > val.back()) {
+      const double v2 = val.back(), w2 = wt.back();
+      const int l2 = len.back();
+      val.pop_back(); wt.pop_back(); len.pop_back();
+      const double v1 = val.back(), w1 = wt.back();
+      const int l1 = len.back();
+      val.pop_back(); wt.pop_back(); len.pop_back();
+      val.push_back((v1 * w1 + v2 * w2) / (w1 + w2));
+      wt.push_back(w1 + w2);
+      len.push_back(l1 + l2);
+    }
+  }
+  int k = 0;
+  for (size_t b = 0; b < val.size(); ++b)
+    for (int t = 0; t < len[b]; ++t) e_out[k++] = static_cast<float>(val[b]);
+  for (k = 1; k < K; ++k)
+    if (e_out[k] <= e_out[k - 1]) e_out[k] = std::nextafter(e_out[k - 1], 1.0f);
+  if (e_raw_out)
+    for (k = 0; k < K; ++k) e_raw_out[k] = raw[k];
+  return MPR_OK;
+}
+
 mpr_status mpr_accumulator_device(mpr_ctx* c, double** acc_dev, int64_t* n) {
   if (!c || !acc_dev || !n) return MPR_ERR_INVALID_ARG;
   if (c->stage < ST_PARAMS || !c->acc.p) return fail(c, MPR_ERR_STATE, "no accumulator yet");

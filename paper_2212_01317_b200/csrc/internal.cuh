@@ -104,4 +104,10 @@ void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R,
 void launch_acc_reduce(const float* X, int64_t g_begin, int64_t g_count, int R, int r_lo, int r_hi,
                        double* acc, cudaStream_t st);
 
+// ---- calib.cu (row f2) ----
+// Sweeps K*reps unconditional lattices (n_eq + n_meas sweeps); fx_host receives the
+// fixed-point energy of lattice l = k*reps + rep after sweep s at [(s-1)*K*reps + l].
+cudaError_t run_calibration(const float* T_host, int K, int L, float q, int n_eq, int n_meas, int reps,
+                            uint64_t seed, long long* fx_host, cudaStream_t st);
+
 }  // namespace mpr

@@ -277,6 +277,9 @@ static void* sweep_kernel_ptr(int variant) {
     case 2: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, false>);
     case 6: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 128, false>);
     case 7: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 128, true>);
+    case 8: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 2, 256, true>);
+    case 9: return reinterpret_cast<void*>(k_sweep_half<Q, E, 5, 2, 256, true>);
+    case 10: return reinterpret_cast<void*>(k_sweep_half<Q, E, 3, 2, 256, true>);
     default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true>);  // 5
   }
 }

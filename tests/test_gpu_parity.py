@@ -353,3 +353,18 @@ def test_sv_mpr_beats_mpr_on_heterogeneous_field(P):
     for name in ("BST", "SST"):
         assert r[f"ratio_AAE_{name}"] < 0.9 and r[f"ratio_RASE_{name}"] < 1.0
         assert r[f"win_rate_RASE_{name}"] == 1.0
+
+
+@pytest.mark.slow
+def test_gpu_calibration_table_equals_shipped(P, calib):
+    """Row f2: the e(T) table built on the GPU with the recipe of scripts/make_calibration.py
+    is bit-identical to the shipped table the oracle wrote (same chains, exact fixed-point
+    energies, same averaging and monotone fit)."""
+    Tk, ek = calib
+    m = P.LeMpr(P.Config(), calib)
+    e, raw = P.mpr_build_calibration(m.ctx, Tk, L=128, q=0.5, n_eq=400, n_meas=800, reps=2, seed=20221202)
+    m.close()
+    assert_bitwise(e, ek, "GPU calibration table")
+    # and it is a valid table: strictly increasing, harmonic at low T
+    assert np.all(np.diff(e) > 0)
+    assert abs(e[0] - (-1 + Tk[0] * 129 / 512)) < 3e-6
