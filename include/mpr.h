@@ -66,7 +66,14 @@ typedef struct {
   const float *calib_e;  /* e_k = e(T_k), strictly increasing (host pointers, copied)  */
   int calib_n;           /* K >= 2                                                     */
   int64_t max_batch;     /* max realizations simulated concurrently (0 => automatic)  */
+  int order;             /* mpr_order: update order of a sweep (ARITH §H)              */
 } mpr_config;
+
+/* MPR_ORDER_SC: single checkerboard, colour A then B.
+ * MPR_ORDER_DC: double checkerboard (row f3): even l_b-tiles (A, B),
+ * then odd tiles (A, B). DC supports mpr_simulate / mpr_simulate_range only (the fused
+ * energy trace, the adaptive protocol and row slabs need the SC order: INVALID_ARG). */
+typedef enum { MPR_ORDER_SC = 0, MPR_ORDER_DC = 1 } mpr_order;
 
 /* Fill *cfg with the defaults above (calibration pointers NULL: the caller must set
  * them; the Python binding loads the shipped table). */

@@ -421,6 +421,26 @@ int64_t oracle_sweep(float *phi, const uint8_t *mask, const float *beta, int Lx,
     return acc;
 }
 
+/* Double-checkerboard sweep (row f3; "first only the even (odd) numbered
+ * tiles are updated in parallel and then only the odd (even) tiles", tiles = the l_b x l_b
+ * blocks of the temperature estimate): phases (even tiles, A), (even tiles, B),
+ * (odd tiles, A), (odd tiles, B); tile parity = (r/l_b + c/l_b) mod 2 (ARITH §H). */
+int64_t oracle_sweep_dc(float *phi, const uint8_t *mask, const float *beta, int Lx, int Ly, float q,
+                        float J, uint32_t sweep, int64_t m, uint64_t seed, int lb)
+{
+    int64_t acc = 0;
+    for (int tile = 0; tile < 2; ++tile)
+        for (int colour = 0; colour < 2; ++colour)
+            for (int r = 0; r < Ly; ++r)
+                for (int c = 0; c < Lx; ++c) {
+                    int64_t i = (int64_t)r * Lx + c;
+                    if (((r + c) & 1) != colour || mask[i]) continue;
+                    if (((r / lb + c / lb) & 1) != tile) continue;
+                    acc += update_site(phi, Lx, Ly, r, c, beta[i], q, J, sweep, m, seed);
+                }
+    return acc;
+}
+
 /* One colour half of sweep `sweep` restricted to rows [r0, r1) (a row slab of the
  * checkerboard update): the gap sites of that colour in those rows, in row-major
  * order. Returns #accepted. */
@@ -458,6 +478,7 @@ int64_t oracle_run_chain(float *phi, const uint8_t *mask, const float *beta, int
 typedef struct {
     float q, J;
     int lb, rs, ns, init_mode, n_avg;
+    int order;  /* 0 = single checkerboard (SC), 1 = double checkerboard (DC, row f3) */
 } oracle_cfg;
 
 /* Parameter stage (a1-a5): transform, block stats, block T, median, expand, smooth,
@@ -509,7 +530,9 @@ void oracle_simulate(const float *phi0, const uint8_t *mask, const float *beta, 
         memcpy(phi, phi0, sizeof(float) * (size_t)n);
         oracle_init(phi, mask, Lx, Ly, cfg->lb, SP, NK, cfg->init_mode, m, seed);
         for (int s = 1; s <= S; ++s) {
-            nacc += oracle_sweep(phi, mask, beta, Lx, Ly, cfg->q, cfg->J, (uint32_t)s, m, seed, 0);
+            nacc += cfg->order == 1
+                        ? oracle_sweep_dc(phi, mask, beta, Lx, Ly, cfg->q, cfg->J, (uint32_t)s, m, seed, cfg->lb)
+                        : oracle_sweep(phi, mask, beta, Lx, Ly, cfg->q, cfg->J, (uint32_t)s, m, seed, 0);
             if (s > S - cfg->n_avg)
                 for (int64_t i = 0; i < n; ++i)
                     if (!mask[i]) acc[i] += (double)phi[i];
@@ -587,7 +610,10 @@ void oracle_simulate_adaptive(const float *phi0, const uint8_t *mask, const floa
         oracle_init(phi, mask, Lx, Ly, cfg->lb, SP, NK, cfg->init_mode, m, seed);
         int eq = 0, stop = S_max;
         for (int s = 1; s <= stop; ++s) {
-            oracle_sweep(phi, mask, beta, Lx, Ly, cfg->q, cfg->J, (uint32_t)s, m, seed, 0);
+            if (cfg->order == 1)
+                oracle_sweep_dc(phi, mask, beta, Lx, Ly, cfg->q, cfg->J, (uint32_t)s, m, seed, cfg->lb);
+            else
+                oracle_sweep(phi, mask, beta, Lx, Ly, cfg->q, cfg->J, (uint32_t)s, m, seed, 0);
             e[s] = oracle_energy_from_fx(oracle_grid_energy_fx(phi, Lx, Ly, cfg->q), Lx, Ly);
             if (energy) energy[(m - m_begin) * S_max + (s - 1)] = e[s];
             if (eq) {

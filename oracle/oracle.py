@@ -50,7 +50,7 @@ _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 
 class _Cfg(C.Structure):
     _fields_ = [("q", C.c_float), ("J", C.c_float), ("lb", C.c_int), ("rs", C.c_int),
-                ("ns", C.c_int), ("init_mode", C.c_int), ("n_avg", C.c_int)]
+                ("ns", C.c_int), ("init_mode", C.c_int), ("n_avg", C.c_int), ("order", C.c_int)]
 
 
 def _declare(L):
@@ -91,6 +91,9 @@ def _declare(L):
     L.oracle_half_sweep_rows.argtypes = [_f32p, _u8p, _f32p, C.c_int, C.c_int, C.c_float, C.c_float, C.c_uint32,
                                          C.c_int64, C.c_uint64, C.c_int, C.c_int, C.c_int]
     L.oracle_half_sweep_rows.restype = C.c_int64
+    L.oracle_sweep_dc.argtypes = [_f32p, _u8p, _f32p, C.c_int, C.c_int, C.c_float, C.c_float, C.c_uint32,
+                                  C.c_int64, C.c_uint64, C.c_int]
+    L.oracle_sweep_dc.restype = C.c_int64
     L.oracle_simulate_window.argtypes = [_f32p, _u8p, _f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.c_int, _i64p, _i64p, C.c_int, C.c_float, C.c_float, C.c_int64,
                                          C.c_int, C.c_uint64, _f32p]
@@ -253,6 +256,14 @@ def run_chain(phi, mask, beta, s_begin, s_end, m=0, seed=1, q=0.5, J=1.0):
     return sp, n
 
 
+def sweep_dc(phi, mask, beta, sweep_index, m, seed, lb, q=0.5, J=1.0) -> int:
+    """One double-checkerboard sweep in place (row f3, ARITH §H). Returns #accepted."""
+    assert phi.dtype == np.float32 and phi.flags.c_contiguous
+    mask = np.ascontiguousarray(mask, np.uint8); beta = np.ascontiguousarray(beta, np.float32)
+    return lib().oracle_sweep_dc(phi.ravel(), mask.ravel(), beta.ravel(), phi.shape[1], phi.shape[0], float(q),
+                                 float(J), int(sweep_index), int(m), int(seed), int(lb))
+
+
 def half_sweep_rows(phi, mask, beta, sweep, m, seed, colour, r0, r1, q=0.5, J=1.0) -> int:
     """Colour half of one checkerboard sweep over rows [r0, r1) only (row slab), in place."""
     assert phi.dtype == np.float32 and phi.flags.c_contiguous
@@ -310,7 +321,8 @@ def simulate_adaptive(params, mask, cfg, M, seed, n_fit=20, n_f=5, S_max=500, m_
     s_eq = np.zeros(R, np.int32)
     en = np.zeros(R * S_max, np.float64) if energy else None
     ph = np.zeros(R * Lx * Ly, np.float32) if states else None
-    c = _Cfg(cfg.q, cfg.J, cfg.lb, cfg.rs, cfg.ns, 0 if cfg.init == "block_mean" else 1, cfg.n_avg)
+    c = _Cfg(cfg.q, cfg.J, cfg.lb, cfg.rs, cfg.ns, 0 if cfg.init == "block_mean" else 1, cfg.n_avg,
+             1 if cfg.order == "dc" else 0)
     lib().oracle_simulate_adaptive(params.phi0.ravel(), mask.ravel(), params.beta.ravel(), Lx, Ly, C.byref(c),
                                    params.SP.ravel(), params.NK.ravel(), int(m_begin), int(m_end), int(n_fit),
                                    int(n_f), int(S_max), int(seed), acc, s_eq,
@@ -329,6 +341,7 @@ class OracleConfig:
     ns: int = 5
     init: str = "block_mean"   # or "random"
     n_avg: int = 1
+    order: str = "sc"          # "sc" single checkerboard, "dc" double checkerboard (row f3)
 
 
 @dataclass
@@ -355,7 +368,8 @@ def parameters(z, mask, cfg: OracleConfig, Tk, ek) -> OracleParams:
     SP = np.zeros(nby * nbx, np.int64); NK = np.zeros(nby * nbx, np.int64)
     Tb = np.zeros(nby * nbx, np.float32)
     lo, hi = C.c_float(), C.c_float()
-    c = _Cfg(cfg.q, cfg.J, cfg.lb, cfg.rs, cfg.ns, 0 if cfg.init == "block_mean" else 1, cfg.n_avg)
+    c = _Cfg(cfg.q, cfg.J, cfg.lb, cfg.rs, cfg.ns, 0 if cfg.init == "block_mean" else 1, cfg.n_avg,
+             1 if cfg.order == "dc" else 0)
     st = lib().oracle_parameters(np.where(mask != 0, z, np.float32(0)).astype(np.float32).ravel(),
                                  mask.ravel(), Lx, Ly, C.byref(c),
                                  np.ascontiguousarray(Tk, np.float32), np.ascontiguousarray(ek, np.float32),
@@ -376,7 +390,8 @@ def simulate(params: OracleParams, mask, cfg: OracleConfig, M, S, seed, m_begin=
     en = np.zeros(R * S, np.float64) if energy else None
     ph = np.zeros(R * Lx * Ly, np.float32) if states else None
     nacc = C.c_int64()
-    c = _Cfg(cfg.q, cfg.J, cfg.lb, cfg.rs, cfg.ns, 0 if cfg.init == "block_mean" else 1, cfg.n_avg)
+    c = _Cfg(cfg.q, cfg.J, cfg.lb, cfg.rs, cfg.ns, 0 if cfg.init == "block_mean" else 1, cfg.n_avg,
+             1 if cfg.order == "dc" else 0)
     lib().oracle_simulate(params.phi0.ravel(), mask.ravel(), params.beta.ravel(), Lx, Ly, C.byref(c),
                           params.SP.ravel(), params.NK.ravel(), int(m_begin), int(m_end), int(S),
                           int(seed), acc, en.ctypes.data if energy else None,

@@ -42,7 +42,7 @@ class mpr_config(C.Structure):
     _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("J", C.c_float), ("q", C.c_float),
                 ("l_b", C.c_int), ("r_s", C.c_int), ("n_s", C.c_int), ("init", C.c_int),
                 ("n_avg", C.c_int), ("calib_T", C.POINTER(C.c_float)), ("calib_e", C.POINTER(C.c_float)),
-                ("calib_n", C.c_int), ("max_batch", C.c_int64)]
+                ("calib_n", C.c_int), ("max_batch", C.c_int64), ("order", C.c_int)]
 
 
 class mpr_info(C.Structure):
@@ -263,6 +263,7 @@ class Config:
     n_avg: int = 1
     device: int = 0
     max_batch: int = 0
+    order: str = "sc"   # "sc" single checkerboard, "dc" double checkerboard (row f3)
 
 
 class LeMpr:
@@ -278,6 +279,7 @@ class LeMpr:
         c.device, c.J, c.q, c.l_b, c.r_s, c.n_s = cfg.device, cfg.J, cfg.q, cfg.l_b, cfg.r_s, cfg.n_s
         c.init = MPR_INIT_BLOCK_MEAN if cfg.init == "block_mean" else MPR_INIT_RANDOM
         c.n_avg, c.max_batch = cfg.n_avg, cfg.max_batch
+        c.order = 1 if cfg.order == "dc" else 0
         c.stream = stream
         c.calib_T = self._T.ctypes.data_as(C.POINTER(C.c_float))
         c.calib_e = self._e.ctypes.data_as(C.POINTER(C.c_float))

@@ -52,7 +52,7 @@ struct BatchKey {
   uint32_t pair_base;
   int32_t sweeps;
   uint32_t k0, k1;
-  int n_avg, init, r_lo, r_hi, timing, variant;
+  int n_avg, init, r_lo, r_hi, timing, variant, order;
   float q, J;
   void *G, *A, *rec, *acc;
   long long* energy;
@@ -107,7 +107,8 @@ struct mpr_ctx {
   std::vector<int> rowoff_h;  // host copy of the gap-id row offsets (2*Ly)
   // device memory
   DBuf z, mask, phiK, scal, calTd, caled, rowcnt, rowoff, gid, rec, bstats, Tb, T, T2, G, A, acc,
-      energy, out, tmp, win;
+      energy, out, tmp, win, dclist, dccnt;
+  int64_t dc_off[5] = {0, 0, 0, 0, 0};  // DC phase segments of dclist (row f3)
   DevScalars* hsc = nullptr;  // pinned host mirror of the device scalars
 };
 
@@ -155,6 +156,7 @@ mpr_status validate_cfg(const mpr_config* cfg, std::string& why) {
   if (cfg->init != MPR_INIT_BLOCK_MEAN && cfg->init != MPR_INIT_RANDOM) { why = "init must be BLOCK_MEAN or RANDOM"; return MPR_ERR_INVALID_ARG; }
   if (cfg->n_avg < 1) { why = "n_avg must be >= 1"; return MPR_ERR_INVALID_ARG; }
   if (cfg->max_batch < 0) { why = "max_batch must be >= 0"; return MPR_ERR_INVALID_ARG; }
+  if (cfg->order != MPR_ORDER_SC && cfg->order != MPR_ORDER_DC) { why = "order must be SC or DC"; return MPR_ERR_INVALID_ARG; }
   if (!cfg->calib_T || !cfg->calib_e || cfg->calib_n < 2 || cfg->calib_n > 256) {
     why = "calibration table must have 2..256 points";
     return MPR_ERR_INVALID_ARG;
@@ -369,7 +371,7 @@ void mpr_destroy(mpr_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   DBuf* bufs[] = {&c->z, &c->mask, &c->phiK, &c->scal, &c->calTd, &c->caled, &c->rowcnt, &c->rowoff,
                   &c->gid, &c->rec, &c->bstats, &c->Tb, &c->T, &c->T2, &c->G, &c->A, &c->acc,
-                  &c->energy, &c->out, &c->tmp, &c->win};
+                  &c->energy, &c->out, &c->tmp, &c->win, &c->dclist, &c->dccnt};
   for (DBuf* b : bufs) b->release();
   if (c->hsc) cudaFreeHost(c->hsc);
   for (auto& e : c->graphs)
@@ -455,6 +457,26 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   c->sum_SB_fx = c->hsc->sum_SB;
   if (c->hsc->n_avail == 0 && !c->degenerate)
     return fail(c, MPR_ERR_NO_SAMPLE_BONDS, "no block has a sample-sample bond (PAPER.md:108)");
+  if (c->cfg.order == MPR_ORDER_DC && c->P > 0) {
+    // phase lists of the double checkerboard (row f3): count, offsets, scatter
+    CK(c->dccnt.ensure(4 * sizeof(unsigned long long)), "alloc dc counts");
+    CK(c->dclist.ensure(sizeof(uint32_t) * c->P), "alloc dc list");
+    unsigned long long cnt[4];
+    launch_dc_count(c->rec.as<GapRec>(), c->P, c->Lx, lb, c->dccnt.as<unsigned long long>(), st);
+    CKL("dc_count");
+    CK(cudaMemcpyAsync(cnt, c->dccnt.p, sizeof cnt, cudaMemcpyDeviceToHost, st), "D2H dc counts");
+    CK(cudaStreamSynchronize(st), "dc sync");
+    c->dc_off[0] = 0;
+    for (int p = 0; p < 4; ++p) c->dc_off[p + 1] = c->dc_off[p] + static_cast<int64_t>(cnt[p]);
+    unsigned long long cur[4] = {0, static_cast<unsigned long long>(c->dc_off[1]),
+                                 static_cast<unsigned long long>(c->dc_off[2]),
+                                 static_cast<unsigned long long>(c->dc_off[3])};
+    CK(cudaMemcpyAsync(c->dccnt.p, cur, sizeof cur, cudaMemcpyHostToDevice, st), "H2D dc cursors");
+    launch_dc_scatter(c->rec.as<GapRec>(), c->P, c->Lx, lb, c->dccnt.as<unsigned long long>(),
+                      c->dclist.as<uint32_t>(), st);
+    CKL("dc_scatter");
+    CK(cudaStreamSynchronize(st), "dc sync");
+  }
   c->stage = ST_PARAMS;
   c->M_total = 0;
   return MPR_OK;
@@ -518,10 +540,20 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
     a.sweep = static_cast<uint32_t>(s);
     a.accumulate = avg && (s > k.sweeps - k.n_avg);
     a.energy = k.energy ? k.energy + (s - 1) : nullptr;
-    for (int colour = 0; colour < 2; ++colour) {
+    // SC: colour A then B (contiguous gap-id ranges); DC: (even tiles A, B), (odd tiles A, B)
+    const int nphase = k.order == MPR_ORDER_DC ? 4 : 2;
+    for (int ph = 0; ph < nphase; ++ph) {
+      const int colour = ph & 1;
       a.is_b = colour;
-      a.g_begin = colour ? k.PA : 0;
-      a.g_count = colour ? k.P - k.PA : k.PA;
+      if (k.order == MPR_ORDER_DC) {
+        a.glist = c->dclist.as<uint32_t>() + c->dc_off[ph];
+        a.g_begin = 0;
+        a.g_count = c->dc_off[ph + 1] - c->dc_off[ph];
+      } else {
+        a.glist = nullptr;
+        a.g_begin = colour ? k.PA : 0;
+        a.g_count = colour ? k.P - k.PA : k.PA;
+      }
       if (a.g_count > 0) {
         launch_sweep_half(a, c->sweep_grid, k.variant, st);
         CKL("sweep_half");
@@ -555,6 +587,8 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
   c->sweeps = sweeps;
   c->launches = 0;
   const uint32_t k0 = static_cast<uint32_t>(seed & 0xffffffffu), k1 = static_cast<uint32_t>(seed >> 32);
+  if (c->energy_enabled && c->cfg.order != MPR_ORDER_SC)
+    return fail(c, MPR_ERR_INVALID_ARG, "the fused energy trace needs the SC order");
   if (c->energy_enabled) {
     if (c->energy_M != M || c->energy_S != sweeps) {
       CK(c->energy.ensure(sizeof(long long) * M * sweeps), "alloc energy");
@@ -587,6 +621,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
     key.P = c->P; key.PA = c->PA; key.Rb = Rb; key.pair_base = pair_base; key.sweeps = sweeps;
     key.k0 = k0; key.k1 = k1; key.n_avg = c->cfg.n_avg; key.init = c->cfg.init; key.r_lo = r_lo; key.r_hi = r_hi;
     key.timing = c->timing; key.variant = c->sweep_variant; key.q = c->cfg.q; key.J = c->cfg.J;
+    key.order = c->cfg.order;
     key.G = c->G.p; key.A = c->A.p; key.rec = c->rec.p; key.acc = c->acc.p;
     key.energy = c->energy_enabled ? c->energy.as<long long>() + mb * sweeps : nullptr;
     int64_t nsweep_launch = 0;
@@ -655,6 +690,8 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
   const int n_avg = c->cfg.n_avg;
   if (M < 1 || n_fit < 3 || n_f < 1 || max_sweeps < n_avg + 1 || M >= (int64_t(1) << 32))
     return fail(c, MPR_ERR_INVALID_ARG, "need M >= 1, n_fit >= 3, n_f >= 1, max_sweeps > n_avg");
+  if (c->cfg.order != MPR_ORDER_SC)
+    return fail(c, MPR_ERR_INVALID_ARG, "the adaptive protocol needs the SC order (fused energy)");
   mpr_status st0 = mpr_reset_accumulator(c);
   if (st0 != MPR_OK) return st0;
   CK(cudaSetDevice(c->device), "set device");
@@ -783,6 +820,7 @@ mpr_status mpr_slab_begin(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed, 
   if (m_begin < 0 || m_end > M || m_begin >= m_end) return fail(c, MPR_ERR_INVALID_ARG, "bad realization range");
   if (row_begin < 0 || row_end > c->Ly || row_begin >= row_end) return fail(c, MPR_ERR_INVALID_ARG, "bad row range");
   if (c->energy_enabled) return fail(c, MPR_ERR_INVALID_ARG, "energy trace is not supported in slab mode");
+  if (c->cfg.order != MPR_ORDER_SC) return fail(c, MPR_ERR_INVALID_ARG, "slab mode needs the SC order");
   if (!c->acc.p) {
     mpr_status s = mpr_reset_accumulator(c);
     if (s != MPR_OK) return s;

@@ -74,13 +74,20 @@ void launch_scatter_state(const float* phiK, const int32_t* gid, const float* G,
 void launch_scatter_acc(const int32_t* gid, const double* acc, int64_t n, double* out,
                         cudaStream_t st);
 
+// double-checkerboard phase lists (row f3): counts per phase (2*tile parity + colour),
+// then a scatter of the gap ids into [cursor[p], ...) segments of `list`
+void launch_dc_count(const GapRec* rec, int64_t P, int64_t Lx, int lb, unsigned long long* cnt, cudaStream_t st);
+void launch_dc_scatter(const GapRec* rec, int64_t P, int64_t Lx, int lb, unsigned long long* cursor,
+                       uint32_t* list, cudaStream_t st);
+
 // ---- launchers (sweep.cu) ----
 struct SweepArgs {
   const GapRec* rec;
   float* G;          // state, [P][R] floats (gap-site major, realization minor)
   float* A;          // accumulator of the last n_avg sweeps, same layout (nullable)
   int64_t g_begin;   // first gap id of this colour
-  int64_t g_count;   // gap sites of this colour
+  int64_t g_count;   // gap sites of this colour (or of the list)
+  const uint32_t* glist;  // nullable: gap ids of this phase (DC order), else the range
   int R;             // realization stride of the batch (even)
   int npairs;        // realization pairs in the batch
   uint32_t pair_base;// global pair index of pair 0 (= m_base / 2)

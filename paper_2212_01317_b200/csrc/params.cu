@@ -642,4 +642,52 @@ void launch_scatter_acc(const int32_t* gid, const double* acc, int64_t n, double
   k_scatter_acc<<<grid_for(n, 256), 256, 0, st>>>(gid, acc, n, out);
 }
 
+// ---- double-checkerboard phase lists (row f3, ARITH §H): phase = 2*tile parity + colour
+namespace {
+__device__ __forceinline__ int dc_phase(uint32_t site, int64_t Lx, int lb) {
+  const int64_t r = site / Lx, c = site - r * Lx;
+  return static_cast<int>((((r / lb) + (c / lb)) & 1) * 2 + ((r + c) & 1));
+}
+
+__global__ void k_dc_count(const GapRec* __restrict__ rec, int64_t P, int64_t Lx, int lb,
+                           unsigned long long* __restrict__ cnt) {
+  unsigned long long c[4] = {0, 0, 0, 0};
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < P; g += (int64_t)gridDim.x * blockDim.x)
+    ++c[dc_phase(rec[g].site, Lx, lb)];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const unsigned long long v = warp_sum_ull(c[k]);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&cnt[k], v);
+  }
+}
+
+// Scatter gap ids into their phase segment; warp-aggregated cursors keep a warp's ids in
+// order (coalesced state access in the sweep). The order inside a phase is free.
+__global__ void k_dc_scatter(const GapRec* __restrict__ rec, int64_t P, int64_t Lx, int lb,
+                             unsigned long long* __restrict__ cursor, uint32_t* __restrict__ list) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < P; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = base + threadIdx.x;
+    const bool in = g < P;
+    const int ph = in ? dc_phase(rec[g].site, Lx, lb) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, ph);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long pos = 0;
+    if (in && lane == leader) pos = atomicAdd(&cursor[ph], static_cast<unsigned long long>(__popc(peers)));
+    pos = __shfl_sync(0xffffffffu, pos, leader);
+    if (in) list[pos + __popc(peers & ((1u << lane) - 1u))] = static_cast<uint32_t>(g);
+  }
+}
+}  // namespace
+
+void launch_dc_count(const GapRec* rec, int64_t P, int64_t Lx, int lb, unsigned long long* cnt, cudaStream_t st) {
+  cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), st);
+  if (P > 0) k_dc_count<<<grid_for(P, 256), 256, 0, st>>>(rec, P, Lx, lb, cnt);
+}
+
+void launch_dc_scatter(const GapRec* rec, int64_t P, int64_t Lx, int lb, unsigned long long* cursor,
+                       uint32_t* list, cudaStream_t st) {
+  if (P > 0) k_dc_scatter<<<grid_for(P, 256), 256, 0, st>>>(rec, P, Lx, lb, cursor, list);
+}
+
 }  // namespace mpr

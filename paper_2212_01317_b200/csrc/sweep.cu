@@ -190,11 +190,12 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   if (live) {
     const uint32_t pair = a.pair_base + static_cast<uint32_t>(sp.j);
     for (uint32_t g = sp.g0; g < gcount; g += sp.gstride) {
-      const uint32_t gg = gbegin + g;
+      // DC order (row f3): the phase's gap ids come from a list; SC: a contiguous range
+      const uint32_t gg = a.glist ? a.glist[g] : gbegin + g;
       const GapRec rec = a.rec[gg];
       const uint32_t self_off = gg * R + j2;
       const float2 cur = *reinterpret_cast<const float2*>(a.G + self_off);
-      if (PF) {
+      if (PF && !a.glist) {
         const uint32_t gn = gg + sp.gstride;
         if (gn < gbegin + gcount) {
           if (PF == 1) {

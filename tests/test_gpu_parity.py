@@ -58,7 +58,8 @@ def gpu_run(P, z, mask, cfg, calib, M, S, seed, energy=False):
 
 
 def ocfg(cfg):
-    return O.OracleConfig(q=cfg.q, J=cfg.J, lb=cfg.l_b, rs=cfg.r_s, ns=cfg.n_s, init=cfg.init, n_avg=cfg.n_avg)
+    return O.OracleConfig(q=cfg.q, J=cfg.J, lb=cfg.l_b, rs=cfg.r_s, ns=cfg.n_s, init=cfg.init, n_avg=cfg.n_avg,
+                          order=cfg.order)
 
 
 def compare(P, z, mask, truth, cfg, calib, M, S, seed, energy=False, exact_pred=True):
@@ -368,3 +369,24 @@ def test_gpu_calibration_table_equals_shipped(P, calib):
     # and it is a valid table: strictly increasing, harmonic at low T
     assert np.all(np.diff(e) > 0)
     assert abs(e[0] - (-1 + Tk[0] * 129 / 512)) < 3e-6
+
+
+@pytest.mark.parametrize("lb", [8, 2])
+def test_dc_order_bit_exact(P, calib, lb):
+    """Row f3: double-checkerboard update order (even tiles A, B; odd tiles A, B), states and
+    predictions bit-exact vs the oracle."""
+    truth, z, mask = make_problem(52, 0.5, Lx=47, corr_len=6.0)
+    compare(P, z, mask, truth, P.Config(l_b=lb, order="dc", n_s=1, r_s=1), calib, 6, 12, 31)
+
+
+def test_dc_rejects_sc_only_features(P, calib):
+    truth, z, mask = make_problem(32, 0.5, corr_len=5.0)
+    m = P.LeMpr(P.Config(order="dc", l_b=8), calib)
+    m.set_data(z, mask)
+    m.estimate_local_params()
+    with pytest.raises(P.MprError):
+        m.simulate_adaptive(2, 1, max_sweeps=40)
+    m.set_energy_trace(True)
+    with pytest.raises(P.MprError):
+        m.simulate(2, 3, 1)
+    m.close()

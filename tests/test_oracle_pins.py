@@ -535,3 +535,51 @@ def test_adaptive_protocol_invariants(calib):
     p = O.parameters(z, mask, cfg, Tk, ek)
     r = O.simulate_adaptive(p, mask, cfg, 2, 21, n_fit=20, n_f=5, S_max=15)
     assert r["s_eq"].tolist() == [-12, -12]
+
+
+# ------------------------------------------------------ row f3: double checkerboard
+def test_dc_with_one_tile_is_sc():
+    """With a single tile (l_b >= L) the DC sweep is the SC sweep, bit for bit."""
+    rng = np.random.default_rng(12)
+    phi = (rng.random((14, 11)) * 2 * np.pi).astype(np.float32)
+    mask = (rng.random((14, 11)) > 0.5).astype(np.uint8)
+    beta = (rng.random((14, 11)) * 30 + 1).astype(np.float32)
+    a, b = phi.copy(), phi.copy()
+    for s in range(1, 6):
+        O.sweep(a, mask, beta, s, 4, 9)
+        O.sweep_dc(b, mask, beta, s, 4, 9, lb=64)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    c = phi.copy()
+    for s in range(1, 6):
+        O.sweep_dc(c, mask, beta, s, 4, 9, lb=2)
+    assert not np.array_equal(a, c)  # with several tiles the order (and chain) differs
+
+
+@pytest.mark.slow
+def test_dc_coupled_gaps_detailed_balance():
+    """The DC order samples the same Gibbs density: two adjacent gaps in different tiles
+    (l_b = 2) of a 4x4 lattice, means vs 2-D quadrature (brute force)."""
+    rng = np.random.default_rng(7)
+    phi = (rng.random((4, 4)) * 2 * np.pi).astype(np.float32)
+    mask = np.ones((4, 4), np.uint8); mask[1, 1] = 0; mask[1, 2] = 0
+    T, q, n = 0.4, 0.5, 721
+    g = np.linspace(0, 2 * np.pi, n)
+    a = sum(np.cos(q * (g - v)) for v in [phi[0, 1], phi[2, 1], phi[1, 0]])
+    b = sum(np.cos(q * (g - v)) for v in [phi[0, 2], phi[2, 2], phi[1, 3]])
+    logp = (a[:, None] + b[None, :] + np.cos(q * (g[:, None] - g[None, :]))) / T
+    Pd = np.exp(logp - logp.max()); dx = g[1] - g[0]
+    Pd /= Pd.sum() * dx * dx
+    ex = float((g[:, None] * Pd).sum() * dx * dx); ey = float((g[None, :] * Pd).sum() * dx * dx)
+    beta = np.full((4, 4), 1 / T, np.float32)
+    mx, my = [], []
+    for m in range(8):
+        ph = phi.copy(); ph[1, 1] = 1.0; ph[1, 2] = 5.0
+        sx = sy = 0.0
+        for s in range(1, 6001):
+            O.sweep_dc(ph, mask, beta, s, m, 5, lb=2)
+            if s > 100:
+                sx += ph[1, 1]; sy += ph[1, 2]
+        mx.append(sx / 5900); my.append(sy / 5900)
+    se = lambda v: np.std(v) / np.sqrt(len(v))  # noqa: E731
+    assert abs(np.mean(mx) - ex) < 5 * se(mx) + 3e-3
+    assert abs(np.mean(my) - ey) < 5 * se(my) + 3e-3
