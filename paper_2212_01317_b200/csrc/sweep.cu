@@ -171,7 +171,7 @@ __device__ __forceinline__ Split split_work(int npairs) {
 
 // Direct-load variant: record, own state and neighbour states loaded from global memory
 // at the start of each item (PF: register-free prefetch of the next item).
-template <bool QHALF, bool ENERGY, int MINB, int PF, int NT, bool BFEXP>
+template <bool QHALF, bool ENERGY, int MINB, int PF, int NT, bool BFEXP, bool LIST>
 __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   const Split sp = split_work(a.npairs);
   // 32-bit element offsets: the host caps the batch so that P * R < 2^31
@@ -191,11 +191,11 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
     const uint32_t pair = a.pair_base + static_cast<uint32_t>(sp.j);
     for (uint32_t g = sp.g0; g < gcount; g += sp.gstride) {
       // DC order (row f3): the phase's gap ids come from a list; SC: a contiguous range
-      const uint32_t gg = a.glist ? a.glist[g] : gbegin + g;
+      const uint32_t gg = LIST ? a.glist[g] : gbegin + g;
       const GapRec rec = a.rec[gg];
       const uint32_t self_off = gg * R + j2;
       const float2 cur = *reinterpret_cast<const float2*>(a.G + self_off);
-      if (PF && !a.glist) {
+      if (PF && !LIST) {
         const uint32_t gn = gg + sp.gstride;
         if (gn < gbegin + gcount) {
           if (PF == 1) {
@@ -267,37 +267,38 @@ __global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X,
 
 }  // namespace
 
-// Kernel variants (tuning knob, MPR_SWEEP_VARIANT): register cap via min blocks per SM.
-template <bool Q, bool E>
+// Kernel variants (tuning knob, MPR_SWEEP_VARIANT; profiles/r01_summary.md records every
+// alternative measured): 0 = plain, 2 = + register-free L2 prefetch of the next item,
+// 5 (default) = 2 + branch-free exp, 8 = 5 capped at 64 registers (32 warps/SM).
+// C2 half-sweep: v0 106.5, v2 103.3, v5 99.3, v8 101.8 us; C4: v5 4.15, v8 4.02 ms.
+// LIST: the gap ids of the phase come from a list (double-checkerboard order, row f3).
+template <bool Q, bool E, bool LIST>
 static void* sweep_kernel_ptr(int variant) {
   switch (variant) {
-    case 0: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 0, 256, false>);
-    case 1: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 1, 256, false>);
-    case 3: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 1, 256, false>);
-    case 4: return reinterpret_cast<void*>(k_sweep_half<Q, E, 2, 0, 256, false>);
-    case 2: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, false>);
-    case 6: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 128, false>);
-    case 7: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 128, true>);
-    case 8: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 2, 256, true>);
-    case 9: return reinterpret_cast<void*>(k_sweep_half<Q, E, 5, 2, 256, true>);
-    case 10: return reinterpret_cast<void*>(k_sweep_half<Q, E, 3, 2, 256, true>);
-    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true>);  // 5
+    case 0: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 0, 256, false, LIST>);
+    case 2: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, false, LIST>);
+    case 8: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 2, 256, true, LIST>);
+    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST>);  // 5
   }
 }
 
-static int sweep_threads(int variant) { return (variant == 6 || variant == 7) ? 128 : 256; }
+static int sweep_threads(int) { return 256; }
 
 static size_t sweep_smem(int) { return 0; }
 
-static void* sweep_kernel(bool qhalf, bool energy, int variant) {
-  if (qhalf) return energy ? sweep_kernel_ptr<true, true>(variant) : sweep_kernel_ptr<true, false>(variant);
-  return energy ? sweep_kernel_ptr<false, true>(variant) : sweep_kernel_ptr<false, false>(variant);
+static void* sweep_kernel(bool qhalf, bool energy, bool list, int variant) {
+  if (list) {
+    if (qhalf) return energy ? sweep_kernel_ptr<true, true, true>(variant) : sweep_kernel_ptr<true, false, true>(variant);
+    return energy ? sweep_kernel_ptr<false, true, true>(variant) : sweep_kernel_ptr<false, false, true>(variant);
+  }
+  if (qhalf) return energy ? sweep_kernel_ptr<true, true, false>(variant) : sweep_kernel_ptr<true, false, false>(variant);
+  return energy ? sweep_kernel_ptr<false, true, false>(variant) : sweep_kernel_ptr<false, false, false>(variant);
 }
 
 int sweep_grid_size(int device, int variant) {
   int sms = 0, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, variant), sweep_threads(variant),
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, false, variant), sweep_threads(variant),
                                                 sweep_smem(variant));
   if (per < 1) per = 1;
   return sms * per;
@@ -313,7 +314,7 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   if (g < 1) g = 1;
   const bool qhalf = (a.q == 0.5f);
   const bool energy = (a.energy != nullptr);
-  void* fn = sweep_kernel(qhalf, energy, variant);
+  void* fn = sweep_kernel(qhalf, energy, a.glist != nullptr, variant);
   void* args[] = {const_cast<SweepArgs*>(&a)};
   cudaLaunchKernel(fn, dim3(static_cast<unsigned>(g)), dim3(nt), args, sweep_smem(variant), st);
 }
