@@ -70,3 +70,32 @@ def test_init_without_gpu_fails_loudly():
     from paper_2212_01317_b200 import LeMpr, MprError
     with pytest.raises(MprError):
         LeMpr()
+
+
+def _build_c_example(tmp_path):
+    import subprocess
+    from paper_2212_01317_b200 import _build
+    _build.build()
+    exe = str(tmp_path / "mpr_fill_c")
+    subprocess.check_call(["gcc", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "fill.c"), "-L", PKG, "-lmpr",
+                           f"-Wl,-rpath,{PKG}", "-lm", "-o", exe])
+    return exe
+
+
+def test_c_example_compiles_and_links_against_the_abi(tmp_path):
+    """The boundary is plain C: a C program compiles against include/mpr.h and links libmpr.so."""
+    assert os.path.exists(_build_c_example(tmp_path))
+
+
+@pytest.mark.gpu
+def test_c_example_runs(tmp_path):
+    import subprocess
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    exe = _build_c_example(tmp_path)
+    out = subprocess.run([exe, os.path.join(PKG, "data", "calib_q0.5.txt")], capture_output=True, text=True,
+                         timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert "0 sample mismatches" in out.stdout
