@@ -309,6 +309,8 @@ def run_mpr(args):
     # e2e through the public API with pinned host buffers, H2D + D2H inside the timed region
     e2e = None
     if not args.no_e2e:
+        for _ in range(max(args.warmup, 1)):  # first use of the host-buffer path, untimed
+            step_host()
         barrier()
         w0 = time.perf_counter()
         for _ in range(args.steps):
