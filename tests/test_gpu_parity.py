@@ -390,3 +390,31 @@ def test_dc_rejects_sc_only_features(P, calib):
     with pytest.raises(P.MprError):
         m.simulate(2, 3, 1)
     m.close()
+
+
+def test_nccl_allreduce_on_accumulator_view(P, calib):
+    """The bench's N>1 path in miniature: an NCCL process group (world size 1 here) reduces
+    the library-owned accumulator in place through the zero-copy torch view."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2212_01317_b200.sharding import allreduce_accumulator, distributed_fill
+    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        truth, z, mask = make_problem(40, 0.5, corr_len=6.0)
+        m = P.LeMpr(P.Config(l_b=8), calib, stream=torch.cuda.current_stream().cuda_stream)
+        pred = distributed_fill(m, z, mask, M=6, sweeps=8, seed=3)
+        acc = m.accumulator_tensor()
+        before = acc.clone()
+        dist.all_reduce(acc)          # in place on the library's buffer
+        allreduce_accumulator(acc)    # world size 1: no-op
+        torch.cuda.synchronize()
+        assert torch.equal(acc, before)
+        ref = gpu_run(P, z, mask, P.Config(l_b=8), calib, 6, 8, 3)["pred"]
+        assert_bitwise(pred, ref, "distributed_fill at world size 1")
+        m.close()
+    finally:
+        dist.destroy_process_group()
