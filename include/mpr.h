@@ -121,14 +121,15 @@ mpr_status mpr_simulate(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed);
 /* Adaptive equilibration (n_fit = 20 "memory length of the energy time
  * series", n_f = 5 "frequency of verification"; test of ARITH §K, reading R20): every
  * realization sweeps until, at a check sweep s = n_fit + k*n_f, the least-squares slope
- * of its last n_fit whole-grid energies (ARITH §J, exact fixed point) is >= -2 sigma /
- * n_fit; it then averages the next n_avg sweeps and stops. No check passes before
- * max_sweeps - n_avg => equilibrium is declared there (returned negated). s_eq_out
- * (nullable, host, M int32) receives each realization's equilibrium sweep. Replaces any
- * previous accumulation; predict as after mpr_simulate. Errors: M < 1, n_fit < 3,
- * n_f < 1, max_sweeps <= n_avg -> INVALID_ARG. */
+ * of its last n_fit whole-grid energies (ARITH §J, exact fixed point) is >=
+ * -max(2 sigma / n_fit, slope_tol); it then averages the next n_avg sweeps and stops.
+ * slope_tol (energy per sweep, >= 0; 0 = SPEC's rule) is SPEC's configurable tolerance.
+ * No check passes before max_sweeps - n_avg => equilibrium is declared there (returned
+ * negated). s_eq_out (nullable, host, M int32) receives each realization's equilibrium
+ * sweep. Replaces any previous accumulation; predict as after mpr_simulate. Errors:
+ * M < 1, n_fit < 3, n_f < 1, max_sweeps <= n_avg, slope_tol < 0 -> INVALID_ARG. */
 mpr_status mpr_simulate_adaptive(mpr_ctx *ctx, int64_t M, uint64_t seed, int32_t n_fit, int32_t n_f,
-                                 int32_t max_sweeps, int32_t *s_eq_out);
+                                 int32_t max_sweeps, double slope_tol, int32_t *s_eq_out);
 
 /* Calibration curve e(T) on the GPU (row f2; the T <-> e relation the energy matching of
  * PAPER.md:90 inverts, construction deferred to [mz-dth18]; reading R2):

@@ -569,7 +569,7 @@ double oracle_energy_from_fx(int64_t E_fx, int Lx, int Ly)
 
 /* Equilibrium test of ARITH §K on y[0 .. n_fit-1] (the last n_fit energies): least-squares
  * slope b against t = 0..n_fit-1, residual scale, tau = 2 sigma / n_fit; 1 iff b >= -tau. */
-int oracle_equilibrium_test(const double *y, int n_fit)
+int oracle_equilibrium_test(const double *y, int n_fit, double slope_tol)
 {
     double xbar = (double)(n_fit - 1) / 2.0;
     double sy = 0.0;
@@ -589,6 +589,7 @@ int oracle_equilibrium_test(const double *y, int n_fit)
         sse = sse + res * res;
     }
     double tau = 2.0 * sqrt(sse / (double)(n_fit - 2)) / (double)n_fit;
+    if (slope_tol > tau) tau = slope_tol;  /* tau = max(2 sigma / n_fit, slope_tol) */
     return b >= -tau;
 }
 
@@ -599,7 +600,8 @@ int oracle_equilibrium_test(const double *y, int n_fit)
  * energy (nullable, (m_end-m_begin)*S_max) the per-sweep energies (0 after the stop). */
 void oracle_simulate_adaptive(const float *phi0, const uint8_t *mask, const float *beta, int Lx, int Ly,
                               const oracle_cfg *cfg, const int64_t *SP, const int64_t *NK,
-                              int64_t m_begin, int64_t m_end, int n_fit, int n_f, int S_max, uint64_t seed,
+                              int64_t m_begin, int64_t m_end, int n_fit, int n_f, int S_max, double slope_tol,
+                              uint64_t seed,
                               double *acc, int32_t *s_eq, double *energy, float *phi_out)
 {
     int64_t n = (int64_t)Lx * Ly;
@@ -622,7 +624,7 @@ void oracle_simulate_adaptive(const float *phi0, const uint8_t *mask, const floa
                 continue;
             }
             int check = s >= n_fit + n_f && (s - n_fit) % n_f == 0 && s + cfg->n_avg <= S_max;
-            if (check && oracle_equilibrium_test(&e[s - n_fit + 1], n_fit)) {
+            if (check && oracle_equilibrium_test(&e[s - n_fit + 1], n_fit, slope_tol)) {
                 eq = s;
                 stop = s + cfg->n_avg;
             } else if (s == S_max - cfg->n_avg) {

@@ -115,10 +115,11 @@ def _declare(L):
     L.oracle_grid_energy_fx.restype = C.c_int64
     L.oracle_energy_from_fx.argtypes = [C.c_int64, C.c_int, C.c_int]
     L.oracle_energy_from_fx.restype = C.c_double
-    L.oracle_equilibrium_test.argtypes = [_f64p, C.c_int]
+    L.oracle_equilibrium_test.argtypes = [_f64p, C.c_int, C.c_double]
     L.oracle_equilibrium_test.restype = C.c_int
     L.oracle_simulate_adaptive.argtypes = [_f32p, _u8p, _f32p, C.c_int, C.c_int, C.POINTER(_Cfg), _i64p, _i64p,
-                                           C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_uint64, _f64p,
+                                           C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64,
+                                           _f64p,
                                            np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS"), C.c_void_p,
                                            C.c_void_p]
 
@@ -303,14 +304,14 @@ def energy_from_fx(E_fx, Lx, Ly) -> float:
     return lib().oracle_energy_from_fx(int(E_fx), int(Lx), int(Ly))
 
 
-def equilibrium_test(y) -> bool:
+def equilibrium_test(y, slope_tol=0.0) -> bool:
     """ARITH §K slope test on the last n_fit energies."""
     y = np.ascontiguousarray(y, np.float64)
-    return bool(lib().oracle_equilibrium_test(y, len(y)))
+    return bool(lib().oracle_equilibrium_test(y, len(y), float(slope_tol)))
 
 
 def simulate_adaptive(params, mask, cfg, M, seed, n_fit=20, n_f=5, S_max=500, m_begin=0, m_end=None,
-                      energy=False, states=False):
+                      energy=False, states=False, slope_tol=0.0):
     """Row f1 protocol (ARITH §K) for realizations [m_begin, m_end): returns
     dict(acc, s_eq (negative = forced by the cap), energy, phi)."""
     m_end = M if m_end is None else m_end
@@ -325,7 +326,7 @@ def simulate_adaptive(params, mask, cfg, M, seed, n_fit=20, n_f=5, S_max=500, m_
              1 if cfg.order == "dc" else 0)
     lib().oracle_simulate_adaptive(params.phi0.ravel(), mask.ravel(), params.beta.ravel(), Lx, Ly, C.byref(c),
                                    params.SP.ravel(), params.NK.ravel(), int(m_begin), int(m_end), int(n_fit),
-                                   int(n_f), int(S_max), int(seed), acc, s_eq,
+                                   int(n_f), int(S_max), float(slope_tol), int(seed), acc, s_eq,
                                    en.ctypes.data if energy else None, ph.ctypes.data if states else None)
     return dict(acc=acc.reshape(Ly, Lx), s_eq=s_eq, energy=None if en is None else en.reshape(R, S_max),
                 phi=None if ph is None else ph.reshape(R, Ly, Lx))

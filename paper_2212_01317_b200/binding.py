@@ -90,7 +90,7 @@ def load_library(path: str = LIB_PATH):
     L.mpr_slab_row_states.restype = C.c_int
     L.mpr_slab_end.argtypes = [vp]; L.mpr_slab_end.restype = C.c_int
     L.mpr_sync.argtypes = [vp]; L.mpr_sync.restype = C.c_int
-    L.mpr_simulate_adaptive.argtypes = [vp, i64, u64, i32, i32, i32, vp]
+    L.mpr_simulate_adaptive.argtypes = [vp, i64, u64, i32, i32, i32, C.c_double, vp]
     L.mpr_simulate_adaptive.restype = C.c_int
     L.mpr_build_calibration.argtypes = [vp, vp, i32, i32, C.c_float, i32, i32, i32, u64, vp, vp]
     L.mpr_build_calibration.restype = C.c_int
@@ -225,11 +225,12 @@ def mpr_build_calibration(ctx, T, L=128, q=0.5, n_eq=400, n_meas=800, reps=2, se
     return e, raw
 
 
-def mpr_simulate_adaptive(ctx, M, seed, n_fit=20, n_f=5, max_sweeps=500) -> np.ndarray:
+def mpr_simulate_adaptive(ctx, M, seed, n_fit=20, n_f=5, max_sweeps=500, slope_tol=0.0) -> np.ndarray:
     """Adaptive equilibration (ARITH §K); returns s_eq per realization
     (negative = forced by max_sweeps)."""
     s_eq = np.zeros(M, np.int32)
-    _check(ctx, load_library().mpr_simulate_adaptive(ctx, M, seed, n_fit, n_f, max_sweeps, s_eq.ctypes.data))
+    _check(ctx, load_library().mpr_simulate_adaptive(ctx, M, seed, n_fit, n_f, max_sweeps, float(slope_tol),
+                                                     s_eq.ctypes.data))
     return s_eq
 
 
@@ -315,8 +316,8 @@ class LeMpr:
     def simulate_range(self, M, sweeps, seed, m_begin, m_end):
         mpr_simulate_range(self.ctx, M, sweeps, seed, m_begin, m_end)
 
-    def simulate_adaptive(self, M, seed, n_fit=20, n_f=5, max_sweeps=500):
-        return mpr_simulate_adaptive(self.ctx, M, seed, n_fit, n_f, max_sweeps)
+    def simulate_adaptive(self, M, seed, n_fit=20, n_f=5, max_sweeps=500, slope_tol=0.0):
+        return mpr_simulate_adaptive(self.ctx, M, seed, n_fit, n_f, max_sweeps, slope_tol)
 
     def reset_accumulator(self):
         mpr_reset_accumulator(self.ctx)

@@ -196,7 +196,7 @@ double energy_from_fx(const mpr_ctx* c, long long E_fx) {
 }
 
 // ARITH §K slope test on y[0 .. n_fit-1], every operation in the written order.
-bool equilibrium_reached(const double* y, int n_fit) {
+bool equilibrium_reached(const double* y, int n_fit, double slope_tol) {
   const double xbar = static_cast<double>(n_fit - 1) / 2.0;
   double sy = 0.0;
   for (int t = 0; t < n_fit; ++t) sy = sy + y[t];
@@ -214,7 +214,8 @@ bool equilibrium_reached(const double* y, int n_fit) {
     const double res = y[t] - a - b * static_cast<double>(t);
     sse = sse + res * res;
   }
-  const double tau = 2.0 * std::sqrt(sse / static_cast<double>(n_fit - 2)) / static_cast<double>(n_fit);
+  double tau = 2.0 * std::sqrt(sse / static_cast<double>(n_fit - 2)) / static_cast<double>(n_fit);
+  if (slope_tol > tau) tau = slope_tol;  // tau = max(2 sigma / n_fit, slope_tol)
   return b >= -tau;
 }
 
@@ -684,8 +685,9 @@ mpr_status mpr_simulate(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed) {
 // device for the whole batch; at check sweeps the host reads the fixed-point energies,
 // decides, and uploads the per-realization accumulation windows.
 mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n_fit, int32_t n_f,
-                                 int32_t max_sweeps, int32_t* s_eq_out) {
+                                 int32_t max_sweeps, double slope_tol, int32_t* s_eq_out) {
   if (!c) return MPR_ERR_INVALID_ARG;
+  if (!(slope_tol >= 0.0) || !std::isfinite(slope_tol)) return fail(c, MPR_ERR_INVALID_ARG, "slope_tol must be >= 0");
   if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "simulate before estimate_local_params");
   const int n_avg = c->cfg.n_avg;
   if (M < 1 || n_fit < 3 || n_f < 1 || max_sweeps < n_avg + 1 || M >= (int64_t(1) << 32))
@@ -777,7 +779,7 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
           if (check) {
             for (int t = 0; t < n_fit; ++t)
               y[t] = energy_from_fx(c, c->sum_SB_fx + fx[static_cast<size_t>(r) * max_sweeps + (s - n_fit + t)]);
-            ok = equilibrium_reached(y.data(), n_fit);
+            ok = equilibrium_reached(y.data(), n_fit, slope_tol);
           }
           if (ok || forced) {
             eq[r] = ok ? s : -s;

@@ -30,6 +30,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--max-L", type=int, default=16384)
+    ap.add_argument("--only-paper", action="store_true")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
@@ -42,7 +43,7 @@ def main():
             fields[L] = heterogeneous_field(L)
         return fields[L]
 
-    def run(L, p, M, S=30, rs=2, adaptive=False, tag=""):
+    def run(L, p, M, S=30, rs=2, adaptive=False, tag="", slope_tol=0.0):
         truth = field(L)
         mask = random_mask(L, L, p)
         z = np.where(mask != 0, truth, np.float32(0)).astype(np.float32)
@@ -57,7 +58,7 @@ def main():
             eng.set_data_device(zd.data_ptr(), md.data_ptr(), L, L)
             eng.estimate_local_params()
             if adaptive:
-                s = eng.simulate_adaptive(M, 7, n_fit=20, n_f=5, max_sweeps=500)
+                s = eng.simulate_adaptive(M, 7, n_fit=20, n_f=5, max_sweeps=500, slope_tol=slope_tol)
                 sweeps_used.append(float(np.mean(np.abs(s)) + 1))
             else:
                 eng.simulate(M, S, 7)
@@ -77,30 +78,31 @@ def main():
         eng.set_data(z, mask)
         eng.estimate_local_params()
         if adaptive:
-            eng.simulate_adaptive(M, 7, n_fit=20, n_f=5, max_sweeps=500)
+            eng.simulate_adaptive(M, 7, n_fit=20, n_f=5, max_sweeps=500, slope_tol=slope_tol)
         else:
             eng.simulate(M, S, 7)
         eng.predict()
         e2e = 1e3 * (time.perf_counter() - w0)
         sw = float(np.mean(sweeps_used)) if adaptive else S
-        rec = dict(tag=tag, L=L, p=p, gap_sites=Pg, M=M, window=2 * rs + 1, protocol="adaptive" if adaptive else f"S={S}",
+        rec = dict(tag=tag, L=L, p=p, gap_sites=Pg, M=M, window=2 * rs + 1, protocol=f"adaptive tol={slope_tol:g}" if adaptive else f"S={S}",
                    mean_sweeps=sw, fill_ms=t, e2e_fill_ms=e2e, updates_per_s=Pg * sw * M / (t / 1e3))
         print(json.dumps(rec), flush=True)
         eng.close()
 
-    Ls = [L for L in (256, 1024, 2048, 4096, 8192, 16384) if L <= a.max_L]
+    Ls = [] if a.only_paper else [L for L in (256, 1024, 2048, 4096, 8192, 16384) if L <= a.max_L]
     for L in Ls:                       # size sweep (p = 0.5, w = 5, M = 10)
         run(L, 0.5, 10, tag="size")
-    for p in (0.33, 0.5, 0.9):         # missing-ratio sweep at 4096^2
+    for p in (() if a.only_paper else (0.33, 0.5, 0.9)):  # missing-ratio sweep at 4096^2
         run(4096, p, 10, tag="ratio")
-    for rs in (1, 2, 4, 7):            # smoothing window 3..15 at 4096^2
+    for rs in (() if a.only_paper else (1, 2, 4, 7)):     # smoothing window 3..15 at 4096^2
         run(4096, 0.5, 10, rs=rs, tag="window")
-    for M in (10, 100, 1000):          # realization count at 1024^2
+    for M in (() if a.only_paper else (10, 100, 1000)):   # realization count at 1024^2
         run(1024, 0.5, M, tag="realizations")
     for L in (256, 2048, 8192):        # the paper's sizes at p = 0.85 (Tables 2-3), one chain
         if L <= a.max_L:
-            run(L, 0.85, 1, adaptive=True, tag="paper-point adaptive M=1")
-            run(L, 0.85, 100, adaptive=True, tag="paper-point adaptive M=100")
+            for tol in (0.0, 1e-5):
+                run(L, 0.85, 1, adaptive=True, tag="paper-point adaptive M=1", slope_tol=tol)
+                run(L, 0.85, 100, adaptive=True, tag="paper-point adaptive M=100", slope_tol=tol)
 
 
 if __name__ == "__main__":

@@ -418,3 +418,21 @@ def test_nccl_allreduce_on_accumulator_view(P, calib):
         m.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_adaptive_with_slope_tolerance(P, calib):
+    """The relaxed test (slope_tol > 0) stops earlier and still agrees with the oracle."""
+    Tk, ek = calib
+    truth, z, mask = make_problem(48, 0.5, corr_len=6.0)
+    cfg = P.Config()
+    m = P.LeMpr(cfg, calib)
+    m.set_data(z, mask)
+    m.estimate_local_params()
+    s_eq = m.simulate_adaptive(4, 12, n_fit=20, n_f=5, max_sweeps=200, slope_tol=2e-5)
+    pred = m.predict()
+    m.close()
+    oc = ocfg(cfg)
+    p = O.parameters(z, mask, oc, Tk, ek)
+    r = O.simulate_adaptive(p, mask, oc, 4, 12, n_fit=20, n_f=5, S_max=200, slope_tol=2e-5)
+    assert s_eq.tolist() == r["s_eq"].tolist() and all(25 <= s < 200 for s in s_eq)
+    assert_bitwise(pred, O.predict(np.nan_to_num(z), mask, r["acc"], 4, 1, p.zmin, p.zmax, 0), "predictions")

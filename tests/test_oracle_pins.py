@@ -583,3 +583,11 @@ def test_dc_coupled_gaps_detailed_balance():
     se = lambda v: np.std(v) / np.sqrt(len(v))  # noqa: E731
     assert abs(np.mean(mx) - ex) < 5 * se(mx) + 3e-3
     assert abs(np.mean(my) - ey) < 5 * se(my) + 3e-3
+
+
+def test_equilibrium_slope_tolerance():
+    """slope_tol (SPEC's configurable tolerance) relaxes the rule to b >= -max(tau, slope_tol)."""
+    y = -0.95 - 1e-4 * np.arange(20)
+    assert not O.equilibrium_test(y)
+    assert not O.equilibrium_test(y, slope_tol=5e-5)
+    assert O.equilibrium_test(y, slope_tol=2e-4)
