@@ -75,7 +75,7 @@ struct mpr_ctx {
   int stage = ST_INIT;
   std::string err;
   int sweep_grid = 0;
-  int sweep_variant = 5;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
+  int sweep_variant = 12;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
   // problem
   int64_t Lx = 0, Ly = 0, n = 0;
   int64_t P = 0, PA = 0, n_known = 0;

@@ -10,7 +10,9 @@ namespace mpr {
 
 constexpr float kTwoPiF = 0x1.921fb6p+2f;  // ARITH notation TWO_PI_F
 
-// ARITH §A — Philox4x32-10. The 32x32->64 products are single IMAD.WIDE.U32.
+// ARITH §A — Philox4x32-10. The 32x32->64 products are single IMAD.WIDE.U32 (the split
+// IMAD.HI.U32 + IMAD form was measured slower inside the packed sweep kernel:
+// profiles/r01_summary.md).
 struct Words4 {
   uint32_t w0, w1, w2, w3;
 };
@@ -108,6 +110,60 @@ __device__ __forceinline__ float exp_spec(float x) {
   const float scale = __int_as_float((ni + 127) << 23);
   const float r = __fmul_rn(p, scale);
   return x < -80.0f ? 0.0f : r;
+}
+
+// ---- Packed f32x2 forms (sm_100a FFMA2 / FADD2 / FMUL2) ------------------------------
+// Each component is rounded exactly like the scalar __fmaf_rn / __fadd_rn / __fmul_rn, so
+// the two realizations of a pair can share one instruction without changing a bit.
+// ptxas 12.9 caveat (checked in SASS): a FMUL2 whose result feeds a FADD2 is contracted
+// into one FFMA2 even with explicit .rn, which would drop a rounding. The packed code
+// below therefore never feeds a packed product into a packed add; the one place ARITH
+// has a product followed by an add (exp_spec's x*log2e + 1.5*2^23) stays scalar.
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+
+// cos_half_spec on both components (ARITH §B with the 4^-k coefficients).
+__device__ __forceinline__ float2 cos_half_spec2(float2 d) {
+  const float2 t = __fmul2_rn(d, d);
+  float2 p = __ffma2_rn(f2(0x1.e0c79cp-42f), t, f2(-0x1.2392p-32f));
+  p = __ffma2_rn(p, t, f2(0x1.9fb7a2p-24f));
+  p = __ffma2_rn(p, t, f2(-0x1.6c12aep-16f));
+  p = __ffma2_rn(p, t, f2(0x1.555536p-9f));
+  p = __ffma2_rn(p, t, f2(-0.125f));
+  p = __ffma2_rn(p, t, f2(1.0f));
+  return p;
+}
+
+// cos_spec on both components (ARITH §B).
+__device__ __forceinline__ float2 cos_spec2(float2 x) {
+  const float2 t = __fmul2_rn(x, x);
+  float2 p = __ffma2_rn(f2(0x1.e0c79cp-30f), t, f2(-0x1.2392p-22f));
+  p = __ffma2_rn(p, t, f2(0x1.9fb7a2p-16f));
+  p = __ffma2_rn(p, t, f2(-0x1.6c12aep-10f));
+  p = __ffma2_rn(p, t, f2(0x1.555536p-5f));
+  p = __ffma2_rn(p, t, f2(-0.5f));
+  p = __ffma2_rn(p, t, f2(1.0f));
+  return p;
+}
+
+// exp_spec_fast on both components (ARITH §C): the rounding add is scalar (see above),
+// everything after it packed.
+__device__ __forceinline__ float2 exp_spec_fast2(float2 x) {
+  const float vx = __fmul_rn(x.x, 0x1.715476p+0f);
+  const float vy = __fmul_rn(x.y, 0x1.715476p+0f);
+  const float2 tm = make_float2(__fadd_rn(vx, 12582912.0f), __fadd_rn(vy, 12582912.0f));
+  const float2 n = __fadd2_rn(tm, f2(-12582912.0f));  // exact
+  const float2 nn = make_float2(-n.x, -n.y);
+  float2 f = __ffma2_rn(nn, f2(0x1.62e430p-1f), x);
+  f = __ffma2_rn(nn, f2(-0x1.05c610p-29f), f);
+  float2 p = __ffma2_rn(f2(0x1.6ac2a0p-10f), f, f2(0x1.126e38p-7f));
+  p = __ffma2_rn(p, f, f2(0x1.555890p-5f));
+  p = __ffma2_rn(p, f, f2(0x1.555408p-3f));
+  p = __ffma2_rn(p, f, f2(0x1.fffffap-2f));
+  p = __ffma2_rn(p, f, f2(1.0f));
+  p = __ffma2_rn(p, f, f2(1.0f));
+  const int nx = __float_as_int(tm.x) - 0x4b400000, ny = __float_as_int(tm.y) - 0x4b400000;
+  const float2 r = __fmul2_rn(p, make_float2(__int_as_float((nx + 127) << 23), __int_as_float((ny + 127) << 23)));
+  return make_float2(x.x < -80.0f ? 0.0f : r.x, x.y < -80.0f ? 0.0f : r.y);
 }
 
 // Order-preserving key of a float for integer atomicMin/atomicMax.

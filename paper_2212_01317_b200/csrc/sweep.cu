@@ -80,6 +80,64 @@ __device__ __forceinline__ float metropolis(float cur, const float (&nbv)[4], ui
   return accepted ? prop : cur;
 }
 
+// ARITH §H for both realizations of a pair at once, on packed f32x2 instructions: the
+// x / y components follow exactly the scalar operation sequence of metropolis() above
+// (each FFMA2/FADD2/FMUL2 component rounds like its scalar twin), so the results are
+// bit-identical while the FP instruction count of an item halves.
+template <bool QHALF, bool ENERGY, bool FULL>
+__device__ __forceinline__ float2 metropolis_pair(float2 cur, const float2 (&nb)[4], uint32_t flags,
+                                                  uint32_t sel, float beta, float q, float J,
+                                                  const Words4& w, bool& acc0, bool& acc1,
+                                                  long long& e0, long long& e1) {
+  const float2 prop = __fmul2_rn(make_float2(__uint2float_rn(w.w0 >> 8), __uint2float_rn(w.w2 >> 8)),
+                                 f2(0x1.921fb6p-22f));
+  float2 s_cur = f2(0.0f), s_new = f2(0.0f);
+  long long ec0 = 0, en0 = 0, ec1 = 0, en1 = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 mnb = make_float2(-nb[k].x, -nb[k].y);
+    float2 dc = __fadd2_rn(cur, mnb), dn = __fadd2_rn(prop, mnb);
+    float2 cc, cn;
+    if (QHALF) {
+      cc = cos_half_spec2(dc);
+      cn = cos_half_spec2(dn);
+    } else {
+      cc = cos_spec2(__fmul2_rn(f2(q), dc));
+      cn = cos_spec2(__fmul2_rn(f2(q), dn));
+    }
+    if (!FULL) {
+      const bool has = ((flags >> (2 * k)) & 3u) != 0u;
+      cc = has ? cc : f2(0.0f);
+      cn = has ? cn : f2(0.0f);
+    }
+    if (FULL && k == 0) {
+      s_cur = cc;
+      s_new = cn;
+    } else {
+      s_cur = __fadd2_rn(s_cur, cc);
+      s_new = __fadd2_rn(s_new, cn);
+    }
+    if (ENERGY && ((sel >> k) & 1u)) {
+      const float2 sc = __fmul2_rn(cc, f2(0x1p32f)), sn = __fmul2_rn(cn, f2(0x1p32f));
+      ec0 += __float2ll_rn(sc.x);
+      ec1 += __float2ll_rn(sc.y);
+      en0 += __float2ll_rn(sn.x);
+      en1 += __float2ll_rn(sn.y);
+    }
+  }
+  const float2 dE = __fmul2_rn(f2(J), __fadd2_rn(s_cur, make_float2(-s_new.x, -s_new.y)));
+  const float2 x = __fmul2_rn(dE, f2(-beta));  // == -(dE * beta): RN is sign-symmetric
+  const float2 e = exp_spec_fast2(x);
+  const float2 u = __fmul2_rn(make_float2(__uint2float_rn(w.w1 >> 8), __uint2float_rn(w.w3 >> 8)), f2(0x1p-24f));
+  acc0 = (dE.x <= 0.0f) | (u.x < e.x);
+  acc1 = (dE.y <= 0.0f) | (u.y < e.y);
+  if (ENERGY) {
+    e0 += acc0 ? en0 : ec0;
+    e1 += acc1 ? en1 : ec1;
+  }
+  return make_float2(acc0 ? prop.x : cur.x, acc1 ? prop.y : cur.y);
+}
+
 // Every neighbour present: each 2-bit field of flags is non-zero.
 __device__ __forceinline__ bool all_present(uint32_t f) {
   return ((f | (f >> 1)) & 0x55u) == 0x55u;
@@ -87,11 +145,10 @@ __device__ __forceinline__ bool all_present(uint32_t f) {
 
 // One work item (gap site, realization pair) once its record and the states it reads
 // are in registers: Philox, two Metropolis updates, store, fused epilogues.
-template <bool QHALF, bool ENERGY, bool BFEXP>
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK>
 __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& rec, float2 cur,
-                                             const float (&nv0)[4], const float (&nv1)[4],
-                                             uint32_t self_off, uint32_t pair, long long& e0, long long& e1,
-                                             bool accum0, bool accum1) {
+                                             const float2 (&nb)[4], uint32_t self_off, uint32_t pair,
+                                             long long& e0, long long& e1, bool accum0, bool accum1) {
   uint32_t sel = 0;
   if (ENERGY) {
 #pragma unroll
@@ -103,10 +160,20 @@ __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& r
   const Words4 w = philox4x32_10(rec.site, a.sweep, pair, 2u, a.k0, a.k1);
   bool acc0, acc1;
   float n0, n1;
-  if (all_present(rec.flags)) {
+  if (PK) {
+    const float2 nn = all_present(rec.flags)
+        ? metropolis_pair<QHALF, ENERGY, true>(cur, nb, rec.flags, sel, rec.beta, a.q, a.J, w, acc0, acc1, e0, e1)
+        : metropolis_pair<QHALF, ENERGY, false>(cur, nb, rec.flags, sel, rec.beta, a.q, a.J, w, acc0, acc1, e0, e1);
+    n0 = nn.x;
+    n1 = nn.y;
+  } else if (all_present(rec.flags)) {
+    const float nv0[4] = {nb[0].x, nb[1].x, nb[2].x, nb[3].x};
+    const float nv1[4] = {nb[0].y, nb[1].y, nb[2].y, nb[3].y};
     n0 = metropolis<QHALF, ENERGY, true, BFEXP>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
     n1 = metropolis<QHALF, ENERGY, true, BFEXP>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
   } else {
+    const float nv0[4] = {nb[0].x, nb[1].x, nb[2].x, nb[3].x};
+    const float nv1[4] = {nb[0].y, nb[1].y, nb[2].y, nb[3].y};
     n0 = metropolis<QHALF, ENERGY, false, BFEXP>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
     n1 = metropolis<QHALF, ENERGY, false, BFEXP>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
   }
@@ -171,7 +238,7 @@ __device__ __forceinline__ Split split_work(int npairs) {
 
 // Direct-load variant: record, own state and neighbour states loaded from global memory
 // at the start of each item (PF: register-free prefetch of the next item).
-template <bool QHALF, bool ENERGY, int MINB, int PF, int NT, bool BFEXP, bool LIST>
+template <bool QHALF, bool ENERGY, int MINB, int PF, int NT, bool BFEXP, bool LIST, bool PK>
 __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   const Split sp = split_work(a.npairs);
   // 32-bit element offsets: the host caps the batch so that P * R < 2^31
@@ -187,7 +254,44 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
     // adaptive protocol: a pair whose two realizations have finished is frozen
     if (a.win_hi) live = static_cast<int>(a.sweep) <= max(a.win_hi[2 * sp.j], a.win_hi[2 * sp.j + 1]);
   }
-  if (live) {
+  if (live && PF == 3) {
+    // Record one item ahead: the 32-byte record of item g + gstride is loaded into registers
+    // while item g computes, so an item waits for one dependent round trip (its neighbour
+    // states), not two (record, then states). Plus the L2 prefetch of the next own state.
+    const uint32_t pair = a.pair_base + static_cast<uint32_t>(sp.j);
+    uint32_t g = sp.g0;
+    uint32_t gg = 0;
+    GapRec rec{};
+    if (g < gcount) {
+      gg = LIST ? a.glist[g] : gbegin + g;
+      rec = a.rec[gg];
+    }
+    for (; g < gcount; g += sp.gstride) {
+      const uint32_t gn = g + sp.gstride;
+      uint32_t ggn = 0;
+      GapRec recn{};
+      if (gn < gcount) {
+        ggn = LIST ? a.glist[gn] : gbegin + gn;
+        recn = a.rec[ggn];
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.G + (ggn * R + j2)));
+      }
+      const uint32_t self_off = gg * R + j2;
+      const float2 cur = *reinterpret_cast<const float2*>(a.G + self_off);
+      float2 nb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
+        if (ty == NB_GAP) {
+          nb[k] = *reinterpret_cast<const float2*>(a.G + (static_cast<uint32_t>(rec.nb[k]) * R + j2));
+        } else {
+          nb[k] = f2(__int_as_float(rec.nb[k]));
+        }
+      }
+      process_item<QHALF, ENERGY, BFEXP, PK>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
+      rec = recn;
+      gg = ggn;
+    }
+  } else if (live) {
     const uint32_t pair = a.pair_base + static_cast<uint32_t>(sp.j);
     for (uint32_t g = sp.g0; g < gcount; g += sp.gstride) {
       // DC order (row f3): the phase's gap ids come from a list; SC: a contiguous range
@@ -207,21 +311,17 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
           }
         }
       }
-      float nv0[4], nv1[4];
+      float2 nb[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
         if (ty == NB_GAP) {
-          const float2 v = *reinterpret_cast<const float2*>(a.G + (static_cast<uint32_t>(rec.nb[k]) * R + j2));
-          nv0[k] = v.x;
-          nv1[k] = v.y;
+          nb[k] = *reinterpret_cast<const float2*>(a.G + (static_cast<uint32_t>(rec.nb[k]) * R + j2));
         } else {
-          const float f = __int_as_float(rec.nb[k]);
-          nv0[k] = f;
-          nv1[k] = f;
+          nb[k] = f2(__int_as_float(rec.nb[k]));
         }
       }
-      process_item<QHALF, ENERGY, BFEXP>(a, rec, cur, nv0, nv1, self_off, pair, e0, e1, accum0, accum1);
+      process_item<QHALF, ENERGY, BFEXP, PK>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
     }
   }
   if (ENERGY) energy_epilogue(a, a.npairs, sp.active && live, sp.j, e0, e1);
@@ -269,16 +369,24 @@ __global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X,
 
 // Kernel variants (tuning knob, MPR_SWEEP_VARIANT; profiles/r01_summary.md records every
 // alternative measured): 0 = plain, 2 = + register-free L2 prefetch of the next item,
-// 5 (default) = 2 + branch-free exp, 8 = 5 capped at 64 registers (32 warps/SM).
-// C2 half-sweep: v0 106.5, v2 103.3, v5 99.3, v8 101.8 us; C4: v5 4.15, v8 4.02 ms.
+// 5 = 2 + branch-free exp, 8 = 5 capped at 64 registers (32 warps/SM), 10 = 5 on packed
+// f32x2 arithmetic, 11 = 10 capped at 64 registers, 12 (default) = 10 + record one item
+// ahead, 13 = 12 capped at 64 registers, 14 = 12 with 3 CTAs/SM declared.
+// Half-sweep, us: C2 v0 106.5, v2 103.3, v5 99.6, v8 101.8, v10 98.3, v11 99.7, v12 97.9;
+// C3 v5 2231, v10 2253, v12 2130; C4 v5 4149, v10 4138, v11 3958, v12 3797.
 // LIST: the gap ids of the phase come from a list (double-checkerboard order, row f3).
 template <bool Q, bool E, bool LIST>
 static void* sweep_kernel_ptr(int variant) {
   switch (variant) {
-    case 0: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 0, 256, false, LIST>);
-    case 2: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, false, LIST>);
-    case 8: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 2, 256, true, LIST>);
-    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST>);  // 5
+    case 0: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 0, 256, false, LIST, false>);
+    case 2: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, false, LIST, false>);
+    case 5: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, false>);
+    case 8: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 2, 256, true, LIST, false>);
+    case 10: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, true>);
+    case 11: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 2, 256, true, LIST, true>);
+    case 13: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);
+    case 14: return reinterpret_cast<void*>(k_sweep_half<Q, E, 3, 3, 256, true, LIST, true>);
+    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 3, 256, true, LIST, true>);  // 12
   }
 }
 

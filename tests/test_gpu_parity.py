@@ -436,3 +436,15 @@ def test_adaptive_with_slope_tolerance(P, calib):
     r = O.simulate_adaptive(p, mask, oc, 4, 12, n_fit=20, n_f=5, S_max=200, slope_tol=2e-5)
     assert s_eq.tolist() == r["s_eq"].tolist() and all(25 <= s < 200 for s in s_eq)
     assert_bitwise(pred, O.predict(np.nan_to_num(z), mask, r["acc"], 4, 1, p.zmin, p.zmax, 0), "predictions")
+
+
+@pytest.mark.parametrize("variant", [0, 2, 5, 8, 10, 11, 12, 13, 14])
+def test_every_sweep_variant_bit_exact(P, calib, variant, monkeypatch):
+    """Each half-sweep kernel variant (scalar / packed f32x2 arithmetic, prefetch, record one
+    item ahead, register caps; MPR_SWEEP_VARIANT) reproduces the oracle bit for bit: q = 1/2
+    with the energy trace, generic q, and the DC order (glist path)."""
+    monkeypatch.setenv("MPR_SWEEP_VARIANT", str(variant))
+    truth, z, mask = make_problem(48, 0.45, Lx=53, corr_len=6.0)
+    compare(P, z, mask, truth, P.Config(), calib, 7, 9, 1234 + variant, energy=True)
+    compare(P, z, mask, truth, P.Config(q=0.35, J=1.3, r_s=1), calib, 4, 6, 99)
+    compare(P, z, mask, truth, P.Config(order="dc", l_b=8, r_s=1), calib, 5, 6, 7)
