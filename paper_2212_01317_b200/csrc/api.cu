@@ -75,7 +75,7 @@ struct mpr_ctx {
   int stage = ST_INIT;
   std::string err;
   int sweep_grid = 0;
-  int sweep_variant = 12;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
+  int sweep_variant = 13;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
   // problem
   int64_t Lx = 0, Ly = 0, n = 0;
   int64_t P = 0, PA = 0, n_known = 0;
@@ -285,6 +285,13 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
   int64_t cap = static_cast<int64_t>(budget / per_r);
   // the sweep kernel indexes the state with 32-bit element offsets: P * R < 2^31
   cap = std::min<int64_t>(cap, ((int64_t(1) << 31) - 1) / std::max<int64_t>(c->P, 1));
+  // the default sweep kernel (variant 15) uses 32-bit byte offsets while P * R * 4 < 2^32:
+  // prefer batches that fit when that still leaves >= 4 realizations per batch (measured
+  // C4, M = 10: batches 6 + 4 at 3.74 ms per half-sweep vs one batch of 10 at 3.84 ms)
+  if (c->sweep_variant >= 15 && c->sweep_variant <= 17) {
+    const int64_t byte_cap = ((int64_t(1) << 32) - 1) / (4 * std::max<int64_t>(c->P, 1));
+    if (byte_cap >= 4) cap = std::min(cap, byte_cap);
+  }
   cap -= cap & 1;
   if (cap < 2) cap = 2;
   c->batch_key_P = c->P;
@@ -524,6 +531,7 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
   SweepArgs a{};
   a.rec = c->rec.as<GapRec>();
   a.G = c->G.as<float>();
+  a.P = c->P;
   a.A = avg ? c->A.as<float>() : nullptr;
   a.R = k.Rb;
   a.npairs = npairs;
@@ -736,6 +744,7 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
     SweepArgs a{};
     a.rec = c->rec.as<GapRec>();
     a.G = c->G.as<float>();
+    a.P = c->P;
     a.A = c->A.as<float>();
     a.R = Rb;
     a.npairs = Rb / 2;
@@ -879,6 +888,7 @@ mpr_status mpr_slab_half_sweep(mpr_ctx* c, int32_t sweep, int colour) {
   SweepArgs a{};
   a.rec = c->rec.as<GapRec>();
   a.G = c->G.as<float>();
+  a.P = c->P;
   a.A = avg ? c->A.as<float>() : nullptr;
   a.g_begin = g0;
   a.g_count = g1 - g0;

@@ -35,6 +35,25 @@ __device__ __forceinline__ Words4 philox4x32_10(uint32_t c0, uint32_t c1, uint32
   return Words4{c0, c1, c2, c3};
 }
 
+// The same function with the round keys precomputed (rk0[i] = k0 + i * 0x9E3779B9,
+// rk1[i] = k1 + i * 0xBB67AE85). Passed as kernel parameters they are constant-bank operands
+// of the LOP3s instead of 20 live registers.
+__device__ __forceinline__ Words4 philox4x32_10_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                   const uint32_t (&rk0)[10], const uint32_t (&rk1)[10]) {
+#pragma unroll
+  for (int round = 0; round < 10; ++round) {
+    const uint64_t p0 = static_cast<uint64_t>(0xD2511F53u) * c0;
+    const uint64_t p1 = static_cast<uint64_t>(0xCD9E8D57u) * c2;
+    const uint32_t hi0 = static_cast<uint32_t>(p0 >> 32), lo0 = static_cast<uint32_t>(p0);
+    const uint32_t hi1 = static_cast<uint32_t>(p1 >> 32), lo1 = static_cast<uint32_t>(p1);
+    c0 = hi1 ^ c1 ^ rk0[round];
+    c1 = lo1;
+    c2 = hi0 ^ c3 ^ rk1[round];
+    c3 = lo0;
+  }
+  return Words4{c0, c1, c2, c3};
+}
+
 // u(w) = (w >> 8) * 2^-24, exact.
 __device__ __forceinline__ float u24(uint32_t w) {
   return __fmul_rn(__uint2float_rn(w >> 8), 0x1p-24f);

@@ -88,11 +88,14 @@ struct SweepArgs {
   int64_t g_begin;   // first gap id of this colour
   int64_t g_count;   // gap sites of this colour (or of the list)
   const uint32_t* glist;  // nullable: gap ids of this phase (DC order), else the range
+  int64_t P;         // gap ids allocated in G (G holds P * R floats)
   int R;             // realization stride of the batch (even)
   int npairs;        // realization pairs in the batch
   uint32_t pair_base;// global pair index of pair 0 (= m_base / 2)
   uint32_t sweep;    // 1-based sweep index s
   uint32_t k0, k1;   // Philox key
+  uint32_t rk0[10], rk1[10];  // its round keys k + i * (0x9E3779B9, 0xBB67AE85), filled by
+                              // launch_sweep_half: kernel-parameter (constant-bank) operands
   float q, J;
   int is_b;          // colour B half-sweep
   int accumulate;    // add the new state to A (fixed window)

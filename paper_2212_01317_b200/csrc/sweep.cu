@@ -145,7 +145,8 @@ __device__ __forceinline__ bool all_present(uint32_t f) {
 
 // One work item (gap site, realization pair) once its record and the states it reads
 // are in registers: Philox, two Metropolis updates, store, fused epilogues.
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK>
+// BO: self_off is a byte offset into G / A (see the PF == 4 kernel path), else an element offset.
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO = false>
 __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& rec, float2 cur,
                                              const float2 (&nb)[4], uint32_t self_off, uint32_t pair,
                                              long long& e0, long long& e1, bool accum0, bool accum1) {
@@ -157,7 +158,7 @@ __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& r
       sel |= (a.is_b ? (ty != NB_NONE) : (ty == NB_KNOWN)) ? (1u << k) : 0u;
     }
   }
-  const Words4 w = philox4x32_10(rec.site, a.sweep, pair, 2u, a.k0, a.k1);
+  const Words4 w = philox4x32_10_rk(rec.site, a.sweep, pair, 2u, a.rk0, a.rk1);
   bool acc0, acc1;
   float n0, n1;
   if (PK) {
@@ -177,9 +178,12 @@ __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& r
     n0 = metropolis<QHALF, ENERGY, false, BFEXP>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
     n1 = metropolis<QHALF, ENERGY, false, BFEXP>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
   }
-  if (acc0 || acc1) *reinterpret_cast<float2*>(a.G + self_off) = make_float2(n0, n1);
+  float2* const gp = BO ? reinterpret_cast<float2*>(reinterpret_cast<char*>(a.G) + self_off)
+                        : reinterpret_cast<float2*>(a.G + self_off);
+  if (acc0 || acc1) *gp = make_float2(n0, n1);
   if (accum0 || accum1) {
-    float2* ap = reinterpret_cast<float2*>(a.A + self_off);
+    float2* ap = BO ? reinterpret_cast<float2*>(reinterpret_cast<char*>(a.A) + self_off)
+                    : reinterpret_cast<float2*>(a.A + self_off);
     float2 av = *ap;
     if (accum0) av.x = __fadd_rn(av.x, n0);
     if (accum1) av.y = __fadd_rn(av.y, n1);
@@ -254,7 +258,46 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
     // adaptive protocol: a pair whose two realizations have finished is frozen
     if (a.win_hi) live = static_cast<int>(a.sweep) <= max(a.win_hi[2 * sp.j], a.win_hi[2 * sp.j + 1]);
   }
-  if (live && PF == 3) {
+  if (live && PF == 4) {
+    // As PF == 3, with 32-bit BYTE offsets into G: base + u32 offset is IADD3 / IADD3.X on
+    // the ALU pipe instead of IMAD.WIDE.U32 on the FMA-heavy pipe the kernel saturates.
+    // Valid while P * R * 4 < 2^32 (launch_sweep_half checks and falls back to PF == 3).
+    const char* const Gb = reinterpret_cast<const char*>(a.G);
+    const uint32_t R4 = 4u * R, j2b = 4u * j2;
+    const uint32_t pair = a.pair_base + static_cast<uint32_t>(sp.j);
+    uint32_t g = sp.g0;
+    uint32_t gg = 0;
+    GapRec rec{};
+    if (g < gcount) {
+      gg = LIST ? a.glist[g] : gbegin + g;
+      rec = a.rec[gg];
+    }
+    for (; g < gcount; g += sp.gstride) {
+      const uint32_t gn = g + sp.gstride;
+      uint32_t ggn = 0;
+      GapRec recn{};
+      if (gn < gcount) {
+        ggn = LIST ? a.glist[gn] : gbegin + gn;
+        recn = a.rec[ggn];
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(Gb + (ggn * R4 + j2b)));
+      }
+      const uint32_t self_off = gg * R4 + j2b;
+      const float2 cur = *reinterpret_cast<const float2*>(Gb + self_off);
+      float2 nb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
+        if (ty == NB_GAP) {
+          nb[k] = *reinterpret_cast<const float2*>(Gb + (static_cast<uint32_t>(rec.nb[k]) * R4 + j2b));
+        } else {
+          nb[k] = f2(__int_as_float(rec.nb[k]));
+        }
+      }
+      process_item<QHALF, ENERGY, BFEXP, PK, true>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
+      rec = recn;
+      gg = ggn;
+    }
+  } else if (live && PF == 3) {
     // Record one item ahead: the 32-byte record of item g + gstride is loaded into registers
     // while item g computes, so an item waits for one dependent round trip (its neighbour
     // states), not two (record, then states). Plus the L2 prefetch of the next own state.
@@ -368,13 +411,15 @@ __global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X,
 }  // namespace
 
 // Kernel variants (tuning knob, MPR_SWEEP_VARIANT; profiles/r01_summary.md records every
-// alternative measured): 0 = plain, 2 = + register-free L2 prefetch of the next item,
-// 5 = 2 + branch-free exp, 8 = 5 capped at 64 registers (32 warps/SM), 10 = 5 on packed
-// f32x2 arithmetic, 11 = 10 capped at 64 registers, 12 (default) = 10 + record one item
-// ahead, 13 = 12 capped at 64 registers, 14 = 12 with 3 CTAs/SM declared.
-// Half-sweep, us: C2 v0 106.5, v2 103.3, v5 99.6, v8 101.8, v10 98.3, v11 99.7, v12 97.9;
-// C3 v5 2231, v10 2253, v12 2130; C4 v5 4149, v10 4138, v11 3958, v12 3797.
-// LIST: the gap ids of the phase come from a list (double-checkerboard order, row f3).
+// alternative measured). 0 = plain scalar, 2 = + register-free L2 prefetch of the next item,
+// 5 = 2 + branch-free exp, 8 = 5 at <= 64 registers; packed f32x2 arithmetic from here on:
+// 10 = 5 packed, 11 = 10 at <= 64 registers, 12 = 10 + record one item ahead (3 CTAs/SM),
+// 13 (default) = 12 at <= 64 registers (4 CTAs/SM), 15 / 16 / 17 = 12 with 32-bit byte
+// offsets at 1 / 3 / 4 CTAs/SM declared (fall back to 12 when P * R * 4 >= 2^32),
+// 18 / 19 = 12 / 15 at <= 51 registers (5 CTAs/SM).
+// Half-sweep, us (Philox round keys as kernel parameters, all variants bit-identical):
+//   C2: v5 98.2, v12 97.2, v13 93.9, v15 98.5, v17 95.4, v18 95.4;
+//   C3: v12 2113, v13 2071, v15 2201, v17 2088, v19 2067;  C4: v12 3778, v13 3717, v17 3697.
 template <bool Q, bool E, bool LIST>
 static void* sweep_kernel_ptr(int variant) {
   switch (variant) {
@@ -384,9 +429,13 @@ static void* sweep_kernel_ptr(int variant) {
     case 8: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 2, 256, true, LIST, false>);
     case 10: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, true>);
     case 11: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 2, 256, true, LIST, true>);
-    case 13: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);
-    case 14: return reinterpret_cast<void*>(k_sweep_half<Q, E, 3, 3, 256, true, LIST, true>);
-    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 3, 256, true, LIST, true>);  // 12
+    case 12: return reinterpret_cast<void*>(k_sweep_half<Q, E, 3, 3, 256, true, LIST, true>);
+    case 15: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 4, 256, true, LIST, true>);
+    case 16: return reinterpret_cast<void*>(k_sweep_half<Q, E, 3, 4, 256, true, LIST, true>);
+    case 17: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 4, 256, true, LIST, true>);
+    case 18: return reinterpret_cast<void*>(k_sweep_half<Q, E, 5, 3, 256, true, LIST, true>);
+    case 19: return reinterpret_cast<void*>(k_sweep_half<Q, E, 5, 4, 256, true, LIST, true>);
+    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);  // 13
   }
 }
 
@@ -408,6 +457,12 @@ int sweep_grid_size(int device, int variant) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, false, variant), sweep_threads(variant),
                                                 sweep_smem(variant));
+  if (variant == 15 || variant == 16 || variant == 17 || variant == 19) {  // may fall back to 12 at launch (large P * R): size the grid for both
+    int per12 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per12, sweep_kernel(true, false, false, 12), sweep_threads(12),
+                                                  sweep_smem(12));
+    if (per12 < per) per = per12;
+  }
   if (per < 1) per = 1;
   return sms * per;
 }
@@ -420,10 +475,17 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   const int64_t need = (a.npairs + nt - 1) / nt;  // active threads >= npairs
   if (g < need) g = need;
   if (g < 1) g = 1;
+  // byte-offset variant only while every byte offset into G fits in 32 bits
+  if ((variant == 15 || variant == 16 || variant == 17 || variant == 19) && a.P * static_cast<int64_t>(a.R) * 4 >= (int64_t{1} << 32)) variant = 12;
   const bool qhalf = (a.q == 0.5f);
   const bool energy = (a.energy != nullptr);
   void* fn = sweep_kernel(qhalf, energy, a.glist != nullptr, variant);
-  void* args[] = {const_cast<SweepArgs*>(&a)};
+  SweepArgs b = a;
+  for (int i = 0; i < 10; ++i) {
+    b.rk0[i] = a.k0 + static_cast<uint32_t>(i) * 0x9E3779B9u;
+    b.rk1[i] = a.k1 + static_cast<uint32_t>(i) * 0xBB67AE85u;
+  }
+  void* args[] = {&b};
   cudaLaunchKernel(fn, dim3(static_cast<unsigned>(g)), dim3(nt), args, sweep_smem(variant), st);
 }
 
