@@ -428,39 +428,61 @@ __global__ void __launch_bounds__(256) k_expand(const float* __restrict__ Tb, in
 }
 
 // One SST pass: clipped (2rs+1)^2 window mean with exact int64 window sums (ARITH §F).
-// 32x32 output tile per CTA; the (32+2rs)^2 input tile is converted once to fixed point
-// in shared memory, summed horizontally, then vertically.
+// 32x32 output tile per CTA of 32 x 8 threads: the (32+2rs)^2 input tile is converted once
+// to fixed point in shared memory, summed horizontally (one column per lane), then
+// vertically with a sliding window over the 4 output rows of each thread. Integer sums are
+// exact, so the order of the additions does not change a bit.
 __global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
                                                 float* __restrict__ Tout, int64_t Lx, int64_t Ly,
                                                 int rs) {
   extern __shared__ long long smem[];
-  const int W = kTile + 2 * rs;
-  long long* Q = smem;             // W x W
-  long long* H = smem + W * W;     // W x kTile
+  const int W = kTile + 2 * rs, w = 2 * rs + 1;
+  long long* Q = smem;             // W rows x W cols
+  long long* H = smem + W * W;     // W rows x kTile cols
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (int64_t)blockIdx.y * kTile;
-  for (int t = threadIdx.x; t < W * W; t += blockDim.x) {
-    const int y = t / W, x = t - y * W;
-    const int64_t r = r0 - rs + y, c = c0 - rs + x;
-    Q[t] = (r >= 0 && r < Ly && c >= 0 && c < Lx) ? __float2ll_rn(__fmul_rn(Tin[r * Lx + c], 0x1p40f)) : 0;
+  const bool interior = r0 - rs >= 0 && c0 - rs >= 0 && r0 + kTile + rs <= Ly && c0 + kTile + rs <= Lx;
+  if (interior) {  // whole halo tile inside the grid: no bounds checks, one row pointer per row
+    const float* base = Tin + (r0 - rs) * Lx + (c0 - rs);
+    for (int y = ty; y < W; y += 8) {
+      const float* row = base + y * Lx;
+      long long* q = Q + y * W;
+      for (int x = tx; x < W; x += 32) q[x] = __float2ll_rn(__fmul_rn(__ldg(row + x), 0x1p40f));
+    }
+  } else {
+    for (int y = ty; y < W; y += 8) {
+      const int64_t r = r0 - rs + y;
+      const bool rin = r >= 0 && r < Ly;
+      for (int x = tx; x < W; x += 32) {
+        const int64_t c = c0 - rs + x;
+        Q[y * W + x] = (rin && c >= 0 && c < Lx) ? __float2ll_rn(__fmul_rn(Tin[r * Lx + c], 0x1p40f)) : 0;
+      }
+    }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < W * kTile; t += blockDim.x) {
-    const int y = t / kTile, x = t - y * kTile;
+  for (int y = ty; y < W; y += 8) {
+    const long long* q = Q + y * W + tx;
     long long s = 0;
-    for (int d = 0; d <= 2 * rs; ++d) s += Q[y * W + x + d];
-    H[t] = s;
+    for (int d = 0; d < w; ++d) s += q[d];
+    H[y * kTile + tx] = s;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < kTile * kTile; t += blockDim.x) {
-    const int y = t / kTile, x = t - y * kTile;
-    const int64_t r = r0 + y, c = c0 + x;
-    if (r >= Ly || c >= Lx) continue;
-    long long s = 0;
-    for (int d = 0; d <= 2 * rs; ++d) s += H[(y + d) * kTile + x];
+  const int64_t c = c0 + tx;
+  if (c >= Lx) return;
+  const int64_t ca = c - rs > 0 ? c - rs : 0, cb = c + rs < Lx - 1 ? c + rs : Lx - 1;
+  const int ncol = static_cast<int>(cb - ca + 1);
+  const int yb = ty * (kTile / 8);
+  float* out = Tout + (r0 + yb) * Lx + c;
+  long long s = 0;
+  for (int d = 0; d < w; ++d) s += H[(yb + d) * kTile + tx];
+#pragma unroll
+  for (int k = 0; k < kTile / 8; ++k) {
+    const int64_t r = r0 + yb + k;
+    if (k > 0) s += H[(yb + k + w - 1) * kTile + tx] - H[(yb + k - 1) * kTile + tx];
+    if (r >= Ly) break;
     const int64_t ra = r - rs > 0 ? r - rs : 0, rb = r + rs < Ly - 1 ? r + rs : Ly - 1;
-    const int64_t ca = c - rs > 0 ? c - rs : 0, cb = c + rs < Lx - 1 ? c + rs : Lx - 1;
-    const double cnt = static_cast<double>((rb - ra + 1) * (cb - ca + 1));
-    Tout[r * Lx + c] = __double2float_rn(__ddiv_rn(__ll2double_rn(s) * 0x1p-40, cnt));
+    const double cnt = static_cast<double>(static_cast<int>(rb - ra + 1) * ncol);
+    out[k * Lx] = __double2float_rn(__ddiv_rn(__ll2double_rn(s) * 0x1p-40, cnt));
   }
 }
 

@@ -136,6 +136,21 @@ def test_small_blocks_many_fallbacks(P, calib):
     assert g["info"]["n_blocks_fallback"] > 0
 
 
+@pytest.mark.parametrize("rs,ns", [(0, 2), (1, 3), (3, 5), (7, 2), (16, 1)])
+def test_sst_field_bit_exact_window_sizes(P, calib, rs, ns):
+    """a5 at window widths 1..33 (r_s <= 16, the C-ABI limit) on a ragged grid large enough
+    for interior (no bounds check) and edge tiles of k_smooth: T is bit-exact vs the oracle."""
+    Tk, ek = calib
+    truth, z, mask = make_problem(161, 0.4, Lx=198, corr_len=8.0)
+    cfg = P.Config(r_s=rs, n_s=ns, l_b=16)
+    m = P.LeMpr(cfg, calib)
+    m.set_data(z, mask)
+    T = m.estimate_local_params(want_T=True)
+    m.close()
+    p = O.parameters(z, mask, ocfg(cfg), Tk, ek)
+    assert_bitwise(T, p.T, f"T field r_s={rs} n_s={ns}")
+
+
 def test_sharded_ranges_equal_single_call(P, calib):
     """simulate_range over [0,4) then [4,10) == simulate(10) bit for bit (global realization ids)."""
     truth, z, mask = make_problem(40, 0.5, corr_len=6.0)
