@@ -467,3 +467,41 @@ def test_every_sweep_variant_bit_exact(P, calib, variant, monkeypatch):
     compare(P, z, mask, truth, P.Config(), calib, 7, 9, 1234 + variant, energy=True)
     compare(P, z, mask, truth, P.Config(q=0.35, J=1.3, r_s=1), calib, 4, 6, 99)
     compare(P, z, mask, truth, P.Config(order="dc", l_b=8, r_s=1), calib, 5, 6, 7)
+
+
+def _fuzz_case(k):
+    """Seeded random small problem + configuration (case k)."""
+    rng = np.random.default_rng(9000 + k)
+    Ly, Lx = int(rng.integers(2, 41)), int(rng.integers(2, 41))
+    p = float(rng.uniform(0.05, 0.95))
+    gaps = "cloud" if (rng.random() < 0.3 and min(Ly, Lx) >= 8) else "random"
+    truth, z, mask = make_problem(Ly, p, Lx=Lx, gaps=gaps, corr_len=float(rng.uniform(2, 12)),
+                                  seed_field=int(rng.integers(1 << 30)), seed_mask=int(rng.integers(1 << 30)))
+    order = "dc" if rng.random() < 0.25 else "sc"
+    cfg_kw = dict(l_b=int(rng.integers(2, 48)), r_s=int(rng.integers(0, 5)), n_s=int(rng.integers(0, 4)),
+                  q=0.5 if rng.random() < 0.5 else float(rng.uniform(0.1, 0.5)), J=float(rng.uniform(0.5, 2.0)),
+                  init="random" if rng.random() < 0.5 else "block_mean", order=order,
+                  max_batch=int(rng.choice([0, 2, 4])))
+    M, S = int(rng.integers(1, 8)), int(rng.integers(1, 9))
+    cfg_kw["n_avg"] = 1 if rng.random() < 0.7 else int(rng.integers(1, S + 1))
+    return truth, z, mask, cfg_kw, M, S, int(rng.integers(1 << 40)), order == "sc"
+
+
+@pytest.mark.parametrize("k", range(150))
+def test_fuzz_small_problems_bit_exact(P, calib, k):
+    """Randomised small problems (2..40 sites per side, any missing ratio, random or cloud
+    gaps) under random configurations (l_b, r_s, n_s, q, J, init, SC/DC order, batch
+    splits, M, S, n_avg): states bit-exact vs the oracle (predictions too when n_avg = 1,
+    else within the n_avg tolerance), or the same rejection on both sides."""
+    truth, z, mask, cfg_kw, M, S, seed, energy = _fuzz_case(k)
+    cfg = P.Config(**cfg_kw)
+    Tk, ek = calib
+    if O.parameters(z, mask, ocfg(cfg), Tk, ek).status < 0:
+        # the oracle rejects the problem (too few samples / no sample bond): so must the library
+        m = P.LeMpr(cfg, calib)
+        with pytest.raises(P.MprError):
+            m.set_data(z, mask)
+            m.estimate_local_params()
+        m.close()
+        return
+    compare(P, z, mask, truth, cfg, calib, M, S, seed, energy=energy, exact_pred=cfg.n_avg == 1)
