@@ -630,11 +630,10 @@ void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int rs
                    cudaStream_t st) {
   const int W = kTile + 2 * rs;
   const size_t smem = sizeof(long long) * (static_cast<size_t>(W) * W + static_cast<size_t>(W) * kTile);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_smooth, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  // > 48 KB of dynamic shared memory needs the opt-in, per device: set it on the calling
+  // thread's current device whenever a large window asks for it (r_s >= 16)
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_smooth, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((Ly + kTile - 1) / kTile));
   k_smooth<<<grid, 256, smem, st>>>(Tin, Tout, Lx, Ly, rs);
 }
