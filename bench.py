@@ -336,7 +336,8 @@ def run_mpr(args):
                            "l2": "flushed between timed steps (256 MiB write, outside the events)"},
                 "fill_time_ms": total_ms / args.steps,
                 "gpu_launches": int(launches),
-                "roofline": {"bound": "alu", "kernel": "k_sweep_half", "achieved": alu_achieved,
+                "roofline": {"bound": "alu", "kernel": sweep_kernel_name(info.get("sweep_variant", 0), info.get("batch", 0)),
+                             "achieved": alu_achieved,
                              "peak": alu_peak, "unit": "Gop/s",
                              "frac": (alu_achieved / alu_peak) if alu_achieved else None,
                              "traffic": traffic,
@@ -362,6 +363,14 @@ def run_mpr(args):
     if ws > 1:
         dist.destroy_process_group()
     return 0
+
+
+def sweep_kernel_name(variant, batch):
+    """Name of the half-sweep kernel the library launched (mpr_info.sweep_variant and the
+    realization batch: the quad kernel needs an even pair count)."""
+    if variant in (22, 23) and batch % 4 == 0:
+        return f"k_sweep_quad (variant {variant}: two realization pairs per thread)"
+    return f"k_sweep_half (variant {13 if variant in (22, 23) else variant})"
 
 
 def main():

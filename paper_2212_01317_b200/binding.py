@@ -51,7 +51,8 @@ class mpr_info(C.Structure):
                 ("degenerate_range", C.c_int), ("n_blocks", C.c_int64), ("n_blocks_fallback", C.c_int64),
                 ("median_T", C.c_float), ("M", C.c_int64), ("sweeps", C.c_int64), ("batch", C.c_int64),
                 ("kernel_launches", C.c_int64), ("total_launches", C.c_int64), ("sweep_launches", C.c_int64),
-                ("sweep_ms", C.c_double), ("last_m_base", C.c_int64), ("last_batch", C.c_int64)]
+                ("sweep_ms", C.c_double), ("last_m_base", C.c_int64), ("last_batch", C.c_int64),
+                ("sweep_variant", C.c_int32)]
 
 
 _lib = None

@@ -370,6 +370,75 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   if (ENERGY) energy_epilogue(a, a.npairs, sp.active && live, sp.j, e0, e1);
 }
 
+// Two realization pairs (four realizations) of one gap site per thread: the record, the
+// flag decoding, the neighbour addresses and the loop overhead are shared by both pairs,
+// and the own / neighbour states move as float4. Each pair still draws its own Philox
+// call and runs metropolis_pair, so the results are those of k_sweep_half bit for bit.
+// Requires an even number of pairs and no energy trace (launch_sweep_half falls back).
+template <bool QHALF, int MINB, bool LIST>
+__global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
+  const int nq = a.npairs / 2;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int total = gridDim.x * blockDim.x;
+  const int active = (total / nq) * nq;
+  if (tid >= active) return;
+  const int jq = tid % nq;
+  const uint32_t gstride = static_cast<uint32_t>(active / nq);
+  const uint32_t R = static_cast<uint32_t>(a.R), j4 = 4u * static_cast<uint32_t>(jq);
+  const uint32_t gcount = static_cast<uint32_t>(a.g_count), gbegin = static_cast<uint32_t>(a.g_begin);
+  bool accA0, accA1, accB0, accB1;
+  accum_flags(a, 2 * jq, accA0, accA1);
+  accum_flags(a, 2 * jq + 1, accB0, accB1);
+  bool liveA = true, liveB = true;
+  if (a.win_hi) {  // adaptive protocol: a pair whose two realizations have finished is frozen
+    const int sw = static_cast<int>(a.sweep);
+    liveA = sw <= max(a.win_hi[4 * jq], a.win_hi[4 * jq + 1]);
+    liveB = sw <= max(a.win_hi[4 * jq + 2], a.win_hi[4 * jq + 3]);
+    if (!liveA && !liveB) return;
+  }
+  const uint32_t pairA = a.pair_base + 2u * static_cast<uint32_t>(jq), pairB = pairA + 1u;
+  long long e0 = 0, e1 = 0;  // unused (no energy trace in this kernel)
+  uint32_t g = static_cast<uint32_t>(tid / nq);
+  uint32_t gg = 0;
+  GapRec rec{};
+  if (g < gcount) {
+    gg = LIST ? a.glist[g] : gbegin + g;
+    rec = a.rec[gg];
+  }
+  for (; g < gcount; g += gstride) {
+    const uint32_t gn = g + gstride;
+    uint32_t ggn = 0;
+    GapRec recn{};
+    if (gn < gcount) {
+      ggn = LIST ? a.glist[gn] : gbegin + gn;
+      recn = a.rec[ggn];
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.G + (ggn * R + j4)));
+    }
+    const uint32_t self_off = gg * R + j4;
+    const float4 cur = *reinterpret_cast<const float4*>(a.G + self_off);
+    float2 nbA[4], nbB[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
+      if (ty == NB_GAP) {
+        const float4 v = *reinterpret_cast<const float4*>(a.G + (static_cast<uint32_t>(rec.nb[k]) * R + j4));
+        nbA[k] = make_float2(v.x, v.y);
+        nbB[k] = make_float2(v.z, v.w);
+      } else {
+        nbA[k] = nbB[k] = f2(__int_as_float(rec.nb[k]));
+      }
+    }
+    if (liveA)
+      process_item<QHALF, false, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off, pairA, e0, e1,
+                                             accA0, accA1);
+    if (liveB)
+      process_item<QHALF, false, true, true>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 2u, pairB, e0,
+                                             e1, accB0, accB1);
+    rec = recn;
+    gg = ggn;
+  }
+}
+
 // a6: initial states of a batch (ARITH §G).
 __global__ void __launch_bounds__(256) k_init_states(const GapRec* __restrict__ rec,
                                                      float* __restrict__ G, float* __restrict__ A,
@@ -416,10 +485,13 @@ __global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X,
 // 10 = 5 packed, 11 = 10 at <= 64 registers, 12 = 10 + record one item ahead (3 CTAs/SM),
 // 13 (default) = 12 at <= 64 registers (4 CTAs/SM), 15 / 16 / 17 = 12 with 32-bit byte
 // offsets at 1 / 3 / 4 CTAs/SM declared (fall back to 12 when P * R * 4 >= 2^32),
-// 18 / 19 = 12 / 15 at <= 51 registers (5 CTAs/SM).
+// 18 / 19 = 12 / 15 at <= 51 registers (5 CTAs/SM), 22 (default) / 23 = k_sweep_quad (two
+// pairs per thread, float4 state moves) at 4 / 3 CTAs/SM (fall back to 13 for an odd pair
+// count or the energy trace).
 // Half-sweep, us (Philox round keys as kernel parameters, all variants bit-identical):
 //   C2: v5 98.2, v12 97.2, v13 93.9, v15 98.5, v17 95.4, v18 95.4;
-//   C3: v12 2113, v13 2071, v15 2201, v17 2088, v19 2067;  C4: v12 3778, v13 3717, v17 3697.
+//   C3: v12 2113, v13 2071, v15 2201, v17 2088, v19 2067;  C4: v12 3778, v13 3717, v17 3697;
+//   v22: C2 87.1, C3 1838, C4 (batches 8 + 2) 3402.
 template <bool Q, bool E, bool LIST>
 static void* sweep_kernel_ptr(int variant) {
   switch (variant) {
@@ -435,7 +507,7 @@ static void* sweep_kernel_ptr(int variant) {
     case 17: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 4, 256, true, LIST, true>);
     case 18: return reinterpret_cast<void*>(k_sweep_half<Q, E, 5, 3, 256, true, LIST, true>);
     case 19: return reinterpret_cast<void*>(k_sweep_half<Q, E, 5, 4, 256, true, LIST, true>);
-    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);  // 13
+    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);  // 13 (and 22/23's fallback)
   }
 }
 
@@ -443,7 +515,19 @@ static int sweep_threads(int) { return 256; }
 
 static size_t sweep_smem(int) { return 0; }
 
+static bool is_quad(int variant) { return variant == 22 || variant == 23; }
+
+static void* quad_kernel(bool qhalf, bool list, int variant) {
+  if (variant == 23) {
+    if (list) return qhalf ? reinterpret_cast<void*>(k_sweep_quad<true, 3, true>) : reinterpret_cast<void*>(k_sweep_quad<false, 3, true>);
+    return qhalf ? reinterpret_cast<void*>(k_sweep_quad<true, 3, false>) : reinterpret_cast<void*>(k_sweep_quad<false, 3, false>);
+  }
+  if (list) return qhalf ? reinterpret_cast<void*>(k_sweep_quad<true, 4, true>) : reinterpret_cast<void*>(k_sweep_quad<false, 4, true>);
+  return qhalf ? reinterpret_cast<void*>(k_sweep_quad<true, 4, false>) : reinterpret_cast<void*>(k_sweep_quad<false, 4, false>);
+}
+
 static void* sweep_kernel(bool qhalf, bool energy, bool list, int variant) {
+  if (is_quad(variant)) return quad_kernel(qhalf, list, variant);
   if (list) {
     if (qhalf) return energy ? sweep_kernel_ptr<true, true, true>(variant) : sweep_kernel_ptr<true, false, true>(variant);
     return energy ? sweep_kernel_ptr<false, true, true>(variant) : sweep_kernel_ptr<false, false, true>(variant);
@@ -457,28 +541,37 @@ int sweep_grid_size(int device, int variant) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, false, variant), sweep_threads(variant),
                                                 sweep_smem(variant));
-  if (variant == 15 || variant == 16 || variant == 17 || variant == 19) {  // may fall back to 12 at launch (large P * R): size the grid for both
-    int per12 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per12, sweep_kernel(true, false, false, 12), sweep_threads(12),
-                                                  sweep_smem(12));
-    if (per12 < per) per = per12;
+  // variants that may fall back at launch (byte offsets: large P * R -> 12; quads: odd
+  // pair count or energy trace -> 13): size the grid for both kernels
+  const int fb = (variant == 15 || variant == 16 || variant == 17 || variant == 19) ? 12 : is_quad(variant) ? 13 : -1;
+  if (fb >= 0) {
+    int perf = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perf, sweep_kernel(true, false, false, fb), sweep_threads(fb),
+                                                  sweep_smem(fb));
+    if (perf < per) per = perf;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perf, sweep_kernel(true, true, false, fb), sweep_threads(fb),
+                                                  sweep_smem(fb));
+    if (perf < per) per = perf;
   }
   if (per < 1) per = 1;
   return sms * per;
 }
 
 void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st) {
-  const int nt = sweep_threads(variant);
-  const int64_t items = a.g_count * a.npairs;
-  int64_t g = (items + nt - 1) / nt;
-  if (g > grid) g = grid;
-  const int64_t need = (a.npairs + nt - 1) / nt;  // active threads >= npairs
-  if (g < need) g = need;
-  if (g < 1) g = 1;
-  // byte-offset variant only while every byte offset into G fits in 32 bits
-  if ((variant == 15 || variant == 16 || variant == 17 || variant == 19) && a.P * static_cast<int64_t>(a.R) * 4 >= (int64_t{1} << 32)) variant = 12;
   const bool qhalf = (a.q == 0.5f);
   const bool energy = (a.energy != nullptr);
+  // byte-offset variant only while every byte offset into G fits in 32 bits
+  if ((variant == 15 || variant == 16 || variant == 17 || variant == 19) && a.P * static_cast<int64_t>(a.R) * 4 >= (int64_t{1} << 32)) variant = 12;
+  // quad variants: an even number of pairs (float4 alignment) and no energy trace
+  if (is_quad(variant) && (energy || (a.npairs & 1))) variant = 13;
+  const int nt = sweep_threads(variant);
+  const int64_t units = is_quad(variant) ? a.npairs / 2 : a.npairs;  // threads per gap site
+  const int64_t items = a.g_count * units;
+  int64_t g = (items + nt - 1) / nt;
+  if (g > grid) g = grid;
+  const int64_t need = (units + nt - 1) / nt;  // active threads >= units
+  if (g < need) g = need;
+  if (g < 1) g = 1;
   void* fn = sweep_kernel(qhalf, energy, a.glist != nullptr, variant);
   SweepArgs b = a;
   for (int i = 0; i < 10; ++i) {

@@ -457,16 +457,20 @@ def test_adaptive_with_slope_tolerance(P, calib):
     assert_bitwise(pred, O.predict(np.nan_to_num(z), mask, r["acc"], 4, 1, p.zmin, p.zmax, 0), "predictions")
 
 
-@pytest.mark.parametrize("variant", [0, 2, 5, 8, 10, 11, 12, 13, 15, 16, 17, 18, 19])
+@pytest.mark.parametrize("variant", [0, 2, 5, 8, 10, 11, 12, 13, 15, 16, 17, 18, 19, 22, 23])
 def test_every_sweep_variant_bit_exact(P, calib, variant, monkeypatch):
     """Each half-sweep kernel variant (scalar / packed f32x2 arithmetic, prefetch, record one
-    item ahead, register caps; MPR_SWEEP_VARIANT) reproduces the oracle bit for bit: q = 1/2
-    with the energy trace, generic q, and the DC order (glist path)."""
+    item ahead, register caps, byte offsets, two pairs per thread; MPR_SWEEP_VARIANT)
+    reproduces the oracle bit for bit: q = 1/2 with the energy trace, generic q, the DC
+    order (glist path), and even pair counts without energy (the quad kernels' domain)."""
     monkeypatch.setenv("MPR_SWEEP_VARIANT", str(variant))
     truth, z, mask = make_problem(48, 0.45, Lx=53, corr_len=6.0)
     compare(P, z, mask, truth, P.Config(), calib, 7, 9, 1234 + variant, energy=True)
     compare(P, z, mask, truth, P.Config(q=0.35, J=1.3, r_s=1), calib, 4, 6, 99)
     compare(P, z, mask, truth, P.Config(order="dc", l_b=8, r_s=1), calib, 5, 6, 7)
+    # even pair counts without the energy trace (the quad-pair kernels run, no fallback)
+    compare(P, z, mask, truth, P.Config(), calib, 8, 7, 55)
+    compare(P, z, mask, truth, P.Config(order="dc", l_b=8, max_batch=4), calib, 12, 5, 56)
 
 
 def _fuzz_case(k):
