@@ -374,68 +374,86 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
 // flag decoding, the neighbour addresses and the loop overhead are shared by both pairs,
 // and the own / neighbour states move as float4. Each pair still draws its own Philox
 // call and runs metropolis_pair, so the results are those of k_sweep_half bit for bit.
-// Requires an even number of pairs and no energy trace (launch_sweep_half falls back).
-template <bool QHALF, int MINB, bool LIST>
+// Requires an even number of pairs (float4 alignment; launch_sweep_half falls back).
+template <bool QHALF, bool ENERGY, int MINB, bool LIST>
 __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
   const int nq = a.npairs / 2;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int total = gridDim.x * blockDim.x;
-  const int active = (total / nq) * nq;
-  if (tid >= active) return;
+  const int nactive = (total / nq) * nq;
+  const bool active = tid < nactive;
   const int jq = tid % nq;
-  const uint32_t gstride = static_cast<uint32_t>(active / nq);
+  const uint32_t gstride = static_cast<uint32_t>(nactive / nq);
   const uint32_t R = static_cast<uint32_t>(a.R), j4 = 4u * static_cast<uint32_t>(jq);
   const uint32_t gcount = static_cast<uint32_t>(a.g_count), gbegin = static_cast<uint32_t>(a.g_begin);
-  bool accA0, accA1, accB0, accB1;
-  accum_flags(a, 2 * jq, accA0, accA1);
-  accum_flags(a, 2 * jq + 1, accB0, accB1);
-  bool liveA = true, liveB = true;
-  if (a.win_hi) {  // adaptive protocol: a pair whose two realizations have finished is frozen
-    const int sw = static_cast<int>(a.sweep);
-    liveA = sw <= max(a.win_hi[4 * jq], a.win_hi[4 * jq + 1]);
-    liveB = sw <= max(a.win_hi[4 * jq + 2], a.win_hi[4 * jq + 3]);
-    if (!liveA && !liveB) return;
+  bool accA0 = false, accA1 = false, accB0 = false, accB1 = false;
+  bool liveA = active, liveB = active;
+  if (active) {
+    accum_flags(a, 2 * jq, accA0, accA1);
+    accum_flags(a, 2 * jq + 1, accB0, accB1);
+    if (a.win_hi) {  // adaptive protocol: a pair whose two realizations have finished is frozen
+      const int sw = static_cast<int>(a.sweep);
+      liveA = sw <= max(a.win_hi[4 * jq], a.win_hi[4 * jq + 1]);
+      liveB = sw <= max(a.win_hi[4 * jq + 2], a.win_hi[4 * jq + 3]);
+    }
   }
   const uint32_t pairA = a.pair_base + 2u * static_cast<uint32_t>(jq), pairB = pairA + 1u;
-  long long e0 = 0, e1 = 0;  // unused (no energy trace in this kernel)
-  uint32_t g = static_cast<uint32_t>(tid / nq);
-  uint32_t gg = 0;
-  GapRec rec{};
-  if (g < gcount) {
-    gg = LIST ? a.glist[g] : gbegin + g;
-    rec = a.rec[gg];
-  }
-  for (; g < gcount; g += gstride) {
-    const uint32_t gn = g + gstride;
-    uint32_t ggn = 0;
-    GapRec recn{};
-    if (gn < gcount) {
-      ggn = LIST ? a.glist[gn] : gbegin + gn;
-      recn = a.rec[ggn];
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.G + (ggn * R + j4)));
+  long long eA0 = 0, eA1 = 0, eB0 = 0, eB1 = 0;
+  if (liveA || liveB) {
+    uint32_t g = static_cast<uint32_t>(tid / nq);
+    uint32_t gg = 0;
+    GapRec rec{};
+    if (g < gcount) {
+      gg = LIST ? a.glist[g] : gbegin + g;
+      rec = a.rec[gg];
     }
-    const uint32_t self_off = gg * R + j4;
-    const float4 cur = *reinterpret_cast<const float4*>(a.G + self_off);
-    float2 nbA[4], nbB[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
-      if (ty == NB_GAP) {
-        const float4 v = *reinterpret_cast<const float4*>(a.G + (static_cast<uint32_t>(rec.nb[k]) * R + j4));
-        nbA[k] = make_float2(v.x, v.y);
-        nbB[k] = make_float2(v.z, v.w);
-      } else {
-        nbA[k] = nbB[k] = f2(__int_as_float(rec.nb[k]));
+    for (; g < gcount; g += gstride) {
+      const uint32_t gn = g + gstride;
+      uint32_t ggn = 0;
+      GapRec recn{};
+      if (gn < gcount) {
+        ggn = LIST ? a.glist[gn] : gbegin + gn;
+        recn = a.rec[ggn];
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.G + (ggn * R + j4)));
       }
+      const uint32_t self_off = gg * R + j4;
+      const float4 cur = *reinterpret_cast<const float4*>(a.G + self_off);
+      float2 nbA[4], nbB[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
+        if (ty == NB_GAP) {
+          const float4 v = *reinterpret_cast<const float4*>(a.G + (static_cast<uint32_t>(rec.nb[k]) * R + j4));
+          nbA[k] = make_float2(v.x, v.y);
+          nbB[k] = make_float2(v.z, v.w);
+        } else {
+          nbA[k] = nbB[k] = f2(__int_as_float(rec.nb[k]));
+        }
+      }
+      if (liveA)
+        process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off, pairA, eA0, eA1,
+                                                accA0, accA1);
+      if (liveB)
+        process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 2u, pairB, eB0,
+                                                eB1, accB0, accB1);
+      rec = recn;
+      gg = ggn;
     }
-    if (liveA)
-      process_item<QHALF, false, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off, pairA, e0, e1,
-                                             accA0, accA1);
-    if (liveB)
-      process_item<QHALF, false, true, true>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 2u, pairB, e0,
-                                             e1, accB0, accB1);
-    rec = recn;
-    gg = ggn;
+  }
+  if (ENERGY) {  // a8 epilogue for realizations 4jq .. 4jq+3 (as energy_epilogue)
+    __shared__ unsigned long long es[2 * kMaxPairs];
+    for (int t = threadIdx.x; t < 2 * a.npairs; t += blockDim.x) es[t] = 0ull;
+    __syncthreads();
+    if (active && (eA0 != 0 || eA1 != 0 || eB0 != 0 || eB1 != 0)) {
+      atomicAdd(&es[4 * jq], static_cast<unsigned long long>(eA0));
+      atomicAdd(&es[4 * jq + 1], static_cast<unsigned long long>(eA1));
+      atomicAdd(&es[4 * jq + 2], static_cast<unsigned long long>(eB0));
+      atomicAdd(&es[4 * jq + 3], static_cast<unsigned long long>(eB1));
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 2 * a.npairs; t += blockDim.x)
+      if (t >= a.r_valid_lo && t < a.r_valid_hi && es[t] != 0ull)
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.energy + static_cast<int64_t>(t) * a.energy_stride), es[t]);
   }
 }
 
@@ -487,7 +505,7 @@ __global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X,
 // offsets at 1 / 3 / 4 CTAs/SM declared (fall back to 12 when P * R * 4 >= 2^32),
 // 18 / 19 = 12 / 15 at <= 51 registers (5 CTAs/SM), 22 (default) / 23 = k_sweep_quad (two
 // pairs per thread, float4 state moves) at 4 / 3 CTAs/SM (fall back to 13 for an odd pair
-// count or the energy trace).
+// count).
 // Half-sweep, us (Philox round keys as kernel parameters, all variants bit-identical):
 //   C2: v5 98.2, v12 97.2, v13 93.9, v15 98.5, v17 95.4, v18 95.4;
 //   C3: v12 2113, v13 2071, v15 2201, v17 2088, v19 2067;  C4: v12 3778, v13 3717, v17 3697;
@@ -517,17 +535,20 @@ static size_t sweep_smem(int) { return 0; }
 
 static bool is_quad(int variant) { return variant == 22 || variant == 23; }
 
-static void* quad_kernel(bool qhalf, bool list, int variant) {
-  if (variant == 23) {
-    if (list) return qhalf ? reinterpret_cast<void*>(k_sweep_quad<true, 3, true>) : reinterpret_cast<void*>(k_sweep_quad<false, 3, true>);
-    return qhalf ? reinterpret_cast<void*>(k_sweep_quad<true, 3, false>) : reinterpret_cast<void*>(k_sweep_quad<false, 3, false>);
-  }
-  if (list) return qhalf ? reinterpret_cast<void*>(k_sweep_quad<true, 4, true>) : reinterpret_cast<void*>(k_sweep_quad<false, 4, true>);
-  return qhalf ? reinterpret_cast<void*>(k_sweep_quad<true, 4, false>) : reinterpret_cast<void*>(k_sweep_quad<false, 4, false>);
+template <bool Q, bool E>
+static void* quad_kernel_ptr(bool list, int variant) {
+  if (variant == 23)
+    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false>);
+  return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false>);
+}
+
+static void* quad_kernel(bool qhalf, bool energy, bool list, int variant) {
+  if (qhalf) return energy ? quad_kernel_ptr<true, true>(list, variant) : quad_kernel_ptr<true, false>(list, variant);
+  return energy ? quad_kernel_ptr<false, true>(list, variant) : quad_kernel_ptr<false, false>(list, variant);
 }
 
 static void* sweep_kernel(bool qhalf, bool energy, bool list, int variant) {
-  if (is_quad(variant)) return quad_kernel(qhalf, list, variant);
+  if (is_quad(variant)) return quad_kernel(qhalf, energy, list, variant);
   if (list) {
     if (qhalf) return energy ? sweep_kernel_ptr<true, true, true>(variant) : sweep_kernel_ptr<true, false, true>(variant);
     return energy ? sweep_kernel_ptr<false, true, true>(variant) : sweep_kernel_ptr<false, false, true>(variant);
@@ -562,8 +583,8 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   const bool energy = (a.energy != nullptr);
   // byte-offset variant only while every byte offset into G fits in 32 bits
   if ((variant == 15 || variant == 16 || variant == 17 || variant == 19) && a.P * static_cast<int64_t>(a.R) * 4 >= (int64_t{1} << 32)) variant = 12;
-  // quad variants: an even number of pairs (float4 alignment) and no energy trace
-  if (is_quad(variant) && (energy || (a.npairs & 1))) variant = 13;
+  // quad variants need an even number of pairs (float4 alignment)
+  if (is_quad(variant) && (a.npairs & 1)) variant = 13;
   const int nt = sweep_threads(variant);
   const int64_t units = is_quad(variant) ? a.npairs / 2 : a.npairs;  // threads per gap site
   const int64_t items = a.g_count * units;
