@@ -370,36 +370,49 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   if (ENERGY) energy_epilogue(a, a.npairs, sp.active && live, sp.j, e0, e1);
 }
 
-// Two realization pairs (four realizations) of one gap site per thread: the record, the
-// flag decoding, the neighbour addresses and the loop overhead are shared by both pairs,
-// and the own / neighbour states move as float4. Each pair still draws its own Philox
-// call and runs metropolis_pair, so the results are those of k_sweep_half bit for bit.
-// Requires an even number of pairs (float4 alignment; launch_sweep_half falls back).
-template <bool QHALF, bool ENERGY, int MINB, bool LIST>
+// NP realization pairs (2 NP realizations) of one gap site per thread (NP = 2; NP = 4 was
+// measured no faster: profiles/r01_summary.md): the
+// record, the flag decoding, the neighbour addresses and the loop overhead are shared by
+// the NP pairs, and the own / neighbour states move as float4 (two pairs each). Each pair
+// still draws its own Philox call and runs metropolis_pair, so the results are those of
+// k_sweep_half bit for bit. Requires npairs % NP == 0 (launch_sweep_half falls back).
+template <bool QHALF, bool ENERGY, int MINB, bool LIST, int NP = 2>
 __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
-  const int nq = a.npairs / 2;
+  constexpr int NQ = NP / 2;  // float4 quads per thread
+  const int nq = a.npairs / NP;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int total = gridDim.x * blockDim.x;
   const int nactive = (total / nq) * nq;
   const bool active = tid < nactive;
   const int jq = tid % nq;
   const uint32_t gstride = static_cast<uint32_t>(nactive / nq);
-  const uint32_t R = static_cast<uint32_t>(a.R), j4 = 4u * static_cast<uint32_t>(jq);
+  const uint32_t R = static_cast<uint32_t>(a.R), j4 = 2u * NP * static_cast<uint32_t>(jq);
   const uint32_t gcount = static_cast<uint32_t>(a.g_count), gbegin = static_cast<uint32_t>(a.g_begin);
-  bool accA0 = false, accA1 = false, accB0 = false, accB1 = false;
-  bool liveA = active, liveB = active;
+  bool acc[NP][2];
+  bool live[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    acc[p][0] = acc[p][1] = false;
+    live[p] = active;
+  }
   if (active) {
-    accum_flags(a, 2 * jq, accA0, accA1);
-    accum_flags(a, 2 * jq + 1, accB0, accB1);
-    if (a.win_hi) {  // adaptive protocol: a pair whose two realizations have finished is frozen
-      const int sw = static_cast<int>(a.sweep);
-      liveA = sw <= max(a.win_hi[4 * jq], a.win_hi[4 * jq + 1]);
-      liveB = sw <= max(a.win_hi[4 * jq + 2], a.win_hi[4 * jq + 3]);
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      accum_flags(a, NP * jq + p, acc[p][0], acc[p][1]);
+      if (a.win_hi) {  // adaptive protocol: a pair whose two realizations have finished is frozen
+        const int sw = static_cast<int>(a.sweep), r = 2 * (NP * jq + p);
+        live[p] = sw <= max(a.win_hi[r], a.win_hi[r + 1]);
+      }
     }
   }
-  const uint32_t pairA = a.pair_base + 2u * static_cast<uint32_t>(jq), pairB = pairA + 1u;
-  long long eA0 = 0, eA1 = 0, eB0 = 0, eB1 = 0;
-  if (liveA || liveB) {
+  bool any_live = false;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) any_live |= live[p];
+  const uint32_t pair0 = a.pair_base + static_cast<uint32_t>(NP * jq);
+  long long e[NP][2];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) e[p][0] = e[p][1] = 0;
+  if (any_live) {
     uint32_t g = static_cast<uint32_t>(tid / nq);
     uint32_t gg = 0;
     GapRec rec{};
@@ -417,38 +430,46 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
         asm volatile("prefetch.global.L2 [%0];" ::"l"(a.G + (ggn * R + j4)));
       }
       const uint32_t self_off = gg * R + j4;
-      const float4 cur = *reinterpret_cast<const float4*>(a.G + self_off);
-      float2 nbA[4], nbB[4];
+      uint32_t nb_off[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
-        if (ty == NB_GAP) {
-          const float4 v = *reinterpret_cast<const float4*>(a.G + (static_cast<uint32_t>(rec.nb[k]) * R + j4));
-          nbA[k] = make_float2(v.x, v.y);
-          nbB[k] = make_float2(v.z, v.w);
-        } else {
-          nbA[k] = nbB[k] = f2(__int_as_float(rec.nb[k]));
+      for (int k = 0; k < 4; ++k) nb_off[k] = static_cast<uint32_t>(rec.nb[k]) * R + j4;
+#pragma unroll
+      for (int qd = 0; qd < NQ; ++qd) {
+        const float4 cur = *reinterpret_cast<const float4*>(a.G + self_off + 4u * qd);
+        float2 nbA[4], nbB[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
+          if (ty == NB_GAP) {
+            const float4 v = *reinterpret_cast<const float4*>(a.G + nb_off[k] + 4u * qd);
+            nbA[k] = make_float2(v.x, v.y);
+            nbB[k] = make_float2(v.z, v.w);
+          } else {
+            nbA[k] = nbB[k] = f2(__int_as_float(rec.nb[k]));
+          }
         }
+        const int pa = 2 * qd, pb = 2 * qd + 1;
+        if (live[pa])
+          process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
+                                                  pair0 + pa, e[pa][0], e[pa][1], acc[pa][0], acc[pa][1]);
+        if (live[pb])
+          process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 4u * qd + 2u,
+                                                  pair0 + pb, e[pb][0], e[pb][1], acc[pb][0], acc[pb][1]);
       }
-      if (liveA)
-        process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off, pairA, eA0, eA1,
-                                                accA0, accA1);
-      if (liveB)
-        process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 2u, pairB, eB0,
-                                                eB1, accB0, accB1);
       rec = recn;
       gg = ggn;
     }
   }
-  if (ENERGY) {  // a8 epilogue for realizations 4jq .. 4jq+3 (as energy_epilogue)
+  if (ENERGY) {  // a8 epilogue for realizations 2 NP jq .. 2 NP jq + 2 NP - 1 (as energy_epilogue)
     __shared__ unsigned long long es[2 * kMaxPairs];
     for (int t = threadIdx.x; t < 2 * a.npairs; t += blockDim.x) es[t] = 0ull;
     __syncthreads();
-    if (active && (eA0 != 0 || eA1 != 0 || eB0 != 0 || eB1 != 0)) {
-      atomicAdd(&es[4 * jq], static_cast<unsigned long long>(eA0));
-      atomicAdd(&es[4 * jq + 1], static_cast<unsigned long long>(eA1));
-      atomicAdd(&es[4 * jq + 2], static_cast<unsigned long long>(eB0));
-      atomicAdd(&es[4 * jq + 3], static_cast<unsigned long long>(eB1));
+    if (active) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (e[p][h] != 0) atomicAdd(&es[2 * (NP * jq + p) + h], static_cast<unsigned long long>(e[p][h]));
     }
     __syncthreads();
     for (int t = threadIdx.x; t < 2 * a.npairs; t += blockDim.x)
@@ -534,6 +555,7 @@ static int sweep_threads(int) { return 256; }
 static size_t sweep_smem(int) { return 0; }
 
 static bool is_quad(int variant) { return variant == 22 || variant == 23; }
+static int pairs_per_thread(int variant) { return is_quad(variant) ? 2 : 1; }
 
 template <bool Q, bool E>
 static void* quad_kernel_ptr(bool list, int variant) {
@@ -562,17 +584,16 @@ int sweep_grid_size(int device, int variant) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, false, variant), sweep_threads(variant),
                                                 sweep_smem(variant));
-  // variants that may fall back at launch (byte offsets: large P * R -> 12; quads: odd
-  // pair count or energy trace -> 13): size the grid for both kernels
+  // variants that may fall back at launch (byte offsets: large P * R -> 12; two-pair
+  // kernels: odd pair count -> 13): size the grid for both kernels
   const int fb = (variant == 15 || variant == 16 || variant == 17 || variant == 19) ? 12 : is_quad(variant) ? 13 : -1;
   if (fb >= 0) {
-    int perf = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perf, sweep_kernel(true, false, false, fb), sweep_threads(fb),
-                                                  sweep_smem(fb));
-    if (perf < per) per = perf;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perf, sweep_kernel(true, true, false, fb), sweep_threads(fb),
-                                                  sweep_smem(fb));
-    if (perf < per) per = perf;
+    for (int e = 0; e < 2; ++e) {
+      int perf = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perf, sweep_kernel(true, e != 0, false, fb), sweep_threads(fb),
+                                                    sweep_smem(fb));
+      if (perf < per) per = perf;
+    }
   }
   if (per < 1) per = 1;
   return sms * per;
@@ -583,10 +604,10 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   const bool energy = (a.energy != nullptr);
   // byte-offset variant only while every byte offset into G fits in 32 bits
   if ((variant == 15 || variant == 16 || variant == 17 || variant == 19) && a.P * static_cast<int64_t>(a.R) * 4 >= (int64_t{1} << 32)) variant = 12;
-  // quad variants need an even number of pairs (float4 alignment)
+  // the two-pair kernels need an even pair count (float4 alignment)
   if (is_quad(variant) && (a.npairs & 1)) variant = 13;
   const int nt = sweep_threads(variant);
-  const int64_t units = is_quad(variant) ? a.npairs / 2 : a.npairs;  // threads per gap site
+  const int64_t units = a.npairs / pairs_per_thread(variant);  // threads per gap site
   const int64_t items = a.g_count * units;
   int64_t g = (items + nt - 1) / nt;
   if (g > grid) g = grid;

@@ -471,6 +471,7 @@ def test_every_sweep_variant_bit_exact(P, calib, variant, monkeypatch):
     # even pair counts without the energy trace (the quad-pair kernels run, no fallback)
     compare(P, z, mask, truth, P.Config(), calib, 8, 7, 55)
     compare(P, z, mask, truth, P.Config(order="dc", l_b=8, max_batch=4), calib, 12, 5, 56)
+    compare(P, z, mask, truth, P.Config(), calib, 16, 5, 57, energy=True)  # 8k realizations
 
 
 def _fuzz_case(k):
