@@ -510,3 +510,36 @@ def test_fuzz_small_problems_bit_exact(P, calib, k):
         m.close()
         return
     compare(P, z, mask, truth, cfg, calib, M, S, seed, energy=energy, exact_pred=cfg.n_avg == 1)
+
+
+def test_context_lifecycle_releases_device_memory(P, calib):
+    """20 full init -> fill -> destroy cycles (graphs, batches, energy buffers, slabs)
+    leave the device's free memory where it was: the context frees what it allocates."""
+    import torch
+    truth, z, mask = make_problem(96, 0.5, corr_len=8.0)
+
+    def cycle(k):
+        m = P.LeMpr(P.Config(max_batch=4 if k % 2 else 0), calib)
+        m.set_data(z, mask)
+        m.set_energy_trace(k % 3 == 0)
+        m.estimate_local_params()
+        m.simulate(6, 5, k)
+        m.predict()
+        if k % 4 == 1:
+            m.set_energy_trace(False)  # slab mode has no energy trace
+            m.reset_accumulator()
+            m.slab_begin(4, 3, k, 0, 4, 0, 48)
+            for s in range(1, 4):
+                for colour in (0, 1):
+                    m.slab_half_sweep(s, colour)
+            m.slab_end()
+        m.close()
+
+    cycle(0)  # first use: lazily created device state (CUDA context, module load)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for k in range(1, 21):
+        cycle(k)
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 <= 4 << 20, f"device memory not released: {(free0 - free1) / 2**20:.1f} MiB"
