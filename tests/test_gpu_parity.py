@@ -543,3 +543,38 @@ def test_context_lifecycle_releases_device_memory(P, calib):
     torch.cuda.synchronize()
     free1 = torch.cuda.mem_get_info()[0]
     assert free0 - free1 <= 4 << 20, f"device memory not released: {(free0 - free1) / 2**20:.1f} MiB"
+
+
+def test_concurrent_contexts_on_separate_streams(P, calib):
+    """The header's thread-safety rule: distinct contexts may run concurrently. Two host
+    threads drive two contexts on two CUDA streams (ctypes drops the GIL in the calls);
+    each result equals its sequential run bit for bit."""
+    import threading
+    import torch
+    probs = [make_problem(80, 0.4, corr_len=7.0), make_problem(72, 0.6, Lx=90, corr_len=5.0, gaps="cloud")]
+    cfgs = [P.Config(), P.Config(l_b=16, r_s=1, init="random")]
+    ref = [gpu_run(P, z, mask, cfg, calib, 10, 12, 3 + i)["pred"] for i, ((_, z, mask), cfg) in enumerate(zip(probs, cfgs))]
+    out, errs = [None, None], []
+
+    def work(i):
+        try:
+            st = torch.cuda.Stream()
+            _, z, mask = probs[i]
+            m = P.LeMpr(cfgs[i], calib, stream=st.cuda_stream)
+            for _ in range(5):
+                m.set_data(z, mask)
+                m.estimate_local_params()
+                m.simulate(10, 12, 3 + i)
+                out[i] = m.predict()
+            m.close()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for i in range(2):
+        assert_bitwise(out[i], ref[i], f"context {i} under concurrency")
