@@ -503,16 +503,33 @@ __global__ void __launch_bounds__(256) k_init_states(const GapRec* __restrict__ 
 }
 
 // a9 (realization sum): acc[g] += sum_{r in [r_lo, r_hi)} X[g][r], fp64, r ascending —
-// the same summation order as the oracle (ARITH §I).
-__global__ void __launch_bounds__(256) k_acc_reduce(const float* __restrict__ X, int64_t g_begin,
-                                                    int64_t g_end, int R, int r_lo, int r_hi,
-                                                    double* __restrict__ acc) {
-  for (int64_t g = g_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < g_end;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    double s = acc[g];
-    const float* x = X + g * R;
-    for (int r = r_lo; r < r_hi; ++r) s = __dadd_rn(s, static_cast<double>(x[r]));
-    acc[g] = s;
+// the same summation order as the oracle (ARITH §I). A CTA owns 256 gap sites; their
+// rows are staged through shared memory 32 realizations at a time (each warp reads
+// 128-byte row segments, coalesced), then every thread adds its own row in order. The
+// padded row stride (33) makes the per-thread reads bank-conflict free.
+constexpr int kAccTile = 256, kAccChunk = 32;
+__global__ void __launch_bounds__(kAccTile) k_acc_reduce(const float* __restrict__ X, int64_t g_begin,
+                                                         int64_t g_end, int R, int r_lo, int r_hi,
+                                                         double* __restrict__ acc) {
+  __shared__ float sm[kAccTile * (kAccChunk + 1)];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t g0 = g_begin + (int64_t)blockIdx.x * kAccTile; g0 < g_end; g0 += (int64_t)gridDim.x * kAccTile) {
+    const int64_t g = g0 + threadIdx.x;
+    double s = g < g_end ? acc[g] : 0.0;
+    for (int rc = r_lo; rc < r_hi; rc += kAccChunk) {
+      const int nr = min(kAccChunk, r_hi - rc);
+      __syncthreads();
+      for (int row = warp; row < kAccTile; row += kAccTile / 32) {
+        const int64_t gg = g0 + row;
+        if (gg < g_end && lane < nr) sm[row * (kAccChunk + 1) + lane] = X[gg * R + rc + lane];
+      }
+      __syncthreads();
+      if (g < g_end) {
+        const float* x = sm + threadIdx.x * (kAccChunk + 1);
+        for (int r = 0; r < nr; ++r) s = __dadd_rn(s, static_cast<double>(x[r]));
+      }
+    }
+    if (g < g_end) acc[g] = s;
   }
 }
 
@@ -638,10 +655,10 @@ void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R,
 void launch_acc_reduce(const float* X, int64_t g_begin, int64_t g_count, int R, int r_lo, int r_hi,
                        double* acc, cudaStream_t st) {
   if (g_count <= 0) return;
-  int64_t g = (g_count + 255) / 256;
-  if (g > 148 * 32) g = 148 * 32;
+  int64_t g = (g_count + kAccTile - 1) / kAccTile;
+  if (g > 148 * 16) g = 148 * 16;
   if (g < 1) g = 1;
-  k_acc_reduce<<<static_cast<unsigned>(g), 256, 0, st>>>(X, g_begin, g_begin + g_count, R, r_lo, r_hi, acc);
+  k_acc_reduce<<<static_cast<unsigned>(g), kAccTile, 0, st>>>(X, g_begin, g_begin + g_count, R, r_lo, r_hi, acc);
 }
 
 }  // namespace mpr
