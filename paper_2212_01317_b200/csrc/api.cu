@@ -146,6 +146,25 @@ mpr_status check_launch(mpr_ctx* c, const char* where) {
     ++c->total_launches;                        \
   } while (0)
 
+// Makes the context's device current for the duration of a call and restores the caller's
+// current device afterwards (the library must not move e.g. torch's current device).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+#define SET_DEVICE(c)                                                     \
+  DeviceGuard dev_guard_((c)->device);                                   \
+  if (dev_guard_.err != cudaSuccess) return cuda_fail(c, dev_guard_.err, "set device")
+
 mpr_status validate_cfg(const mpr_config* cfg, std::string& why) {
   if (!cfg) { why = "cfg is NULL"; return MPR_ERR_INVALID_ARG; }
   if (!(cfg->J > 0.0f) || !std::isfinite(cfg->J)) { why = "J must be finite and > 0"; return MPR_ERR_INVALID_ARG; }
@@ -349,7 +368,8 @@ mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
   c->cale.assign(cfg->calib_e, cfg->calib_e + cfg->calib_n);
   c->cfg.calib_T = c->calT.data();
   c->cfg.calib_e = c->cale.data();
-  cudaError_t e = cudaSetDevice(c->device);
+  DeviceGuard dev_guard(c->device);
+  cudaError_t e = dev_guard.err;
   if (e == cudaSuccess) {
     if (cfg->stream) {
       c->stream = static_cast<cudaStream_t>(cfg->stream);
@@ -380,7 +400,7 @@ mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
 
 void mpr_destroy(mpr_ctx* c) {
   if (!c) return;
-  cudaSetDevice(c->device);
+  DeviceGuard dev_guard(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   DBuf* bufs[] = {&c->z, &c->mask, &c->phiK, &c->scal, &c->calTd, &c->caled, &c->rowcnt, &c->rowoff,
                   &c->gid, &c->rec, &c->bstats, &c->Tb, &c->T, &c->T2, &c->G, &c->A, &c->acc,
@@ -402,7 +422,7 @@ mpr_status mpr_set_data(mpr_ctx* c, const float* grid, const uint8_t* mask, int6
   if (!grid || !mask) return fail(c, MPR_ERR_INVALID_ARG, "grid and mask must be non-NULL");
   mpr_status s = check_dims(c, Lx, Ly);
   if (s != MPR_OK) return s;
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   s = alloc_inputs(c, Lx, Ly);
   if (s != MPR_OK) return s;
   CK(cudaMemcpyAsync(c->z.p, grid, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream), "H2D grid");
@@ -415,7 +435,7 @@ mpr_status mpr_set_data_device(mpr_ctx* c, const float* grid, const uint8_t* mas
   if (!grid || !mask) return fail(c, MPR_ERR_INVALID_ARG, "grid and mask must be non-NULL");
   mpr_status s = check_dims(c, Lx, Ly);
   if (s != MPR_OK) return s;
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   s = alloc_inputs(c, Lx, Ly);
   if (s != MPR_OK) return s;
   CK(cudaMemcpyAsync(c->z.p, grid, sizeof(float) * c->n, cudaMemcpyDeviceToDevice, c->stream), "D2D grid");
@@ -426,7 +446,7 @@ mpr_status mpr_set_data_device(mpr_ctx* c, const float* grid, const uint8_t* mas
 mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   if (!c) return MPR_ERR_INVALID_ARG;
   if (c->stage < ST_DATA) return fail(c, MPR_ERR_STATE, "estimate_local_params before set_data");
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   cudaStream_t st = c->stream;
   const int lb = c->cfg.l_b;
   c->nbx = (c->Lx + lb - 1) / lb;
@@ -512,7 +532,7 @@ mpr_status mpr_set_kernel_timing(mpr_ctx* c, int enable) {
 mpr_status mpr_reset_accumulator(mpr_ctx* c) {
   if (!c) return MPR_ERR_INVALID_ARG;
   if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "reset_accumulator before estimate_local_params");
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   CK(c->acc.ensure(sizeof(double) * std::max<int64_t>(c->P, 1)), "alloc acc");
   CK(cudaMemsetAsync(c->acc.p, 0, sizeof(double) * std::max<int64_t>(c->P, 1), c->stream), "zero acc");
   c->M_total = 0;
@@ -595,7 +615,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
     mpr_status s = mpr_reset_accumulator(c);
     if (s != MPR_OK) return s;
   }
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   cudaStream_t st = c->stream;
   c->M_total = M;
   c->sweeps = sweeps;
@@ -709,7 +729,7 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
     return fail(c, MPR_ERR_INVALID_ARG, "the adaptive protocol needs the SC order (fused energy)");
   mpr_status st0 = mpr_reset_accumulator(c);
   if (st0 != MPR_OK) return st0;
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   cudaStream_t st = c->stream;
   c->M_total = M;
   c->sweeps = max_sweeps;
@@ -841,7 +861,7 @@ mpr_status mpr_slab_begin(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed, 
     mpr_status s = mpr_reset_accumulator(c);
     if (s != MPR_OK) return s;
   }
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   cudaStream_t st = c->stream;
   c->rowoff_h.resize(static_cast<size_t>(2 * c->Ly));
   CK(cudaMemcpyAsync(c->rowoff_h.data(), c->rowoff.p, sizeof(int) * 2 * c->Ly, cudaMemcpyDeviceToHost, st),
@@ -885,7 +905,7 @@ mpr_status mpr_slab_half_sweep(mpr_ctx* c, int32_t sweep, int colour) {
   if (sweep < 1 || sweep > c->slab_S || (colour != 0 && colour != 1))
     return fail(c, MPR_ERR_INVALID_ARG, "bad sweep or colour");
   if (c->degenerate || c->P == 0) return MPR_OK;
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   const int64_t g0 = gap_row_offset(c, colour, c->slab_row0);
   const int64_t g1 = gap_row_offset(c, colour, c->slab_row1);
   if (g1 <= g0) return MPR_OK;
@@ -926,7 +946,7 @@ mpr_status mpr_slab_row_states(mpr_ctx* c, int64_t row, int colour, float** dev_
 mpr_status mpr_slab_end(mpr_ctx* c) {
   if (!c) return MPR_ERR_INVALID_ARG;
   if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_end without slab_begin");
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   c->slab_active = 0;
   if (!(c->degenerate || c->P == 0)) {
     const bool avg = c->cfg.n_avg > 1;
@@ -945,7 +965,7 @@ mpr_status mpr_slab_end(mpr_ctx* c) {
 
 mpr_status mpr_sync(mpr_ctx* c) {
   if (!c) return MPR_ERR_INVALID_ARG;
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   CK(cudaStreamSynchronize(c->stream), "sync");
   return MPR_OK;
 }
@@ -958,7 +978,7 @@ mpr_status mpr_build_calibration(mpr_ctx* c, const float* T, int32_t K, int32_t 
   for (int k = 0; k < K; ++k)
     if (!(T[k] > 0.0f) || !std::isfinite(T[k]) || (k > 0 && !(T[k] > T[k - 1])))
       return fail(c, MPR_ERR_INVALID_ARG, "calibration temperatures must be positive and increasing");
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   const int nlat = K * reps, S = n_eq + n_meas;
   std::vector<long long> fx(static_cast<size_t>(nlat) * S);
   CK(run_calibration(T, K, L, q, n_eq, n_meas, reps, seed, fx.data(), c->stream), "calibration sweeps");
@@ -1027,7 +1047,7 @@ static mpr_status predict_impl(mpr_ctx* c, float* out_dev) {
 mpr_status mpr_predict(mpr_ctx* c, float* out) {
   if (!c) return MPR_ERR_INVALID_ARG;
   if (!out) return fail(c, MPR_ERR_INVALID_ARG, "out is NULL");
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   CK(c->out.ensure(sizeof(float) * c->n), "alloc out");
   mpr_status s = predict_impl(c, c->out.as<float>());
   if (s != MPR_OK) return s;
@@ -1039,7 +1059,7 @@ mpr_status mpr_predict(mpr_ctx* c, float* out) {
 mpr_status mpr_predict_device(mpr_ctx* c, float* out_dev) {
   if (!c) return MPR_ERR_INVALID_ARG;
   if (!out_dev) return fail(c, MPR_ERR_INVALID_ARG, "out is NULL");
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   mpr_status s = predict_impl(c, out_dev);
   if (s != MPR_OK) return s;
   CK(cudaStreamSynchronize(c->stream), "predict sync");
@@ -1075,7 +1095,7 @@ mpr_status mpr_get_info(mpr_ctx* c, mpr_info* info) {
 
 mpr_status mpr_debug_get(mpr_ctx* c, mpr_buffer which, int64_t index, void* host_out) {
   if (!c || !host_out) return MPR_ERR_INVALID_ARG;
-  CK(cudaSetDevice(c->device), "set device");
+  SET_DEVICE(c);
   cudaStream_t st = c->stream;
   switch (which) {
     case MPR_BUF_PHI_KNOWN:
