@@ -25,7 +25,10 @@
  *    Re-calling an earlier stage invalidates the later ones; out-of-order calls
  *    return MPR_ERR_STATE.
  *  - Every call returns a status; on failure mpr_last_error(ctx) holds one line.
- *  - A context is single-owner (not thread-safe); distinct contexts are independent.
+ *  - A context is single-owner (not thread-safe); distinct contexts are independent
+ *    and may be driven concurrently from different host threads.
+ *  - Each call makes ctx's device current while it runs and restores the calling
+ *    thread's current device before returning.
  */
 #ifndef MPR_H_
 #define MPR_H_
