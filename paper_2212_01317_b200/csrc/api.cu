@@ -75,7 +75,7 @@ struct mpr_ctx {
   int stage = ST_INIT;
   std::string err;
   int sweep_grid = 0;
-  int sweep_variant = 22;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
+  int sweep_variant = 28;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
   // problem
   int64_t Lx = 0, Ly = 0, n = 0;
   int64_t P = 0, PA = 0, n_known = 0;
@@ -317,7 +317,7 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
   // the default sweep kernel (variant 22) moves two realization pairs per thread and needs
   // an even pair count per batch: split R = 4k + 2 as 4k + 2 (e.g. M = 10 -> 8 + 2; the
   // 2-realization batch runs the one-pair kernel)
-  if ((c->sweep_variant == 22 || c->sweep_variant == 23) && B % 4 == 2 && B > 2) B -= 2;
+  if ((c->sweep_variant == 22 || c->sweep_variant == 23 || c->sweep_variant == 27 || c->sweep_variant == 28) && B % 4 == 2 && B > 2) B -= 2;
   c->batch_key_P = c->P;
   c->batch_key_R = R;
   c->batch_cached = B;

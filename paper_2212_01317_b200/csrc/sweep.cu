@@ -147,9 +147,23 @@ __device__ __forceinline__ bool all_present(uint32_t f) {
 // are in registers: Philox, two Metropolis updates, store, fused epilogues.
 // BO: self_off is a byte offset into G / A (see the PF == 4 kernel path), else an element offset.
 template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO = false>
+__device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec& rec, float2 cur,
+                                               const float2 (&nb)[4], uint32_t self_off, const Words4& w,
+                                               long long& e0, long long& e1, bool accum0, bool accum1);
+
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO = false>
 __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& rec, float2 cur,
                                              const float2 (&nb)[4], uint32_t self_off, uint32_t pair,
                                              long long& e0, long long& e1, bool accum0, bool accum1) {
+  const Words4 w = philox4x32_10_rk(rec.site, a.sweep, pair, 2u, a.rk0, a.rk1);
+  process_item_w<QHALF, ENERGY, BFEXP, PK, BO>(a, rec, cur, nb, self_off, w, e0, e1, accum0, accum1);
+}
+
+// The item once its Philox words are known (the quad kernel may draw them early).
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO>
+__device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec& rec, float2 cur,
+                                               const float2 (&nb)[4], uint32_t self_off, const Words4& w,
+                                               long long& e0, long long& e1, bool accum0, bool accum1) {
   uint32_t sel = 0;
   if (ENERGY) {
 #pragma unroll
@@ -158,7 +172,6 @@ __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& r
       sel |= (a.is_b ? (ty != NB_NONE) : (ty == NB_KNOWN)) ? (1u << k) : 0u;
     }
   }
-  const Words4 w = philox4x32_10_rk(rec.site, a.sweep, pair, 2u, a.rk0, a.rk1);
   bool acc0, acc1;
   float n0, n1;
   if (PK) {
@@ -376,7 +389,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
 // the NP pairs, and the own / neighbour states move as float4 (two pairs each). Each pair
 // still draws its own Philox call and runs metropolis_pair, so the results are those of
 // k_sweep_half bit for bit. Requires npairs % NP == 0 (launch_sweep_half falls back).
-template <bool QHALF, bool ENERGY, int MINB, bool LIST, int NP = 2>
+template <bool QHALF, bool ENERGY, int MINB, bool LIST, int NP = 2, bool EARLY = false>
 __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
   constexpr int NQ = NP / 2;  // float4 quads per thread
   const int nq = a.npairs / NP;
@@ -429,6 +442,13 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
         recn = a.rec[ggn];
         asm volatile("prefetch.global.L2 [%0];" ::"l"(a.G + (ggn * R + j4)));
       }
+      // EARLY: draw every pair's Philox words as soon as the record is here, before the
+      // state loads are consumed, so the load latency is covered by the integer work
+      Words4 wpre[NP];
+      if (EARLY) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) wpre[p] = philox4x32_10_rk(rec.site, a.sweep, pair0 + p, 2u, a.rk0, a.rk1);
+      }
       const uint32_t self_off = gg * R + j4;
       uint32_t nb_off[4];
 #pragma unroll
@@ -449,12 +469,22 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
           }
         }
         const int pa = 2 * qd, pb = 2 * qd + 1;
-        if (live[pa])
-          process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
-                                                  pair0 + pa, e[pa][0], e[pa][1], acc[pa][0], acc[pa][1]);
-        if (live[pb])
-          process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 4u * qd + 2u,
-                                                  pair0 + pb, e[pb][0], e[pb][1], acc[pb][0], acc[pb][1]);
+        if (EARLY) {
+          if (live[pa])
+            process_item_w<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
+                                                      wpre[pa], e[pa][0], e[pa][1], acc[pa][0], acc[pa][1]);
+          if (live[pb])
+            process_item_w<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.z, cur.w), nbB,
+                                                      self_off + 4u * qd + 2u, wpre[pb], e[pb][0], e[pb][1],
+                                                      acc[pb][0], acc[pb][1]);
+        } else {
+          if (live[pa])
+            process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
+                                                    pair0 + pa, e[pa][0], e[pa][1], acc[pa][0], acc[pa][1]);
+          if (live[pb])
+            process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 4u * qd + 2u,
+                                                    pair0 + pb, e[pb][0], e[pb][1], acc[pb][0], acc[pb][1]);
+        }
       }
       rec = recn;
       gg = ggn;
@@ -541,13 +571,14 @@ __global__ void __launch_bounds__(kAccTile) k_acc_reduce(const float* __restrict
 // 10 = 5 packed, 11 = 10 at <= 64 registers, 12 = 10 + record one item ahead (3 CTAs/SM),
 // 13 (default) = 12 at <= 64 registers (4 CTAs/SM), 15 / 16 / 17 = 12 with 32-bit byte
 // offsets at 1 / 3 / 4 CTAs/SM declared (fall back to 12 when P * R * 4 >= 2^32),
-// 18 / 19 = 12 / 15 at <= 51 registers (5 CTAs/SM), 22 (default) / 23 = k_sweep_quad (two
-// pairs per thread, float4 state moves) at 4 / 3 CTAs/SM (fall back to 13 for an odd pair
-// count).
+// 18 / 19 = 12 / 15 at <= 51 registers (5 CTAs/SM), 22 / 23 = k_sweep_quad (two pairs per
+// thread, float4 state moves) at 4 / 3 CTAs/SM, 27 / 28 (default) = 22 / 23 with both
+// pairs' Philox words drawn before the state loads are consumed (all fall back to 13 for
+// an odd pair count).
 // Half-sweep, us (Philox round keys as kernel parameters, all variants bit-identical):
 //   C2: v5 98.2, v12 97.2, v13 93.9, v15 98.5, v17 95.4, v18 95.4;
 //   C3: v12 2113, v13 2071, v15 2201, v17 2088, v19 2067;  C4: v12 3778, v13 3717, v17 3697;
-//   v22: C2 87.1, C3 1838, C4 (batches 8 + 2) 3402.
+//   v22: C2 87.1, C3 1838, C4 (batches 8 + 2) 3402;  v28: C2 84.8, C3 1783, C4 3386.
 template <bool Q, bool E, bool LIST>
 static void* sweep_kernel_ptr(int variant) {
   switch (variant) {
@@ -571,11 +602,15 @@ static int sweep_threads(int) { return 256; }
 
 static size_t sweep_smem(int) { return 0; }
 
-static bool is_quad(int variant) { return variant == 22 || variant == 23; }
+static bool is_quad(int variant) { return variant == 22 || variant == 23 || variant == 27 || variant == 28; }
 static int pairs_per_thread(int variant) { return is_quad(variant) ? 2 : 1; }
 
 template <bool Q, bool E>
 static void* quad_kernel_ptr(bool list, int variant) {
+  if (variant == 27)
+    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true, 2, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false, 2, true>);
+  if (variant == 28)
+    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true, 2, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false, 2, true>);
   if (variant == 23)
     return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false>);
   return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false>);
