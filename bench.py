@@ -195,7 +195,8 @@ def run_mpr(args):
     calib = Pk.load_calibration()
     cfg = Pk.Config(device=local)
     eng = Pk.LeMpr(cfg, calib, stream=stream.cuda_stream)
-    from paper_2212_01317_b200.sharding import allreduce_accumulator, exchange_halo, row_range, shard_range
+    from paper_2212_01317_b200.sharding import (allreduce_accumulator, exchange_halo, row_range, shard_range,
+                                                slab_realization_chunks)
     rows = args.decomp == "rows"
     if rows:  # strong scaling: the whole M on every rank, the grid split into row slabs
         M_glob = M
@@ -222,13 +223,14 @@ def run_mpr(args):
         if not rows:
             eng.simulate_range(M_glob, S, SEED_SIM, m0, m1)
             return
-        eng.slab_begin(M_glob, S, SEED_SIM, 0, M_glob, r0, r1)
-        for s in range(1, S + 1):
-            for colour in (0, 1):
-                eng.slab_half_sweep(s, colour)
-                if ws > 1:
-                    exchange_halo(eng, colour, r0, r1, rank, ws)
-        eng.slab_end()
+        for c0, c1 in slab_realization_chunks(M_glob):
+            eng.slab_begin(M_glob, S, SEED_SIM, c0, c1, r0, r1)
+            for s in range(1, S + 1):
+                for colour in (0, 1):
+                    eng.slab_half_sweep(s, colour)
+                    if ws > 1:
+                        exchange_halo(eng, colour, r0, r1, rank, ws)
+            eng.slab_end()
 
     def step_device():
         eng.set_data_device(z_dev.data_ptr(), m_dev.data_ptr(), Lx, Ly)
@@ -336,7 +338,9 @@ def run_mpr(args):
                            "l2": "flushed between timed steps (256 MiB write, outside the events)"},
                 "fill_time_ms": total_ms / args.steps,
                 "gpu_launches": int(launches),
-                "roofline": {"bound": "alu", "kernel": sweep_kernel_name(info.get("sweep_variant", 0), info.get("batch", 0)),
+                "roofline": {"bound": "alu", "kernel": sweep_kernel_name(info.get("sweep_variant", 0),
+                                                               (lambda c: c[1] - c[0])(slab_realization_chunks(M_glob)[0])
+                                                               if rows else info.get("batch", 0)),
                              "achieved": alu_achieved,
                              "peak": alu_peak, "unit": "Gop/s",
                              "frac": (alu_achieved / alu_peak) if alu_achieved else None,

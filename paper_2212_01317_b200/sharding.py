@@ -32,6 +32,19 @@ def shard_range(M: int, world: int, rank: int) -> tuple[int, int]:
     return min(2 * p0, M), min(2 * p1, M)
 
 
+def slab_realization_chunks(M: int) -> list[tuple[int, int]]:
+    """Realization ranges a row-slab fill runs one after the other (each is one state batch
+    of mpr_slab_begin). The default sweep kernel moves two realization pairs per thread and
+    needs a multiple of 4 realizations, so M = 4k + r runs as [0, 4k) then [4k, M). The
+    chains do not depend on the split (global Philox ids, ARITH §A)."""
+    if M < 1:
+        raise ValueError("M must be >= 1")
+    k = (M // 4) * 4
+    if k == 0 or k == M:
+        return [(0, M)]
+    return [(0, k), (k, M)]
+
+
 class Engine(Protocol):
     def set_data(self, grid, mask): ...
     def estimate_local_params(self, want_T: bool = False): ...
@@ -92,13 +105,14 @@ def distributed_fill_slabs(engine, grid, mask, M: int, sweeps: int, seed: int, g
     engine.set_data(grid, mask)
     engine.estimate_local_params()
     engine.reset_accumulator()
-    engine.slab_begin(M, sweeps, seed, 0, M, r0, r1)
-    for s in range(1, sweeps + 1):
-        for colour in (0, 1):
-            engine.slab_half_sweep(s, colour)
-            if world > 1:
-                exchange_halo(engine, colour, r0, r1, rank, world, group)
-    engine.slab_end()
+    for m0, m1 in slab_realization_chunks(M):
+        engine.slab_begin(M, sweeps, seed, m0, m1, r0, r1)
+        for s in range(1, sweeps + 1):
+            for colour in (0, 1):
+                engine.slab_half_sweep(s, colour)
+                if world > 1:
+                    exchange_halo(engine, colour, r0, r1, rank, world, group)
+        engine.slab_end()
     allreduce_accumulator(engine.accumulator_tensor(), group)
     return engine.predict()
 

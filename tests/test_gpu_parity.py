@@ -232,22 +232,25 @@ def _emulated_slabs(P, z, mask, cfg, calib, M, S, seed, world):
     Ly = z.shape[0]
     engs = [P.LeMpr(cfg, calib) for _ in range(world)]
     ranges = [row_range(Ly, world, w) for w in range(world)]
-    for e, (r0, r1) in zip(engs, ranges):
-        e.set_data(z, mask); e.estimate_local_params(); e.reset_accumulator()
-        e.slab_begin(M, S, seed, 0, M, r0, r1)
-    for s in range(1, S + 1):
-        for colour in (0, 1):
-            for e in engs:
-                e.slab_half_sweep(s, colour)
-            for e in engs:
-                e.sync()
-            for w in range(world - 1):  # boundary between slab w and w+1
-                r = ranges[w][1]
-                engs[w + 1].row_view(r - 1, colour).copy_(engs[w].row_view(r - 1, colour))  # w's last row
-                engs[w].row_view(r, colour).copy_(engs[w + 1].row_view(r, colour))          # w+1's first row
-            torch.cuda.synchronize()
+    from paper_2212_01317_b200.sharding import slab_realization_chunks
     for e in engs:
-        e.slab_end()
+        e.set_data(z, mask); e.estimate_local_params(); e.reset_accumulator()
+    for c0, c1 in slab_realization_chunks(M):  # the same realization split as bench / sharding
+        for e, (r0, r1) in zip(engs, ranges):
+            e.slab_begin(M, S, seed, c0, c1, r0, r1)
+        for s in range(1, S + 1):
+            for colour in (0, 1):
+                for e in engs:
+                    e.slab_half_sweep(s, colour)
+                for e in engs:
+                    e.sync()
+                for w in range(world - 1):  # boundary between slab w and w+1
+                    r = ranges[w][1]
+                    engs[w + 1].row_view(r - 1, colour).copy_(engs[w].row_view(r - 1, colour))  # w's last row
+                    engs[w].row_view(r, colour).copy_(engs[w + 1].row_view(r, colour))          # w+1's first row
+                torch.cuda.synchronize()
+        for e in engs:
+            e.slab_end()
     total = sum(e.accumulator_tensor().clone() for e in engs)
     engs[0].accumulator_tensor().copy_(total)
     torch.cuda.synchronize()

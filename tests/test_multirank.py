@@ -129,10 +129,9 @@ class OracleSlabEngine(OracleEngine):
         rows = slice(self.r0, self.r1)
         gaps = np.zeros(self.mask.shape, bool)
         gaps[rows] = self.mask[rows] == 0
-        acc = np.zeros(self.mask.shape)
+        acc = self.acc.numpy().reshape(self.mask.shape)  # a view: adds land in self.acc
         for k in range(self.phi.shape[0]):  # realization order, as the oracle accumulates
             acc[gaps] += self.phi[k][gaps].astype(np.float64)
-        self.acc += torch.from_numpy(acc.ravel())
 
 
 def _slab_worker(rank, world, port, out):
@@ -144,7 +143,7 @@ def _slab_worker(rank, world, port, out):
     from tests.conftest import read_calibration
     truth, z, mask = make_problem(21, 0.6, Lx=18, corr_len=5.0)
     eng = OracleSlabEngine(read_calibration(), O.OracleConfig(lb=8, rs=1, ns=2))
-    out[rank] = distributed_fill_slabs(eng, z, mask, M=3, sweeps=5, seed=41)
+    out[rank] = distributed_fill_slabs(eng, z, mask, M=6, sweeps=5, seed=41)  # chunks [0,4), [4,6)
     dist.destroy_process_group()
 
 
@@ -158,7 +157,7 @@ def test_gloo_row_slabs_bit_exact(calib, world):
     out = mgr.dict()
     mp.spawn(_slab_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     truth, z, mask = make_problem(21, 0.6, Lx=18, corr_len=5.0)
-    ref = O.fill(z, mask, O.OracleConfig(lb=8, rs=1, ns=2), *calib, M=3, S=5, seed=41)["pred"]
+    ref = O.fill(z, mask, O.OracleConfig(lb=8, rs=1, ns=2), *calib, M=6, S=5, seed=41)["pred"]
     for r in range(world):
         assert np.array_equal(out[r].view(np.uint32), ref.view(np.uint32))
 
@@ -167,3 +166,17 @@ def test_row_range():
     from paper_2212_01317_b200.sharding import row_range
     rr = [row_range(10, 3, r) for r in range(3)]
     assert rr == [(0, 3), (3, 6), (6, 10)]
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 4, 5, 6, 7, 8, 10, 64, 100, 101])
+def test_slab_realization_chunks(M):
+    """Row-slab realization split: covers [0, M) once, in order, the first chunk a multiple of
+    4 whenever M >= 4 (the two-pair sweep kernel's batch), at most two chunks."""
+    from paper_2212_01317_b200.sharding import slab_realization_chunks
+    ch = slab_realization_chunks(M)
+    assert ch[0][0] == 0 and ch[-1][1] == M and len(ch) <= 2
+    assert all(a < b for a, b in ch) and all(ch[i][1] == ch[i + 1][0] for i in range(len(ch) - 1))
+    if M >= 4:
+        assert ch[0][1] % 4 == 0
+    if len(ch) == 2:
+        assert ch[1][1] - ch[1][0] < 4
