@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--ref-sample-realizations", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
+                    help="row slabs at N > 1: the sweep kernel writes the boundary rows into the "
+                         "neighbours' IPC-mapped state buffers (peer), or NCCL send/recv (nccl)")
     ap.add_argument("--decomp", default="realizations", choices=["realizations", "rows"],
                     help="multi-GPU split: realization shards (weak scaling, default) or row slabs "
                          "with one-row halos (strong scaling)")
@@ -195,8 +198,8 @@ def run_mpr(args):
     calib = Pk.load_calibration()
     cfg = Pk.Config(device=local)
     eng = Pk.LeMpr(cfg, calib, stream=stream.cuda_stream)
-    from paper_2212_01317_b200.sharding import (allreduce_accumulator, exchange_halo, row_range, shard_range,
-                                                slab_realization_chunks)
+    from paper_2212_01317_b200.sharding import (allreduce_accumulator, connect_peer_halo, exchange_halo, row_range,
+                                                shard_range, slab_realization_chunks)
     rows = args.decomp == "rows"
     if rows:  # strong scaling: the whole M on every rank, the grid split into row slabs
         M_glob = M
@@ -223,12 +226,18 @@ def run_mpr(args):
         if not rows:
             eng.simulate_range(M_glob, S, SEED_SIM, m0, m1)
             return
+        peer = ws > 1 and args.halo == "peer"
         for c0, c1 in slab_realization_chunks(M_glob):
             eng.slab_begin(M_glob, S, SEED_SIM, c0, c1, r0, r1)
+            if peer:
+                connect_peer_halo(eng, rank, ws)
             for s in range(1, S + 1):
                 for colour in (0, 1):
                     eng.slab_half_sweep(s, colour)
-                    if ws > 1:
+                    if peer:  # the kernels wrote the halos into the neighbours' buffers
+                        eng.sync()
+                        dist.barrier()
+                    elif ws > 1:
                         exchange_halo(eng, colour, r0, r1, rank, ws)
             eng.slab_end()
 
@@ -334,7 +343,8 @@ def run_mpr(args):
                 "scaling": "strong" if rows else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": desc, "L": c["L"], "p": c["p"], "gaps": c["gaps"], "gap_sites": P,
                            "M_per_rank": M, "M_total": M_glob, "sweeps": S,
-                           "updates_per_step": updates_per_step, "parallelism": f"row slabs x{ws}" if rows else f"realizations x{ws}",
+                           "updates_per_step": updates_per_step, "parallelism": (f"row slabs x{ws}" + (f", {args.halo} halo" if ws > 1 else "")) if rows
+                           else f"realizations x{ws}",
                            "l2": "flushed between timed steps (256 MiB write, outside the events)"},
                 "fill_time_ms": total_ms / args.steps,
                 "gpu_launches": int(launches),

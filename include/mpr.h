@@ -183,6 +183,39 @@ mpr_status mpr_slab_begin(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed
                           int64_t m_end, int64_t row_begin, int64_t row_end);
 mpr_status mpr_slab_half_sweep(mpr_ctx *ctx, int32_t sweep, int colour);
 mpr_status mpr_slab_row_states(mpr_ctx *ctx, int64_t row, int colour, float **dev_ptr, int64_t *count);
+
+/* Fused halo exchange over peer memory (the B200-native form of the exchange above).
+ *
+ * Every rank's state buffer has the same global layout (gap-site major, realization
+ * minor, all gap ids of the grid). Between mpr_slab_begin and mpr_slab_end a rank may
+ * register the state buffers of its neighbouring slabs. Its half-sweep kernel then also
+ * stores every state it changes in its first own row into the upper neighbour's buffer,
+ * and in its last own row into the lower neighbour's buffer, at the same offsets. Those
+ * are exactly the neighbours' ghost rows, so no exchange call or copy is needed.
+ *
+ * The caller still orders half-sweeps across ranks: all kernels of half-sweep h must
+ * complete before any rank starts h + 1 (for example mpr_sync followed by a
+ * process-group barrier). States that are not accepted are not rewritten; the ghost
+ * copies agree because initial states are a pure function of the global ids.
+ *
+ *   mpr_slab_state_ipc_handle: writes the MPR_IPC_HANDLE_BYTES-byte cudaIpcMemHandle_t
+ *       of ctx's state buffer to handle_out, for a neighbour in another process.
+ *   mpr_slab_state_device: the state buffer's device pointer, for a neighbour in this
+ *       process.
+ *   mpr_slab_set_peer: side 0 = upper neighbour (rows < row_begin), 1 = lower neighbour
+ *       (rows >= row_end). Pass exactly one of:
+ *         - ipc_handle: another process's buffer, opened with cudaIpcOpenMemHandle
+ *           (lazy peer access over NVLink);
+ *         - dev_ptr: device memory of this process. Peer access is enabled if it lives
+ *           on another device; INVALID_ARG if that device is not P2P-reachable.
+ *       Both NULL clears the side.
+ * Registrations end at mpr_slab_end (IPC mappings are closed). A later mpr_slab_begin
+ * may reallocate the buffer, so handles and pointers are exchanged again after each
+ * mpr_slab_begin. */
+#define MPR_IPC_HANDLE_BYTES 64
+mpr_status mpr_slab_state_ipc_handle(mpr_ctx *ctx, void *handle_out);
+mpr_status mpr_slab_state_device(mpr_ctx *ctx, float **dev_ptr);
+mpr_status mpr_slab_set_peer(mpr_ctx *ctx, int side, const void *ipc_handle, float *dev_ptr);
 mpr_status mpr_slab_end(mpr_ctx *ctx);
 mpr_status mpr_sync(mpr_ctx *ctx);
 

@@ -29,6 +29,7 @@ EXPORTED = ["mpr_config_default", "mpr_init", "mpr_destroy", "mpr_last_error", "
             "mpr_simulate_range", "mpr_accumulator_device", "mpr_predict", "mpr_predict_device",
             "mpr_get_info", "mpr_debug_get", "mpr_set_energy_trace", "mpr_set_kernel_timing", "mpr_version",
             "mpr_slab_begin", "mpr_slab_half_sweep", "mpr_slab_row_states", "mpr_slab_end", "mpr_sync",
+            "mpr_slab_state_ipc_handle", "mpr_slab_state_device", "mpr_slab_set_peer",
             "mpr_simulate_adaptive", "mpr_build_calibration"]
 
 
@@ -89,6 +90,9 @@ def load_library(path: str = LIB_PATH):
     L.mpr_slab_half_sweep.argtypes = [vp, i32, C.c_int]; L.mpr_slab_half_sweep.restype = C.c_int
     L.mpr_slab_row_states.argtypes = [vp, i64, C.c_int, C.POINTER(vp), C.POINTER(i64)]
     L.mpr_slab_row_states.restype = C.c_int
+    L.mpr_slab_state_ipc_handle.argtypes = [vp, vp]; L.mpr_slab_state_ipc_handle.restype = C.c_int
+    L.mpr_slab_state_device.argtypes = [vp, C.POINTER(vp)]; L.mpr_slab_state_device.restype = C.c_int
+    L.mpr_slab_set_peer.argtypes = [vp, C.c_int, vp, vp]; L.mpr_slab_set_peer.restype = C.c_int
     L.mpr_slab_end.argtypes = [vp]; L.mpr_slab_end.restype = C.c_int
     L.mpr_sync.argtypes = [vp]; L.mpr_sync.restype = C.c_int
     L.mpr_simulate_adaptive.argtypes = [vp, i64, u64, i32, i32, i32, C.c_double, vp]
@@ -206,6 +210,26 @@ def mpr_slab_row_states(ctx, row, colour):
     p, n = C.c_void_p(), C.c_int64()
     _check(ctx, load_library().mpr_slab_row_states(ctx, row, colour, C.byref(p), C.byref(n)))
     return p.value, n.value
+
+
+MPR_IPC_HANDLE_BYTES = 64
+
+
+def mpr_slab_state_ipc_handle(ctx) -> bytes:
+    buf = C.create_string_buffer(MPR_IPC_HANDLE_BYTES)
+    _check(ctx, load_library().mpr_slab_state_ipc_handle(ctx, buf))
+    return buf.raw
+
+
+def mpr_slab_state_device(ctx) -> int:
+    p = C.c_void_p()
+    _check(ctx, load_library().mpr_slab_state_device(ctx, C.byref(p)))
+    return p.value
+
+
+def mpr_slab_set_peer(ctx, side, ipc_handle: bytes | None = None, dev_ptr: int | None = None) -> None:
+    h = C.create_string_buffer(ipc_handle, MPR_IPC_HANDLE_BYTES) if ipc_handle is not None else None
+    _check(ctx, load_library().mpr_slab_set_peer(ctx, side, h, dev_ptr))
 
 
 def mpr_slab_end(ctx) -> None:
@@ -391,6 +415,19 @@ class LeMpr:
 
     def commit_row(self, row, colour, tensor):
         """Received halo rows land in place (row_view is zero-copy): nothing to do."""
+
+    def state_ipc_handle(self) -> bytes:
+        """cudaIpcMemHandle_t of this slab's state buffer (for a neighbour process)."""
+        return mpr_slab_state_ipc_handle(self.ctx)
+
+    def state_device(self) -> int:
+        """Device pointer of this slab's state buffer (for a neighbour in this process)."""
+        return mpr_slab_state_device(self.ctx)
+
+    def set_peer(self, side, ipc_handle=None, dev_ptr=None):
+        """Register the upper (side 0) / lower (side 1) neighbour's state buffer: the
+        half-sweep kernel then writes the boundary rows into it (fused halo exchange)."""
+        mpr_slab_set_peer(self.ctx, side, ipc_handle, dev_ptr)
 
     def slab_end(self):
         mpr_slab_end(self.ctx)

@@ -104,6 +104,8 @@ struct mpr_ctx {
   int64_t slab_row0 = 0, slab_row1 = 0, slab_m0 = 0, slab_m1 = 0, slab_mb = 0;
   int slab_R = 0, slab_S = 0;
   uint32_t slab_k0 = 0, slab_k1 = 0;
+  float* slab_peer[2] = {nullptr, nullptr};   // neighbouring slabs' state buffers
+  bool slab_peer_ipc[2] = {false, false};     // opened with cudaIpcOpenMemHandle
   std::vector<int> rowoff_h;  // host copy of the gap-id row offsets (2*Ly)
   // device memory
   DBuf z, mask, phiK, scal, calTd, caled, rowcnt, rowoff, gid, rec, bstats, Tb, T, T2, G, A, acc,
@@ -164,6 +166,13 @@ struct DeviceGuard {
 #define SET_DEVICE(c)                                                     \
   DeviceGuard dev_guard_((c)->device);                                   \
   if (dev_guard_.err != cudaSuccess) return cuda_fail(c, dev_guard_.err, "set device")
+
+// Forget a registered neighbour state buffer (row slabs), closing an IPC mapping.
+void clear_peer(mpr_ctx* c, int side) {
+  if (c->slab_peer_ipc[side] && c->slab_peer[side]) cudaIpcCloseMemHandle(c->slab_peer[side]);
+  c->slab_peer[side] = nullptr;
+  c->slab_peer_ipc[side] = false;
+}
 
 mpr_status validate_cfg(const mpr_config* cfg, std::string& why) {
   if (!cfg) { why = "cfg is NULL"; return MPR_ERR_INVALID_ARG; }
@@ -402,6 +411,8 @@ void mpr_destroy(mpr_ctx* c) {
   if (!c) return;
   DeviceGuard dev_guard(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  clear_peer(c, 0);
+  clear_peer(c, 1);
   DBuf* bufs[] = {&c->z, &c->mask, &c->phiK, &c->scal, &c->calTd, &c->caled, &c->rowcnt, &c->rowoff,
                   &c->gid, &c->rec, &c->bstats, &c->Tb, &c->T, &c->T2, &c->G, &c->A, &c->acc,
                   &c->energy, &c->out, &c->tmp, &c->win, &c->dclist, &c->dccnt};
@@ -928,6 +939,13 @@ mpr_status mpr_slab_half_sweep(mpr_ctx* c, int32_t sweep, int colour) {
   a.is_b = colour;
   a.accumulate = avg && (sweep > c->slab_S - c->cfg.n_avg);
   a.energy = nullptr;
+  // fused halo: the first own row goes to the upper neighbour, the last to the lower one
+  const int64_t brow[2] = {c->slab_row0, c->slab_row1 - 1};
+  for (int k = 0; k < 2; ++k) {
+    a.peer[k] = c->slab_peer[k];
+    a.peer_lo[k] = static_cast<uint32_t>(gap_row_offset(c, colour, brow[k]) * c->slab_R);
+    a.peer_hi[k] = static_cast<uint32_t>(gap_row_offset(c, colour, brow[k] + 1) * c->slab_R);
+  }
   launch_sweep_half(a, c->sweep_grid, c->sweep_variant, c->stream);
   CKL("sweep_half");
   return MPR_OK;
@@ -943,11 +961,60 @@ mpr_status mpr_slab_row_states(mpr_ctx* c, int64_t row, int colour, float** dev_
   return MPR_OK;
 }
 
+mpr_status mpr_slab_state_ipc_handle(mpr_ctx* c, void* handle_out) {
+  if (!c || !handle_out) return MPR_ERR_INVALID_ARG;
+  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_state_ipc_handle outside slab_begin/slab_end");
+  SET_DEVICE(c);
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->G.p), "cudaIpcGetMemHandle");
+  static_assert(sizeof(cudaIpcMemHandle_t) == MPR_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle_out, &h, sizeof h);
+  return MPR_OK;
+}
+
+mpr_status mpr_slab_state_device(mpr_ctx* c, float** dev_ptr) {
+  if (!c || !dev_ptr) return MPR_ERR_INVALID_ARG;
+  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_state_device outside slab_begin/slab_end");
+  *dev_ptr = c->G.as<float>();
+  return MPR_OK;
+}
+
+mpr_status mpr_slab_set_peer(mpr_ctx* c, int side, const void* ipc_handle, float* dev_ptr) {
+  if (!c || (side != 0 && side != 1) || (ipc_handle && dev_ptr)) return MPR_ERR_INVALID_ARG;
+  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_set_peer outside slab_begin/slab_end");
+  SET_DEVICE(c);
+  clear_peer(c, side);
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, sizeof h);
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    c->slab_peer[side] = static_cast<float*>(p);
+    c->slab_peer_ipc[side] = true;
+  } else if (dev_ptr) {
+    cudaPointerAttributes at{};
+    CK(cudaPointerGetAttributes(&at, dev_ptr), "peer pointer attributes");
+    if (at.type != cudaMemoryTypeDevice) return fail(c, MPR_ERR_INVALID_ARG, "peer pointer is not device memory");
+    if (at.device != c->device) {
+      int ok = 0;
+      CK(cudaDeviceCanAccessPeer(&ok, c->device, at.device), "peer access query");
+      if (!ok) return fail(c, MPR_ERR_INVALID_ARG, "peer device not reachable (no P2P)");
+      cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return cuda_fail(c, e, "enable peer access");
+    }
+    c->slab_peer[side] = dev_ptr;
+  }
+  return MPR_OK;
+}
+
 mpr_status mpr_slab_end(mpr_ctx* c) {
   if (!c) return MPR_ERR_INVALID_ARG;
   if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_end without slab_begin");
   SET_DEVICE(c);
   c->slab_active = 0;
+  clear_peer(c, 0);
+  clear_peer(c, 1);
   if (!(c->degenerate || c->P == 0)) {
     const bool avg = c->cfg.n_avg > 1;
     const int r_lo = static_cast<int>(c->slab_m0 - c->slab_mb), r_hi = static_cast<int>(c->slab_m1 - c->slab_mb);

@@ -193,7 +193,19 @@ __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec&
   }
   float2* const gp = BO ? reinterpret_cast<float2*>(reinterpret_cast<char*>(a.G) + self_off)
                         : reinterpret_cast<float2*>(a.G + self_off);
-  if (acc0 || acc1) *gp = make_float2(n0, n1);
+  if (acc0 || acc1) {
+    const float2 nv = make_float2(n0, n1);
+    *gp = nv;
+    // row slabs: a changed state of a boundary row also lands in the neighbour's buffer
+    // (its ghost row), so the halo exchange is part of the half-sweep itself
+    if (a.peer[0] != nullptr || a.peer[1] != nullptr) {
+      const uint32_t e = BO ? self_off >> 2 : self_off;
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (a.peer[k] != nullptr && e >= a.peer_lo[k] && e < a.peer_hi[k])
+          *reinterpret_cast<float2*>(a.peer[k] + e) = nv;
+    }
+  }
   if (accum0 || accum1) {
     float2* ap = BO ? reinterpret_cast<float2*>(reinterpret_cast<char*>(a.A) + self_off)
                     : reinterpret_cast<float2*>(a.A + self_off);

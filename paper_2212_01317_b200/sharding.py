@@ -94,10 +94,29 @@ def exchange_halo(engine, colour: int, r0: int, r1: int, rank: int, world: int, 
         engine.commit_row(row, colour, t)
 
 
-def distributed_fill_slabs(engine, grid, mask, M: int, sweeps: int, seed: int, group=None):
+def connect_peer_halo(engine, rank: int, world: int, group=None) -> None:
+    """Fused halo exchange set-up (after every slab_begin): all-gather the ranks' state
+    buffer IPC handles and register the neighbours' buffers, so each half-sweep kernel
+    writes its boundary rows straight into the neighbours' ghost rows over NVLink."""
+    handles = [None] * world
+    dist.all_gather_object(handles, engine.state_ipc_handle(), group=group)
+    if rank > 0:
+        engine.set_peer(0, ipc_handle=handles[rank - 1])
+    if rank < world - 1:
+        engine.set_peer(1, ipc_handle=handles[rank + 1])
+    dist.barrier(group=group)  # every mapping is in place before any kernel writes through it
+
+
+def distributed_fill_slabs(engine, grid, mask, M: int, sweeps: int, seed: int, group=None, halo: str = "peer"):
     """SPMD gap fill with the grid split into row slabs (one per rank) and a one-row halo
     exchange per colour half-sweep; every rank runs all M realizations on its rows. The
-    chains are bit-identical to the single-GPU run (global Philox counters)."""
+    chains are bit-identical to the single-GPU run (global Philox counters).
+
+    halo="peer": the half-sweep kernel writes the boundary rows into the neighbours'
+    state buffers (IPC-mapped peer memory); the host only orders half-sweeps (sync +
+    barrier). halo="nccl": the boundary rows are sent with NCCL point-to-point calls."""
+    if halo not in ("peer", "nccl"):
+        raise ValueError("halo must be 'peer' or 'nccl'")
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     Ly = grid.shape[0]
@@ -105,12 +124,18 @@ def distributed_fill_slabs(engine, grid, mask, M: int, sweeps: int, seed: int, g
     engine.set_data(grid, mask)
     engine.estimate_local_params()
     engine.reset_accumulator()
+    peer = halo == "peer" and world > 1
     for m0, m1 in slab_realization_chunks(M):
         engine.slab_begin(M, sweeps, seed, m0, m1, r0, r1)
+        if peer:
+            connect_peer_halo(engine, rank, world, group)
         for s in range(1, sweeps + 1):
             for colour in (0, 1):
                 engine.slab_half_sweep(s, colour)
-                if world > 1:
+                if peer:  # the kernels wrote the halos; finish the half-sweep everywhere
+                    engine.sync()
+                    dist.barrier(group=group)
+                elif world > 1:
                     exchange_halo(engine, colour, r0, r1, rank, world, group)
         engine.slab_end()
     allreduce_accumulator(engine.accumulator_tensor(), group)

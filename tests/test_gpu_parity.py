@@ -224,9 +224,12 @@ def test_c2_full_size_sampled(P, calib):
     m.close()
 
 
-def _emulated_slabs(P, z, mask, cfg, calib, M, S, seed, world):
-    """Row slabs of `world` contexts on one GPU; halo rows exchanged by device copies through
-    the same zero-copy row views the NCCL path sends from and receives into."""
+def _emulated_slabs(P, z, mask, cfg, calib, M, S, seed, world, halo="copy"):
+    """Row slabs of `world` contexts on one GPU. halo="copy": halo rows exchanged by device
+    copies through the same zero-copy row views the NCCL path sends from and receives
+    into. halo="peer": each context registers its neighbours' state buffers and the
+    half-sweep kernels write the boundary rows into them (the fused exchange); the host
+    only finishes every context's half-sweep before the next one starts."""
     import torch
     from paper_2212_01317_b200.sharding import row_range
     Ly = z.shape[0]
@@ -238,13 +241,19 @@ def _emulated_slabs(P, z, mask, cfg, calib, M, S, seed, world):
     for c0, c1 in slab_realization_chunks(M):  # the same realization split as bench / sharding
         for e, (r0, r1) in zip(engs, ranges):
             e.slab_begin(M, S, seed, c0, c1, r0, r1)
+        if halo == "peer":
+            for w, e in enumerate(engs):
+                if w > 0:
+                    e.set_peer(0, dev_ptr=engs[w - 1].state_device())
+                if w < world - 1:
+                    e.set_peer(1, dev_ptr=engs[w + 1].state_device())
         for s in range(1, S + 1):
             for colour in (0, 1):
                 for e in engs:
                     e.slab_half_sweep(s, colour)
                 for e in engs:
                     e.sync()
-                for w in range(world - 1):  # boundary between slab w and w+1
+                for w in range(world - 1 if halo == "copy" else 0):  # boundary between slab w and w+1
                     r = ranges[w][1]
                     engs[w + 1].row_view(r - 1, colour).copy_(engs[w].row_view(r - 1, colour))  # w's last row
                     engs[w].row_view(r, colour).copy_(engs[w + 1].row_view(r, colour))          # w+1's first row
@@ -260,15 +269,49 @@ def _emulated_slabs(P, z, mask, cfg, calib, M, S, seed, world):
     return pred
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_row_slabs_emulated_bit_exact(P, calib, world):
-    """Row-slab mode: slabs with one-row halo exchanges reproduce the
-    single-context predictions bit for bit (and therefore the oracle's)."""
+@pytest.mark.parametrize("halo", ["copy", "peer"])
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_row_slabs_emulated_bit_exact(P, calib, world, halo):
+    """Row-slab mode: slabs with one-row halo exchanges (row copies, or
+    the kernels writing into the neighbours' buffers) reproduce the single-context
+    predictions bit for bit (and therefore the oracle's)."""
     truth, z, mask = make_problem(61, 0.5, Lx=52, corr_len=6.0)
     cfg = P.Config(l_b=8, n_s=2, r_s=1)
     ref = gpu_run(P, z, mask, cfg, calib, 6, 10, 123)["pred"]
-    got = _emulated_slabs(P, z, mask, cfg, calib, 6, 10, 123, world)
-    assert_bitwise(got, ref, f"row slabs x{world}")
+    got = _emulated_slabs(P, z, mask, cfg, calib, 6, 10, 123, world, halo=halo)
+    assert_bitwise(got, ref, f"row slabs x{world} ({halo})")
+
+
+def _ipc_slab_worker(rank, world, port, out):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2212_01317_b200 as P
+    from paper_2212_01317_b200.sharding import distributed_fill_slabs
+    truth, z, mask = make_problem(61, 0.5, Lx=52, corr_len=6.0)
+    eng = P.LeMpr(P.Config(l_b=8, n_s=2, r_s=1), P.load_calibration())
+    out[rank] = distributed_fill_slabs(eng, z, mask, M=6, sweeps=10, seed=123, halo="peer")
+    eng.close()
+    dist.destroy_process_group()
+
+
+def test_row_slabs_ipc_peer_halo_two_processes(P, calib):
+    """The multi-process form of the fused halo: two processes (one GPU here, so both map
+    each other's state buffer with cudaIpcOpenMemHandle), handles all-gathered over a gloo
+    group, boundary rows written by the kernels, sync + barrier per half-sweep. Both ranks'
+    predictions equal the single-context run bit for bit."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    out = mp.get_context("spawn").Manager().dict()
+    mp.spawn(_ipc_slab_worker, args=(2, port, out), nprocs=2, join=True)
+    truth, z, mask = make_problem(61, 0.5, Lx=52, corr_len=6.0)
+    ref = gpu_run(P, z, mask, P.Config(l_b=8, n_s=2, r_s=1), calib, 6, 10, 123)["pred"]
+    for r in range(2):
+        assert_bitwise(out[r], ref, f"IPC peer-halo slabs, rank {r}")
 
 
 def _full_size_sampled(P, calib, L, p, gaps, nu, M, S, windows):

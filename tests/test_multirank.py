@@ -101,10 +101,28 @@ class OracleSlabEngine(OracleEngine):
     updated by oracle.half_sweep_rows, halo rows exchanged through row_view/commit_row."""
 
     def slab_begin(self, M, sweeps, seed, m0, m1, r0, r1):
+        from multiprocessing import shared_memory
         self.M, self.S, self.seed, self.m0, self.m1, self.r0, self.r1 = M, sweeps, seed, m0, m1, r0, r1
-        self.phi = np.stack([self.O.init_angles(self.p.phi0, self.mask, self.cfg.lb, self.p.SP, self.p.NK,
-                                                0 if self.cfg.init == "block_mean" else 1, m, seed)
-                             for m in range(m0, m1)])
+        init = np.stack([self.O.init_angles(self.p.phi0, self.mask, self.cfg.lb, self.p.SP, self.p.NK,
+                                            0 if self.cfg.init == "block_mean" else 1, m, seed)
+                         for m in range(m0, m1)])
+        # the state lives in a shared-memory segment so neighbour processes can write into it,
+        # as the GPU kernel writes into IPC-mapped neighbour buffers (halo="peer")
+        self.shm = shared_memory.SharedMemory(create=True, size=init.nbytes)
+        self.phi = np.ndarray(init.shape, init.dtype, buffer=self.shm.buf)
+        self.phi[...] = init
+        self.peers = [None, None]
+
+    def state_ipc_handle(self):
+        return self.shm.name.encode()
+
+    def set_peer(self, side, ipc_handle=None, dev_ptr=None):
+        from multiprocessing import shared_memory
+        seg = shared_memory.SharedMemory(name=ipc_handle.decode())
+        self.peers[side] = (seg, np.ndarray(self.phi.shape, self.phi.dtype, buffer=seg.buf))
+
+    def sync(self):
+        pass
 
     def slab_half_sweep(self, s, colour):
         for k, m in enumerate(range(self.m0, self.m1)):
@@ -112,6 +130,11 @@ class OracleSlabEngine(OracleEngine):
             self.O.half_sweep_rows(ph, self.mask, self.p.beta, s, m, self.seed, colour, self.r0, self.r1,
                                    q=self.cfg.q, J=self.cfg.J)
             self.phi[k] = ph
+        # fused halo: the boundary rows' colour-c gap states land in the neighbours' buffers
+        for side, row in ((0, self.r0), (1, self.r1 - 1)):
+            if self.peers[side] is not None:
+                cols = self._cols(row, colour)
+                self.peers[side][1][:, row, cols] = self.phi[:, row, cols]
 
     def _cols(self, row, colour):
         Lx = self.mask.shape[1]
@@ -132,9 +155,17 @@ class OracleSlabEngine(OracleEngine):
         acc = self.acc.numpy().reshape(self.mask.shape)  # a view: adds land in self.acc
         for k in range(self.phi.shape[0]):  # realization order, as the oracle accumulates
             acc[gaps] += self.phi[k][gaps].astype(np.float64)
+        for side in (0, 1):
+            if self.peers[side] is not None:
+                self.peers[side][0].close()
+        self.peers = [None, None]
+        dist.barrier()  # no neighbour still writes into this segment
+        self.phi = self.phi.copy()
+        self.shm.close()
+        self.shm.unlink()
 
 
-def _slab_worker(rank, world, port, out):
+def _slab_worker(rank, world, port, out, halo):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import oracle as O
@@ -143,19 +174,23 @@ def _slab_worker(rank, world, port, out):
     from tests.conftest import read_calibration
     truth, z, mask = make_problem(21, 0.6, Lx=18, corr_len=5.0)
     eng = OracleSlabEngine(read_calibration(), O.OracleConfig(lb=8, rs=1, ns=2))
-    out[rank] = distributed_fill_slabs(eng, z, mask, M=6, sweeps=5, seed=41)  # chunks [0,4), [4,6)
+    out[rank] = distributed_fill_slabs(eng, z, mask, M=6, sweeps=5, seed=41, halo=halo)  # chunks [0,4), [4,6)
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("halo", ["peer", "nccl"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_gloo_row_slabs_bit_exact(calib, world):
+def test_gloo_row_slabs_bit_exact(calib, world, halo):
     """Row-slab decomposition with one-row halos per colour half-sweep reproduces the
-    single-process chains bit for bit (global Philox counters)."""
+    single-process chains bit for bit (global Philox counters). halo="peer"
+    runs the fused-exchange protocol (handle all-gather, neighbour registration, boundary
+    rows written into the neighbours' shared buffers, sync + barrier per half-sweep);
+    halo="nccl" the point-to-point exchange."""
     import oracle as O
     from inputs.synth import make_problem
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_slab_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    mp.spawn(_slab_worker, args=(world, _free_port(), out, halo), nprocs=world, join=True)
     truth, z, mask = make_problem(21, 0.6, Lx=18, corr_len=5.0)
     ref = O.fill(z, mask, O.OracleConfig(lb=8, rs=1, ns=2), *calib, M=6, S=5, seed=41)["pred"]
     for r in range(world):
