@@ -146,21 +146,23 @@ __device__ __forceinline__ bool all_present(uint32_t f) {
 // One work item (gap site, realization pair) once its record and the states it reads
 // are in registers: Philox, two Metropolis updates, store, fused epilogues.
 // BO: self_off is a byte offset into G / A (see the PF == 4 kernel path), else an element offset.
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO = false>
+// PEER: the launch may carry neighbour state buffers (row slabs, fused halo): checked at
+// run time; kernels instantiated with PEER = false skip the check altogether.
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO = false, bool PEER = true>
 __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec& rec, float2 cur,
                                                const float2 (&nb)[4], uint32_t self_off, const Words4& w,
                                                long long& e0, long long& e1, bool accum0, bool accum1);
 
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO = false>
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO = false, bool PEER = true>
 __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& rec, float2 cur,
                                              const float2 (&nb)[4], uint32_t self_off, uint32_t pair,
                                              long long& e0, long long& e1, bool accum0, bool accum1) {
   const Words4 w = philox4x32_10_rk(rec.site, a.sweep, pair, 2u, a.rk0, a.rk1);
-  process_item_w<QHALF, ENERGY, BFEXP, PK, BO>(a, rec, cur, nb, self_off, w, e0, e1, accum0, accum1);
+  process_item_w<QHALF, ENERGY, BFEXP, PK, BO, PEER>(a, rec, cur, nb, self_off, w, e0, e1, accum0, accum1);
 }
 
 // The item once its Philox words are known (the quad kernel may draw them early).
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO>
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO, bool PEER>
 __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec& rec, float2 cur,
                                                const float2 (&nb)[4], uint32_t self_off, const Words4& w,
                                                long long& e0, long long& e1, bool accum0, bool accum1) {
@@ -198,7 +200,7 @@ __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec&
     *gp = nv;
     // row slabs: a changed state of a boundary row also lands in the neighbour's buffer
     // (its ghost row), so the halo exchange is part of the half-sweep itself
-    if (a.peer[0] != nullptr || a.peer[1] != nullptr) {
+    if (PEER && (a.peer[0] != nullptr || a.peer[1] != nullptr)) {
       const uint32_t e = BO ? self_off >> 2 : self_off;
 #pragma unroll
       for (int k = 0; k < 2; ++k)
@@ -401,7 +403,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
 // the NP pairs, and the own / neighbour states move as float4 (two pairs each). Each pair
 // still draws its own Philox call and runs metropolis_pair, so the results are those of
 // k_sweep_half bit for bit. Requires npairs % NP == 0 (launch_sweep_half falls back).
-template <bool QHALF, bool ENERGY, int MINB, bool LIST, int NP = 2, bool EARLY = false>
+template <bool QHALF, bool ENERGY, int MINB, bool LIST, int NP = 2, bool EARLY = false, bool PEER = false>
 __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
   constexpr int NQ = NP / 2;  // float4 quads per thread
   const int nq = a.npairs / NP;
@@ -483,18 +485,18 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
         const int pa = 2 * qd, pb = 2 * qd + 1;
         if (EARLY) {
           if (live[pa])
-            process_item_w<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
+            process_item_w<QHALF, ENERGY, true, true, false, PEER>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
                                                       wpre[pa], e[pa][0], e[pa][1], acc[pa][0], acc[pa][1]);
           if (live[pb])
-            process_item_w<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.z, cur.w), nbB,
+            process_item_w<QHALF, ENERGY, true, true, false, PEER>(a, rec, make_float2(cur.z, cur.w), nbB,
                                                       self_off + 4u * qd + 2u, wpre[pb], e[pb][0], e[pb][1],
                                                       acc[pb][0], acc[pb][1]);
         } else {
           if (live[pa])
-            process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
+            process_item<QHALF, ENERGY, true, true, false, PEER>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
                                                     pair0 + pa, e[pa][0], e[pa][1], acc[pa][0], acc[pa][1]);
           if (live[pb])
-            process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 4u * qd + 2u,
+            process_item<QHALF, ENERGY, true, true, false, PEER>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 4u * qd + 2u,
                                                     pair0 + pb, e[pb][0], e[pb][1], acc[pb][0], acc[pb][1]);
         }
       }
@@ -617,24 +619,28 @@ static size_t sweep_smem(int) { return 0; }
 static bool is_quad(int variant) { return variant == 22 || variant == 23 || variant == 27 || variant == 28; }
 static int pairs_per_thread(int variant) { return is_quad(variant) ? 2 : 1; }
 
-template <bool Q, bool E>
+template <bool Q, bool E, bool PE>
 static void* quad_kernel_ptr(bool list, int variant) {
   if (variant == 27)
-    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true, 2, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false, 2, true>);
+    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true, 2, true, PE>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false, 2, true, PE>);
   if (variant == 28)
-    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true, 2, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false, 2, true>);
+    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true, 2, true, PE>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false, 2, true, PE>);
   if (variant == 23)
-    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false>);
-  return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false>);
+    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true, 2, false, PE>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false, 2, false, PE>);
+  return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true, 2, false, PE>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false, 2, false, PE>);
 }
 
-static void* quad_kernel(bool qhalf, bool energy, bool list, int variant) {
-  if (qhalf) return energy ? quad_kernel_ptr<true, true>(list, variant) : quad_kernel_ptr<true, false>(list, variant);
-  return energy ? quad_kernel_ptr<false, true>(list, variant) : quad_kernel_ptr<false, false>(list, variant);
+// peer: the launch writes into neighbour state buffers (row slabs with the fused halo)
+static void* quad_kernel(bool qhalf, bool energy, bool list, int variant, bool peer) {
+  if (peer) {  // slab mode: no energy trace
+    return qhalf ? quad_kernel_ptr<true, false, true>(list, variant) : quad_kernel_ptr<false, false, true>(list, variant);
+  }
+  if (qhalf) return energy ? quad_kernel_ptr<true, true, false>(list, variant) : quad_kernel_ptr<true, false, false>(list, variant);
+  return energy ? quad_kernel_ptr<false, true, false>(list, variant) : quad_kernel_ptr<false, false, false>(list, variant);
 }
 
-static void* sweep_kernel(bool qhalf, bool energy, bool list, int variant) {
-  if (is_quad(variant)) return quad_kernel(qhalf, energy, list, variant);
+static void* sweep_kernel(bool qhalf, bool energy, bool list, int variant, bool peer = false) {
+  if (is_quad(variant)) return quad_kernel(qhalf, energy, list, variant, peer);
   if (list) {
     if (qhalf) return energy ? sweep_kernel_ptr<true, true, true>(variant) : sweep_kernel_ptr<true, false, true>(variant);
     return energy ? sweep_kernel_ptr<false, true, true>(variant) : sweep_kernel_ptr<false, false, true>(variant);
@@ -678,7 +684,8 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   const int64_t need = (units + nt - 1) / nt;  // active threads >= units
   if (g < need) g = need;
   if (g < 1) g = 1;
-  void* fn = sweep_kernel(qhalf, energy, a.glist != nullptr, variant);
+  const bool peer = a.peer[0] != nullptr || a.peer[1] != nullptr;
+  void* fn = sweep_kernel(qhalf, energy, a.glist != nullptr, variant, peer);
   SweepArgs b = a;
   for (int i = 0; i < 10; ++i) {
     b.rk0[i] = a.k0 + static_cast<uint32_t>(i) * 0x9E3779B9u;
