@@ -323,10 +323,14 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
   cap -= cap & 1;
   if (cap < 2) cap = 2;
   int64_t B = std::min(R, cap);
-  // the default sweep kernel (variant 22) moves two realization pairs per thread and needs
-  // an even pair count per batch: split R = 4k + 2 as 4k + 2 (e.g. M = 10 -> 8 + 2; the
-  // 2-realization batch runs the one-pair kernel)
-  if ((c->sweep_variant == 22 || c->sweep_variant == 23 || c->sweep_variant == 27 || c->sweep_variant == 28) && B % 4 == 2 && B > 2) B -= 2;
+  // The default sweep kernel (variants 22-28) moves two realization pairs per thread and
+  // needs an even pair count per batch: split R = 4k + 2 as 4k + 2 (e.g. M = 10 -> 8 + 2;
+  // the 2-realization batch runs the one-pair kernel). Only for large grids: a separate 2-realization batch costs a full launch sequence,
+  // which small, latency-bound problems do not win back (256^2..1024^2, M = 10: measured
+  // 0.36 -> 0.50 ms and 1.25 -> 1.39 ms when split; 16384^2: 3.85 -> 3.40 ms / half-sweep).
+  if ((c->sweep_variant == 22 || c->sweep_variant == 23 || c->sweep_variant == 27 || c->sweep_variant == 28) &&
+      B % 4 == 2 && B > 2 && c->P >= (int64_t(1) << 21))
+    B -= 2;
   c->batch_key_P = c->P;
   c->batch_key_R = R;
   c->batch_cached = B;
