@@ -382,9 +382,9 @@ def run_mpr(args):
 def sweep_kernel_name(variant, batch):
     """Name of the half-sweep kernel the library launched (mpr_info.sweep_variant and the
     realization batch: the quad kernel needs an even pair count)."""
-    if variant in (22, 23, 27, 28) and batch % 4 == 0:
+    if variant in (22, 28) and batch % 4 == 0:
         return f"k_sweep_quad (variant {variant}: two realization pairs per thread)"
-    return f"k_sweep_half (variant {13 if variant in (22, 23, 27, 28) else variant})"
+    return f"k_sweep_half (variant {13 if variant in (22, 28) else variant})"
 
 
 def main():

@@ -313,23 +313,15 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
   int64_t cap = static_cast<int64_t>(budget / per_r);
   // the sweep kernel indexes the state with 32-bit element offsets: P * R < 2^31
   cap = std::min<int64_t>(cap, ((int64_t(1) << 31) - 1) / std::max<int64_t>(c->P, 1));
-  // the default sweep kernel (variant 15) uses 32-bit byte offsets while P * R * 4 < 2^32:
-  // prefer batches that fit when that still leaves >= 4 realizations per batch (measured
-  // C4, M = 10: batches 6 + 4 at 3.74 ms per half-sweep vs one batch of 10 at 3.84 ms)
-  if (c->sweep_variant >= 15 && c->sweep_variant <= 17) {
-    const int64_t byte_cap = ((int64_t(1) << 32) - 1) / (4 * std::max<int64_t>(c->P, 1));
-    if (byte_cap >= 4) cap = std::min(cap, byte_cap);
-  }
   cap -= cap & 1;
   if (cap < 2) cap = 2;
   int64_t B = std::min(R, cap);
-  // The default sweep kernel (variants 22-28) moves two realization pairs per thread and
+  // The default sweep kernel (variants 22, 28) moves two realization pairs per thread and
   // needs an even pair count per batch: split R = 4k + 2 as 4k + 2 (e.g. M = 10 -> 8 + 2;
   // the 2-realization batch runs the one-pair kernel). Only for large grids: a separate 2-realization batch costs a full launch sequence,
   // which small, latency-bound problems do not win back (256^2..1024^2, M = 10: measured
   // 0.36 -> 0.50 ms and 1.25 -> 1.39 ms when split; 16384^2: 3.85 -> 3.40 ms / half-sweep).
-  if ((c->sweep_variant == 22 || c->sweep_variant == 23 || c->sweep_variant == 27 || c->sweep_variant == 28) &&
-      B % 4 == 2 && B > 2 && c->P >= (int64_t(1) << 21))
+  if ((c->sweep_variant == 22 || c->sweep_variant == 28) && B % 4 == 2 && B > 2 && c->P >= (int64_t(1) << 21))
     B -= 2;
   c->batch_key_P = c->P;
   c->batch_key_R = R;

@@ -145,24 +145,23 @@ __device__ __forceinline__ bool all_present(uint32_t f) {
 
 // One work item (gap site, realization pair) once its record and the states it reads
 // are in registers: Philox, two Metropolis updates, store, fused epilogues.
-// BO: self_off is a byte offset into G / A (see the PF == 4 kernel path), else an element offset.
 // PEER: the launch may carry neighbour state buffers (row slabs, fused halo): checked at
 // run time; kernels instantiated with PEER = false skip the check altogether.
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO = false, bool PEER = true>
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool PEER = true>
 __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec& rec, float2 cur,
                                                const float2 (&nb)[4], uint32_t self_off, const Words4& w,
                                                long long& e0, long long& e1, bool accum0, bool accum1);
 
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO = false, bool PEER = true>
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool PEER = true>
 __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& rec, float2 cur,
                                              const float2 (&nb)[4], uint32_t self_off, uint32_t pair,
                                              long long& e0, long long& e1, bool accum0, bool accum1) {
   const Words4 w = philox4x32_10_rk(rec.site, a.sweep, pair, 2u, a.rk0, a.rk1);
-  process_item_w<QHALF, ENERGY, BFEXP, PK, BO, PEER>(a, rec, cur, nb, self_off, w, e0, e1, accum0, accum1);
+  process_item_w<QHALF, ENERGY, BFEXP, PK, PEER>(a, rec, cur, nb, self_off, w, e0, e1, accum0, accum1);
 }
 
 // The item once its Philox words are known (the quad kernel may draw them early).
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool BO, bool PEER>
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool PEER>
 __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec& rec, float2 cur,
                                                const float2 (&nb)[4], uint32_t self_off, const Words4& w,
                                                long long& e0, long long& e1, bool accum0, bool accum1) {
@@ -193,24 +192,21 @@ __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec&
     n0 = metropolis<QHALF, ENERGY, false, BFEXP>(cur.x, nv0, rec.flags, sel, rec.beta, a.q, a.J, w.w0, w.w1, acc0, e0);
     n1 = metropolis<QHALF, ENERGY, false, BFEXP>(cur.y, nv1, rec.flags, sel, rec.beta, a.q, a.J, w.w2, w.w3, acc1, e1);
   }
-  float2* const gp = BO ? reinterpret_cast<float2*>(reinterpret_cast<char*>(a.G) + self_off)
-                        : reinterpret_cast<float2*>(a.G + self_off);
+  float2* const gp = reinterpret_cast<float2*>(a.G + self_off);
   if (acc0 || acc1) {
     const float2 nv = make_float2(n0, n1);
     *gp = nv;
     // row slabs: a changed state of a boundary row also lands in the neighbour's buffer
     // (its ghost row), so the halo exchange is part of the half-sweep itself
     if (PEER && (a.peer[0] != nullptr || a.peer[1] != nullptr)) {
-      const uint32_t e = BO ? self_off >> 2 : self_off;
 #pragma unroll
       for (int k = 0; k < 2; ++k)
-        if (a.peer[k] != nullptr && e >= a.peer_lo[k] && e < a.peer_hi[k])
-          *reinterpret_cast<float2*>(a.peer[k] + e) = nv;
+        if (a.peer[k] != nullptr && self_off >= a.peer_lo[k] && self_off < a.peer_hi[k])
+          *reinterpret_cast<float2*>(a.peer[k] + self_off) = nv;
     }
   }
   if (accum0 || accum1) {
-    float2* ap = BO ? reinterpret_cast<float2*>(reinterpret_cast<char*>(a.A) + self_off)
-                    : reinterpret_cast<float2*>(a.A + self_off);
+    float2* ap = reinterpret_cast<float2*>(a.A + self_off);
     float2 av = *ap;
     if (accum0) av.x = __fadd_rn(av.x, n0);
     if (accum1) av.y = __fadd_rn(av.y, n1);
@@ -285,46 +281,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
     // adaptive protocol: a pair whose two realizations have finished is frozen
     if (a.win_hi) live = static_cast<int>(a.sweep) <= max(a.win_hi[2 * sp.j], a.win_hi[2 * sp.j + 1]);
   }
-  if (live && PF == 4) {
-    // As PF == 3, with 32-bit BYTE offsets into G: base + u32 offset is IADD3 / IADD3.X on
-    // the ALU pipe instead of IMAD.WIDE.U32 on the FMA-heavy pipe the kernel saturates.
-    // Valid while P * R * 4 < 2^32 (launch_sweep_half checks and falls back to PF == 3).
-    const char* const Gb = reinterpret_cast<const char*>(a.G);
-    const uint32_t R4 = 4u * R, j2b = 4u * j2;
-    const uint32_t pair = a.pair_base + static_cast<uint32_t>(sp.j);
-    uint32_t g = sp.g0;
-    uint32_t gg = 0;
-    GapRec rec{};
-    if (g < gcount) {
-      gg = LIST ? a.glist[g] : gbegin + g;
-      rec = a.rec[gg];
-    }
-    for (; g < gcount; g += sp.gstride) {
-      const uint32_t gn = g + sp.gstride;
-      uint32_t ggn = 0;
-      GapRec recn{};
-      if (gn < gcount) {
-        ggn = LIST ? a.glist[gn] : gbegin + gn;
-        recn = a.rec[ggn];
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(Gb + (ggn * R4 + j2b)));
-      }
-      const uint32_t self_off = gg * R4 + j2b;
-      const float2 cur = *reinterpret_cast<const float2*>(Gb + self_off);
-      float2 nb[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
-        if (ty == NB_GAP) {
-          nb[k] = *reinterpret_cast<const float2*>(Gb + (static_cast<uint32_t>(rec.nb[k]) * R4 + j2b));
-        } else {
-          nb[k] = f2(__int_as_float(rec.nb[k]));
-        }
-      }
-      process_item<QHALF, ENERGY, BFEXP, PK, true>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
-      rec = recn;
-      gg = ggn;
-    }
-  } else if (live && PF == 3) {
+  if (live && PF == 3) {
     // Record one item ahead: the 32-byte record of item g + gstride is loaded into registers
     // while item g computes, so an item waits for one dependent round trip (its neighbour
     // states), not two (record, then states). Plus the L2 prefetch of the next own state.
@@ -485,18 +442,18 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
         const int pa = 2 * qd, pb = 2 * qd + 1;
         if (EARLY) {
           if (live[pa])
-            process_item_w<QHALF, ENERGY, true, true, false, PEER>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
+            process_item_w<QHALF, ENERGY, true, true, PEER>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
                                                       wpre[pa], e[pa][0], e[pa][1], acc[pa][0], acc[pa][1]);
           if (live[pb])
-            process_item_w<QHALF, ENERGY, true, true, false, PEER>(a, rec, make_float2(cur.z, cur.w), nbB,
+            process_item_w<QHALF, ENERGY, true, true, PEER>(a, rec, make_float2(cur.z, cur.w), nbB,
                                                       self_off + 4u * qd + 2u, wpre[pb], e[pb][0], e[pb][1],
                                                       acc[pb][0], acc[pb][1]);
         } else {
           if (live[pa])
-            process_item<QHALF, ENERGY, true, true, false, PEER>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
+            process_item<QHALF, ENERGY, true, true, PEER>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
                                                     pair0 + pa, e[pa][0], e[pa][1], acc[pa][0], acc[pa][1]);
           if (live[pb])
-            process_item<QHALF, ENERGY, true, true, false, PEER>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 4u * qd + 2u,
+            process_item<QHALF, ENERGY, true, true, PEER>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 4u * qd + 2u,
                                                     pair0 + pb, e[pb][0], e[pb][1], acc[pb][0], acc[pb][1]);
         }
       }
@@ -579,55 +536,38 @@ __global__ void __launch_bounds__(kAccTile) k_acc_reduce(const float* __restrict
 
 }  // namespace
 
-// Kernel variants (tuning knob, MPR_SWEEP_VARIANT; profiles/r01_summary.md records every
-// alternative measured). 0 = plain scalar, 2 = + register-free L2 prefetch of the next item,
-// 5 = 2 + branch-free exp, 8 = 5 at <= 64 registers; packed f32x2 arithmetic from here on:
-// 10 = 5 packed, 11 = 10 at <= 64 registers, 12 = 10 + record one item ahead (3 CTAs/SM),
-// 13 (default) = 12 at <= 64 registers (4 CTAs/SM), 15 / 16 / 17 = 12 with 32-bit byte
-// offsets at 1 / 3 / 4 CTAs/SM declared (fall back to 12 when P * R * 4 >= 2^32),
-// 18 / 19 = 12 / 15 at <= 51 registers (5 CTAs/SM), 22 / 23 = k_sweep_quad (two pairs per
-// thread, float4 state moves) at 4 / 3 CTAs/SM, 27 / 28 (default) = 22 / 23 with both
-// pairs' Philox words drawn before the state loads are consumed (all fall back to 13 for
-// an odd pair count).
-// Half-sweep, us (Philox round keys as kernel parameters, all variants bit-identical):
-//   C2: v5 98.2, v12 97.2, v13 93.9, v15 98.5, v17 95.4, v18 95.4;
-//   C3: v12 2113, v13 2071, v15 2201, v17 2088, v19 2067;  C4: v12 3778, v13 3717, v17 3697;
-//   v22: C2 87.1, C3 1838, C4 (batches 8 + 2) 3402;  v28: C2 84.8, C3 1783, C4 3386.
+// Kernel variants (tuning knob, MPR_SWEEP_VARIANT). profiles/r01_summary.md records every
+// alternative measured, including the ones no longer built: 32-bit byte offsets, register
+// caps at 3/5 CTAs, two records ahead with neighbour prefetch, four pairs per thread, and
+// split IMAD.HI/IMAD Philox products. All variants are bit-identical.
+//   5  = one pair per thread, scalar arithmetic, L2 prefetch of the next item
+//        (the first optimised kernel, kept as the scalar reference);
+//   13 = one pair per thread, packed f32x2, record one item ahead, 4 CTAs/SM
+//        (the fallback of 22/28 for odd pair counts);
+//   22 = k_sweep_quad: two pairs per thread, float4 state moves, 4 CTAs/SM;
+//   28 = 22 with both pairs' Philox words drawn before the state loads are used,
+//        3 CTAs/SM (default).
+// Half-sweep, us (C2 / C3 / C4 at M = 10):
+//   v5  99.5 / 2229 / 4127;  v13 93.9 / 2071 / 3717;
+//   v22 87.1 / 1838 / 3402;  v28 84.5 / 1780 / 3351.
 template <bool Q, bool E, bool LIST>
 static void* sweep_kernel_ptr(int variant) {
-  switch (variant) {
-    case 0: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 0, 256, false, LIST, false>);
-    case 2: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, false, LIST, false>);
-    case 5: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, false>);
-    case 8: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 2, 256, true, LIST, false>);
-    case 10: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, true>);
-    case 11: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 2, 256, true, LIST, true>);
-    case 12: return reinterpret_cast<void*>(k_sweep_half<Q, E, 3, 3, 256, true, LIST, true>);
-    case 15: return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 4, 256, true, LIST, true>);
-    case 16: return reinterpret_cast<void*>(k_sweep_half<Q, E, 3, 4, 256, true, LIST, true>);
-    case 17: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 4, 256, true, LIST, true>);
-    case 18: return reinterpret_cast<void*>(k_sweep_half<Q, E, 5, 3, 256, true, LIST, true>);
-    case 19: return reinterpret_cast<void*>(k_sweep_half<Q, E, 5, 4, 256, true, LIST, true>);
-    default: return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);  // 13 (and 22/23's fallback)
-  }
+  if (variant == 5) return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, false>);
+  return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);  // 13 (and 22/28's fallback)
 }
 
 static int sweep_threads(int) { return 256; }
 
 static size_t sweep_smem(int) { return 0; }
 
-static bool is_quad(int variant) { return variant == 22 || variant == 23 || variant == 27 || variant == 28; }
+static bool is_quad(int variant) { return variant == 22 || variant == 28; }
 static int pairs_per_thread(int variant) { return is_quad(variant) ? 2 : 1; }
 
 template <bool Q, bool E, bool PE>
 static void* quad_kernel_ptr(bool list, int variant) {
-  if (variant == 27)
-    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true, 2, true, PE>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false, 2, true, PE>);
   if (variant == 28)
     return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true, 2, true, PE>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false, 2, true, PE>);
-  if (variant == 23)
-    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true, 2, false, PE>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false, 2, false, PE>);
-  return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true, 2, false, PE>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false, 2, false, PE>);
+  return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true, 2, false, PE>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false, 2, false, PE>);  // 22
 }
 
 // peer: the launch writes into neighbour state buffers (row slabs with the fused halo)
@@ -654,9 +594,8 @@ int sweep_grid_size(int device, int variant) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, false, variant), sweep_threads(variant),
                                                 sweep_smem(variant));
-  // variants that may fall back at launch (byte offsets: large P * R -> 12; two-pair
-  // kernels: odd pair count -> 13): size the grid for both kernels
-  const int fb = (variant == 15 || variant == 16 || variant == 17 || variant == 19) ? 12 : is_quad(variant) ? 13 : -1;
+  // the two-pair kernels fall back to 13 for an odd pair count: size the grid for both
+  const int fb = is_quad(variant) ? 13 : -1;
   if (fb >= 0) {
     for (int e = 0; e < 2; ++e) {
       int perf = 0;
@@ -672,8 +611,6 @@ int sweep_grid_size(int device, int variant) {
 void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st) {
   const bool qhalf = (a.q == 0.5f);
   const bool energy = (a.energy != nullptr);
-  // byte-offset variant only while every byte offset into G fits in 32 bits
-  if ((variant == 15 || variant == 16 || variant == 17 || variant == 19) && a.P * static_cast<int64_t>(a.R) * 4 >= (int64_t{1} << 32)) variant = 12;
   // the two-pair kernels need an even pair count (float4 alignment)
   if (is_quad(variant) && (a.npairs & 1)) variant = 13;
   const int nt = sweep_threads(variant);

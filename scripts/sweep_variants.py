@@ -26,7 +26,7 @@ def sm_clock():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--variants", default="0,1,2,3,4")
+    ap.add_argument("--variants", default="5,13,22,28")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--M", type=int, default=None)
     ap.add_argument("--max-batch", default="0", help="comma list of max_batch values to try")
