@@ -29,6 +29,14 @@ namespace {
 
 constexpr int kMaxPairs = 512;  // batch <= 1024 realizations
 
+// Programmatic dependent launch (the batch's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, see launch_pdl): a kernel may be
+// scheduled while its predecessor drains; pdl_wait() blocks until the predecessor's
+// memory operations are complete and visible, pdl_trigger() (after a CTA's last global
+// write) lets the successor start launching. Both are no-ops without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 template <bool QHALF>
 __device__ __forceinline__ float cosq(float d, float q) {
   if (QHALF) return cos_half_spec(d);
@@ -267,6 +275,7 @@ __device__ __forceinline__ Split split_work(int npairs) {
 // at the start of each item (PF: register-free prefetch of the next item).
 template <bool QHALF, bool ENERGY, int MINB, int PF, int NT, bool BFEXP, bool LIST, bool PK>
 __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
+  pdl_wait();
   const Split sp = split_work(a.npairs);
   // 32-bit element offsets: the host caps the batch so that P * R < 2^31
   const uint32_t R = static_cast<uint32_t>(a.R);
@@ -352,6 +361,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
     }
   }
   if (ENERGY) energy_epilogue(a, a.npairs, sp.active && live, sp.j, e0, e1);
+  pdl_trigger();
 }
 
 // NP realization pairs (2 NP realizations) of one gap site per thread (NP = 2; NP = 4 was
@@ -362,6 +372,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
 // k_sweep_half bit for bit. Requires npairs % NP == 0 (launch_sweep_half falls back).
 template <bool QHALF, bool ENERGY, int MINB, bool LIST, int NP = 2, bool EARLY = false, bool PEER = false>
 __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
+  pdl_wait();
   constexpr int NQ = NP / 2;  // float4 quads per thread
   const int nq = a.npairs / NP;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -477,6 +488,7 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
       if (t >= a.r_valid_lo && t < a.r_valid_hi && es[t] != 0ull)
         atomicAdd(reinterpret_cast<unsigned long long*>(a.energy + static_cast<int64_t>(t) * a.energy_stride), es[t]);
   }
+  pdl_trigger();
 }
 
 // a6: initial states of a batch (ARITH §G).
@@ -485,6 +497,7 @@ __global__ void __launch_bounds__(256) k_init_states(const GapRec* __restrict__ 
                                                      int64_t P, int R, int npairs,
                                                      uint32_t pair_base, int random_init,
                                                      uint32_t k0, uint32_t k1) {
+  pdl_wait();
   const int64_t items = P * npairs;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < items;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -501,6 +514,7 @@ __global__ void __launch_bounds__(256) k_init_states(const GapRec* __restrict__ 
     *reinterpret_cast<float2*>(G + g * R + 2 * j) = v;
     if (A) *reinterpret_cast<float2*>(A + g * R + 2 * j) = make_float2(0.0f, 0.0f);
   }
+  pdl_trigger();
 }
 
 // a9 (realization sum): acc[g] += sum_{r in [r_lo, r_hi)} X[g][r], fp64, r ascending —
@@ -512,6 +526,7 @@ constexpr int kAccTile = 256, kAccChunk = 32;
 __global__ void __launch_bounds__(kAccTile) k_acc_reduce(const float* __restrict__ X, int64_t g_begin,
                                                          int64_t g_end, int R, int r_lo, int r_hi,
                                                          double* __restrict__ acc) {
+  pdl_wait();
   __shared__ float sm[kAccTile * (kAccChunk + 1)];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t g0 = g_begin + (int64_t)blockIdx.x * kAccTile; g0 < g_end; g0 += (int64_t)gridDim.x * kAccTile) {
@@ -532,6 +547,7 @@ __global__ void __launch_bounds__(kAccTile) k_acc_reduce(const float* __restrict
     }
     if (g < g_end) acc[g] = s;
   }
+  pdl_trigger();
 }
 
 }  // namespace
@@ -608,6 +624,21 @@ int sweep_grid_size(int device, int variant) {
   return sms * per;
 }
 
+// Launch with the programmatic-stream-serialization attribute (PDL, see pdl_wait).
+static void launch_pdl(const void* fn, unsigned grid, unsigned block, void** args, size_t smem, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st) {
   const bool qhalf = (a.q == 0.5f);
   const bool energy = (a.energy != nullptr);
@@ -629,7 +660,7 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
     b.rk1[i] = a.k1 + static_cast<uint32_t>(i) * 0xBB67AE85u;
   }
   void* args[] = {&b};
-  cudaLaunchKernel(fn, dim3(static_cast<unsigned>(g)), dim3(nt), args, sweep_smem(variant), st);
+  launch_pdl(fn, static_cast<unsigned>(g), static_cast<unsigned>(nt), args, sweep_smem(variant), st);
 }
 
 void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,
@@ -639,8 +670,8 @@ void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R,
   int64_t g = (items + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
   if (g < 1) g = 1;
-  k_init_states<<<static_cast<unsigned>(g), 256, 0, st>>>(rec, G, A, P, R, npairs, pair_base,
-                                                          random_init, k0, k1);
+  void* args[] = {const_cast<GapRec**>(&rec), &G, &A, &P, &R, &npairs, &pair_base, &random_init, &k0, &k1};
+  launch_pdl(reinterpret_cast<const void*>(k_init_states), static_cast<unsigned>(g), 256, args, 0, st);
 }
 
 void launch_acc_reduce(const float* X, int64_t g_begin, int64_t g_count, int R, int r_lo, int r_hi,
@@ -649,7 +680,9 @@ void launch_acc_reduce(const float* X, int64_t g_begin, int64_t g_count, int R, 
   int64_t g = (g_count + kAccTile - 1) / kAccTile;
   if (g > 148 * 16) g = 148 * 16;
   if (g < 1) g = 1;
-  k_acc_reduce<<<static_cast<unsigned>(g), kAccTile, 0, st>>>(X, g_begin, g_begin + g_count, R, r_lo, r_hi, acc);
+  int64_t g_end = g_begin + g_count;
+  void* args[] = {const_cast<float**>(&X), &g_begin, &g_end, &R, &r_lo, &r_hi, &acc};
+  launch_pdl(reinterpret_cast<const void*>(k_acc_reduce), static_cast<unsigned>(g), kAccTile, args, 0, st);
 }
 
 }  // namespace mpr
