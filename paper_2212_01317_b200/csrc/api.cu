@@ -753,8 +753,17 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
   CK(c->A.ensure(sizeof(float) * c->P * R), "alloc accumulator state");
   CK(c->energy.ensure(sizeof(long long) * R * max_sweeps), "alloc energy");
   CK(c->win.ensure(sizeof(int) * 2 * R), "alloc windows");
-  std::vector<long long> fx(static_cast<size_t>(R * max_sweeps));
-  std::vector<int> win(static_cast<size_t>(2 * R));
+  // pinned host staging: at a check only the last n_fit energies of every realization
+  // come back (one strided 2-D copy), and the windows go down from pinned memory
+  long long* fx = nullptr;
+  int* win = nullptr;
+  CK(cudaMallocHost(reinterpret_cast<void**>(&fx), sizeof(long long) * R * n_fit), "pinned energies");
+  struct PinnedFree {
+    void* p;
+    ~PinnedFree() { if (p) cudaFreeHost(p); }
+  } fx_free{fx};
+  CK(cudaMallocHost(reinterpret_cast<void**>(&win), sizeof(int) * 2 * R), "pinned windows");
+  PinnedFree win_free{win};
   std::vector<double> y(static_cast<size_t>(n_fit));
   for (int64_t mb = 0; mb < M; mb += R) {
     const int64_t span = std::min<int64_t>(R, M - mb);
@@ -767,7 +776,7 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
       win[Rb + r] = r < r_hi ? INT32_MAX : 0;
     }
     std::vector<int> eq(static_cast<size_t>(Rb), 0);
-    CK(cudaMemcpyAsync(c->win.p, win.data(), sizeof(int) * 2 * Rb, cudaMemcpyHostToDevice, st), "H2D windows");
+    CK(cudaMemcpyAsync(c->win.p, win, sizeof(int) * 2 * Rb, cudaMemcpyHostToDevice, st), "H2D windows");
     CK(cudaMemsetAsync(c->energy.p, 0, sizeof(long long) * Rb * max_sweeps, st), "zero energy");
     launch_init_states(c->rec.as<GapRec>(), c->G.as<float>(), c->A.as<float>(), c->P, Rb, Rb / 2,
                        static_cast<uint32_t>(mb / 2), c->cfg.init == MPR_INIT_RANDOM, k0, k1, st);
@@ -811,15 +820,21 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
       const bool check = s >= n_fit + n_f && (s - n_fit) % n_f == 0 && s + n_avg <= max_sweeps;
       const bool forced = s == max_sweeps - n_avg;
       if (pending > 0 && (check || forced)) {
-        CK(cudaMemcpyAsync(fx.data(), c->energy.p, sizeof(long long) * Rb * max_sweeps, cudaMemcpyDeviceToHost, st),
-           "D2H energy");
+        // energies of sweeps s-n_fit+1 .. s of every realization: rows of n_fit values at
+        // pitch max_sweeps (the forced decision needs none)
+        if (check) {
+          CK(cudaMemcpy2DAsync(fx, sizeof(long long) * n_fit,
+                               c->energy.as<long long>() + (s - n_fit), sizeof(long long) * max_sweeps,
+                               sizeof(long long) * n_fit, Rb, cudaMemcpyDeviceToHost, st),
+             "D2H energy window");
+        }
         CK(cudaStreamSynchronize(st), "check sync");
         for (int r = 0; r < r_hi; ++r) {
           if (eq[r] != 0) continue;
           bool ok = false;
           if (check) {
             for (int t = 0; t < n_fit; ++t)
-              y[t] = energy_from_fx(c, c->sum_SB_fx + fx[static_cast<size_t>(r) * max_sweeps + (s - n_fit + t)]);
+              y[t] = energy_from_fx(c, c->sum_SB_fx + fx[static_cast<size_t>(r) * n_fit + t]);
             ok = equilibrium_reached(y.data(), n_fit, slope_tol);
           }
           if (ok || forced) {
@@ -829,7 +844,7 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
             --pending;
           }
         }
-        CK(cudaMemcpyAsync(c->win.p, win.data(), sizeof(int) * 2 * Rb, cudaMemcpyHostToDevice, st), "H2D windows");
+        CK(cudaMemcpyAsync(c->win.p, win, sizeof(int) * 2 * Rb, cudaMemcpyHostToDevice, st), "H2D windows");
       }
     }
     launch_acc_reduce(c->A.as<float>(), 0, c->P, Rb, 0, r_hi, c->acc.as<double>(), st);
