@@ -623,3 +623,28 @@ def test_concurrent_contexts_on_separate_streams(P, calib):
     assert not errs, errs
     for i in range(2):
         assert_bitwise(out[i], ref[i], f"context {i} under concurrency")
+
+
+@pytest.mark.slow
+def test_block_mean_init_equilibrates_faster_than_random(P, calib):
+    """Row f1 energy-trace product (fig:Equi_energies): averaged over the
+    realizations, the whole-grid energy of MPR with RANDOM init starts far above its plateau
+    and needs many sweeps, while BLOCK_MEAN init (BST/SST) starts near the plateau."""
+    from inputs.synth import heterogeneous_field, random_mask
+    L = 256
+    truth = heterogeneous_field(L, nu=0.5, corr_len=2.0, spread=1.0)
+    mask = random_mask(L, L, 0.3)
+    z = np.where(mask != 0, truth, np.float32(np.nan)).astype(np.float32)
+    res = {}
+    for name, cfg in (("MPR", P.Config(l_b=L, n_s=0, init="random")), ("BST", P.Config(l_b=32, n_s=0))):
+        m = P.LeMpr(cfg, calib)
+        m.set_data(z, mask)
+        m.set_energy_trace(True)
+        m.estimate_local_params()
+        m.simulate(20, 50, 7)
+        curve = m.debug(P.binding.MPR_BUF_ENERGY).mean(axis=0)
+        m.close()
+        e_eq = curve[-10:].mean()
+        res[name] = (curve[0] - e_eq, int(np.argmax(np.abs(curve - e_eq) <= 1e-3 * abs(e_eq)) + 1))
+    assert res["MPR"][0] > 10 * res["BST"][0] > 0
+    assert res["MPR"][1] >= 10 and res["BST"][1] < res["MPR"][1]
