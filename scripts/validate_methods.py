@@ -6,6 +6,7 @@ filled on the GPU; AAE and RASE (Eq.(3)) are averaged over the thinnings (MAAE, 
 reported with the paired error ratios err_SV-MPR / err_MPR of fig:err-p.
 
   python scripts/validate_methods.py [--L 256] [--K 20] [--M 20] [--ps 0.3,0.5,0.7,0.85]
+  python scripts/validate_methods.py --sweep lb|ns --L 512 --K 10   (SST vs l_b / n_s at p = 0.7)
 """
 from __future__ import annotations
 
@@ -62,6 +63,47 @@ def run(L=256, K=20, M=20, S=30, ps=(0.3, 0.5, 0.7, 0.85), skew=True, seed_field
     return rows
 
 
+def run_param_sweep(param, values, L=512, K=10, M=20, S=30, p=0.7, skew=True, seed_field=2212):
+    """SV-MPR SST error ratios to MPR versus one parameter: the block side l_b (BST and SST)
+    or the number of smoothing passes n_s (SST; n_s = 0 is BST). Same fields and thinnings
+    as run(); one JSON line per value."""
+    import paper_2212_01317_b200 as P
+    from inputs.synth import heterogeneous_field, random_mask
+    truth = heterogeneous_field(L, corr_len=max(L / 32, 4.0), skew=skew, seed=seed_field)
+    calib = P.load_calibration()
+    mpr = P.LeMpr(P.Config(l_b=max(L, 2), n_s=0), calib)
+    masks = [random_mask(L, L, p, seed=1000 + k) for k in range(K)]
+    base = []
+    for k, mask in enumerate(masks):
+        z = np.where(mask != 0, truth, np.nan).astype(np.float32)
+        mpr.set_data(z, mask)
+        mpr.estimate_local_params()
+        mpr.simulate(M, S, 20221202 + k)
+        base.append(errors(mpr.predict(), truth, mask))
+    mpr.close()
+    base = np.array(base)
+    rows = []
+    for v in values:
+        cfg = P.Config(l_b=v, n_s=5, r_s=2) if param == "lb" else P.Config(l_b=32, n_s=v, r_s=2)
+        eng = P.LeMpr(cfg, calib)
+        errs = []
+        for k, mask in enumerate(masks):
+            z = np.where(mask != 0, truth, np.nan).astype(np.float32)
+            eng.set_data(z, mask)
+            eng.estimate_local_params()
+            eng.simulate(M, S, 20221202 + k)
+            errs.append(errors(eng.predict(), truth, mask))
+        eng.close()
+        ra = np.array(errs) / base
+        rec = {"sweep": param, param: v, "L": L, "p": p, "K": K, "M": M, "S": S,
+               "MAAE_MPR": float(base[:, 0].mean()), "MRASE_MPR": float(base[:, 1].mean()),
+               "MAAE": float(np.array(errs)[:, 0].mean()), "MRASE": float(np.array(errs)[:, 1].mean()),
+               "ratio_AAE": float(ra[:, 0].mean()), "ratio_RASE": float(ra[:, 1].mean())}
+        rows.append(rec)
+        print(json.dumps(rec), flush=True)
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--L", type=int, default=256)
@@ -70,8 +112,16 @@ def main():
     ap.add_argument("--S", type=int, default=30)
     ap.add_argument("--ps", default="0.3,0.5,0.7,0.85")
     ap.add_argument("--no-skew", action="store_true")
+    ap.add_argument("--sweep", default="p", choices=["p", "lb", "ns"],
+                    help="p: MPR/BST/SST vs missing ratio; lb: SST vs block side; ns: vs smoothing passes")
+    ap.add_argument("--values", default=None, help="comma list for --sweep lb / ns")
     a = ap.parse_args()
-    run(a.L, a.K, a.M, a.S, tuple(float(x) for x in a.ps.split(",")), skew=not a.no_skew)
+    if a.sweep == "p":
+        run(a.L, a.K, a.M, a.S, tuple(float(x) for x in a.ps.split(",")), skew=not a.no_skew)
+    else:
+        vals = a.values or ("8,16,32,64,128" if a.sweep == "lb" else "0,1,2,5,10")
+        run_param_sweep(a.sweep, [int(x) for x in vals.split(",")], L=a.L, K=a.K, M=a.M, S=a.S,
+                        skew=not a.no_skew)
 
 
 if __name__ == "__main__":
