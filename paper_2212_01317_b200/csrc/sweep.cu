@@ -271,8 +271,9 @@ __device__ __forceinline__ Split split_work(int npairs) {
   return s;
 }
 
-// Direct-load variant: record, own state and neighbour states loaded from global memory
-// at the start of each item (PF: register-free prefetch of the next item).
+// One realization pair per thread. PF = 2: record, own and neighbour states loaded at the
+// start of each item, with a register-free L2 prefetch of the next item; PF = 3: the next
+// item's record is loaded one item ahead (below).
 template <bool QHALF, bool ENERGY, int MINB, int PF, int NT, bool BFEXP, bool LIST, bool PK>
 __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   pdl_wait();
@@ -335,16 +336,11 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
       const GapRec rec = a.rec[gg];
       const uint32_t self_off = gg * R + j2;
       const float2 cur = *reinterpret_cast<const float2*>(a.G + self_off);
-      if (PF && !LIST) {
+      if (PF == 2 && !LIST) {  // register-free L2 prefetch of the next item's record and state
         const uint32_t gn = gg + sp.gstride;
         if (gn < gbegin + gcount) {
-          if (PF == 1) {
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.rec + gn));
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.G + (gn * R + j2)));
-          } else {
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rec + gn));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.G + (gn * R + j2)));
-          }
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.rec + gn));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.G + (gn * R + j2)));
         }
       }
       float2 nb[4];
@@ -364,12 +360,13 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   pdl_trigger();
 }
 
-// NP realization pairs (2 NP realizations) of one gap site per thread (NP = 2; NP = 4 was
-// measured no faster: profiles/r01_summary.md): the
-// record, the flag decoding, the neighbour addresses and the loop overhead are shared by
-// the NP pairs, and the own / neighbour states move as float4 (two pairs each). Each pair
-// still draws its own Philox call and runs metropolis_pair, so the results are those of
-// k_sweep_half bit for bit. Requires npairs % NP == 0 (launch_sweep_half falls back).
+// NP realization pairs (2 NP realizations) of one gap site per thread (NP = 2 is built;
+// NP = 4 measured no faster, profiles/r01_summary.md). The record, the flag decoding, the
+// neighbour addresses and the loop overhead are shared by the NP pairs, and the own /
+// neighbour states move as float4 (two pairs each). Each pair still draws its own Philox
+// call and runs metropolis_pair, so the results are those of k_sweep_half bit for bit.
+// Requires npairs % NP == 0 (launch_sweep_half falls back). EARLY: every pair's Philox
+// words are drawn right after the record arrives; PEER: fused halo stores (row slabs).
 template <bool QHALF, bool ENERGY, int MINB, bool LIST, int NP = 2, bool EARLY = false, bool PEER = false>
 __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
   pdl_wait();
