@@ -13,7 +13,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmpr.so")
+# MPR_LIB: load another build of the library (A/B timing of kernel changes)
+LIB_PATH = os.environ.get("MPR_LIB", os.path.join(_PKG, "libmpr.so"))
 
 MPR_OK, MPR_ERR_INVALID_ARG, MPR_ERR_STATE, MPR_ERR_TOO_FEW_SAMPLES, MPR_ERR_NO_SAMPLE_BONDS, \
     MPR_ERR_CUDA, MPR_ERR_OOM = range(7)

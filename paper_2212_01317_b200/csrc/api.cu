@@ -93,6 +93,7 @@ struct mpr_ctx {
   int64_t sweep_launches = 0;
   double sweep_ms = 0.0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_check = nullptr;  // adaptive protocol: status copy of the last device check
   // CUDA graphs of the per-batch launch sequence (replayed when the key repeats)
   int use_graphs = 1;
   std::vector<GraphEntry> graphs = std::vector<GraphEntry>(8);
@@ -223,29 +224,6 @@ double energy_from_fx(const mpr_ctx* c, long long E_fx) {
   return (-static_cast<double>(E_fx) * 0x1p-32) / nb;
 }
 
-// ARITH §K slope test on y[0 .. n_fit-1], every operation in the written order.
-bool equilibrium_reached(const double* y, int n_fit, double slope_tol) {
-  const double xbar = static_cast<double>(n_fit - 1) / 2.0;
-  double sy = 0.0;
-  for (int t = 0; t < n_fit; ++t) sy = sy + y[t];
-  const double ybar = sy / static_cast<double>(n_fit);
-  double sxx = 0.0, sxy = 0.0;
-  for (int t = 0; t < n_fit; ++t) {
-    const double dx = static_cast<double>(t) - xbar;
-    sxx = sxx + dx * dx;
-    sxy = sxy + dx * (y[t] - ybar);
-  }
-  const double b = sxy / sxx;
-  const double a = ybar - b * xbar;
-  double sse = 0.0;
-  for (int t = 0; t < n_fit; ++t) {
-    const double res = y[t] - a - b * static_cast<double>(t);
-    sse = sse + res * res;
-  }
-  double tau = 2.0 * std::sqrt(sse / static_cast<double>(n_fit - 2)) / static_cast<double>(n_fit);
-  if (slope_tol > tau) tau = slope_tol;  // tau = max(2 sigma / n_fit, slope_tol)
-  return b >= -tau;
-}
 
 mpr_status stage_data(mpr_ctx* c) {
   cudaStream_t st = c->stream;
@@ -418,6 +396,7 @@ void mpr_destroy(mpr_ctx* c) {
     if (e.exec) cudaGraphExecDestroy(e.exec);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->ev_check) cudaEventDestroy(c->ev_check);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -753,18 +732,23 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
   CK(c->A.ensure(sizeof(float) * c->P * R), "alloc accumulator state");
   CK(c->energy.ensure(sizeof(long long) * R * max_sweeps), "alloc energy");
   CK(c->win.ensure(sizeof(int) * 2 * R), "alloc windows");
-  // pinned host staging: at a check only the last n_fit energies of every realization
-  // come back (one strided 2-D copy), and the windows go down from pinned memory
-  long long* fx = nullptr;
-  int* win = nullptr;
-  CK(cudaMallocHost(reinterpret_cast<void**>(&fx), sizeof(long long) * R * n_fit), "pinned energies");
+  // Decisions are taken on the device (k_adaptive_check, ARITH §K bit for bit), so the host
+  // never stalls the GPU for a check: it reads the device status (undecided count, last
+  // window end) one check late from pinned memory, while the next n_f sweeps are already
+  // queued. Sweeps issued after every realization finished are no-ops (frozen pairs).
+  CK(c->tmp.ensure(sizeof(int) * (R + 2)), "alloc decisions");
+  int* eq_d = c->tmp.as<int>();
+  int* status_d = eq_d + R;
+  int* hbuf = nullptr;  // pinned: [0, 2*R) windows; [2R, 2R+2) status; [2R+2, 3R+2) decisions
+  CK(cudaMallocHost(reinterpret_cast<void**>(&hbuf), sizeof(int) * (3 * R + 2)), "pinned staging");
   struct PinnedFree {
     void* p;
     ~PinnedFree() { if (p) cudaFreeHost(p); }
-  } fx_free{fx};
-  CK(cudaMallocHost(reinterpret_cast<void**>(&win), sizeof(int) * 2 * R), "pinned windows");
-  PinnedFree win_free{win};
-  std::vector<double> y(static_cast<size_t>(n_fit));
+  } hbuf_free{hbuf};
+  int* win = hbuf;
+  volatile int* status_h = hbuf + 2 * R;
+  int* eq_h = hbuf + 2 * R + 2;
+  if (!c->ev_check) CK(cudaEventCreateWithFlags(&c->ev_check, cudaEventDisableTiming), "event");
   for (int64_t mb = 0; mb < M; mb += R) {
     const int64_t span = std::min<int64_t>(R, M - mb);
     const int Rb = static_cast<int>(span + (span & 1));
@@ -775,9 +759,14 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
       win[r] = r < r_hi ? INT32_MAX : 0;
       win[Rb + r] = r < r_hi ? INT32_MAX : 0;
     }
-    std::vector<int> eq(static_cast<size_t>(Rb), 0);
+    status_h[0] = r_hi;
+    status_h[1] = 0;
     CK(cudaMemcpyAsync(c->win.p, win, sizeof(int) * 2 * Rb, cudaMemcpyHostToDevice, st), "H2D windows");
+    CK(cudaMemcpyAsync(status_d, const_cast<int*>(status_h), sizeof(int) * 2, cudaMemcpyHostToDevice, st),
+       "H2D status");
+    CK(cudaMemsetAsync(eq_d, 0, sizeof(int) * Rb, st), "zero decisions");
     CK(cudaMemsetAsync(c->energy.p, 0, sizeof(long long) * Rb * max_sweeps, st), "zero energy");
+    CK(cudaStreamSynchronize(st), "adaptive batch start");  // the pinned windows are reused below
     launch_init_states(c->rec.as<GapRec>(), c->G.as<float>(), c->A.as<float>(), c->P, Rb, Rb / 2,
                        static_cast<uint32_t>(mb / 2), c->cfg.init == MPR_INIT_RANDOM, k0, k1, st);
     CKL("init_states");
@@ -799,12 +788,22 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
     a.energy_stride = max_sweeps;
     a.r_valid_lo = 0;
     a.r_valid_hi = r_hi;
-    int pending = r_hi;
-    for (int32_t s = 1; s <= max_sweeps; ++s) {
-      // stop once every realization has passed the end of its averaging window
-      int stop_all = 0;
-      for (int r = 0; r < r_hi; ++r) stop_all = std::max(stop_all, win[Rb + r] == INT32_MAX ? max_sweeps : win[Rb + r]);
-      if (pending == 0 && s > stop_all) break;
+    AdaptiveCheckArgs ca{};
+    ca.energy = c->energy.as<long long>();
+    ca.energy_stride = max_sweeps;
+    ca.sum_known_fx = c->sum_SB_fx;
+    ca.n_bonds = static_cast<double>(2 * c->Lx * c->Ly - c->Lx - c->Ly);
+    ca.n_fit = n_fit;
+    ca.n_avg = n_avg;
+    ca.r_hi = r_hi;
+    ca.slope_tol = slope_tol;
+    ca.win_lo = c->win.as<int>();
+    ca.win_hi = c->win.as<int>() + Rb;
+    ca.eq = eq_d;
+    ca.status = status_d;
+    bool status_pending = false;  // a status copy is in flight behind ev_check
+    int stop_all = INT32_MAX;     // known once the device reports no undecided realization
+    for (int32_t s = 1; s <= max_sweeps && s <= stop_all; ++s) {
       a.sweep = static_cast<uint32_t>(s);
       a.energy = c->energy.as<long long>() + (s - 1);
       for (int colour = 0; colour < 2; ++colour) {
@@ -819,40 +818,37 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
       }
       const bool check = s >= n_fit + n_f && (s - n_fit) % n_f == 0 && s + n_avg <= max_sweeps;
       const bool forced = s == max_sweeps - n_avg;
-      if (pending > 0 && (check || forced)) {
-        // energies of sweeps s-n_fit+1 .. s of every realization: rows of n_fit values at
-        // pitch max_sweeps (the forced decision needs none)
-        if (check) {
-          CK(cudaMemcpy2DAsync(fx, sizeof(long long) * n_fit,
-                               c->energy.as<long long>() + (s - n_fit), sizeof(long long) * max_sweeps,
-                               sizeof(long long) * n_fit, Rb, cudaMemcpyDeviceToHost, st),
-             "D2H energy window");
+      if (check || forced) {
+        // the previous check's status: its copy was issued n_f sweeps ago, so waiting for it
+        // leaves n_f sweeps of queued work on the GPU (no bubble) and bounds how far the
+        // host runs ahead of the decisions (at most n_f no-op sweeps after the last one)
+        if (status_pending) {
+          CK(cudaEventSynchronize(c->ev_check), "status wait");
+          status_pending = false;
+          if (status_h[0] == 0) stop_all = status_h[1];
         }
-        CK(cudaStreamSynchronize(st), "check sync");
-        for (int r = 0; r < r_hi; ++r) {
-          if (eq[r] != 0) continue;
-          bool ok = false;
-          if (check) {
-            for (int t = 0; t < n_fit; ++t)
-              y[t] = energy_from_fx(c, c->sum_SB_fx + fx[static_cast<size_t>(r) * n_fit + t]);
-            ok = equilibrium_reached(y.data(), n_fit, slope_tol);
-          }
-          if (ok || forced) {
-            eq[r] = ok ? s : -s;
-            win[r] = s;
-            win[Rb + r] = s + n_avg;
-            --pending;
-          }
+        if (stop_all != INT32_MAX) continue;
+        ca.s = s;
+        ca.check = check;
+        ca.forced = forced;
+        launch_adaptive_check(ca, st);
+        CKL("adaptive_check");
+        ++c->launches;
+        if (!status_pending) {
+          CK(cudaMemcpyAsync(const_cast<int*>(status_h), status_d, sizeof(int) * 2, cudaMemcpyDeviceToHost, st),
+             "D2H status");
+          CK(cudaEventRecord(c->ev_check, st), "event record");
+          status_pending = true;
         }
-        CK(cudaMemcpyAsync(c->win.p, win, sizeof(int) * 2 * Rb, cudaMemcpyHostToDevice, st), "H2D windows");
       }
     }
+    CK(cudaMemcpyAsync(eq_h, eq_d, sizeof(int) * Rb, cudaMemcpyDeviceToHost, st), "D2H decisions");
     launch_acc_reduce(c->A.as<float>(), 0, c->P, Rb, 0, r_hi, c->acc.as<double>(), st);
     CKL("acc_reduce");
     ++c->launches;
     CK(cudaStreamSynchronize(st), "adaptive sync");
     if (s_eq_out)
-      for (int r = 0; r < r_hi; ++r) s_eq_out[mb + r] = eq[static_cast<size_t>(r)];
+      for (int r = 0; r < r_hi; ++r) s_eq_out[mb + r] = eq_h[r];
     c->last_m_base = mb;
     c->last_R = Rb;
   }

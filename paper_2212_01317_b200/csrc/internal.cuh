@@ -116,6 +116,24 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
 void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,
                         uint32_t pair_base, int random_init, uint32_t k0, uint32_t k1,
                         cudaStream_t st);
+// Adaptive protocol (row f1, ARITH §K) decided on the device: after sweep s, every
+// undecided realization r < r_hi runs the slope test on its energies of sweeps
+// s-n_fit+1 .. s (check) or is forced (forced), exactly as the host test would. A decided
+// realization gets eq[r] = +-s and the averaging window (s, s + n_avg] in win_lo/win_hi;
+// status[0] counts the undecided realizations, status[1] is the largest window end.
+struct AdaptiveCheckArgs {
+  const long long* energy;  // [R][energy_stride] fixed-point bond sums (ARITH §J)
+  int64_t energy_stride;
+  long long sum_known_fx;   // fixed-point sum of the known-known bonds
+  double n_bonds;           // N_bonds of ARITH §J
+  int s, n_fit, n_avg, check, forced, r_hi;
+  double slope_tol;
+  int* win_lo;
+  int* win_hi;
+  int* eq;
+  int* status;
+};
+void launch_adaptive_check(const AdaptiveCheckArgs& a, cudaStream_t st);
 void launch_acc_reduce(const float* X, int64_t g_begin, int64_t g_count, int R, int r_lo, int r_hi,
                        double* acc, cudaStream_t st);
 

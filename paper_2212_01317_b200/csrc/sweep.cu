@@ -27,7 +27,6 @@ namespace mpr {
 
 namespace {
 
-constexpr int kMaxPairs = 512;  // batch <= 1024 realizations
 
 // Programmatic dependent launch (the batch's kernels are launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization, see launch_pdl): a kernel may be
@@ -236,18 +235,35 @@ __device__ __forceinline__ void accum_flags(const SweepArgs& a, int j, bool& f0,
 }
 
 // a8: per-realization fixed-point bond sums of this CTA -> global int64 atomics, one per
-// realization (exact, so the result does not depend on the order: ARITH §J).
-__device__ __forceinline__ void energy_epilogue(const SweepArgs& a, int npairs, bool active, int j, long long e0,
-                                                long long e1) {
-  __shared__ unsigned long long es[2 * kMaxPairs];
-  for (int t = threadIdx.x; t < 2 * npairs; t += blockDim.x) es[t] = 0ull;
+// realization and CTA (exact, so the result does not depend on the order: ARITH §J).
+// Thread tid holds the K values of realizations K*u .. K*u+K-1, u = tid % nunits (`unit`),
+// added into one shared slot per realization. When nunits divides 32 (a batch of 2, 4,
+// ..., 32 / K realizations), up to 256 threads would hit each slot, so the lanes of a
+// warp that share a unit (lanes equal mod nunits) are first reduced with shuffles and only
+// lanes < nunits issue the shared atomics. Needs blockDim.x == 256 and every thread.
+constexpr int kMaxRealizations = 1024;
+template <int K>
+__device__ __forceinline__ void energy_epilogue_k(const SweepArgs& a, int nunits, int unit, bool active,
+                                                  long long (&v)[K]) {
+  __shared__ unsigned long long es[kMaxRealizations];
+  for (int t = threadIdx.x; t < K * nunits; t += blockDim.x) es[t] = 0ull;
   __syncthreads();
-  if (active && (e0 != 0 || e1 != 0)) {
-    atomicAdd(&es[2 * j], static_cast<unsigned long long>(e0));
-    atomicAdd(&es[2 * j + 1], static_cast<unsigned long long>(e1));
+  if (!active)
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = 0;
+  bool issue = active;
+  if (nunits <= 16 && (32 % nunits) == 0) {  // lane l has unit (l + const) % nunits: warp-periodic
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      for (int off = 16; off >= nunits; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+    issue = (threadIdx.x & 31) < nunits;
   }
+  if (issue)
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (v[k] != 0) atomicAdd(&es[unit * K + k], static_cast<unsigned long long>(v[k]));
   __syncthreads();
-  for (int t = threadIdx.x; t < 2 * npairs; t += blockDim.x)
+  for (int t = threadIdx.x; t < K * nunits; t += blockDim.x)
     if (t >= a.r_valid_lo && t < a.r_valid_hi && es[t] != 0ull)
       atomicAdd(reinterpret_cast<unsigned long long*>(a.energy + static_cast<int64_t>(t) * a.energy_stride), es[t]);
 }
@@ -356,7 +372,10 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
       process_item<QHALF, ENERGY, BFEXP, PK>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
     }
   }
-  if (ENERGY) energy_epilogue(a, a.npairs, sp.active && live, sp.j, e0, e1);
+  if (ENERGY) {
+    long long v[2] = {e0, e1};
+    energy_epilogue_k<2>(a, a.npairs, sp.j, sp.active && live, v);
+  }
   pdl_trigger();
 }
 
@@ -469,21 +488,14 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
       gg = ggn;
     }
   }
-  if (ENERGY) {  // a8 epilogue for realizations 2 NP jq .. 2 NP jq + 2 NP - 1 (as energy_epilogue)
-    __shared__ unsigned long long es[2 * kMaxPairs];
-    for (int t = threadIdx.x; t < 2 * a.npairs; t += blockDim.x) es[t] = 0ull;
-    __syncthreads();
-    if (active) {
+  if (ENERGY) {  // a8 epilogue for realizations 2 NP jq .. 2 NP jq + 2 NP - 1
+    long long v[2 * NP];
 #pragma unroll
-      for (int p = 0; p < NP; ++p)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (e[p][h] != 0) atomicAdd(&es[2 * (NP * jq + p) + h], static_cast<unsigned long long>(e[p][h]));
+    for (int p = 0; p < NP; ++p) {
+      v[2 * p] = e[p][0];
+      v[2 * p + 1] = e[p][1];
     }
-    __syncthreads();
-    for (int t = threadIdx.x; t < 2 * a.npairs; t += blockDim.x)
-      if (t >= a.r_valid_lo && t < a.r_valid_hi && es[t] != 0ull)
-        atomicAdd(reinterpret_cast<unsigned long long*>(a.energy + static_cast<int64_t>(t) * a.energy_stride), es[t]);
+    energy_epilogue_k<2 * NP>(a, nq, jq, active, v);
   }
   pdl_trigger();
 }
@@ -547,7 +559,59 @@ __global__ void __launch_bounds__(kAccTile) k_acc_reduce(const float* __restrict
   pdl_trigger();
 }
 
+// Row f1 check on the device: the host's ARITH §K test (api.cu equilibrium_reached), every
+// fp64 operation an explicit round-to-nearest intrinsic in the same order, so the
+// decisions are the host's (and the oracle's) bit for bit.
+__device__ double energy_from_fx_dev(long long E_fx, double n_bonds) {
+  return __ddiv_rn(__dmul_rn(-__ll2double_rn(E_fx), 0x1p-32), n_bonds);
+}
+
+__global__ void k_adaptive_check(const AdaptiveCheckArgs a) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.r_hi || a.eq[r] != 0) return;
+  bool ok = false;
+  if (a.check) {
+    const long long* e = a.energy + static_cast<int64_t>(r) * a.energy_stride + (a.s - a.n_fit);
+    const int n = a.n_fit;
+    const double xbar = __ddiv_rn(static_cast<double>(n - 1), 2.0);
+    double sy = 0.0;
+    for (int t = 0; t < n; ++t) sy = __dadd_rn(sy, energy_from_fx_dev(a.sum_known_fx + e[t], a.n_bonds));
+    const double ybar = __ddiv_rn(sy, static_cast<double>(n));
+    double sxx = 0.0, sxy = 0.0;
+    for (int t = 0; t < n; ++t) {
+      const double y = energy_from_fx_dev(a.sum_known_fx + e[t], a.n_bonds);
+      const double dx = __dsub_rn(static_cast<double>(t), xbar);
+      sxx = __dadd_rn(sxx, __dmul_rn(dx, dx));
+      sxy = __dadd_rn(sxy, __dmul_rn(dx, __dsub_rn(y, ybar)));
+    }
+    const double b = __ddiv_rn(sxy, sxx);
+    const double ai = __dsub_rn(ybar, __dmul_rn(b, xbar));
+    double sse = 0.0;
+    for (int t = 0; t < n; ++t) {
+      const double y = energy_from_fx_dev(a.sum_known_fx + e[t], a.n_bonds);
+      const double res = __dsub_rn(__dsub_rn(y, ai), __dmul_rn(b, static_cast<double>(t)));
+      sse = __dadd_rn(sse, __dmul_rn(res, res));
+    }
+    double tau = __ddiv_rn(__dmul_rn(2.0, __dsqrt_rn(__ddiv_rn(sse, static_cast<double>(n - 2)))),
+                           static_cast<double>(n));
+    if (a.slope_tol > tau) tau = a.slope_tol;
+    ok = b >= -tau;
+  }
+  if (ok || a.forced) {
+    a.eq[r] = ok ? a.s : -a.s;
+    a.win_lo[r] = a.s;
+    a.win_hi[r] = a.s + a.n_avg;
+    atomicSub(&a.status[0], 1);
+    atomicMax(&a.status[1], a.s + a.n_avg);
+  }
+}
+
 }  // namespace
+
+void launch_adaptive_check(const AdaptiveCheckArgs& a, cudaStream_t st) {
+  const int nt = 128;
+  k_adaptive_check<<<(a.r_hi + nt - 1) / nt, nt, 0, st>>>(a);
+}
 
 // Kernel variants (tuning knob, MPR_SWEEP_VARIANT). profiles/r01_summary.md records every
 // alternative measured, including the ones no longer built: 32-bit byte offsets, register
