@@ -104,7 +104,7 @@ float oracle_bond_energy(float phi_i, float phi_j, float q, float J)
 
 /* ---------------------------------------------------------------- ARITH §D */
 /* Linear map of the data to spin angles in [0, 2pi]. Returns 1 when the
- * sample range is degenerate (z_max == z_min), 0 otherwise, -1 if no samples.
+ * sample range is degenerate (z_max == z_min), 0 otherwise, -1 with fewer than 2 samples.
  * phi is written at known sites only (gaps set to 0). */
 int oracle_transform(const float *z, const uint8_t *mask, int64_t n,
                      float *zmin_out, float *zmax_out, float *phi)
@@ -120,7 +120,7 @@ int oracle_transform(const float *z, const uint8_t *mask, int64_t n,
     zmin = zmin + 0.0f;   /* ARITH §D: -0 becomes +0 */
     zmax = zmax + 0.0f;
     *zmin_out = zmin; *zmax_out = zmax;
-    if (N == 0) return -1;
+    if (N < 2) return -1;   /* fewer than 2 samples: rejected */
     int degenerate = (zmax == zmin);
     float range = zmax - zmin;
     float s = degenerate ? 0.0f : TWO_PI_F / range;

@@ -537,7 +537,10 @@ def _fuzz_case(k):
     return truth, z, mask, cfg_kw, M, S, int(rng.integers(1 << 40)), order == "sc"
 
 
-@pytest.mark.parametrize("k", range(150))
+FUZZ_CASES = int(__import__("os").environ.get("MPR_FUZZ_CASES", "150"))
+
+
+@pytest.mark.parametrize("k", range(FUZZ_CASES))
 def test_fuzz_small_problems_bit_exact(P, calib, k):
     """Randomised small problems (2..40 sites per side, any missing ratio, random or cloud
     gaps) under random configurations (l_b, r_s, n_s, q, J, init, SC/DC order, batch

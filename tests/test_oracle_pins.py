@@ -92,6 +92,20 @@ def test_transform_degenerate_and_roundtrip():
     assert np.max(np.abs(back - z)) <= 4 * np.spacing(np.float32(hi - lo))
 
 
+def test_too_few_samples_rejected(calib):
+    """SPEC S:31 / SURVEY 8(b): fewer than 2 known sites is an error (status < 0), not a
+    degenerate range; exactly 2 equal samples is the degenerate (accepted) case."""
+    z = np.full((3, 4), 1.5, np.float32)
+    for known in (0, 1):
+        mask = np.zeros((3, 4), np.uint8)
+        mask.flat[:known] = 1
+        assert O.to_angles(z, mask)[3] < 0
+        assert O.parameters(z, mask, O.OracleConfig(lb=2), *calib).status < 0
+    mask = np.zeros((3, 4), np.uint8)
+    mask.flat[:2] = 1
+    assert O.to_angles(z, mask)[3] == 1
+
+
 def test_transform_negative_zero_canonical():
     """ARITH §D: a -0 extremum is returned as +0."""
     z = np.array([[-0.0, 1.0]], np.float32)
