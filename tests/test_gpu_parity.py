@@ -651,3 +651,39 @@ def test_block_mean_init_equilibrates_faster_than_random(P, calib):
         res[name] = (curve[0] - e_eq, int(np.argmax(np.abs(curve - e_eq) <= 1e-3 * abs(e_eq)) + 1))
     assert res["MPR"][0] > 10 * res["BST"][0] > 0
     assert res["MPR"][1] >= 10 and res["BST"][1] < res["MPR"][1]
+
+
+@pytest.mark.parametrize("k", range(int(__import__("os").environ.get("MPR_FUZZ_ADAPTIVE_CASES", "24"))))
+def test_fuzz_adaptive_protocol_matches_oracle(P, calib, k):
+    """Row f1 randomised: small problems under random n_fit, n_f, caps, slope tolerances,
+    n_avg, init and M. The per-realization equilibrium sweeps (decided on the device)
+    equal the oracle's, and so do the predictions (bit-exact for n_avg = 1)."""
+    rng = np.random.default_rng(7000 + k)
+    Ly, Lx = int(rng.integers(6, 40)), int(rng.integers(6, 40))
+    truth, z, mask = make_problem(Ly, float(rng.uniform(0.2, 0.8)), Lx=Lx, corr_len=float(rng.uniform(2, 10)),
+                                  seed_field=int(rng.integers(1 << 30)), seed_mask=int(rng.integers(1 << 30)))
+    n_avg = int(rng.integers(1, 4))
+    cfg = P.Config(l_b=int(rng.integers(4, 33)), n_s=int(rng.integers(0, 3)), r_s=1, n_avg=n_avg,
+                   init="random" if rng.random() < 0.5 else "block_mean")
+    n_fit, n_f = int(rng.integers(4, 25)), int(rng.integers(1, 8))
+    S_max = int(rng.integers(n_avg + 2, 90))
+    tol = float(rng.choice([0.0, 1e-6, 1e-5, 1e-4]))
+    M, seed = int(rng.integers(1, 9)), int(rng.integers(1 << 40))
+    Tk, ek = calib
+    oc = ocfg(cfg)
+    p = O.parameters(z, mask, oc, Tk, ek)
+    if p.status < 0:
+        pytest.skip("problem rejected by the oracle (covered by the fixed-S fuzz)")
+    m = P.LeMpr(cfg, calib)
+    m.set_data(z, mask)
+    m.estimate_local_params()
+    s_eq = m.simulate_adaptive(M, seed, n_fit=n_fit, n_f=n_f, max_sweeps=S_max, slope_tol=tol)
+    pred = m.predict()
+    m.close()
+    r = O.simulate_adaptive(p, mask, oc, M, seed, n_fit=n_fit, n_f=n_f, S_max=S_max, slope_tol=tol)
+    assert s_eq.tolist() == r["s_eq"].tolist()
+    ref = O.predict(np.nan_to_num(z), mask, r["acc"], M, n_avg, p.zmin, p.zmax, 0)
+    if n_avg == 1:
+        assert_bitwise(pred, ref, "adaptive predictions")
+    else:
+        assert np.max(np.abs(pred - ref)) <= 1e-3 * (p.zmax - p.zmin)
