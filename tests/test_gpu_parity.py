@@ -687,3 +687,30 @@ def test_fuzz_adaptive_protocol_matches_oracle(P, calib, k):
         assert_bitwise(pred, ref, "adaptive predictions")
     else:
         assert np.max(np.abs(pred - ref)) <= 1e-3 * (p.zmax - p.zmin)
+
+
+@pytest.mark.parametrize("k", range(int(__import__("os").environ.get("MPR_FUZZ_SLAB_CASES", "12"))))
+def test_fuzz_row_slabs_match_single_context(P, calib, k):
+    """Row slabs randomised: random grids, world sizes 2..5 (contexts on one GPU), halo by
+    row copies or by the kernels writing into the neighbours' buffers, n_avg, M (chunks of
+    4k + remainder): predictions equal the single-context run bit for bit (n_avg = 1) or
+    within the n_avg tolerance."""
+    rng = np.random.default_rng(8000 + k)
+    Ly, Lx = int(rng.integers(12, 70)), int(rng.integers(6, 60))
+    truth, z, mask = make_problem(Ly, float(rng.uniform(0.2, 0.8)), Lx=Lx, corr_len=float(rng.uniform(2, 10)),
+                                  seed_field=int(rng.integers(1 << 30)), seed_mask=int(rng.integers(1 << 30)))
+    n_avg = int(rng.integers(1, 3))
+    cfg = P.Config(l_b=int(rng.integers(4, 24)), n_s=int(rng.integers(0, 3)), r_s=1, n_avg=n_avg,
+                   init="random" if rng.random() < 0.5 else "block_mean")
+    M, S = int(rng.integers(1, 11)), int(rng.integers(n_avg, 9))
+    world = int(rng.integers(2, min(5, Ly // 2) + 1))
+    halo = "peer" if rng.random() < 0.5 else "copy"
+    Tk, ek = calib
+    if O.parameters(z, mask, ocfg(cfg), Tk, ek).status < 0:
+        pytest.skip("problem rejected by the oracle (covered by the fixed-S fuzz)")
+    ref = gpu_run(P, z, mask, cfg, calib, M, S, 99 + k)["pred"]
+    got = _emulated_slabs(P, z, mask, cfg, calib, M, S, 99 + k, world, halo=halo)
+    if n_avg == 1:
+        assert_bitwise(got, ref, f"row slabs x{world} ({halo})")
+    else:
+        assert np.max(np.abs(got - ref)) <= 1e-5 * (np.nanmax(z) - np.nanmin(z))
