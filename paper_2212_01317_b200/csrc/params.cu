@@ -273,13 +273,16 @@ __global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ p
   for (int t = threadIdx.x; t < nslots; t += blockDim.x) { sSB[t] = 0; sNB[t] = 0; sSP[t] = 0; sNK[t] = 0; }
   __syncthreads();
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  // block column of this thread's site column: one 32-bit division per thread (Lx, Ly < 2^31)
+  const int cbl = static_cast<int>(static_cast<uint32_t>(c0 + tx) / static_cast<uint32_t>(lb) - bc0);
   for (int k = 0; k < kTile / 8; ++k) {
     const int64_t r = r0 + ty + 8 * k, c = c0 + tx;
     long long vsb = 0, vnb = 0, vsp = 0, vnk = 0;
     int slot = 0;
     const bool in = r < Ly && c < Lx;
     if (in) {
-      slot = static_cast<int>((r / lb - br0) * nbc + (c / lb - bc0));
+      const int rbl = static_cast<int>(static_cast<uint32_t>(r) / static_cast<uint32_t>(lb) - br0);
+      slot = rbl * nbc + cbl;
       const int64_t i = r * Lx + c;
       if (mask[i]) {
         const float pi = phi[i];
