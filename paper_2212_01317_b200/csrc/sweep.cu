@@ -501,27 +501,49 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
 }
 
 // a6: initial states of a batch (ARITH §G).
+// U realization pairs per work item (U = 2: float4 stores, needs an even pair count).
+// Items t = g * nunits + u are visited with a grid stride; (g, u) advance incrementally, so
+// the loop has no integer division (items < 2^31: the host caps P * R).
+template <int U>
 __global__ void __launch_bounds__(256) k_init_states(const GapRec* __restrict__ rec,
                                                      float* __restrict__ G, float* __restrict__ A,
                                                      int64_t P, int R, int npairs,
                                                      uint32_t pair_base, int random_init,
                                                      uint32_t k0, uint32_t k1) {
   pdl_wait();
-  const int64_t items = P * npairs;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < items;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = t / npairs;
-    const int j = static_cast<int>(t - g * npairs);
-    float2 v;
+  const uint32_t nunits = static_cast<uint32_t>(npairs / U);
+  const uint32_t items = static_cast<uint32_t>(P) * nunits;
+  const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  uint32_t g = t0 / nunits, u = t0 - g * nunits;
+  const uint32_t sg = stride / nunits, su = stride - sg * nunits;
+  for (uint32_t t = t0; t < items; t += stride) {
+    float v[2 * U];
     if (random_init) {
-      const Words4 w = philox4x32_10(rec[g].site, 0u, pair_base + static_cast<uint32_t>(j), 1u, k0, k1);
-      v = make_float2(proposal_angle(w.w0), proposal_angle(w.w2));
+#pragma unroll
+      for (int h = 0; h < U; ++h) {
+        const Words4 w = philox4x32_10(rec[g].site, 0u, pair_base + U * u + h, 1u, k0, k1);
+        v[2 * h] = proposal_angle(w.w0);
+        v[2 * h + 1] = proposal_angle(w.w2);
+      }
     } else {
       const float f = rec[g].init;
-      v = make_float2(f, f);
+#pragma unroll
+      for (int h = 0; h < 2 * U; ++h) v[h] = f;
     }
-    *reinterpret_cast<float2*>(G + g * R + 2 * j) = v;
-    if (A) *reinterpret_cast<float2*>(A + g * R + 2 * j) = make_float2(0.0f, 0.0f);
+    float* gp = G + static_cast<int64_t>(g) * R + 2 * U * u;
+    if (U == 2) {
+      *reinterpret_cast<float4*>(gp) = make_float4(v[0], v[1], v[2 % (2 * U)], v[3 % (2 * U)]);
+      if (A) *reinterpret_cast<float4*>(A + static_cast<int64_t>(g) * R + 4 * u) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      *reinterpret_cast<float2*>(gp) = make_float2(v[0], v[1]);
+      if (A) *reinterpret_cast<float2*>(A + static_cast<int64_t>(g) * R + 2 * u) = make_float2(0.f, 0.f);
+    }
+    g += sg;
+    u += su;
+    if (u >= nunits) {
+      u -= nunits;
+      ++g;
+    }
   }
   pdl_trigger();
 }
@@ -727,12 +749,14 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
 void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,
                         uint32_t pair_base, int random_init, uint32_t k0, uint32_t k1,
                         cudaStream_t st) {
-  const int64_t items = P * npairs;
+  const bool quad = (npairs % 2) == 0;  // float4 items (R % 4 == 0: 16-byte aligned rows)
+  const int64_t items = P * (quad ? npairs / 2 : npairs);
   int64_t g = (items + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
   if (g < 1) g = 1;
   void* args[] = {const_cast<GapRec**>(&rec), &G, &A, &P, &R, &npairs, &pair_base, &random_init, &k0, &k1};
-  launch_pdl(reinterpret_cast<const void*>(k_init_states), static_cast<unsigned>(g), 256, args, 0, st);
+  launch_pdl(quad ? reinterpret_cast<const void*>(k_init_states<2>) : reinterpret_cast<const void*>(k_init_states<1>),
+             static_cast<unsigned>(g), 256, args, 0, st);
 }
 
 void launch_acc_reduce(const float* X, int64_t g_begin, int64_t g_count, int R, int r_lo, int r_hi,
