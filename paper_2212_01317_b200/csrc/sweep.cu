@@ -99,7 +99,9 @@ __device__ __forceinline__ float2 metropolis_pair(float2 cur, const float2 (&nb)
   const float2 prop = __fmul2_rn(make_float2(__uint2float_rn(w.w0 >> 8), __uint2float_rn(w.w2 >> 8)),
                                  f2(0x1.921fb6p-22f));
   float2 s_cur = f2(0.0f), s_new = f2(0.0f);
-  long long ec0 = 0, en0 = 0, ec1 = 0, en1 = 0;
+  // energy trace: the selected bonds' cos values of both branches are kept and only the
+  // chosen branch is converted to fixed point once the decision is known
+  float2 ccs[4], cns[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const float2 mnb = make_float2(-nb[k].x, -nb[k].y);
@@ -124,12 +126,9 @@ __device__ __forceinline__ float2 metropolis_pair(float2 cur, const float2 (&nb)
       s_cur = __fadd2_rn(s_cur, cc);
       s_new = __fadd2_rn(s_new, cn);
     }
-    if (ENERGY && ((sel >> k) & 1u)) {
-      const float2 sc = __fmul2_rn(cc, f2(0x1p32f)), sn = __fmul2_rn(cn, f2(0x1p32f));
-      ec0 += __float2ll_rn(sc.x);
-      ec1 += __float2ll_rn(sc.y);
-      en0 += __float2ll_rn(sn.x);
-      en1 += __float2ll_rn(sn.y);
+    if (ENERGY) {
+      ccs[k] = cc;
+      cns[k] = cn;
     }
   }
   const float2 dE = __fmul2_rn(f2(J), __fadd2_rn(s_cur, make_float2(-s_new.x, -s_new.y)));
@@ -139,8 +138,13 @@ __device__ __forceinline__ float2 metropolis_pair(float2 cur, const float2 (&nb)
   acc0 = (dE.x <= 0.0f) | (u.x < e.x);
   acc1 = (dE.y <= 0.0f) | (u.y < e.y);
   if (ENERGY) {
-    e0 += acc0 ? en0 : ec0;
-    e1 += acc1 ? en1 : ec1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if ((sel >> k) & 1u) {
+        const float2 ch = __fmul2_rn(make_float2(acc0 ? cns[k].x : ccs[k].x, acc1 ? cns[k].y : ccs[k].y), f2(0x1p32f));
+        e0 += __float2ll_rn(ch.x);
+        e1 += __float2ll_rn(ch.y);
+      }
   }
   return make_float2(acc0 ? prop.x : cur.x, acc1 ? prop.y : cur.y);
 }
