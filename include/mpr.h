@@ -129,8 +129,11 @@ mpr_status mpr_simulate(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed);
  * slope_tol (energy per sweep, >= 0; 0 = SPEC's rule) is SPEC's configurable tolerance.
  * No check passes before max_sweeps - n_avg => equilibrium is declared there (returned
  * negated). s_eq_out (nullable, host, M int32) receives each realization's equilibrium
- * sweep. Replaces any previous accumulation; predict as after mpr_simulate. Errors:
- * M < 1, n_fit < 3, n_f < 1, max_sweeps <= n_avg, slope_tol < 0 -> INVALID_ARG. */
+ * sweep. Replaces any previous accumulation; predict as after mpr_simulate. The test
+ * runs on the device after each check sweep (fp64, ARITH §K operation order); the host
+ * trails one check behind, so sweeps issued after the last realization finished are
+ * no-ops. Errors: M < 1, n_fit < 3, n_f < 1, max_sweeps <= n_avg, slope_tol < 0 ->
+ * INVALID_ARG. */
 mpr_status mpr_simulate_adaptive(mpr_ctx *ctx, int64_t M, uint64_t seed, int32_t n_fit, int32_t n_f,
                                  int32_t max_sweeps, double slope_tol, int32_t *s_eq_out);
 
