@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--ref-sample-realizations", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--reduce", default="allreduce", choices=["allreduce", "ordered"],
+                    help="realization sharding at N > 1: one NCCL all-reduce of the accumulators, or the "
+                         "ordered chain (bit-identical to one GPU)")
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
                     help="row slabs at N > 1: the sweep kernel writes the boundary rows into the "
                          "neighbours' IPC-mapped state buffers (peer), or NCCL send/recv (nccl)")
@@ -198,8 +201,11 @@ def run_mpr(args):
     calib = Pk.load_calibration()
     cfg = Pk.Config(device=local)
     eng = Pk.LeMpr(cfg, calib, stream=stream.cuda_stream)
-    from paper_2212_01317_b200.sharding import (allreduce_accumulator, connect_peer_halo, exchange_halo, row_range,
-                                                shard_range, slab_realization_chunks)
+    from paper_2212_01317_b200.sharding import (allreduce_accumulator, connect_peer_halo, exchange_halo,
+                                                ordered_reduce_accumulator, row_range, shard_range,
+                                                slab_realization_chunks)
+    ordered = ws > 1 and args.decomp == "realizations" and args.reduce == "ordered"
+    eng.set_deferred_reduce(ordered)
     rows = args.decomp == "rows"
     if rows:  # strong scaling: the whole M on every rank, the grid split into row slabs
         M_glob = M
@@ -219,7 +225,9 @@ def run_mpr(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def allreduce_acc():
-        if ws > 1:
+        if ordered:
+            ordered_reduce_accumulator(eng, rank, ws)
+        elif ws > 1:
             allreduce_accumulator(eng.accumulator_tensor())
 
     def simulate():
@@ -344,7 +352,7 @@ def run_mpr(args):
                 "config": {"workload": desc, "L": c["L"], "p": c["p"], "gaps": c["gaps"], "gap_sites": P,
                            "M_per_rank": M, "M_total": M_glob, "sweeps": S,
                            "updates_per_step": updates_per_step, "parallelism": (f"row slabs x{ws}" + (f", {args.halo} halo" if ws > 1 else "")) if rows
-                           else f"realizations x{ws}",
+                           else f"realizations x{ws}" + (f", {args.reduce} reduce" if ws > 1 else ""),
                            "l2": "flushed between timed steps (256 MiB write, outside the events)"},
                 "fill_time_ms": total_ms / args.steps,
                 "gpu_launches": int(launches),

@@ -159,6 +159,19 @@ mpr_status mpr_reset_accumulator(mpr_ctx *ctx);
 mpr_status mpr_simulate_range(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed,
                               int64_t m_begin, int64_t m_end);
 
+/* Ordered (deterministic) multi-rank reduction. With the deferred reduce enabled,
+ * mpr_simulate_range keeps the final states of its realizations (the range must fit one
+ * launch batch, else INVALID_ARG) instead of adding them to the accumulator;
+ * mpr_accumulate_states then adds them, realizations in ascending order, to whatever the
+ * accumulator holds at that moment. Chaining the ranks in rank order is then bit-identical
+ * to one GPU: each rank receives the accumulator of the ranks before it (for example
+ * NCCL recv into mpr_accumulator_device), accumulates its own realizations, and sends the
+ * result on; the last rank broadcasts it. The adaptive protocol and row slabs ignore the
+ * setting. A pending deferred batch blocks further simulate calls (STATE) until it is
+ * accumulated; set_data drops it. */
+mpr_status mpr_set_deferred_reduce(mpr_ctx *ctx, int enable);
+mpr_status mpr_accumulate_states(mpr_ctx *ctx);
+
 /* Device view of the per-gap-site accumulator (double, *n entries, gap-site order)
  * so an external collective (NCCL all-reduce) can sum it in place across ranks. The
  * pointer stays owned by ctx and valid until the next set_data/destroy. */

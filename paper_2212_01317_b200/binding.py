@@ -31,6 +31,7 @@ EXPORTED = ["mpr_config_default", "mpr_init", "mpr_destroy", "mpr_last_error", "
             "mpr_get_info", "mpr_debug_get", "mpr_set_energy_trace", "mpr_set_kernel_timing", "mpr_version",
             "mpr_slab_begin", "mpr_slab_half_sweep", "mpr_slab_row_states", "mpr_slab_end", "mpr_sync",
             "mpr_slab_state_ipc_handle", "mpr_slab_state_device", "mpr_slab_set_peer",
+            "mpr_set_deferred_reduce", "mpr_accumulate_states",
             "mpr_simulate_adaptive", "mpr_build_calibration"]
 
 
@@ -94,6 +95,8 @@ def load_library(path: str = LIB_PATH):
     L.mpr_slab_state_ipc_handle.argtypes = [vp, vp]; L.mpr_slab_state_ipc_handle.restype = C.c_int
     L.mpr_slab_state_device.argtypes = [vp, C.POINTER(vp)]; L.mpr_slab_state_device.restype = C.c_int
     L.mpr_slab_set_peer.argtypes = [vp, C.c_int, vp, vp]; L.mpr_slab_set_peer.restype = C.c_int
+    L.mpr_set_deferred_reduce.argtypes = [vp, C.c_int]; L.mpr_set_deferred_reduce.restype = C.c_int
+    L.mpr_accumulate_states.argtypes = [vp]; L.mpr_accumulate_states.restype = C.c_int
     L.mpr_slab_end.argtypes = [vp]; L.mpr_slab_end.restype = C.c_int
     L.mpr_sync.argtypes = [vp]; L.mpr_sync.restype = C.c_int
     L.mpr_simulate_adaptive.argtypes = [vp, i64, u64, i32, i32, i32, C.c_double, vp]
@@ -211,6 +214,14 @@ def mpr_slab_row_states(ctx, row, colour):
     p, n = C.c_void_p(), C.c_int64()
     _check(ctx, load_library().mpr_slab_row_states(ctx, row, colour, C.byref(p), C.byref(n)))
     return p.value, n.value
+
+
+def mpr_set_deferred_reduce(ctx, enable: bool) -> None:
+    _check(ctx, load_library().mpr_set_deferred_reduce(ctx, 1 if enable else 0))
+
+
+def mpr_accumulate_states(ctx) -> None:
+    _check(ctx, load_library().mpr_accumulate_states(ctx))
 
 
 MPR_IPC_HANDLE_BYTES = 64
@@ -416,6 +427,14 @@ class LeMpr:
 
     def commit_row(self, row, colour, tensor):
         """Received halo rows land in place (row_view is zero-copy): nothing to do."""
+
+    def set_deferred_reduce(self, enable=True):
+        """simulate_range keeps its states; accumulate_states adds them later (ordered
+        multi-rank reduction, bit-identical to one GPU)."""
+        mpr_set_deferred_reduce(self.ctx, enable)
+
+    def accumulate_states(self):
+        mpr_accumulate_states(self.ctx)
 
     def state_ipc_handle(self) -> bytes:
         """cudaIpcMemHandle_t of this slab's state buffer (for a neighbour process)."""

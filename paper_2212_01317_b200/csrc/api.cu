@@ -52,7 +52,7 @@ struct BatchKey {
   uint32_t pair_base;
   int32_t sweeps;
   uint32_t k0, k1;
-  int n_avg, init, r_lo, r_hi, timing, variant, order;
+  int n_avg, init, r_lo, r_hi, timing, variant, order, defer;
   float q, J;
   void *G, *A, *rec, *acc;
   long long* energy;
@@ -99,6 +99,10 @@ struct mpr_ctx {
   std::vector<GraphEntry> graphs = std::vector<GraphEntry>(8);
   size_t graph_next = 0;
   int energy_enabled = 0;
+  // ordered (deterministic) multi-rank reduction: simulate_range keeps the batch states and
+  // mpr_accumulate_states adds them later (mpr_set_deferred_reduce)
+  int defer_reduce = 0;
+  int pending_reduce = 0, pending_Rb = 0, pending_r_lo = 0, pending_r_hi = 0;
   int64_t energy_M = 0, energy_S = 0;
   // row-slab mode (mpr_slab_*)
   int slab_active = 0;
@@ -255,6 +259,7 @@ mpr_status stage_data(mpr_ctx* c) {
   c->total_launches += 2;  // row counts, scan, compaction
   CK(cudaStreamSynchronize(st), "set_data sync");
   c->stage = ST_DATA;
+  c->pending_reduce = 0;
   c->M_total = 0;
   return MPR_OK;
 }
@@ -583,9 +588,12 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
     }
   }
   if (k.timing) CK(cudaEventRecordWithFlags(c->ev1, st, ev_flags), "event record");
-  launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), 0, k.P, k.Rb, k.r_lo, k.r_hi, c->acc.as<double>(), st);
-  CKL("acc_reduce");
-  ++c->launches;
+  if (!k.defer) {
+    launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), 0, k.P, k.Rb, k.r_lo, k.r_hi, c->acc.as<double>(),
+                      st);
+    CKL("acc_reduce");
+    ++c->launches;
+  }
   return MPR_OK;
 }
 
@@ -623,6 +631,9 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
   }
   const int64_t mb0 = m_begin & ~int64_t(1);
   const int64_t R = choose_batch(c, m_end - mb0);
+  if (c->defer_reduce && R < m_end - mb0)
+    return fail(c, MPR_ERR_INVALID_ARG, "deferred reduce: the realization range must fit one batch");
+  if (c->pending_reduce) return fail(c, MPR_ERR_STATE, "deferred states not accumulated yet");
   c->batch = R;
   const bool avg = c->cfg.n_avg > 1;
   CK(c->G.ensure(sizeof(float) * c->P * R), "alloc state");
@@ -642,6 +653,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
     key.k0 = k0; key.k1 = k1; key.n_avg = c->cfg.n_avg; key.init = c->cfg.init; key.r_lo = r_lo; key.r_hi = r_hi;
     key.timing = c->timing; key.variant = c->sweep_variant; key.q = c->cfg.q; key.J = c->cfg.J;
     key.order = c->cfg.order;
+    key.defer = c->defer_reduce;
     key.G = c->G.p; key.A = c->A.p; key.rec = c->rec.p; key.acc = c->acc.p;
     key.energy = c->energy_enabled ? c->energy.as<long long>() + mb * sweeps : nullptr;
     int64_t nsweep_launch = 0;
@@ -672,8 +684,8 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
           if (e.exec == exec) nsweep_launch = e.launches;
       }
       CK(cudaGraphLaunch(exec, st), "graph launch");
-      c->launches += nsweep_launch + 2;
-      c->total_launches += nsweep_launch + 2;
+      c->launches += nsweep_launch + (key.defer ? 1 : 2);
+      c->total_launches += nsweep_launch + (key.defer ? 1 : 2);
     } else {
       mpr_status sb = issue_batch(c, key, &nsweep_launch, false);
       if (sb != MPR_OK) return sb;
@@ -687,9 +699,35 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
     }
     c->last_m_base = mb;
     c->last_R = Rb;
+    if (key.defer) {
+      c->pending_reduce = 1;
+      c->pending_Rb = Rb;
+      c->pending_r_lo = r_lo;
+      c->pending_r_hi = r_hi;
+    }
   }
   CK(cudaStreamSynchronize(st), "simulate sync");
   c->stage = ST_SIM;
+  return MPR_OK;
+}
+
+mpr_status mpr_set_deferred_reduce(mpr_ctx* c, int enable) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (c->pending_reduce) return fail(c, MPR_ERR_STATE, "deferred states not accumulated yet");
+  c->defer_reduce = enable ? 1 : 0;
+  return MPR_OK;
+}
+
+mpr_status mpr_accumulate_states(mpr_ctx* c) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (!c->pending_reduce) return fail(c, MPR_ERR_STATE, "no deferred states (simulate_range with deferred reduce)");
+  SET_DEVICE(c);
+  const bool avg = c->cfg.n_avg > 1;
+  launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), 0, c->P, c->pending_Rb, c->pending_r_lo,
+                    c->pending_r_hi, c->acc.as<double>(), c->stream);
+  CKL("acc_reduce");
+  c->pending_reduce = 0;
+  CK(cudaStreamSynchronize(c->stream), "accumulate sync");
   return MPR_OK;
 }
 

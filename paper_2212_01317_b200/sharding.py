@@ -142,15 +142,42 @@ def distributed_fill_slabs(engine, grid, mask, M: int, sweeps: int, seed: int, g
     return engine.predict()
 
 
-def distributed_fill(engine: Engine, grid, mask, M: int, sweeps: int, seed: int, group=None):
+def ordered_reduce_accumulator(engine, rank: int, world: int, group=None) -> None:
+    """Deterministic reduction across ranks, bit-identical to one GPU: the accumulator
+    travels rank 0 -> 1 -> ... -> W-1, each rank adding its realizations (ascending ids,
+    mpr_accumulate_states) on top of the sum of the ranks before it; the last rank
+    broadcasts the total. Needs simulate_range under set_deferred_reduce(True)."""
+    acc = engine.accumulator_tensor()
+    peer = (lambda r: r) if group is None else (lambda r: dist.get_global_rank(group, r))
+    if rank > 0:
+        dist.recv(acc, peer(rank - 1), group=group)
+    engine.accumulate_states()
+    if rank < world - 1:
+        dist.send(acc, peer(rank + 1), group=group)
+    if world > 1:
+        dist.broadcast(acc, peer(world - 1), group=group)
+
+
+def distributed_fill(engine: Engine, grid, mask, M: int, sweeps: int, seed: int, group=None,
+                     reduce: str = "allreduce"):
     """SPMD gap fill: every rank calls this with the same arguments; returns the
-    predictions (identical on every rank)."""
+    predictions (identical on every rank). reduce="allreduce": one all-reduce of the
+    accumulators (equal to one GPU up to fp64 summation order); reduce="ordered": the
+    chained reduction, bit-identical to one GPU."""
+    if reduce not in ("allreduce", "ordered"):
+        raise ValueError("reduce must be 'allreduce' or 'ordered'")
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     m0, m1 = shard_range(M, world, rank)
     engine.set_data(grid, mask)
     engine.estimate_local_params()
     engine.reset_accumulator()
-    engine.simulate_range(M, sweeps, seed, m0, m1)
-    allreduce_accumulator(engine.accumulator_tensor(), group)
+    if reduce == "ordered":
+        engine.set_deferred_reduce(True)
+        engine.simulate_range(M, sweeps, seed, m0, m1)
+        ordered_reduce_accumulator(engine, rank, world, group)
+        engine.set_deferred_reduce(False)
+    else:
+        engine.simulate_range(M, sweeps, seed, m0, m1)
+        allreduce_accumulator(engine.accumulator_tensor(), group)
     return engine.predict()

@@ -714,3 +714,50 @@ def test_fuzz_row_slabs_match_single_context(P, calib, k):
         assert_bitwise(got, ref, f"row slabs x{world} ({halo})")
     else:
         assert np.max(np.abs(got - ref)) <= 1e-5 * (np.nanmax(z) - np.nanmin(z))
+
+
+@pytest.mark.parametrize("world,M", [(2, 12), (3, 10), (4, 7), (2, 100)])
+def test_ordered_reduce_bit_identical_to_single_context(P, calib, world, M):
+    """Realization sharding with the ordered reduction (mpr_set_deferred_reduce +
+    mpr_accumulate_states): contexts on one GPU standing in for ranks simulate their shards
+    independently, then the accumulator is passed on in rank order (device copies where
+    NCCL would send/recv) and each adds its realizations. The predictions equal the
+    single-context run bit for bit."""
+    import torch
+    from paper_2212_01317_b200.sharding import shard_range
+    truth, z, mask = make_problem(72, 0.45, Lx=61, corr_len=6.0)
+    cfg = P.Config()
+    ref = gpu_run(P, z, mask, cfg, calib, M, 9, 4242)["pred"]
+    engs = [P.LeMpr(cfg, calib) for _ in range(world)]
+    for w, e in enumerate(engs):
+        e.set_data(z, mask); e.estimate_local_params(); e.reset_accumulator()
+        e.set_deferred_reduce(True)
+        m0, m1 = shard_range(M, world, w)
+        e.simulate_range(M, 9, 4242, m0, m1)
+    for w, e in enumerate(engs):
+        if w > 0:
+            e.accumulator_tensor().copy_(engs[w - 1].accumulator_tensor())
+            torch.cuda.synchronize()
+        e.accumulate_states()
+    pred = engs[-1].predict()
+    for e in engs:
+        e.close()
+    assert_bitwise(pred, ref, f"ordered reduction over {world} shards")
+
+
+def test_deferred_reduce_state_rules(P, calib):
+    """A pending deferred batch blocks the next simulate call; accumulating twice is a
+    STATE error; a range wider than one batch is rejected."""
+    truth, z, mask = make_problem(32, 0.5, corr_len=5.0)
+    m = P.LeMpr(P.Config(max_batch=4), calib)
+    m.set_data(z, mask); m.estimate_local_params(); m.reset_accumulator()
+    m.set_deferred_reduce(True)
+    with pytest.raises(P.MprError):
+        m.simulate_range(10, 3, 1, 0, 10)  # needs 3 batches of 4
+    m.simulate_range(10, 3, 1, 0, 4)
+    with pytest.raises(P.MprError):
+        m.simulate_range(10, 3, 1, 4, 8)   # previous states not accumulated
+    m.accumulate_states()
+    with pytest.raises(P.MprError):
+        m.accumulate_states()
+    m.close()

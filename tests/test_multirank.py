@@ -45,11 +45,28 @@ class OracleEngine:
         self.acc = torch.zeros(self.z.size, dtype=torch.float64)
         self.M = 0
 
+    deferred = False
+    pending = None
+
+    def set_deferred_reduce(self, enable=True):
+        self.deferred = enable
+
     def simulate_range(self, M, sweeps, seed, m0, m1):
         self.M = M
         if m1 > m0:
-            r = self.O.simulate(self.p, self.mask, self.cfg, M, sweeps, seed, m_begin=m0, m_end=m1)
-            self.acc += torch.from_numpy(r["acc"].ravel())
+            r = self.O.simulate(self.p, self.mask, self.cfg, M, sweeps, seed, m_begin=m0, m_end=m1,
+                                states=self.deferred)
+            if self.deferred:  # keep the final states (n_avg = 1), add them in accumulate_states
+                self.pending = r["phi"]
+            else:
+                self.acc += torch.from_numpy(r["acc"].ravel())
+
+    def accumulate_states(self):
+        acc = self.acc.numpy().reshape(self.mask.shape)  # a view: the adds land in self.acc
+        gaps = self.mask == 0
+        for phi in (self.pending if self.pending is not None else []):  # ascending realization ids
+            acc[gaps] += phi[gaps].astype(np.float64)
+        self.pending = None
 
     def accumulator_tensor(self):
         return self.acc
@@ -66,6 +83,34 @@ def _free_port():
     port = s.getsockname()[1]
     s.close()
     return port
+
+
+def _ordered_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle as O
+    from inputs.synth import make_problem
+    from tests.conftest import read_calibration
+    truth, z, mask = make_problem(24, 0.5, corr_len=5.0)
+    eng = OracleEngine(read_calibration(), O.OracleConfig(lb=8, rs=1, ns=2))
+    out[rank] = distributed_fill(eng, z, mask, M=7, sweeps=6, seed=31, reduce="ordered")
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ordered_reduce_bit_identical_to_single_process(calib, world):
+    """reduce="ordered": the accumulator travels rank 0 -> W-1, each rank adding its
+    realizations in ascending order, so the predictions equal the single-process oracle
+    bit for bit (the all-reduce is only equal up to fp64 summation order)."""
+    import oracle as O
+    from inputs.synth import make_problem
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_ordered_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    truth, z, mask = make_problem(24, 0.5, corr_len=5.0)
+    ref = O.fill(z, mask, O.OracleConfig(lb=8, rs=1, ns=2), *calib, M=7, S=6, seed=31)["pred"]
+    for r in range(world):
+        assert np.array_equal(out[r].view(np.uint32), ref.view(np.uint32))
 
 
 def _worker(rank, world, port, out):
