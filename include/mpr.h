@@ -101,7 +101,10 @@ const char *mpr_last_error(const mpr_ctx *ctx);
  * the gaps with z_min. */
 mpr_status mpr_set_data(mpr_ctx *ctx, const float *grid, const uint8_t *mask, int64_t Lx, int64_t Ly);
 
-/* Same as mpr_set_data with device pointers (no host<->device copy). */
+/* Same as mpr_set_data with device pointers (a device-to-device copy into the context).
+ * Both calls return once the inputs are copied and the sample counts are known; the
+ * gap-site index is still being built on the context stream (later calls are ordered
+ * after it). */
 mpr_status mpr_set_data_device(mpr_ctx *ctx, const float *grid_dev, const uint8_t *mask_dev,
                                int64_t Lx, int64_t Ly);
 

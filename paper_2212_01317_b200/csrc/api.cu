@@ -257,7 +257,8 @@ mpr_status stage_data(mpr_ctx* c) {
                    c->gid.as<int32_t>(), c->rec.as<GapRec>(), st);
   CKL("gap_index");
   c->total_launches += 2;  // row counts, scan, compaction
-  CK(cudaStreamSynchronize(st), "set_data sync");
+  // no final sync: the caller's buffers were copied before the min/max sync above, and
+  // the gap-index kernels only touch context buffers (stream-ordered before later calls)
   c->stage = ST_DATA;
   c->pending_reduce = 0;
   c->M_total = 0;
