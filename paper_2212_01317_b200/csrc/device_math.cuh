@@ -185,6 +185,29 @@ __device__ __forceinline__ float2 exp_spec_fast2(float2 x) {
   return make_float2(x.x < -80.0f ? 0.0f : r.x, x.y < -80.0f ? 0.0f : r.y);
 }
 
+// exp_spec_fast2(x) * 2^24, exactly: the power-of-two scale of the last step carries the
+// extra 2^24 (n >= -116 keeps p * 2^(n+24) normal, so the product is the same exact scaling
+// of p * 2^n). Compared with (float)(w >> 8) it decides u(w) < exp_spec(x) without forming
+// u(w) = (w >> 8) * 2^-24 (ARITH §A/§C: both sides are exact power-of-two scalings).
+__device__ __forceinline__ float2 exp_spec_fast2_x24(float2 x) {
+  const float vx = __fmul_rn(x.x, 0x1.715476p+0f);
+  const float vy = __fmul_rn(x.y, 0x1.715476p+0f);
+  const float2 tm = make_float2(__fadd_rn(vx, 12582912.0f), __fadd_rn(vy, 12582912.0f));
+  const float2 n = __fadd2_rn(tm, f2(-12582912.0f));  // exact
+  const float2 nn = make_float2(-n.x, -n.y);
+  float2 f = __ffma2_rn(nn, f2(0x1.62e430p-1f), x);
+  f = __ffma2_rn(nn, f2(-0x1.05c610p-29f), f);
+  float2 p = __ffma2_rn(f2(0x1.6ac2a0p-10f), f, f2(0x1.126e38p-7f));
+  p = __ffma2_rn(p, f, f2(0x1.555890p-5f));
+  p = __ffma2_rn(p, f, f2(0x1.555408p-3f));
+  p = __ffma2_rn(p, f, f2(0x1.fffffap-2f));
+  p = __ffma2_rn(p, f, f2(1.0f));
+  p = __ffma2_rn(p, f, f2(1.0f));
+  const int nx = __float_as_int(tm.x) - 0x4b400000, ny = __float_as_int(tm.y) - 0x4b400000;
+  const float2 r = __fmul2_rn(p, make_float2(__int_as_float((nx + 127 + 24) << 23), __int_as_float((ny + 127 + 24) << 23)));
+  return make_float2(x.x < -80.0f ? 0.0f : r.x, x.y < -80.0f ? 0.0f : r.y);
+}
+
 // Order-preserving key of a float for integer atomicMin/atomicMax.
 __device__ __forceinline__ int float_to_ordered(float f) {
   const int b = __float_as_int(f);

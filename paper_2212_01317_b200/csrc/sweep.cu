@@ -133,10 +133,10 @@ __device__ __forceinline__ float2 metropolis_pair(float2 cur, const float2 (&nb)
   }
   const float2 dE = __fmul2_rn(f2(J), __fadd2_rn(s_cur, make_float2(-s_new.x, -s_new.y)));
   const float2 x = __fmul2_rn(dE, f2(-beta));  // == -(dE * beta): RN is sign-symmetric
-  const float2 e = exp_spec_fast2(x);
-  const float2 u = __fmul2_rn(make_float2(__uint2float_rn(w.w1 >> 8), __uint2float_rn(w.w3 >> 8)), f2(0x1p-24f));
-  acc0 = (dE.x <= 0.0f) | (u.x < e.x);
-  acc1 = (dE.y <= 0.0f) | (u.y < e.y);
+  // u(w) < exp_spec(x)  <=>  (w >> 8) < exp_spec(x) * 2^24 (exact power-of-two scalings)
+  const float2 e24 = exp_spec_fast2_x24(x);
+  acc0 = (dE.x <= 0.0f) | (__uint2float_rn(w.w1 >> 8) < e24.x);
+  acc1 = (dE.y <= 0.0f) | (__uint2float_rn(w.w3 >> 8) < e24.y);
   if (ENERGY) {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -157,13 +157,14 @@ __device__ __forceinline__ bool all_present(uint32_t f) {
 // One work item (gap site, realization pair) once its record and the states it reads
 // are in registers: Philox, two Metropolis updates, store, fused epilogues.
 // PEER: the launch may carry neighbour state buffers (row slabs, fused halo): checked at
-// run time; kernels instantiated with PEER = false skip the check altogether.
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool PEER = true>
+// run time in the PEER = true instantiations only (launch_sweep_half picks them when the
+// launch has peers); the default kernels carry no peer code.
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool PEER = false>
 __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec& rec, float2 cur,
                                                const float2 (&nb)[4], uint32_t self_off, const Words4& w,
                                                long long& e0, long long& e1, bool accum0, bool accum1);
 
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool PEER = true>
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool PEER = false>
 __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& rec, float2 cur,
                                              const float2 (&nb)[4], uint32_t self_off, uint32_t pair,
                                              long long& e0, long long& e1, bool accum0, bool accum1) {
@@ -294,7 +295,7 @@ __device__ __forceinline__ Split split_work(int npairs) {
 // One realization pair per thread. PF = 2: record, own and neighbour states loaded at the
 // start of each item, with a register-free L2 prefetch of the next item; PF = 3: the next
 // item's record is loaded one item ahead (below).
-template <bool QHALF, bool ENERGY, int MINB, int PF, int NT, bool BFEXP, bool LIST, bool PK>
+template <bool QHALF, bool ENERGY, int MINB, int PF, int NT, bool BFEXP, bool LIST, bool PK, bool PEER = false>
 __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   pdl_wait();
   const Split sp = split_work(a.npairs);
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
           nb[k] = f2(__int_as_float(rec.nb[k]));
         }
       }
-      process_item<QHALF, ENERGY, BFEXP, PK>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
+      process_item<QHALF, ENERGY, BFEXP, PK, PEER>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
       rec = recn;
       gg = ggn;
     }
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
           nb[k] = f2(__int_as_float(rec.nb[k]));
         }
       }
-      process_item<QHALF, ENERGY, BFEXP, PK>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
+      process_item<QHALF, ENERGY, BFEXP, PK, PEER>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
     }
   }
   if (ENERGY) {
@@ -670,9 +671,13 @@ void launch_adaptive_check(const AdaptiveCheckArgs& a, cudaStream_t st) {
 //   v5  99.5 / 2229 / 4127;  v13 93.9 / 2071 / 3717;
 //   v22 87.1 / 1838 / 3402;  v28 84.5 / 1780 / 3351.
 template <bool Q, bool E, bool LIST>
-static void* sweep_kernel_ptr(int variant) {
-  if (variant == 5) return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, false>);
-  return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);  // 13 (and 22/28's fallback)
+static void* sweep_kernel_ptr(int variant, bool peer) {
+  if (variant == 5)
+    return peer ? reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, false, true>)
+                : reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, false>);
+  // 13 (and 22/28's fallback)
+  return peer ? reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true, true>)
+              : reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);
 }
 
 static int sweep_threads(int) { return 256; }
@@ -700,12 +705,16 @@ static void* quad_kernel(bool qhalf, bool energy, bool list, int variant, bool p
 
 static void* sweep_kernel(bool qhalf, bool energy, bool list, int variant, bool peer = false) {
   if (is_quad(variant)) return quad_kernel(qhalf, energy, list, variant, peer);
+  if (peer)  // row slabs with the fused halo: SC order, no energy trace
+    return qhalf ? sweep_kernel_ptr<true, false, false>(variant, true) : sweep_kernel_ptr<false, false, false>(variant, true);
   if (list) {
-    if (qhalf) return energy ? sweep_kernel_ptr<true, true, true>(variant) : sweep_kernel_ptr<true, false, true>(variant);
-    return energy ? sweep_kernel_ptr<false, true, true>(variant) : sweep_kernel_ptr<false, false, true>(variant);
+    if (qhalf)
+      return energy ? sweep_kernel_ptr<true, true, true>(variant, false) : sweep_kernel_ptr<true, false, true>(variant, false);
+    return energy ? sweep_kernel_ptr<false, true, true>(variant, false) : sweep_kernel_ptr<false, false, true>(variant, false);
   }
-  if (qhalf) return energy ? sweep_kernel_ptr<true, true, false>(variant) : sweep_kernel_ptr<true, false, false>(variant);
-  return energy ? sweep_kernel_ptr<false, true, false>(variant) : sweep_kernel_ptr<false, false, false>(variant);
+  if (qhalf)
+    return energy ? sweep_kernel_ptr<true, true, false>(variant, false) : sweep_kernel_ptr<true, false, false>(variant, false);
+  return energy ? sweep_kernel_ptr<false, true, false>(variant, false) : sweep_kernel_ptr<false, false, false>(variant, false);
 }
 
 int sweep_grid_size(int device, int variant) {
