@@ -136,8 +136,8 @@ __device__ __forceinline__ float exp_spec(float x) {
 // the two realizations of a pair can share one instruction without changing a bit.
 // ptxas 12.9 caveat (checked in SASS): a FMUL2 whose result feeds a FADD2 is contracted
 // into one FFMA2 even with explicit .rn, which would drop a rounding. The packed code
-// below therefore never feeds a packed product into a packed add; the one place ARITH
-// has a product followed by an add (exp_spec's x*log2e + 1.5*2^23) stays scalar.
+// below therefore never feeds a packed product into a packed add; where ARITH has a
+// product followed by an add (exp_spec's x*log2e + 1.5*2^23) the add is scalar.
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 
 // cos_half_spec on both components (ARITH §B with the 4^-k coefficients).
@@ -190,9 +190,8 @@ __device__ __forceinline__ float2 exp_spec_fast2(float2 x) {
 // of p * 2^n). Compared with (float)(w >> 8) it decides u(w) < exp_spec(x) without forming
 // u(w) = (w >> 8) * 2^-24 (ARITH §A/§C: both sides are exact power-of-two scalings).
 __device__ __forceinline__ float2 exp_spec_fast2_x24(float2 x) {
-  const float vx = __fmul_rn(x.x, 0x1.715476p+0f);
-  const float vy = __fmul_rn(x.y, 0x1.715476p+0f);
-  const float2 tm = make_float2(__fadd_rn(vx, 12582912.0f), __fadd_rn(vy, 12582912.0f));
+  const float2 v = __fmul2_rn(x, f2(0x1.715476p+0f));  // packed product, scalar adds below
+  const float2 tm = make_float2(__fadd_rn(v.x, 12582912.0f), __fadd_rn(v.y, 12582912.0f));
   const float2 n = __fadd2_rn(tm, f2(-12582912.0f));  // exact
   const float2 nn = make_float2(-n.x, -n.y);
   float2 f = __ffma2_rn(nn, f2(0x1.62e430p-1f), x);
