@@ -4,7 +4,6 @@ adaptive protocol, row slabs (emulated), and the calibration builder."""
 import os
 import sys
 
-import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
