@@ -20,7 +20,8 @@ def main():
         m.set_data(z, mask)
         m.set_energy_trace(energy)
         m.estimate_local_params()
-        m.simulate(5, 6, 3)
+        m.simulate(5, 6, 3)      # odd pair count: the one-pair fallback kernel
+        m.simulate(8, 4, 5)      # two pairs per thread: the quad kernel
         m.predict()
         if cfg.order == "sc":
             m.set_energy_trace(False)
