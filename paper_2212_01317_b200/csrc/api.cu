@@ -87,6 +87,7 @@ struct mpr_ctx {
   long long sum_SB_fx = 0;  // fixed-point bond sum of the known-known bonds (ARITH §J)
   // simulation bookkeeping
   int64_t M_total = 0, sweeps = 0, batch = 0, last_m_base = 0, last_R = 0;
+  int64_t split_min_P = int64_t(1) << 21;  // choose_batch's 4k + 2 split threshold (MPR_SPLIT_MIN_P)
   int64_t batch_key_P = -1, batch_key_R = -1, batch_cached = 0;
   int64_t launches = 0, total_launches = 0;
   int timing = 0;
@@ -305,7 +306,7 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
   // the 2-realization batch runs the one-pair kernel). Only for large grids: a separate 2-realization batch costs a full launch sequence,
   // which small, latency-bound problems do not win back (256^2..1024^2, M = 10: measured
   // 0.36 -> 0.50 ms and 1.25 -> 1.39 ms when split; 16384^2: 3.85 -> 3.40 ms / half-sweep).
-  if ((c->sweep_variant == 22 || c->sweep_variant == 28) && B % 4 == 2 && B > 2 && c->P >= (int64_t(1) << 21))
+  if ((c->sweep_variant == 22 || c->sweep_variant == 28) && B % 4 == 2 && B > 2 && c->P >= c->split_min_P)
     B -= 2;
   c->batch_key_P = c->P;
   c->batch_key_R = R;
@@ -382,6 +383,7 @@ mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
   }
   if (const char* v = std::getenv("MPR_SWEEP_VARIANT")) c->sweep_variant = std::atoi(v);
   if (const char* v = std::getenv("MPR_NO_GRAPHS")) c->use_graphs = std::atoi(v) ? 0 : 1;
+  if (const char* v = std::getenv("MPR_SPLIT_MIN_P")) c->split_min_P = std::atoll(v);
   c->sweep_grid = sweep_grid_size(c->device, c->sweep_variant);
   *out = c;
   return MPR_OK;

@@ -519,6 +519,21 @@ def test_every_sweep_variant_bit_exact(P, calib, variant, monkeypatch):
     compare(P, z, mask, truth, P.Config(), calib, 16, 5, 57, energy=True)  # 8k realizations
 
 
+def test_split_tail_batch_bit_exact(P, calib, monkeypatch):
+    """The 4k + 2 batch split of large problems (MPR_SPLIT_MIN_P = 0 applies it at any size):
+    the two-pair kernel on the 4k batch, the one-pair kernel on the 2-realization tail. States
+    of the tail batch, accumulator, predictions and the energy trace of every realization
+    equal the oracle's, for a full tail (M = 10), a half tail (M = 9, one valid realization),
+    n_avg > 1 with random init, and generic q."""
+    monkeypatch.setenv("MPR_SPLIT_MIN_P", "0")
+    truth, z, mask = make_problem(45, 0.55, Lx=61, corr_len=6.0)
+    g, _ = compare(P, z, mask, truth, P.Config(), calib, 10, 7, 31, energy=True)
+    assert g["info"]["last_batch"] == 2 and g["info"]["last_m_base"] == 8
+    compare(P, z, mask, truth, P.Config(), calib, 9, 6, 32, energy=True)
+    compare(P, z, mask, truth, P.Config(n_avg=3, init="random"), calib, 14, 6, 33, exact_pred=False)
+    compare(P, z, mask, truth, P.Config(q=0.3, J=0.8, r_s=1), calib, 6, 5, 34)
+
+
 def _fuzz_case(k):
     """Seeded random small problem + configuration (case k)."""
     rng = np.random.default_rng(9000 + k)
