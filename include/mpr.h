@@ -263,9 +263,9 @@ typedef struct {
                                                     last_m_base + last_batch) are in
                                                     the state buffer (MPR_BUF_STATE)*/
   int32_t sweep_variant;                         /* half-sweep kernel variant in use
-                                                    (MPR_SWEEP_VARIANT; 22 default:
+                                                    (MPR_SWEEP_VARIANT; 28 default:
                                                     two realization pairs per thread,
-                                                    13 for odd pair counts / energy) */
+                                                    13 for odd pair counts)         */
 } mpr_info;
 mpr_status mpr_get_info(mpr_ctx *ctx, mpr_info *info);
 
