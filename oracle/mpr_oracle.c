@@ -76,6 +76,40 @@ float oracle_cos_spec(float x)
     return p;
 }
 
+/* --------------------------------------------------------------- ARITH §B2 */
+/* sin_spec(x) = x * S(x*x) for x in [-pi_f, pi_f]: odd polynomial of degree 13 whose
+ * even part S is evaluated by Horner in fp32 fmaf (coefficients frozen in ARITH §B2). */
+float oracle_sin_poly(float t)
+{
+    float p = 0x1.27e614p-33f;
+    p = fmaf(p, t, -0x1.a7f884p-26f);
+    p = fmaf(p, t, 0x1.717f0cp-19f);
+    p = fmaf(p, t, -0x1.a01412p-13f);
+    p = fmaf(p, t, 0x1.1110ep-7f);
+    p = fmaf(p, t, -0x1.555552p-3f);
+    p = fmaf(p, t, 1.0f);
+    return p;
+}
+
+float oracle_sin_spec(float x)
+{
+    return x * oracle_sin_poly(x * x);
+}
+
+/* q = 1/2 (h = 1/4): x * S4(x*x) with S4's coefficients c_k * 2^-(4k+2), i.e.
+ * (x/4) * S((x/4)^2) with the power-of-two scalings folded in (ARITH §B2). */
+float oracle_sin_poly_quarter(float t)
+{
+    float p = 0x1.27e614p-59f;
+    p = fmaf(p, t, -0x1.a7f884p-48f);
+    p = fmaf(p, t, 0x1.717f0cp-37f);
+    p = fmaf(p, t, -0x1.a01412p-27f);
+    p = fmaf(p, t, 0x1.1110ep-17f);
+    p = fmaf(p, t, -0x1.555552p-9f);
+    p = fmaf(p, t, 0x1p-2f);
+    return p;
+}
+
 /* ---------------------------------------------------------------- ARITH §C */
 float oracle_exp_spec(float x)
 {
@@ -319,9 +353,51 @@ void oracle_init(float *phi, const uint8_t *mask, int Lx, int Ly, int lb,
 
 /* ------------------------------------------------ ARITH §H */
 /* Energy change dE = E(phi') - E(phi) of moving site (r,c) to angle prop, with
- * E = -J sum_j cos[q(phi - phi_j)] over its in-grid neighbours (Eq.(1)),
- * summed in the order N, S, W, E in fp32 (ARITH §H). */
+ * E = -J sum_j cos[q(phi - phi_j)] over its in-grid neighbours (Eq.(1)).
+ * ARITH §H evaluates it through the identity cos A - cos B = 2 sin((B-A)/2) sin((A+B)/2):
+ *   dE = 2J * sin[q(phi' - phi)/2] * sum_j sin[q((phi' + phi)/2 - phi_j)]
+ * (SURVEY §8(c.2) option (ii); reading R19 in DESIGN.md), in this exact fp32 order:
+ *   h = q/2;  d = phi' - phi;  a0 = h * d;  S1 = a0 * S(a0*a0);  s = phi' + phi;  Sig = +0
+ *   for j in N, S, W, E inside the grid:  x = fma(-2, phi_j, s);  a = h * x;
+ *                                         Sig = fma(a, S(a*a), Sig)
+ *   dE = (2J) * (S1 * Sig)
+ * For q = 1/2 the products by h = 1/4 are folded into the polynomial (S4, ARITH §B2):
+ *   S1 = d * S4(d*d);  Sig = fma(x, S4(x*x), Sig).
+ * h, 2J and 2 phi_j are exact power-of-two scalings. */
 float oracle_delta_energy(const float *phi, int Lx, int Ly, int r, int c, float prop, float q, float J)
+{
+    float cur = phi[(int64_t)r * Lx + c];
+    const int quarter = (q == 0.5f);  /* ARITH §B2: the folded form for q = 1/2 */
+    float h = q * 0.5f;
+    float d = prop - cur;
+    float S1;
+    if (quarter) {
+        S1 = d * oracle_sin_poly_quarter(d * d);
+    } else {
+        float a0 = h * d;
+        S1 = a0 * oracle_sin_poly(a0 * a0);
+    }
+    float s = prop + cur;
+    float sig = +0.0f;
+    int nr[4] = {r - 1, r + 1, r, r};
+    int nc[4] = {c, c, c - 1, c + 1};
+    for (int k = 0; k < 4; ++k) {
+        if (nr[k] < 0 || nr[k] >= Ly || nc[k] < 0 || nc[k] >= Lx) continue;
+        float pj = phi[(int64_t)nr[k] * Lx + nc[k]];
+        float x = fmaf(-2.0f, pj, s);
+        if (quarter) {
+            sig = fmaf(x, oracle_sin_poly_quarter(x * x), sig);
+        } else {
+            float a = h * x;
+            sig = fmaf(a, oracle_sin_poly(a * a), sig);
+        }
+    }
+    return (2.0f * J) * (S1 * sig);
+}
+
+/* The direct form, sum of the bond cosines in the order N, S, W, E: used by the calibration
+ * recipe (ARITH §H, last paragraph), whose table predates the product form. */
+float oracle_delta_energy_direct(const float *phi, int Lx, int Ly, int r, int c, float prop, float q, float J)
 {
     float cur = phi[(int64_t)r * Lx + c];
     float s_cur = +0.0f, s_new = +0.0f;
@@ -668,7 +744,7 @@ static void local_sweep(float *phi, int L, float beta, float q, float step, uint
                 oracle_philox4x32_10(ctr, key, w);
                 float prop = phi[i] + step * (2.0f * oracle_uniform(w[0]) - 1.0f);
                 if (prop < 0.0f || prop > TWO_PI_F) continue;
-                float dE = oracle_delta_energy(phi, L, L, r, c, prop, q, 1.0f);
+                float dE = oracle_delta_energy_direct(phi, L, L, r, c, prop, q, 1.0f);
                 if (dE <= 0.0f || oracle_uniform(w[1]) < oracle_exp_spec(-(dE * beta))) phi[i] = prop;
             }
 }

@@ -57,6 +57,7 @@ def _declare(L):
     L.oracle_philox4x32_10.argtypes = [_u32p, _u32p, _u32p]
     L.oracle_uniform.argtypes = [C.c_uint32]; L.oracle_uniform.restype = C.c_float
     L.oracle_cos_spec.argtypes = [C.c_float]; L.oracle_cos_spec.restype = C.c_float
+    L.oracle_sin_spec.argtypes = [C.c_float]; L.oracle_sin_spec.restype = C.c_float
     L.oracle_exp_spec.argtypes = [C.c_float]; L.oracle_exp_spec.restype = C.c_float
     L.oracle_bond_energy.argtypes = [C.c_float] * 4; L.oracle_bond_energy.restype = C.c_float
     L.oracle_transform.argtypes = [_f32p, _u8p, C.c_int64, C.POINTER(C.c_float),
@@ -85,6 +86,8 @@ def _declare(L):
     L.oracle_delta_energy.argtypes = [_f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float,
                                       C.c_float]
     L.oracle_delta_energy.restype = C.c_float
+    L.oracle_delta_energy_direct.argtypes = L.oracle_delta_energy.argtypes
+    L.oracle_delta_energy_direct.restype = C.c_float
     L.oracle_run_chain.argtypes = [_f32p, _u8p, _f32p, C.c_int, C.c_int, C.c_float, C.c_float, C.c_uint32,
                                    C.c_uint32, C.c_int64, C.c_uint64, C.c_void_p]
     L.oracle_run_chain.restype = C.c_int64
@@ -138,6 +141,10 @@ def uniform(w: int) -> float:
 
 def cos_spec(x: float) -> float:
     return lib().oracle_cos_spec(float(x))
+
+
+def sin_spec(x: float) -> float:
+    return lib().oracle_sin_spec(float(x))
 
 
 def exp_spec(x: float) -> float:
@@ -241,10 +248,17 @@ def sweep(phi, mask, beta, sweep_index, m, seed, q=0.5, J=1.0, reverse=False) ->
 
 
 def delta_energy(phi, r, c, prop, q=0.5, J=1.0) -> float:
-    """dE of moving site (r, c) to `prop` (Eq.(1), ARITH §H)."""
+    """dE of moving site (r, c) to `prop` (Eq.(1); ARITH §H product form)."""
     phi = np.ascontiguousarray(phi, np.float32)
     return lib().oracle_delta_energy(phi.ravel(), phi.shape[1], phi.shape[0], int(r), int(c), float(prop),
                                      float(q), float(J))
+
+
+def delta_energy_direct(phi, r, c, prop, q=0.5, J=1.0) -> float:
+    """dE as the sum of bond-cosine differences (the calibration recipe's form, ARITH §H)."""
+    phi = np.ascontiguousarray(phi, np.float32)
+    return lib().oracle_delta_energy_direct(phi.ravel(), phi.shape[1], phi.shape[0], int(r), int(c),
+                                            float(prop), float(q), float(J))
 
 
 def run_chain(phi, mask, beta, s_begin, s_end, m=0, seed=1, q=0.5, J=1.0):

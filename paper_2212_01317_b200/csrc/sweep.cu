@@ -42,40 +42,47 @@ __device__ __forceinline__ float cosq(float d, float q) {
   return cos_spec(__fmul_rn(q, d));
 }
 
-// ARITH §H for one realization. FULL: all four neighbours exist (interior site), so
-// the sums need no masking and start from the first term (+0 + c == c exactly, since
-// cos_spec never returns -0). Returns the new angle; `sel` selects the bonds whose
-// chosen-branch cos is added to *e_sel (energy epilogue).
+// ARITH §H for one realization: the product form
+//   dE = 2J * sin[q(phi' - phi)/2] * sum_j sin[q((phi' + phi)/2 - phi_j)]
+// with sin_spec(a) = a * S(a*a) (ARITH §B2) and the neighbour sum accumulated by fmaf in the
+// order N, S, W, E; QHALF folds the products by h = q/2 = 1/4 into S4. FULL: all four
+// neighbours exist (interior site), so no term is masked. Returns the new angle; `sel` selects
+// the bonds whose cos (ARITH §B) at the chosen angle is added to *e_sel (energy epilogue).
 template <bool QHALF, bool ENERGY, bool FULL, bool BFEXP>
 __device__ __forceinline__ float metropolis(float cur, const float (&nbv)[4], uint32_t flags,
                                             uint32_t sel, float beta, float q, float J,
                                             uint32_t wa, uint32_t wb, bool& accepted,
                                             long long& e_sel) {
   const float prop = proposal_angle(wa);
-  float s_cur = 0.0f, s_new = 0.0f;
-  long long ec = 0, en = 0;  // ARITH §J fixed-point bond sums of the selected bonds
+  const float h = __fmul_rn(q, 0.5f);
+  const float d = __fsub_rn(prop, cur);
+  float S1;
+  if (QHALF) {
+    S1 = __fmul_rn(d, sin_poly_quarter(__fmul_rn(d, d)));
+  } else {
+    const float a0 = __fmul_rn(h, d);
+    S1 = __fmul_rn(a0, sin_poly(__fmul_rn(a0, a0)));
+  }
+  const float sm = __fadd_rn(prop, cur);
+  float sig = 0.0f;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    float cc = cosq<QHALF>(__fsub_rn(cur, nbv[k]), q);
-    float cn = cosq<QHALF>(__fsub_rn(prop, nbv[k]), q);
+    const float x = __fmaf_rn(-2.0f, nbv[k], sm);
+    float t;
+    if (QHALF) {
+      t = __fmaf_rn(x, sin_poly_quarter(__fmul_rn(x, x)), sig);
+    } else {
+      const float a = __fmul_rn(h, x);
+      t = __fmaf_rn(a, sin_poly(__fmul_rn(a, a)), sig);
+    }
     if (!FULL) {
       const bool has = ((flags >> (2 * k)) & 3u) != 0u;
-      cc = has ? cc : 0.0f;
-      cn = has ? cn : 0.0f;
-    }
-    if (FULL && k == 0) {
-      s_cur = cc;
-      s_new = cn;
+      sig = has ? t : sig;
     } else {
-      s_cur = __fadd_rn(s_cur, cc);
-      s_new = __fadd_rn(s_new, cn);
-    }
-    if (ENERGY && ((sel >> k) & 1u)) {
-      ec += __float2ll_rn(__fmul_rn(cc, 0x1p32f));
-      en += __float2ll_rn(__fmul_rn(cn, 0x1p32f));
+      sig = t;
     }
   }
-  const float dE = __fmul_rn(J, __fsub_rn(s_cur, s_new));
+  const float dE = __fmul_rn(__fmul_rn(2.0f, J), __fmul_rn(S1, sig));
   const float x = -__fmul_rn(dE, beta);
   if (BFEXP) {  // branch-free: exp evaluated by every lane (no divergence around it)
     const float e = exp_spec_fast(x);
@@ -83,70 +90,74 @@ __device__ __forceinline__ float metropolis(float cur, const float (&nbv)[4], ui
   } else {
     accepted = (dE <= 0.0f) || (u24(wb) < exp_spec_fast(x));
   }
-  if (ENERGY) e_sel += accepted ? en : ec;
-  return accepted ? prop : cur;
+  const float nv = accepted ? prop : cur;
+  if (ENERGY) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if ((sel >> k) & 1u) e_sel += __float2ll_rn(__fmul_rn(cosq<QHALF>(__fsub_rn(nv, nbv[k]), q), 0x1p32f));
+  }
+  return nv;
 }
 
 // ARITH §H for both realizations of a pair at once, on packed f32x2 instructions: the
 // x / y components follow exactly the scalar operation sequence of metropolis() above
 // (each FFMA2/FADD2/FMUL2 component rounds like its scalar twin), so the results are
-// bit-identical while the FP instruction count of an item halves.
+// bit-identical while the FP instruction count of an item halves. No packed product feeds
+// a packed add (device_math.cuh: the ptxas FMUL2 -> FADD2 contraction).
 template <bool QHALF, bool ENERGY, bool FULL>
 __device__ __forceinline__ float2 metropolis_pair(float2 cur, const float2 (&nb)[4], uint32_t flags,
                                                   uint32_t sel, float beta, float q, float J,
                                                   const Words4& w, bool& acc0, bool& acc1,
                                                   long long& e0, long long& e1) {
-  const float2 prop = __fmul2_rn(make_float2(__uint2float_rn(w.w0 >> 8), __uint2float_rn(w.w2 >> 8)),
-                                 f2(0x1.921fb6p-22f));
-  float2 s_cur = f2(0.0f), s_new = f2(0.0f);
-  // energy trace: the selected bonds' cos values of both branches are kept and only the
-  // chosen branch is converted to fixed point once the decision is known
-  float2 ccs[4], cns[4];
+  // the proposal product is scalar: it feeds the adds below
+  const float2 prop = make_float2(__fmul_rn(__uint2float_rn(w.w0 >> 8), 0x1.921fb6p-22f),
+                                  __fmul_rn(__uint2float_rn(w.w2 >> 8), 0x1.921fb6p-22f));
+  const float2 d = __fadd2_rn(prop, make_float2(-cur.x, -cur.y));
+  float2 S1;
+  if (QHALF) {
+    S1 = __fmul2_rn(d, sin_poly_quarter2(__fmul2_rn(d, d)));
+  } else {
+    const float2 a0 = __fmul2_rn(f2(__fmul_rn(q, 0.5f)), d);
+    S1 = __fmul2_rn(a0, sin_poly2(__fmul2_rn(a0, a0)));
+  }
+  const float2 sm = __fadd2_rn(prop, cur);
+  float2 sig = f2(0.0f);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const float2 mnb = make_float2(-nb[k].x, -nb[k].y);
-    float2 dc = __fadd2_rn(cur, mnb), dn = __fadd2_rn(prop, mnb);
-    float2 cc, cn;
+    const float2 x = __ffma2_rn(f2(-2.0f), nb[k], sm);
+    float2 t;
     if (QHALF) {
-      cc = cos_half_spec2(dc);
-      cn = cos_half_spec2(dn);
+      t = __ffma2_rn(x, sin_poly_quarter2(__fmul2_rn(x, x)), sig);
     } else {
-      cc = cos_spec2(__fmul2_rn(f2(q), dc));
-      cn = cos_spec2(__fmul2_rn(f2(q), dn));
+      const float2 a = __fmul2_rn(f2(__fmul_rn(q, 0.5f)), x);
+      t = __ffma2_rn(a, sin_poly2(__fmul2_rn(a, a)), sig);
     }
     if (!FULL) {
       const bool has = ((flags >> (2 * k)) & 3u) != 0u;
-      cc = has ? cc : f2(0.0f);
-      cn = has ? cn : f2(0.0f);
-    }
-    if (FULL && k == 0) {
-      s_cur = cc;
-      s_new = cn;
+      sig = has ? t : sig;
     } else {
-      s_cur = __fadd2_rn(s_cur, cc);
-      s_new = __fadd2_rn(s_new, cn);
-    }
-    if (ENERGY) {
-      ccs[k] = cc;
-      cns[k] = cn;
+      sig = t;
     }
   }
-  const float2 dE = __fmul2_rn(f2(J), __fadd2_rn(s_cur, make_float2(-s_new.x, -s_new.y)));
-  const float2 x = __fmul2_rn(dE, f2(-beta));  // == -(dE * beta): RN is sign-symmetric
+  const float2 dE = __fmul2_rn(f2(__fmul_rn(2.0f, J)), __fmul2_rn(S1, sig));
+  const float2 xe = __fmul2_rn(dE, f2(-beta));  // == -(dE * beta): RN is sign-symmetric
   // u(w) < exp_spec(x)  <=>  (w >> 8) < exp_spec(x) * 2^24 (exact power-of-two scalings)
-  const float2 e24 = exp_spec_fast2_x24(x);
+  const float2 e24 = exp_spec_fast2_x24(xe);
   acc0 = (dE.x <= 0.0f) | (__uint2float_rn(w.w1 >> 8) < e24.x);
   acc1 = (dE.y <= 0.0f) | (__uint2float_rn(w.w3 >> 8) < e24.y);
-  if (ENERGY) {
+  const float2 nv = make_float2(acc0 ? prop.x : cur.x, acc1 ? prop.y : cur.y);
+  if (ENERGY) {  // a8: the selected bonds' cos at the chosen angles
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       if ((sel >> k) & 1u) {
-        const float2 ch = __fmul2_rn(make_float2(acc0 ? cns[k].x : ccs[k].x, acc1 ? cns[k].y : ccs[k].y), f2(0x1p32f));
+        const float2 dk = __fadd2_rn(nv, make_float2(-nb[k].x, -nb[k].y));
+        const float2 c = QHALF ? cos_half_spec2(dk) : cos_spec2(__fmul2_rn(f2(q), dk));
+        const float2 ch = __fmul2_rn(c, f2(0x1p32f));
         e0 += __float2ll_rn(ch.x);
         e1 += __float2ll_rn(ch.y);
       }
   }
-  return make_float2(acc0 ? prop.x : cur.x, acc1 ? prop.y : cur.y);
+  return nv;
 }
 
 // Every neighbour present: each 2-bit field of flags is non-zero.
