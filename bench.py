@@ -32,10 +32,11 @@ sys.path.insert(0, ROOT)
 from inputs.synth import CONFIGS, SEED_SIM, make_problem  # noqa: E402
 
 METRIC = "gap-site spin updates/sec (LE-MPR conditional simulation, whole fill)"
-# FP32 lane-ops the arithmetic contract fixes per gap-site update (8 cos_spec
-# of 8 ops, 8 sums, dE/beta 3, exp_spec 12, 4 conversions = 93) + half a Philox4x32-10
-# call (10 rounds x 2 IMAD.WIDE + 2 LOP3 = 40 per pair) = 113.
-ALG_OPS_PER_UPDATE = 113
+# FP32 lane-ops the arithmetic contract fixes per gap-site update (ARITH §H
+# product form: sin of the half difference 9, four neighbour sine terms of 9, the sum
+# phi' + phi 1, dE / beta 3, exp_spec 12, 4 conversions = 65) + half a Philox4x32-10 call
+# (10 rounds x 2 IMAD.WIDE + 2 LOP3 = 40 per pair) = 85.
+ALG_OPS_PER_UPDATE = 85
 UNIT = "updates/s"
 
 
