@@ -8,14 +8,15 @@
 //     shared by all realizations: their angles live in the 32-byte GapRec of each
 //     gap neighbour);
 //   * one work item = (gap site g, realization pair j): a float2 of the state, one
-//     Philox4x32-10 call whose four words serve both realizations (ARITH §A), eight
-//     cos_spec evaluations per realization (ARITH §B, H) and one exp_spec;
+//     Philox4x32-10 call whose four words serve both realizations (ARITH §A), five
+//     sin_spec evaluations per realization (ΔE in the product form, ARITH §B2, H) and
+//     one exp_spec;
 //   * consecutive lanes take consecutive items, so the self and neighbour float2
 //     accesses of a warp are contiguous runs of G (coalesced), and every lane of a
 //     warp does useful work whatever the gap pattern (no idle lanes on frozen sites).
 // The whole-grid energy (a8) and the last-n_avg accumulation (a9) are fused into the
-// epilogue; the energy of each bond is the value of the branch the Metropolis step
-// already chose, so the diagnostic costs no extra cos evaluation.
+// epilogue; the energy of each selected bond is its cos_spec at the angle the Metropolis
+// step chose (evaluated only in the ENERGY kernels).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -678,7 +679,9 @@ void launch_adaptive_check(const AdaptiveCheckArgs& a, cudaStream_t st) {
 //   22 = k_sweep_quad: two pairs per thread, float4 state moves, 4 CTAs/SM;
 //   28 = 22 with both pairs' Philox words drawn before the state loads are used,
 //        3 CTAs/SM (default).
-// Half-sweep, us (C2 / C3 / C4 at M = 10):
+// Half-sweep, us (C2 / C3 / C4 at M = 10), product-form dE (ARITH §H):
+//   v5  92.6 (C2);  v13 89.7 / 1965 / 3525;  v28 72.2 / 1509 / 3082.
+// Direct form (8 cos per update), for comparison:
 //   v5  99.5 / 2229 / 4127;  v13 93.9 / 2071 / 3717;
 //   v22 87.1 / 1838 / 3402;  v28 84.5 / 1780 / 3351.
 template <bool Q, bool E, bool LIST>
