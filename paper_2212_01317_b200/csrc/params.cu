@@ -431,29 +431,34 @@ __global__ void __launch_bounds__(256) k_expand(const float* __restrict__ Tb, in
 }
 
 // One SST pass: clipped (2rs+1)^2 window mean with exact int64 window sums (ARITH §F).
-// 32x32 output tile per CTA of 32 x 8 threads: the (32+2rs)^2 input tile is converted once
-// to fixed point in shared memory, summed horizontally (one column per lane), then
-// vertically with a sliding window over the 4 output rows of each thread. Integer sums are
-// exact, so the order of the additions does not change a bit.
+// Output tile of 32 columns x kSmoothY rows per CTA of 32 x 8 threads: the
+// (32 + 2rs) x (kSmoothY + 2rs) input tile is converted once to fixed point in shared
+// memory, summed horizontally (one column per lane), then vertically with a sliding window
+// over the kSmoothY / 8 output rows of each thread. Integer sums are exact, so the order of
+// the additions does not change a bit. The tall tile amortises the vertical halo and the
+// two barriers; interior tiles use 32-bit offsets from the tile origin.
+constexpr int kSmoothY = 64;
 __global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
                                                 float* __restrict__ Tout, int64_t Lx, int64_t Ly,
                                                 int rs) {
   extern __shared__ long long smem[];
-  const int W = kTile + 2 * rs, w = 2 * rs + 1;
-  long long* Q = smem;             // W rows x W cols
-  long long* H = smem + W * W;     // W rows x kTile cols
+  const int W = kTile + 2 * rs, HY = kSmoothY + 2 * rs, w = 2 * rs + 1;
+  long long* Q = smem;             // HY rows x W cols
+  long long* H = smem + HY * W;    // HY rows x kTile cols
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (int64_t)blockIdx.y * kTile;
-  const bool interior = r0 - rs >= 0 && c0 - rs >= 0 && r0 + kTile + rs <= Ly && c0 + kTile + rs <= Lx;
-  if (interior) {  // whole halo tile inside the grid: no bounds checks, one row pointer per row
+  const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (int64_t)blockIdx.y * kSmoothY;
+  const bool interior = r0 - rs >= 0 && c0 - rs >= 0 && r0 + kSmoothY + rs <= Ly && c0 + kTile + rs <= Lx;
+  if (interior) {  // whole halo tile inside the grid: no bounds checks, 32-bit offsets
     const float* base = Tin + (r0 - rs) * Lx + (c0 - rs);
-    for (int y = ty; y < W; y += 8) {
-      const float* row = base + y * Lx;
+    const uint32_t lx = static_cast<uint32_t>(Lx);
+    for (int y = ty; y < HY; y += 8) {
+      const float* row = base + static_cast<uint32_t>(y) * lx;
       long long* q = Q + y * W;
-      for (int x = tx; x < W; x += 32) q[x] = __float2ll_rn(__fmul_rn(__ldg(row + x), 0x1p40f));
+      q[tx] = __float2ll_rn(__fmul_rn(__ldg(row + tx), 0x1p40f));
+      if (tx < 2 * rs) q[32 + tx] = __float2ll_rn(__fmul_rn(__ldg(row + 32 + tx), 0x1p40f));
     }
   } else {
-    for (int y = ty; y < W; y += 8) {
+    for (int y = ty; y < HY; y += 8) {
       const int64_t r = r0 - rs + y;
       const bool rin = r >= 0 && r < Ly;
       for (int x = tx; x < W; x += 32) {
@@ -463,7 +468,7 @@ __global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
     }
   }
   __syncthreads();
-  for (int y = ty; y < W; y += 8) {
+  for (int y = ty; y < HY; y += 8) {
     const long long* q = Q + y * W + tx;
     long long s = 0;
     for (int d = 0; d < w; ++d) s += q[d];
@@ -474,18 +479,23 @@ __global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
   if (c >= Lx) return;
   const int64_t ca = c - rs > 0 ? c - rs : 0, cb = c + rs < Lx - 1 ? c + rs : Lx - 1;
   const int ncol = static_cast<int>(cb - ca + 1);
-  const int yb = ty * (kTile / 8);
+  constexpr int kRowsPerThread = kSmoothY / 8;
+  const int yb = ty * kRowsPerThread;
   float* out = Tout + (r0 + yb) * Lx + c;
   long long s = 0;
   for (int d = 0; d < w; ++d) s += H[(yb + d) * kTile + tx];
-#pragma unroll
-  for (int k = 0; k < kTile / 8; ++k) {
+  const double full = static_cast<double>(w * ncol);  // rows unclipped (interior of the grid rows)
+#pragma unroll 4
+  for (int k = 0; k < kRowsPerThread; ++k) {
     const int64_t r = r0 + yb + k;
     if (k > 0) s += H[(yb + k + w - 1) * kTile + tx] - H[(yb + k - 1) * kTile + tx];
     if (r >= Ly) break;
-    const int64_t ra = r - rs > 0 ? r - rs : 0, rb = r + rs < Ly - 1 ? r + rs : Ly - 1;
-    const double cnt = static_cast<double>(static_cast<int>(rb - ra + 1) * ncol);
-    out[k * Lx] = __double2float_rn(__ddiv_rn(__ll2double_rn(s) * 0x1p-40, cnt));
+    double cnt = full;
+    if (r - rs < 0 || r + rs > Ly - 1) {
+      const int64_t ra = r - rs > 0 ? r - rs : 0, rb = r + rs < Ly - 1 ? r + rs : Ly - 1;
+      cnt = static_cast<double>(static_cast<int>(rb - ra + 1) * ncol);
+    }
+    out[static_cast<int64_t>(k) * Lx] = __double2float_rn(__ddiv_rn(__ll2double_rn(s) * 0x1p-40, cnt));
   }
 }
 
@@ -631,13 +641,13 @@ void launch_expand(const float* Tb, int64_t Lx, int64_t Ly, int lb, float* T, cu
 
 void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int rs,
                    cudaStream_t st) {
-  const int W = kTile + 2 * rs;
-  const size_t smem = sizeof(long long) * (static_cast<size_t>(W) * W + static_cast<size_t>(W) * kTile);
+  const int W = kTile + 2 * rs, HY = kSmoothY + 2 * rs;
+  const size_t smem = sizeof(long long) * (static_cast<size_t>(HY) * W + static_cast<size_t>(HY) * kTile);
   // > 48 KB of dynamic shared memory needs the opt-in, per device: set it on the calling
   // thread's current device whenever a large window asks for it (r_s >= 16)
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_smooth, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((Ly + kTile - 1) / kTile));
+  dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((Ly + kSmoothY - 1) / kSmoothY));
   k_smooth<<<grid, 256, smem, st>>>(Tin, Tout, Lx, Ly, rs);
 }
 
