@@ -431,23 +431,24 @@ __global__ void __launch_bounds__(256) k_expand(const float* __restrict__ Tb, in
 }
 
 // One SST pass: clipped (2rs+1)^2 window mean with exact int64 window sums (ARITH §F).
-// Output tile of 32 columns x kSmoothY rows per CTA of 32 x 8 threads: the
-// (32 + 2rs) x (kSmoothY + 2rs) input tile is converted once to fixed point in shared
+// Output tile of 32 columns x TY rows per CTA of 32 x 8 threads: the
+// (32 + 2rs) x (TY + 2rs) input tile is converted once to fixed point in shared
 // memory, summed horizontally (one column per lane), then vertically with a sliding window
-// over the kSmoothY / 8 output rows of each thread. Integer sums are exact, so the order of
-// the additions does not change a bit. The tall tile amortises the vertical halo and the
-// two barriers; interior tiles use 32-bit offsets from the tile origin.
-constexpr int kSmoothY = 64;
+// over the TY / 8 output rows of each thread. Integer sums are exact, so the order of
+// the additions does not change a bit. A tall tile (TY = 64) amortises the vertical halo and
+// the two barriers on large grids; small grids keep TY = 32 for more CTAs. Interior tiles
+// use 32-bit offsets from the tile origin.
+template <int TY>
 __global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
                                                 float* __restrict__ Tout, int64_t Lx, int64_t Ly,
                                                 int rs) {
   extern __shared__ long long smem[];
-  const int W = kTile + 2 * rs, HY = kSmoothY + 2 * rs, w = 2 * rs + 1;
+  const int W = kTile + 2 * rs, HY = TY + 2 * rs, w = 2 * rs + 1;
   long long* Q = smem;             // HY rows x W cols
   long long* H = smem + HY * W;    // HY rows x kTile cols
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (int64_t)blockIdx.y * kSmoothY;
-  const bool interior = r0 - rs >= 0 && c0 - rs >= 0 && r0 + kSmoothY + rs <= Ly && c0 + kTile + rs <= Lx;
+  const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (int64_t)blockIdx.y * TY;
+  const bool interior = r0 - rs >= 0 && c0 - rs >= 0 && r0 + TY + rs <= Ly && c0 + kTile + rs <= Lx;
   if (interior) {  // whole halo tile inside the grid: no bounds checks, 32-bit offsets
     const float* base = Tin + (r0 - rs) * Lx + (c0 - rs);
     const uint32_t lx = static_cast<uint32_t>(Lx);
@@ -479,7 +480,7 @@ __global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
   if (c >= Lx) return;
   const int64_t ca = c - rs > 0 ? c - rs : 0, cb = c + rs < Lx - 1 ? c + rs : Lx - 1;
   const int ncol = static_cast<int>(cb - ca + 1);
-  constexpr int kRowsPerThread = kSmoothY / 8;
+  constexpr int kRowsPerThread = TY / 8;
   const int yb = ty * kRowsPerThread;
   float* out = Tout + (r0 + yb) * Lx + c;
   long long s = 0;
@@ -641,14 +642,22 @@ void launch_expand(const float* Tb, int64_t Lx, int64_t Ly, int lb, float* T, cu
 
 void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int rs,
                    cudaStream_t st) {
-  const int W = kTile + 2 * rs, HY = kSmoothY + 2 * rs;
+  // 32 x 64 tiles once the grid has >= 16 waves of them on 148 SMs (C4 16384^2: 1.66 -> 1.16
+  // ms per pass); 32 x 32 below, where more CTAs hide latency better (1024^2: 10.9 vs 13.6 us)
+  const bool tall = (Lx + kTile - 1) / kTile * ((Ly + 63) / 64) >= 148 * 16;
+  const int TY = tall ? 64 : 32;
+  const int W = kTile + 2 * rs, HY = TY + 2 * rs;
   const size_t smem = sizeof(long long) * (static_cast<size_t>(HY) * W + static_cast<size_t>(HY) * kTile);
+  const void* fn = tall ? reinterpret_cast<const void*>(k_smooth<64>) : reinterpret_cast<const void*>(k_smooth<32>);
   // > 48 KB of dynamic shared memory needs the opt-in, per device: set it on the calling
   // thread's current device whenever a large window asks for it (r_s >= 16)
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_smooth, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((Ly + kSmoothY - 1) / kSmoothY));
-  k_smooth<<<grid, 256, smem, st>>>(Tin, Tout, Lx, Ly, rs);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((Ly + TY - 1) / TY));
+  if (tall)
+    k_smooth<64><<<grid, 256, smem, st>>>(Tin, Tout, Lx, Ly, rs);
+  else
+    k_smooth<32><<<grid, 256, smem, st>>>(Tin, Tout, Lx, Ly, rs);
 }
 
 void launch_build_records(const int32_t* gid, const uint8_t* mask, const float* phiK,
