@@ -273,6 +273,48 @@ __global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ p
   for (int t = threadIdx.x; t < nslots; t += blockDim.x) { sSB[t] = 0; sNB[t] = 0; sSP[t] = 0; sNK[t] = 0; }
   __syncthreads();
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  if (nslots == 1) {
+    // the whole tile lies in one l_b block (l_b a multiple of 32, the default 32 included):
+    // each thread sums its 4 sites in registers, then one warp reduction per warp (the sums
+    // are exact integers, so the grouping does not matter)
+    long long vsb = 0, vsp = 0;
+    int vnb = 0, vnk = 0;
+#pragma unroll
+    for (int k = 0; k < kTile / 8; ++k) {
+      const int64_t r = r0 + ty + 8 * k, c = c0 + tx;
+      if (r < Ly && c < Lx) {
+        const int64_t i = r * Lx + c;
+        if (mask[i]) {
+          const float pi = phi[i];
+          vsp += __float2ll_rn(__fmul_rn(pi, 0x1p28f));
+          vnk += 1;
+          if (c + 1 < Lx && mask[i + 1]) {
+            const float bnd = cos_spec(__fmul_rn(q, __fsub_rn(pi, phi[i + 1])));
+            vsb += __float2ll_rn(__fmul_rn(bnd, 0x1p32f));
+            vnb += 1;
+          }
+          if (r + 1 < Ly && mask[i + Lx]) {
+            const float bnd = cos_spec(__fmul_rn(q, __fsub_rn(pi, phi[i + Lx])));
+            vsb += __float2ll_rn(__fmul_rn(bnd, 0x1p32f));
+            vnb += 1;
+          }
+        }
+      }
+    }
+    vsb = warp_sum_ll(vsb);
+    vsp = warp_sum_ll(vsp);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      vnb += __shfl_xor_sync(0xffffffffu, vnb, off);
+      vnk += __shfl_xor_sync(0xffffffffu, vnk, off);
+    }
+    if (tx == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sSB[0]), static_cast<unsigned long long>(vsb));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sNB[0]), static_cast<unsigned long long>(vnb));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sSP[0]), static_cast<unsigned long long>(vsp));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&sNK[0]), static_cast<unsigned long long>(vnk));
+    }
+  } else {
   // block column of this thread's site column: one 32-bit division per thread (Lx, Ly < 2^31)
   const int cbl = static_cast<int>(static_cast<uint32_t>(c0 + tx) / static_cast<uint32_t>(lb) - bc0);
   for (int k = 0; k < kTile / 8; ++k) {
@@ -316,6 +358,7 @@ __global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ p
       atomicAdd(reinterpret_cast<unsigned long long*>(&sSP[slot]), static_cast<unsigned long long>(vsp));
       atomicAdd(reinterpret_cast<unsigned long long*>(&sNK[slot]), static_cast<unsigned long long>(vnk));
     }
+  }
   }
   __syncthreads();
   for (int t = threadIdx.x; t < nslots; t += blockDim.x) {
