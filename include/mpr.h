@@ -65,7 +65,8 @@ typedef struct {
   int n_s;           /* smoothing passes (n_s = 5); 0 => BST              */
   int init;          /* mpr_init_mode                                   */
   int n_avg;         /* sweeps averaged at the end of each realization (>= 1)          */
-  const float *calib_T;  /* calibration table T_k, strictly increasing, 0 < T <= 1e4   */
+  const float *calib_T;  /* calibration table T_k, strictly increasing, 0 < T <= 1e4;
+                            with n_s > 0 also T_max * (2 r_s + 1)^2 < 2^23 (ARITH §E)  */
   const float *calib_e;  /* e_k = e(T_k), strictly increasing (host pointers, copied)  */
   int calib_n;           /* K >= 2                                                     */
   int64_t max_batch;     /* max realizations simulated concurrently (0 => automatic)  */
@@ -95,7 +96,8 @@ const char *mpr_last_error(const mpr_ctx *ctx);
 /* Stage a problem: grid (float32, Lx*Ly) and mask (uint8, Lx*Ly), host memory.
  * Computes z_min/z_max over the samples and the spin angles phi = 2pi(z - z_min)/
  * (z_max - z_min) at the samples (ARITH §D), and builds the gap-site
- * index. Errors: Lx < 2 or Ly < 2 or Lx*Ly >= 2^31 or a non-finite sample ->
+ * index. Errors: Lx < 2 or Ly < 2 or Lx*Ly > 2^30 (the bound under which every int64
+ * fixed-point sum of ARITH §E/§J fits) or a non-finite sample ->
  * INVALID_ARG; fewer than 2 samples -> TOO_FEW_SAMPLES. z_max == z_min is not an
  * error: the DEGENERATE_RANGE flag is set, simulate is a no-op and predict fills
  * the gaps with z_min. */

@@ -17,11 +17,35 @@
  * chain with coupled gap sites under a spatially varying T, which has no Gibbs
  * measure ("actually non-equilibrium"): parity unpinned beyond the invariants
  * and the uniform-T / isolated-site special cases.
+ *
+ * Integer bounds (ARITH §E, §J): inputs with Lx*Ly <= 2^30 and (2 r_s + 1)^2 * T_max < 2^23
+ * (the limits mpr_set_data / mpr_init enforce) keep every int64 fixed-point sum below 2^63.
+ *
+ * Two builds of this one file: liboracle.so (single thread: parity) and liboracle_omp.so
+ * (-fopenmp: the same-colour rows of a half-sweep and the rows of a smoothing pass split
+ * over threads; used only to time the oracle on all host cores). Their results are
+ * bit-identical (test_openmp_build_bit_identical).
  */
+
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* Threads of the OpenMP build (returns the count in use; 1 in the plain build). */
+int oracle_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
+}
 
 #define TWO_PI_F 0x1.921fb6p+2f
 
@@ -308,6 +332,7 @@ void oracle_smooth(float *T, int Lx, int Ly, int rs, int ns)
     int64_t n = (int64_t)Lx * Ly;
     float *out = (float *)malloc(sizeof(float) * (size_t)n);
     for (int pass = 0; pass < ns; ++pass) {
+#pragma omp parallel for schedule(static)
         for (int r = 0; r < Ly; ++r)
             for (int c = 0; c < Lx; ++c) {
                 int r0 = r - rs < 0 ? 0 : r - rs, r1 = r + rs > Ly - 1 ? Ly - 1 : r + rs;
@@ -325,28 +350,49 @@ void oracle_smooth(float *T, int Lx, int Ly, int rs, int ns)
 }
 
 /* ------------------------------------------------------ ARITH §G */
+/* The one definition of both initial angles (ARITH §G), shared by oracle_init and
+ * oracle_simulate_window so the two cannot drift apart.
+ * RANDOM: phi = u(w) * TWO_PI_F with w the INIT word of realization m at global site
+ * `site`: Philox counter (site, sweep 0, m >> 1, tag 1), word w0 for even m, w2 for odd m
+ * (ARITH §A). The angle is uniform on [0, 2pi) (pinned by test_random_init_*). */
+static float init_angle_random(uint32_t site, int64_t m, uint64_t seed)
+{
+    uint32_t ctr[4] = {site, 0u, (uint32_t)(m >> 1), 1u};
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    uint32_t w[4];
+    oracle_philox4x32_10(ctr, key, w);
+    return oracle_uniform((m & 1) ? w[2] : w[0]) * TWO_PI_F;
+}
+
+/* BLOCK_MEAN: the mean known angle of block b, (float)((double)SP_b 2^-28 / NK_b), or the
+ * global sample mean gmean when the block has no sample. */
+static float init_angle_block_mean(int64_t SP_b, int64_t NK_b, float gmean)
+{
+    return NK_b ? (float)(((double)SP_b * 0x1p-28) / (double)NK_b) : gmean;
+}
+
+static float global_mean_angle(const int64_t *SP, const int64_t *NK, int64_t nblocks)
+{
+    int64_t spg = 0, nkg = 0;
+    for (int64_t b = 0; b < nblocks; ++b) { spg += SP[b]; nkg += NK[b]; }
+    return nkg ? (float)(((double)spg * 0x1p-28) / (double)nkg) : 0.0f;
+}
+
 /* init_mode 0 = BLOCK_MEAN, 1 = RANDOM. phi holds known angles; gaps are written. */
 void oracle_init(float *phi, const uint8_t *mask, int Lx, int Ly, int lb,
                  const int64_t *SP, const int64_t *NK, int init_mode, int64_t m, uint64_t seed)
 {
     int nbx = (Lx + lb - 1) / lb, nby = (Ly + lb - 1) / lb;
-    int64_t spg = 0, nkg = 0;
-    for (int b = 0; b < nbx * nby; ++b) { spg += SP[b]; nkg += NK[b]; }
-    float gmean = nkg ? (float)(((double)spg * 0x1p-28) / (double)nkg) : 0.0f;
-    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    float gmean = global_mean_angle(SP, NK, (int64_t)nbx * nby);
     for (int r = 0; r < Ly; ++r)
         for (int c = 0; c < Lx; ++c) {
             int64_t i = (int64_t)r * Lx + c;
             if (mask[i]) continue;
             if (init_mode == 0) {
                 int b = (r / lb) * nbx + (c / lb);
-                phi[i] = NK[b] ? (float)(((double)SP[b] * 0x1p-28) / (double)NK[b]) : gmean;
+                phi[i] = init_angle_block_mean(SP[b], NK[b], gmean);
             } else {
-                uint32_t ctr[4] = {(uint32_t)i, 0u, (uint32_t)(m >> 1), 1u};
-                uint32_t w[4];
-                oracle_philox4x32_10(ctr, key, w);
-                uint32_t word = (m & 1) ? w[2] : w[0];
-                phi[i] = oracle_uniform(word) * TWO_PI_F;
+                phi[i] = init_angle_random((uint32_t)i, m, seed);
             }
         }
 }
@@ -446,10 +492,7 @@ void oracle_simulate_window(const float *phi0, const uint8_t *mask, const float 
                             uint64_t seed, float *phi)
 {
     int nbx = (Lx_g + lb - 1) / lb, nby = (Ly_g + lb - 1) / lb;
-    int64_t spg = 0, nkg = 0;
-    for (int b = 0; b < nbx * nby; ++b) { spg += SP_g[b]; nkg += NK_g[b]; }
-    float gmean = nkg ? (float)(((double)spg * 0x1p-28) / (double)nkg) : 0.0f;
-    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    float gmean = global_mean_angle(SP_g, NK_g, (int64_t)nbx * nby);
     memcpy(phi, phi0, sizeof(float) * (size_t)wLx * (size_t)wLy);
     for (int r = 0; r < wLy; ++r)
         for (int c = 0; c < wLx; ++c) {
@@ -458,12 +501,9 @@ void oracle_simulate_window(const float *phi0, const uint8_t *mask, const float 
             int rg = r + r_off, cg = c + c_off;
             if (init_mode == 0) {
                 int b = (rg / lb) * nbx + (cg / lb);
-                phi[i] = NK_g[b] ? (float)(((double)SP_g[b] * 0x1p-28) / (double)NK_g[b]) : gmean;
+                phi[i] = init_angle_block_mean(SP_g[b], NK_g[b], gmean);
             } else {
-                uint32_t ctr[4] = {(uint32_t)((int64_t)rg * Lx_g + cg), 0u, (uint32_t)(m >> 1), 1u};
-                uint32_t w[4];
-                oracle_philox4x32_10(ctr, key, w);
-                phi[i] = oracle_uniform((m & 1) ? w[2] : w[0]) * TWO_PI_F;
+                phi[i] = init_angle_random((uint32_t)((int64_t)rg * Lx_g + cg), m, seed);
             }
         }
     for (int s = 1; s <= S; ++s)
@@ -480,18 +520,24 @@ void oracle_simulate_window(const float *phi0, const uint8_t *mask, const float 
 
 /* One checkerboard sweep (colour A = (r+c) even, then B) over the gap sites of one
  * realization. reverse != 0 visits each colour's sites in reverse order (parity
- * safety test: the result must not depend on the order). Returns #accepted. */
+ * safety test: the result must not depend on the order). Returns #accepted.
+ * The sites of one colour are independent (each reads only other-colour neighbours,
+ * P:119), so the timing build (liboracle_omp.so, -fopenmp) splits a colour's rows over
+ * threads; without -fopenmp the pragma is ignored. Both builds give the same bits. */
 int64_t oracle_sweep(float *phi, const uint8_t *mask, const float *beta, int Lx, int Ly,
                      float q, float J, uint32_t sweep, int64_t m, uint64_t seed, int reverse)
 {
     int64_t acc = 0;
     for (int colour = 0; colour < 2; ++colour) {
-        int64_t n = (int64_t)Lx * Ly;
-        for (int64_t t = 0; t < n; ++t) {
-            int64_t i = reverse ? n - 1 - t : t;
-            int r = (int)(i / Lx), c = (int)(i % Lx);
-            if (((r + c) & 1) != colour || mask[i]) continue;
-            acc += update_site(phi, Lx, Ly, r, c, beta[i], q, J, sweep, m, seed);
+#pragma omp parallel for schedule(static) reduction(+ : acc)
+        for (int t = 0; t < Ly; ++t) {
+            int r = reverse ? Ly - 1 - t : t;
+            for (int u = 0; u < Lx; ++u) {
+                int c = reverse ? Lx - 1 - u : u;
+                int64_t i = (int64_t)r * Lx + c;
+                if (((r + c) & 1) != colour || mask[i]) continue;
+                acc += update_site(phi, Lx, Ly, r, c, beta[i], q, J, sweep, m, seed);
+            }
         }
     }
     return acc;

@@ -16,29 +16,62 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "mpr_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
 _CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
 
 TWO_PI_F = float(np.float32(2.0 * np.pi))
 
 
+def _build_one(path, extra):
+    if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(_SRC):
+        tmp = path + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *_CFLAGS, *extra, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, path)
+    return path
+
+
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (plain C, no FMA contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *_CFLAGS, "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+    """Compile the oracle with gcc (plain C, no FMA contraction): liboracle.so (single
+    thread, parity) and liboracle_omp.so (the same source with -fopenmp, timing only)."""
+    if force:
+        for p in (_LIB, _LIB_OMP):
+            if os.path.exists(p):
+                os.remove(p)
+    _build_one(_LIB_OMP, ["-fopenmp"])
+    return _build_one(_LIB, [])
 
 
 _lib = None
+_libs = {}
+
+
+def _load(path):
+    if path not in _libs:
+        L = C.CDLL(path)
+        _declare(L)
+        _libs[path] = L
+    return _libs[path]
 
 
 def lib():
     global _lib
     if _lib is None:
-        _lib = C.CDLL(build())
-        _declare(_lib)
+        build()
+        _lib = _load(_LIB)
     return _lib
+
+
+def set_threads(n: int | None) -> int:
+    """Select the build the wrappers below call: n None or 1 -> the single-thread library
+    (parity runs); n > 1 (or 0 = all cores) -> the OpenMP build with n threads (timing the
+    oracle on the host cores). Returns the thread count in use."""
+    global _lib
+    build()
+    if n is None or n == 1:
+        _lib = _load(_LIB)
+        return 1
+    _lib = _load(_LIB_OMP)
+    return int(_lib.oracle_set_threads(int(n) if n > 0 else (os.cpu_count() or 1)))
 
 
 _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
@@ -54,6 +87,7 @@ class _Cfg(C.Structure):
 
 
 def _declare(L):
+    L.oracle_set_threads.argtypes = [C.c_int]; L.oracle_set_threads.restype = C.c_int
     L.oracle_philox4x32_10.argtypes = [_u32p, _u32p, _u32p]
     L.oracle_uniform.argtypes = [C.c_uint32]; L.oracle_uniform.restype = C.c_float
     L.oracle_cos_spec.argtypes = [C.c_float]; L.oracle_cos_spec.restype = C.c_float

@@ -56,6 +56,10 @@ struct BatchKey {
   float q, J;
   void *G, *A, *rec, *acc;
   long long* energy;
+  // DC order: the phase segments baked into the captured launches (a new mask with the same
+  // P and PA can have other phase boundaries)
+  void* dclist;
+  int64_t dc_off[5];
 };
 
 struct GraphEntry {
@@ -195,6 +199,16 @@ mpr_status validate_cfg(const mpr_config* cfg, std::string& why) {
     why = "calibration table must have 2..256 points";
     return MPR_ERR_INVALID_ARG;
   }
+  // ARITH §E: a smoothing window sum of (2 r_s + 1)^2 terms llrint(T * 2^40) stays below
+  // 2^63 iff (2 r_s + 1)^2 * T_max < 2^23 (T never exceeds the table's last T)
+  {
+    const double w = 2.0 * cfg->r_s + 1.0;
+    const float Tmax = cfg->calib_T[cfg->calib_n - 1];
+    if (cfg->n_s > 0 && std::isfinite(Tmax) && w * w * static_cast<double>(Tmax) >= 8388608.0) {
+      why = "calibration T_max * (2 r_s + 1)^2 must be < 2^23 (ARITH §E window-sum bound)";
+      return MPR_ERR_INVALID_ARG;
+    }
+  }
   for (int k = 0; k < cfg->calib_n; ++k) {
     const float T = cfg->calib_T[k], e = cfg->calib_e[k];
     if (!std::isfinite(T) || !std::isfinite(e) || !(T > 0.0f) || T > 1e4f) {
@@ -230,8 +244,19 @@ double energy_from_fx(const mpr_ctx* c, long long E_fx) {
 }
 
 
+// Forget every captured batch graph: their launches bake in buffer pointers and gap-id
+// segments of the problem they were captured for.
+void drop_graphs(mpr_ctx* c) {
+  for (auto& e : c->graphs) {
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+    e.exec = nullptr;
+  }
+  c->graph_next = 0;
+}
+
 mpr_status stage_data(mpr_ctx* c) {
   cudaStream_t st = c->stream;
+  drop_graphs(c);
   const int64_t n = c->n;
   set_scalars_init(c->hsc);
   CK(cudaMemcpyAsync(c->scal.p, c->hsc, sizeof(DevScalars), cudaMemcpyHostToDevice, st), "scalars upload");
@@ -268,7 +293,10 @@ mpr_status stage_data(mpr_ctx* c) {
 
 mpr_status check_dims(mpr_ctx* c, int64_t Lx, int64_t Ly) {
   if (Lx < 2 || Ly < 2) return fail(c, MPR_ERR_INVALID_ARG, "Lx and Ly must be >= 2");
-  if (Lx * Ly >= (int64_t(1) << 31)) return fail(c, MPR_ERR_INVALID_ARG, "Lx*Ly must be < 2^31");
+  // ARITH §E/§J: with Lx*Ly <= 2^30 every int64 fixed-point sum stays below 2^63 (the grid
+  // energy and a one-block SB have < 2^31 bonds of magnitude <= 2^32; SP < 2^30 * 2^31)
+  if (Lx > (int64_t(1) << 30) || Ly > (int64_t(1) << 30) || Lx * Ly > (int64_t(1) << 30))
+    return fail(c, MPR_ERR_INVALID_ARG, "Lx*Ly must be <= 2^30 (ARITH §E fixed-point bounds)");
   return MPR_OK;
 }
 
@@ -443,6 +471,7 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   SET_DEVICE(c);
   cudaStream_t st = c->stream;
   const int lb = c->cfg.l_b;
+  drop_graphs(c);
   c->nbx = (c->Lx + lb - 1) / lb;
   c->nby = (c->Ly + lb - 1) / lb;
   c->nblocks = c->nbx * c->nby;
@@ -659,6 +688,10 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
     key.defer = c->defer_reduce;
     key.G = c->G.p; key.A = c->A.p; key.rec = c->rec.p; key.acc = c->acc.p;
     key.energy = c->energy_enabled ? c->energy.as<long long>() + mb * sweeps : nullptr;
+    if (c->cfg.order == MPR_ORDER_DC) {
+      key.dclist = c->dclist.p;
+      for (int k = 0; k < 5; ++k) key.dc_off[k] = c->dc_off[k];
+    }
     int64_t nsweep_launch = 0;
     if (c->use_graphs) {
       cudaGraphExec_t exec = nullptr;

@@ -69,8 +69,11 @@ def compare(P, z, mask, truth, cfg, calib, M, S, seed, energy=False, exact_pred=
     p = o["params"]
     assert_bitwise(g["phiK"], p.phi0, "phi at samples")
     assert g["info"]["z_min"] == p.zmin and g["info"]["z_max"] == p.zmax
-    nb = p.Tb.size
-    assert np.array_equal(g["stats"][2], p.SP.ravel()) and np.array_equal(g["stats"][3], p.NK.ravel())
+    # block statistics element by element (ARITH §E exact int64): SB, NB, SP, NK
+    SB, NB, SP, NK = O.block_stats(p.phi0, mask, cfg.l_b, cfg.q)
+    for k, (name, ref) in enumerate((("SB", SB), ("NB", NB), ("SP", SP), ("NK", NK))):
+        assert np.array_equal(g["stats"][k], ref.ravel()), f"block statistic {name} differs"
+    assert np.array_equal(SP.ravel(), p.SP.ravel()) and np.array_equal(NK.ravel(), p.NK.ravel())
     assert_bitwise(g["Tb"], p.Tb.ravel(), "block temperatures")
     assert_bitwise(g["T"], p.T, "temperature field")
     for r, st in g["states"].items():

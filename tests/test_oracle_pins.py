@@ -148,6 +148,71 @@ def test_grid_energy_independent_angles():
     assert abs(O.grid_specific_energy(phi) + 4 / np.pi ** 2) < 0.01
 
 
+def _random_init(L, m, seed=20221202):
+    mask = np.zeros((L, L), np.uint8)                      # every site a gap
+    zero = np.zeros(1, np.int64)
+    return O.init_angles(np.zeros((L, L), np.float32), mask, L, zero, zero, 1, m, seed)
+
+
+def test_random_init_energy_matches_independent_uniform_angles():
+    """RANDOM init (ARITH §G): i.i.d. phi ~ U[0, 2pi) gives the whole-grid energy
+    e = -E[cos((x-y)/2)] = -4/pi^2 (closed form, see test_grid_energy_independent_angles).
+    3 SE with the bond covariance of shared sites: var ~ 0.336 + 6 * 0.0384 per bond. A
+    narrower range (e.g. [0, pi): e = -8/pi^2) or a constant init fails by > 50 SE."""
+    L = 128
+    nb = 2 * L * (L - 1)
+    se = math.sqrt((0.5 - 16 / math.pi ** 4 + 6 * (2 / math.pi ** 2 - 16 / math.pi ** 4)) / nb)
+    for m in (0, 1, 7):
+        phi = _random_init(L, m)
+        assert abs(O.grid_specific_energy(phi) + 4 / math.pi ** 2) < 3 * se, m
+
+
+def test_random_init_uniform_distribution_ks_and_moments():
+    """RANDOM init draws from U[0, 2pi_f): Kolmogorov-Smirnov against the uniform law
+    (scipy), the mean pi and variance (2pi)^2/12 within 4 SE, range inside [0, 2pi_f)."""
+    from scipy import stats
+    L = 128
+    n = L * L
+    for m in (0, 1):
+        phi = _random_init(L, m).ravel().astype(np.float64)
+        assert phi.min() >= 0.0 and phi.max() < float(TWO_PI_F)
+        assert stats.kstest(phi, stats.uniform(loc=0.0, scale=float(TWO_PI_F)).cdf).pvalue > 1e-3
+        sd = 2 * math.pi / math.sqrt(12)
+        assert abs(phi.mean() - math.pi) < 4 * sd / math.sqrt(n)
+        assert abs(phi.var() - sd ** 2) < 4 * sd ** 2 * math.sqrt(0.8 / n)
+
+
+def test_random_init_realizations_and_sites_independent():
+    """Different realizations (the two words of one Philox call, m = 0/1, and a different
+    counter, m = 2) and neighbouring sites are uncorrelated: |corr| < 4/sqrt(n)."""
+    L = 128
+    n = L * L
+    a, b, c = (_random_init(L, m).ravel() for m in (0, 1, 2))
+    for x, y in ((a, b), (a, c), (b, c), (a[:-1], a[1:])):
+        assert abs(np.corrcoef(x, y)[0, 1]) < 4 / math.sqrt(n)
+    assert not np.array_equal(_random_init(16, 0, seed=1), _random_init(16, 0, seed=2))
+
+
+def test_openmp_build_bit_identical(calib):
+    """The OpenMP timing build (liboracle_omp.so: same-colour rows and smoothing rows split
+    over threads) computes the same bits as the single-thread parity build."""
+    Tk, ek = calib
+    rng = np.random.default_rng(5)
+    z = rng.standard_normal((37, 45)).astype(np.float32)
+    mask = (rng.random(z.shape) > 0.5).astype(np.uint8)
+    cfg = O.OracleConfig(lb=8, rs=2, ns=3, init="random")
+    try:
+        ref = O.fill(z, mask, cfg, Tk, ek, 4, 6, 11, energy=True, states=True)
+        assert O.set_threads(4) >= 2
+        par = O.fill(z, mask, cfg, Tk, ek, 4, 6, 11, energy=True, states=True)
+    finally:
+        O.set_threads(1)
+    assert np.array_equal(ref["params"].T.view(np.uint32), par["params"].T.view(np.uint32))
+    assert np.array_equal(ref["sim"]["phi"].view(np.uint32), par["sim"]["phi"].view(np.uint32))
+    assert np.array_equal(ref["pred"].view(np.uint32), par["pred"].view(np.uint32))
+    assert np.array_equal(ref["sim"]["energy"], par["sim"]["energy"])
+
+
 # --------------------------------------------------- the worked 4x4 lattice (golden)
 @pytest.fixture(scope="module")
 def worked():
