@@ -3,22 +3,28 @@
 
 One "step" = one pass of the whole hot path over one synthetic
 problem: set_data (device-resident input) -> estimate_local_params -> simulate
-(M realizations x S sweeps) -> [all-reduce of the accumulator over ranks] -> predict.
-The N=1 workload is BASELINE config 2 (1024^2 Matern nu=0.5 heterogeneous field, 33%
-random gaps, M = 100, S = 30, SST l_b=32 r_s=2 n_s=5). Multi-GPU: realizations are
-sharded over ranks (weak scaling: M per rank fixed), then one NCCL all-reduce of the
-per-gap accumulator.
+(M realizations x S sweeps, with the reduction over ranks inside libmpr) -> predict.
+
+Headline line (N=1: BASELINE config 2): 1024^2 Matern nu=0.5 heterogeneous field, 33%
+random gaps, M = 100 per rank, S = 30, SST l_b=32 r_s=2 n_s=5. At N > 1 the realizations
+are sharded inside libmpr (MPR_SHARD_REALIZATIONS over an NCCL communicator: weak
+scaling, M per rank fixed, one NCCL all-reduce of the fp64 accumulators).
+Sub-record "c4_rows" (every N): BASELINE config 4 — 16384^2, 50% random gaps, M = 10,
+S = 30 — split into row slabs over the N ranks (MPR_SHARD_ROWS: strong scaling; the
+north star's < 1 s target), device-resident and end-to-end fill time, the half-sweep
+kernel's roofline, and each rank's H2D (its own rows only) and D2H (its own rows).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C2]
 
 Rank 0 prints ONE JSON line. `--impl reference` times the CPU oracle (the reference arm
-of this tier) on the host cores on a bounded sample of the same workload.
+of this tier) on all host cores on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -38,6 +44,8 @@ METRIC = "gap-site spin updates/sec (LE-MPR conditional simulation, whole fill)"
 # (10 rounds x 2 IMAD.WIDE + 2 LOP3 = 40 per pair) = 85.
 ALG_OPS_PER_UPDATE = 85
 UNIT = "updates/s"
+# how each config scales over ranks: weak (M per rank) or strong (M in total)
+SCALING = {"C1": "weak", "C2": "weak", "C3": "strong", "C4": "strong"}
 
 
 def parse():
@@ -47,22 +55,21 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mpr", choices=["mpr", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
-    ap.add_argument("--M", type=int, default=None, help="realizations per rank (default: config)")
+    ap.add_argument("--M", type=int, default=None, help="realizations (per rank for weak-scaling configs)")
     ap.add_argument("--sweeps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-realizations", type=int, default=4)
-    ap.add_argument("--ref-sample-realizations", type=int, default=2)
+    ap.add_argument("--cpu-sample-realizations", type=int, default=8)
+    ap.add_argument("--ref-sample-realizations", type=int, default=8)
+    ap.add_argument("--cpu-threads", type=int, default=0, help="oracle threads (0 = all host cores)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 row-slab sub-record")
+    ap.add_argument("--c4-steps", type=int, default=3)
     ap.add_argument("--reduce", default="allreduce", choices=["allreduce", "ordered"],
-                    help="realization sharding at N > 1: one NCCL all-reduce of the accumulators, or the "
+                    help="realization shards at N > 1: one NCCL all-reduce of the accumulators, or the "
                          "ordered chain (bit-identical to one GPU)")
-    ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
-                    help="row slabs at N > 1: the sweep kernel writes the boundary rows into the "
-                         "neighbours' IPC-mapped state buffers (peer), or NCCL send/recv (nccl)")
-    ap.add_argument("--decomp", default="realizations", choices=["realizations", "rows"],
-                    help="multi-GPU split: realization shards (weak scaling, default) or row slabs "
-                         "with one-row halos (strong scaling)")
+    ap.add_argument("--decomp", default=None, choices=["realizations", "rows"],
+                    help="multi-GPU split of the headline line (default: rows for C4, realizations otherwise)")
     return ap.parse_args()
 
 
@@ -73,22 +80,49 @@ def dist_env():
     return ws, rank, local
 
 
-def workload(cfg_name, args):
+def load_problem(cfg_name):
+    """The config's synthetic problem; C3/C4 are cached as .npy under /tmp (generation of
+    the 16384^2 field takes ~1 min on the host)."""
     c = dict(CONFIGS[cfg_name])
-    M = args.M or c["M"]
-    S = args.sweeps or c["sweeps"]
+    cache = os.path.join("/tmp", "mpr_inputs")
+    path = os.path.join(cache, f"{cfg_name}_{c['L']}_{c['p']}_{c['gaps']}_{c['nu']}.npz")
+    if c["L"] >= 4096 and os.path.exists(path):
+        d = np.load(path)
+        return c, d["truth"], d["z"], d["mask"]
     truth, z, mask = make_problem(c["L"], c["p"], gaps=c["gaps"], nu=c["nu"])
-    P = int((mask == 0).sum())
-    desc = (f"{cfg_name}: {c['L']}x{c['L']} Whittle-Matern nu={c['nu']} heterogeneous field, "
-            f"{int(round(c['p'] * 100))}% {c['gaps']} gaps, M={M} per rank, S={S} sweeps, "
-            f"SST l_b=32 r_s=2 n_s=5, BLOCK_MEAN init, n_avg=1")
-    return c, M, S, truth, z, mask, P, desc
+    if c["L"] >= 4096:
+        try:
+            os.makedirs(cache, exist_ok=True)
+            tmp = path + f".tmp{os.getpid()}.npz"
+            np.savez(tmp, truth=truth, z=z, mask=mask)
+            os.replace(tmp, path)
+        except OSError:
+            pass
+    return c, truth, z, mask
+
+
+def describe(name, c, M, S, per_rank):
+    return (f"{name}: {c['L']}x{c['L']} Whittle-Matern nu={c['nu']} heterogeneous field, "
+            f"{int(round(c['p'] * 100))}% {c['gaps']} gaps, M={M}{' per rank' if per_rank else ' in total'}, "
+            f"S={S} sweeps, SST l_b=32 r_s=2 n_s=5, BLOCK_MEAN init, n_avg=1")
 
 
 def algorithmic_bytes_per_update(p, n_avg=1, S=30, b_T=4):
     """B_alg = 4/p + 8 + b_T bytes per gap-site update (+ 8 n_avg/S when the
     accumulation is a separate buffer, i.e. n_avg > 1)."""
     return 4.0 / p + 8.0 + b_T + (8.0 * n_avg / S if n_avg > 1 else 0.0)
+
+
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
 
 
 class ClockSampler:
@@ -136,24 +170,31 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def cpu_baseline_sample(z, mask, M_sample, S, c):
-    """Time the CPU oracle, as it stands (single thread), on a bounded sample of the same
-    workload: the full parameter stage + M_sample realizations x S sweeps."""
+def cpu_baseline_sample(z, mask, M_sample, S, c, threads=0):
+    """Time the CPU oracle, as it stands, on a bounded sample of the same workload: the
+    full parameter stage + M_sample realizations x S sweeps, on `threads` host cores (the
+    OpenMP build of the same source: same-colour rows split over threads, bit-identical
+    to the single-thread oracle; 0 = all cores)."""
     import oracle as O
     from paper_2212_01317_b200.binding import load_calibration
     Tk, ek = load_calibration()
     cfg = O.OracleConfig()
-    t0 = time.perf_counter()
-    p = O.parameters(z, mask, cfg, Tk, ek)
-    sim = O.simulate(p, mask, cfg, M_sample, S, SEED_SIM)
-    zin = np.where(mask != 0, z, np.float32(0)).astype(np.float32)
-    O.predict(zin, mask, sim["acc"], M_sample, 1, p.zmin, p.zmax, 0)
-    dt = time.perf_counter() - t0
+    used = O.set_threads(threads)
+    try:
+        t0 = time.perf_counter()
+        p = O.parameters(z, mask, cfg, Tk, ek)
+        sim = O.simulate(p, mask, cfg, M_sample, S, SEED_SIM)
+        zin = np.where(mask != 0, z, np.float32(0)).astype(np.float32)
+        O.predict(zin, mask, sim["acc"], M_sample, 1, p.zmin, p.zmax, 0)
+        dt = time.perf_counter() - t0
+    finally:
+        O.set_threads(1)
     P = int((mask == 0).sum())
     upd = P * S * M_sample
-    return {"value": upd / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+    nproc, model = cpu_info()
+    return {"value": upd / dt, "unit": UNIT, "cores": used, "kind": "oracle", "nproc": nproc, "cpu_model": model,
             "sample": f"{c['L']}x{c['L']} grid, p={c['p']}: full parameter stage + realizations 0..{M_sample - 1} "
-                      f"x {S} sweeps = {upd:.3e} gap-site updates in {dt:.2f} s (single thread, oracle/ as is)",
+                      f"x {S} sweeps = {upd:.3e} gap-site updates in {dt:.2f} s ({used} threads, oracle/ as is)",
             "seconds": dt}
 
 
@@ -161,26 +202,192 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    c, M, S, truth, z, mask, P, desc = workload(args.config, args)
+    c, truth, z, mask = load_problem(args.config)
+    M = args.M or c["M"]
+    S = args.sweeps or c["sweeps"]
+    P = int((mask == 0).sum())
     Ms = max(1, args.ref_sample_realizations)
     for _ in range(args.warmup):
-        cpu_baseline_sample(z, mask, Ms, S, c)
-    times = []
+        cpu_baseline_sample(z, mask, Ms, S, c, args.cpu_threads)
+    times, last = [], None
     for _ in range(args.steps):
-        r = cpu_baseline_sample(z, mask, Ms, S, c)
-        times.append(r["seconds"])
+        last = cpu_baseline_sample(z, mask, Ms, S, c, args.cpu_threads)
+        times.append(last["seconds"])
     total = sum(times)
     value = P * S * Ms * args.steps / total
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": desc, "sample_realizations_per_step": Ms},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "higher_is_better": True, "scaling": SCALING[args.config], "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": describe(args.config, c, M, S, SCALING[args.config] == "weak"),
+                       "sample_realizations_per_step": Ms},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
+                             "nproc": last["nproc"], "cpu_model": last["cpu_model"],
                              "sample": f"per step: parameter stage + {Ms} realizations x {S} sweeps "
-                                       f"({P * S * Ms:.3e} updates), single thread"},
+                                       f"({P * S * Ms:.3e} updates), {last['cores']} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+class Workload:
+    """One config run through libmpr with this rank's communicator: device-resident and
+    end-to-end (pinned host buffers) timings, and the half-sweep kernel's device time."""
+
+    def __init__(self, name, decomp, M, S, comm, ws, rank, local, dev, stream):
+        import torch
+
+        import paper_2212_01317_b200 as Pk
+        self.name, self.decomp, self.S, self.ws, self.rank = name, decomp, S, ws, rank
+        self.c, self.truth, self.z, self.mask = load_problem(name)
+        self.P = int((self.mask == 0).sum())
+        Ly, Lx = self.z.shape
+        self.Ly, self.Lx = Ly, Lx
+        self.M = M
+        self.rows = decomp == "rows"
+        cfg = Pk.Config(device=local, nccl_comm=comm, shard="rows" if self.rows else "realizations",
+                        ordered_reduce=False)
+        self.eng = Pk.LeMpr(cfg, Pk.load_calibration(), stream=stream.cuda_stream)
+        self.Pk, self.torch, self.dev, self.stream = Pk, torch, dev, stream
+        from paper_2212_01317_b200.sharding import row_range
+        self.r0, self.r1 = row_range(Ly, ws, rank) if self.rows else (0, Ly)
+        zs = np.ascontiguousarray(np.nan_to_num(self.z[self.r0:self.r1], nan=0.0))
+        ms = np.ascontiguousarray(self.mask[self.r0:self.r1])
+        # device-resident inputs: the own rows only (row slabs) or the whole grid
+        self.z_dev = torch.from_numpy(zs).to(dev)
+        self.m_dev = torch.from_numpy(ms).to(dev)
+        self.out_dev = torch.empty((Ly, Lx), dtype=torch.float32, device=dev)
+        # pinned host buffers of the e2e leg: the whole grid (the C-ABI copies the own rows)
+        self.z_pin = torch.from_numpy(np.nan_to_num(self.z, nan=0.0)).pin_memory()
+        self.m_pin = torch.from_numpy(self.mask).pin_memory()
+        self.out_pin = torch.empty((self.r1 - self.r0, Lx), dtype=torch.float32).pin_memory()
+        self.lib = Pk.load_library()
+
+    def step_device(self):
+        e = self.eng
+        e.set_data_device(self.z_dev.data_ptr(), self.m_dev.data_ptr(), self.Lx, self.Ly)
+        e.estimate_local_params()
+        e.simulate(self.M, self.S, SEED_SIM)
+        e.predict_device(self.out_dev.data_ptr())
+
+    def step_host(self):
+        e, L, ck = self.eng, self.lib, self.Pk.binding._check
+        ck(e.ctx, L.mpr_set_data(e.ctx, self.z_pin.data_ptr(), self.m_pin.data_ptr(), self.Lx, self.Ly))
+        e.shape = (self.Ly, self.Lx)
+        e.estimate_local_params()
+        e.simulate(self.M, self.S, SEED_SIM)
+        ck(e.ctx, L.mpr_predict_rows(e.ctx, self.out_pin.data_ptr()))  # the own rows
+
+    def updates_per_step(self):
+        return self.P * self.S * self.M
+
+    def h2d_bytes(self):
+        return (self.r1 - self.r0) * self.Lx * 5
+
+    def d2h_bytes(self):
+        return (self.r1 - self.r0) * self.Lx * 4
+
+
+def barrier(dev, ws):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+
+
+def max_over_ranks(x, dev, ws):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def time_workload(w: Workload, steps, warmup, dev, ws, e2e=True, flush=None):
+    """Device-timed steps (CUDA events on the library's stream, max over ranks), the
+    half-sweep kernel's device time, and the e2e wall time through the C-ABI."""
+    import torch
+    for _ in range(max(warmup, 0)):
+        w.step_device()
+    barrier(dev, ws)
+    w.eng.set_kernel_timing(True)
+    launches0 = w.eng.info()["total_launches"]
+    barrier(dev, ws)
+    total_ms = 0.0
+    for _ in range(steps):
+        if flush is not None:
+            flush.fill_(1.0)  # L2 flush between timed steps (256 MiB > 126 MB L2), outside the events
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(w.stream)
+        w.step_device()
+        e1.record(w.stream)
+        e1.synchronize()
+        total_ms += e0.elapsed_time(e1)
+    barrier(dev, ws)
+    info = w.eng.info()
+    w.eng.set_kernel_timing(False)
+    total_ms = max_over_ranks(total_ms, dev, ws)
+    res = {"ms_per_step": total_ms / steps, "launches": info["total_launches"] - launches0,
+           "sweep_ms": info["sweep_ms"], "sweep_launches": info["sweep_launches"], "info": info,
+           "value": w.updates_per_step() * steps / (total_ms / 1000.0)}
+    if e2e:
+        for _ in range(max(warmup, 1)):  # first use of the host-buffer path, untimed
+            w.step_host()
+        barrier(dev, ws)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            w.step_host()
+        barrier(dev, ws)
+        wall = max_over_ranks(time.perf_counter() - t0, dev, ws)
+        res["e2e"] = {"value": w.updates_per_step() * steps / wall, "unit": UNIT,
+                      "h2d_bytes_per_step": int(w.h2d_bytes()), "d2h_bytes_per_step": int(w.d2h_bytes()),
+                      "fill_time_ms": 1000 * wall / steps}
+    return res
+
+
+def sweep_roofline(w: Workload, r, steps, peaks):
+    """The half-sweep kernel (CUDA events on the library's stream around its launches)
+    against the FP32-lane ALU peak, and the SURVEY §8(d) algorithmic-byte view beside it."""
+    info = r["info"]
+    sweep_s = r["sweep_ms"] / 1000.0
+    own_gaps = info["n_gaps"] if not w.rows else int((w.mask[w.r0:w.r1] == 0).sum())
+    m_own = info["m_end"] - info["m_begin"]
+    upd = own_gaps * w.S * m_own * steps
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    b_upd = algorithmic_bytes_per_update(w.c["p"])
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # Gop/s: SMs x FP32 lanes x max SM clock
+    alu = ALG_OPS_PER_UPDATE * upd / sweep_s / 1e9 if sweep_s > 0 else None
+    hbm = b_upd * upd / sweep_s / 1e9 if sweep_s > 0 else None
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "sweep_traffic.json")))
+        if prof.get("config") == w.name:
+            traffic = prof.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    batch = info.get("batch", 0)
+    variant = info.get("sweep_variant", 0)
+    kernel = (f"k_sweep_quad (variant {variant}: two realization pairs per thread)"
+              if variant in (22, 28) and batch % 4 == 0 else f"k_sweep_half (variant {13 if variant in (22, 28) else variant})")
+    return {"bound": "alu", "kernel": kernel, "achieved": alu, "peak": alu_peak, "unit": "Gop/s",
+            "frac": (alu / alu_peak) if alu else None, "traffic": traffic,
+            "algorithmic_ops_per_update": ALG_OPS_PER_UPDATE,
+            "peak_derivation": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (max SM clock)",
+            "sweep_launches_timed": r["sweep_launches"],
+            "sweep_ms_per_launch": r["sweep_ms"] / max(r["sweep_launches"], 1),
+            "sweep_share_of_step": r["sweep_ms"] / max(r["ms_per_step"] * steps, 1e-9),
+            "sweep_updates_per_s": upd / sweep_s if sweep_s > 0 else None,
+            "hbm_view": {"achieved": hbm, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": (hbm / hbm_peak) if hbm else None,
+                         "frac_of_8TBps": (hbm / 8000.0) if hbm else None,
+                         "algorithmic_bytes_per_update": b_upd,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+                         if "hbm_gbs" in peaks else "fallback 6650 GB/s (B200_PROFILING.md)"}}
 
 
 def run_mpr(args):
@@ -188,212 +395,88 @@ def run_mpr(args):
     import torch.distributed as dist
 
     import paper_2212_01317_b200 as Pk
+    from paper_2212_01317_b200.sharding import destroy_nccl_comm, make_nccl_comm
 
     ws, rank, local = dist_env()
     if ws > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    c, M, S, truth, z, mask, P, desc = workload(args.config, args)
-    n = z.size
-    Ly, Lx = z.shape
     stream = torch.cuda.current_stream(dev)
-    calib = Pk.load_calibration()
-    cfg = Pk.Config(device=local)
-    eng = Pk.LeMpr(cfg, calib, stream=stream.cuda_stream)
-    from paper_2212_01317_b200.sharding import (allreduce_accumulator, connect_peer_halo, exchange_halo,
-                                                ordered_reduce_accumulator, row_range, shard_range,
-                                                slab_realization_chunks)
-    ordered = ws > 1 and args.decomp == "realizations" and args.reduce == "ordered"
-    eng.set_deferred_reduce(ordered)
-    rows = args.decomp == "rows"
-    if rows:  # strong scaling: the whole M on every rank, the grid split into row slabs
-        M_glob = M
-        m0, m1 = 0, M
-        r0, r1 = row_range(Ly, ws, rank)
-    else:     # weak scaling: M realizations per rank
-        M_glob = M * ws
-        m0, m1 = shard_range(M_glob, ws, rank)
-
-    # device-resident inputs (the "value" leg) and pinned host buffers (the e2e leg)
-    z_dev = torch.from_numpy(np.nan_to_num(z, nan=0.0)).to(dev)
-    m_dev = torch.from_numpy(mask).to(dev)
-    out_dev = torch.empty((Ly, Lx), dtype=torch.float32, device=dev)
-    z_pin = torch.from_numpy(np.nan_to_num(z, nan=0.0)).pin_memory()
-    m_pin = torch.from_numpy(mask).pin_memory()
-    out_pin = torch.empty((Ly, Lx), dtype=torch.float32).pin_memory()
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-
-    def allreduce_acc():
-        if ordered:
-            ordered_reduce_accumulator(eng, rank, ws)
-        elif ws > 1:
-            allreduce_accumulator(eng.accumulator_tensor())
-
-    def simulate():
-        if not rows:
-            eng.simulate_range(M_glob, S, SEED_SIM, m0, m1)
-            return
-        peer = ws > 1 and args.halo == "peer"
-        for c0, c1 in slab_realization_chunks(M_glob):
-            eng.slab_begin(M_glob, S, SEED_SIM, c0, c1, r0, r1)
-            if peer:
-                connect_peer_halo(eng, rank, ws)
-            for s in range(1, S + 1):
-                for colour in (0, 1):
-                    eng.slab_half_sweep(s, colour)
-                    if peer:  # the kernels wrote the halos into the neighbours' buffers
-                        eng.sync()
-                        dist.barrier()
-                    elif ws > 1:
-                        exchange_halo(eng, colour, r0, r1, rank, ws)
-            eng.slab_end()
-
-    def step_device():
-        eng.set_data_device(z_dev.data_ptr(), m_dev.data_ptr(), Lx, Ly)
-        eng.estimate_local_params()
-        eng.reset_accumulator()
-        simulate()
-        allreduce_acc()
-        eng.predict_device(out_dev.data_ptr())
-
-    def step_host():
-        Pk.binding._check(eng.ctx, Pk.load_library().mpr_set_data(eng.ctx, z_pin.data_ptr(), m_pin.data_ptr(), Lx, Ly))
-        eng.shape = (Ly, Lx)
-        eng.estimate_local_params()
-        eng.reset_accumulator()
-        simulate()
-        allreduce_acc()
-        Pk.binding._check(eng.ctx, Pk.load_library().mpr_predict(eng.ctx, out_pin.data_ptr()))
-
-    def barrier():
-        torch.cuda.synchronize(dev)
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
-    for _ in range(max(args.warmup, 0)):
-        step_device()
-    barrier()
-    eng.set_kernel_timing(True)
-    launches0 = eng.info()["total_launches"]
-    clocks = ClockSampler(local) if not args.no_clocks else None
-    if clocks:
-        clocks.start()
-    barrier()
-    total_ms = 0.0
-    for _ in range(args.steps):
-        flush.fill_(1.0)  # L2 flush between timed steps (256 MiB > 126 MB L2), outside the events
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        step_device()
-        e1.record(stream)
-        e1.synchronize()
-        total_ms += e0.elapsed_time(e1)
-    barrier()
-    info = eng.info()
-    launches = info["total_launches"] - launches0
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    updates_per_step = P * S * M_glob
-    value = updates_per_step * args.steps / (total_ms / 1000.0)
-
-    # dominant kernel: the half-sweep (CUDA events on the library's stream around the sweep loops)
-    sweep_ms, sweep_n = info["sweep_ms"], info["sweep_launches"]
-    P_loc = int((mask[r0:r1] == 0).sum()) if rows else P
-    sweep_updates = P_loc * S * (m1 - m0) * args.steps
-    sweep_s = sweep_ms / 1000.0
-    b_upd = algorithmic_bytes_per_update(c["p"])
+    comm = make_nccl_comm(local) if ws > 1 else None
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    hbm_achieved = b_upd * sweep_updates / sweep_s / 1e9 if sweep_s > 0 else None
-    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e9  # Gop/s: SMs x FP32 lanes x max SM clock
-    alu_achieved = ALG_OPS_PER_UPDATE * sweep_updates / sweep_s / 1e9 if sweep_s > 0 else None
-    traffic = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "sweep_traffic.json")))
-        if prof.get("config") == args.config:
-            traffic = prof.get("dram_bytes_per_launch")
-    except Exception:
-        pass
 
-    # e2e through the public API with pinned host buffers, H2D + D2H inside the timed region
-    e2e = None
-    if not args.no_e2e:
-        for _ in range(max(args.warmup, 1)):  # first use of the host-buffer path, untimed
-            step_host()
-        barrier()
-        w0 = time.perf_counter()
-        for _ in range(args.steps):
-            step_host()
-        barrier()
-        wall = time.perf_counter() - w0
-        tw = torch.tensor([wall], dtype=torch.float64, device=dev)
-        if ws > 1:
-            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
-        wall = float(tw.item())
-        e2e = {"value": updates_per_step * args.steps / wall, "unit": UNIT,
-               "h2d_bytes_per_step": int(n * 4 + n * 1), "d2h_bytes_per_step": int(n * 4),
-               "fill_time_ms": 1000 * wall / args.steps}
+    name = args.config
+    c0 = CONFIGS[name]
+    scaling = SCALING[name]
+    decomp = args.decomp or ("rows" if name == "C4" else "realizations")
+    if decomp == "rows":
+        scaling = "strong"
+    M_arg = args.M or c0["M"]
+    M_glob = M_arg * ws if scaling == "weak" else M_arg
+    S = args.sweeps or c0["sweeps"]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    w = Workload(name, decomp, M_glob, S, comm, ws, rank, local, dev, stream)
+
+    clocks = ClockSampler(local) if not args.no_clocks else None
+    if clocks:
+        clocks.start()
+    r = time_workload(w, args.steps, args.warmup, dev, ws, e2e=not args.no_e2e, flush=flush)
+    roof = sweep_roofline(w, r, args.steps, peaks)
+    c4 = None
+    if not args.no_c4 and name != "C4":
+        del flush
+        w.eng.close()
+        torch.cuda.empty_cache()
+        w4 = Workload("C4", "rows", CONFIGS["C4"]["M"], CONFIGS["C4"]["sweeps"], comm, ws, rank, local, dev, stream)
+        r4 = time_workload(w4, args.c4_steps, args.warmup, dev, ws, e2e=not args.no_e2e)
+        c4 = {"config": {"workload": describe("C4", w4.c, w4.M, w4.S, False), "parallelism": f"row slabs x{ws}",
+                         "rows_per_rank": w4.r1 - w4.r0, "gap_sites": w4.P, "updates_per_step": w4.updates_per_step(),
+                         "input_per_rank": "own rows only (H2D of the slab; device memory holds own rows + 1 ghost "
+                                           "row per side + the r_s n_s temperature halo)"},
+              "steps": args.c4_steps, "warmup": args.warmup, "value": r4["value"], "unit": UNIT,
+              "fill_time_ms": r4["ms_per_step"], "gpu_launches": int(r4["launches"]),
+              "roofline": sweep_roofline(w4, r4, args.c4_steps, peaks), "target": "< 1000 ms end to end on 8 B200"}
+        if "e2e" in r4:
+            c4["e2e"] = r4["e2e"]
+        w4.eng.close()
+    else:
+        w.eng.close()
     ck = clocks.stop() if clocks else None
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "strong" if rows else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": desc, "L": c["L"], "p": c["p"], "gaps": c["gaps"], "gap_sites": P,
-                           "M_per_rank": M, "M_total": M_glob, "sweeps": S,
-                           "updates_per_step": updates_per_step, "parallelism": (f"row slabs x{ws}" + (f", {args.halo} halo" if ws > 1 else "")) if rows
-                           else f"realizations x{ws}" + (f", {args.reduce} reduce" if ws > 1 else ""),
+        line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+                "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": describe(name, w.c, M_arg, S, scaling == "weak"), "L": w.c["L"], "p": w.c["p"],
+                           "gaps": w.c["gaps"], "gap_sites": w.P, "M_per_rank": M_arg if scaling == "weak" else None,
+                           "M_total": M_glob, "sweeps": S, "updates_per_step": w.updates_per_step(),
+                           "parallelism": (f"row slabs x{ws}" if decomp == "rows" else f"realizations x{ws}")
+                           + (" (libmpr + NCCL)" if ws > 1 else ""),
                            "l2": "flushed between timed steps (256 MiB write, outside the events)"},
-                "fill_time_ms": total_ms / args.steps,
-                "gpu_launches": int(launches),
-                "roofline": {"bound": "alu", "kernel": sweep_kernel_name(info.get("sweep_variant", 0),
-                                                               (lambda c: c[1] - c[0])(slab_realization_chunks(M_glob)[0])
-                                                               if rows else info.get("batch", 0)),
-                             "achieved": alu_achieved,
-                             "peak": alu_peak, "unit": "Gop/s",
-                             "frac": (alu_achieved / alu_peak) if alu_achieved else None,
-                             "traffic": traffic,
-                             "algorithmic_ops_per_update": ALG_OPS_PER_UPDATE,
-                             "peak_derivation": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (max SM clock)",
-                             "sweep_launches_timed": sweep_n, "sweep_ms_per_launch": sweep_ms / max(sweep_n, 1),
-                             "sweep_share_of_step": sweep_ms / max(total_ms, 1e-9),
-                             "sweep_updates_per_s": sweep_updates / sweep_s if sweep_s > 0 else None,
-                             "hbm_view": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
-                                          "frac": (hbm_achieved / hbm_peak) if hbm_achieved else None,
-                                          "frac_of_8TBps": (hbm_achieved / 8000.0) if hbm_achieved else None,
-                                          "algorithmic_bytes_per_update": b_upd,
-                                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"
-                                          if "hbm_gbs" in peaks else "fallback 6650 GB/s (B200_PROFILING.md)"}},
+                "fill_time_ms": r["ms_per_step"],
+                "gpu_launches": int(r["launches"]),
+                "roofline": roof,
                 "clocks": ck}
-        if e2e:
-            line["e2e"] = e2e
+        if "e2e" in r:
+            line["e2e"] = r["e2e"]
+        if c4 is not None:
+            line["c4_rows"] = c4
         if not args.no_cpu_baseline and ws == 1:
-            line["cpu_baseline"] = {k: v for k, v in cpu_baseline_sample(z, mask, args.cpu_sample_realizations, S,
-                                                                          c).items() if k != "seconds"}
+            line["cpu_baseline"] = {k: v for k, v in cpu_baseline_sample(w.z, w.mask, args.cpu_sample_realizations, S,
+                                                                          w.c, args.cpu_threads).items()
+                                    if k != "seconds"}
         print(json.dumps(line), flush=True)
-    eng.close()
+    if comm:
+        destroy_nccl_comm(comm)
     if ws > 1:
         dist.destroy_process_group()
     return 0
-
-
-def sweep_kernel_name(variant, batch):
-    """Name of the half-sweep kernel the library launched (mpr_info.sweep_variant and the
-    realization batch: the quad kernel needs an even pair count)."""
-    if variant in (22, 28) and batch % 4 == 0:
-        return f"k_sweep_quad (variant {variant}: two realization pairs per thread)"
-    return f"k_sweep_half (variant {13 if variant in (22, 28) else variant})"
 
 
 def main():

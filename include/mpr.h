@@ -41,6 +41,7 @@ extern "C" {
 #endif
 
 typedef struct mpr_ctx mpr_ctx;
+typedef struct mpr_group mpr_group;  /* in-process communicator (mpr_group_create)      */
 
 typedef enum {
   MPR_OK = 0,
@@ -49,10 +50,33 @@ typedef enum {
   MPR_ERR_TOO_FEW_SAMPLES = 3,  /* fewer than 2 known sites                          */
   MPR_ERR_NO_SAMPLE_BONDS = 4,  /* no block has a sample-sample bond  */
   MPR_ERR_CUDA = 5,             /* a CUDA runtime error; message in mpr_last_error   */
-  MPR_ERR_OOM = 6               /* device allocation failed                          */
+  MPR_ERR_OOM = 6,              /* device allocation failed                          */
+  MPR_ERR_NCCL = 7              /* an NCCL call failed (or libnccl.so.2 is missing)  */
 } mpr_status;
 
 typedef enum { MPR_INIT_BLOCK_MEAN = 0, MPR_INIT_RANDOM = 1 } mpr_init_mode;
+
+/* How a multi-rank context splits the work (the paper itself is single-GPU,
+ * PAPER.md:192). With a communicator (nccl_comm or group) every rank makes the same calls
+ * with the same arguments (SPMD):
+ *  MPR_SHARD_REALIZATIONS: every rank holds the whole problem and computes the (exact,
+ *    deterministic) parameter stage itself; mpr_simulate runs the rank's contiguous,
+ *    pair-aligned range of the global realization ids (rank w of W: pairs
+ *    [w*ceil(M/2)/W, (w+1)*ceil(M/2)/W)) and sums the fp64 accumulators with one
+ *    all-reduce (or the rank-ordered chain when ordered_reduce = 1: bit-identical to one
+ *    GPU). Weak or strong scaling over independent chains.
+ *  MPR_SHARD_ROWS: the grid is split into row slabs, rank w owning rows
+ *    [w*Ly/W, (w+1)*Ly/W); a rank's device memory holds only its rows plus one ghost row
+ *    per side (and max(r_s*n_s, 1) rows of temperature halo), so grids larger than one
+ *    GPU fit. The parameter stage is distributed and exact: (z_min, z_max) and counts by
+ *    all-reduce, the ghost rows of z / mask by neighbour exchange (cross-slab bonds), the
+ *    block sums (ARITH §E, exact int64) by all-reduce so every rank holds every T_b and
+ *    takes the same lower median, the smoothing halo recomputed locally from T_b. Every
+ *    colour half-sweep is followed by the exchange of the colour's boundary-row states
+ *    with the two neighbours (stream ordered with NCCL: no host synchronisation). The
+ *    chains are bit-identical to one GPU (global (site, sweep, realization) Philox
+ *    counters). */
+typedef enum { MPR_SHARD_REALIZATIONS = 0, MPR_SHARD_ROWS = 1 } mpr_shard;
 
 typedef struct {
   int device;        /* CUDA device ordinal                                           */
@@ -71,6 +95,19 @@ typedef struct {
   int calib_n;           /* K >= 2                                                     */
   int64_t max_batch;     /* max realizations simulated concurrently (0 => automatic)  */
   int order;             /* mpr_order: update order of a sweep (ARITH §H)              */
+  /* ---- multi-rank; all zero => one GPU ---------------------- */
+  void *nccl_comm;       /* ncclComm_t of this rank (made with mpr_nccl_comm_init, so it
+                            belongs to the process's libnccl.so.2); not owned. Its device
+                            must be cfg.device. NULL => no NCCL                          */
+  mpr_group *group;      /* in-process communicator instead of NCCL (W contexts of one
+                            process, each driven by its own host thread; host-synchronous
+                            collectives); exclusive with nccl_comm                       */
+  int group_rank;        /* this context's rank in `group`                               */
+  int shard;             /* mpr_shard                                                    */
+  int ordered_reduce;    /* MPR_SHARD_REALIZATIONS: 1 => the accumulator travels rank 0 ->
+                            W-1, each adding its realizations in ascending order, then a
+                            broadcast: bit-identical to one GPU (the realization shard must
+                            fit one launch batch)                                        */
 } mpr_config;
 
 /* MPR_ORDER_SC: single checkerboard, colour A then B.
@@ -83,6 +120,23 @@ typedef enum { MPR_ORDER_SC = 0, MPR_ORDER_DC = 1 } mpr_order;
  * them; the Python binding loads the shipped table). */
 void mpr_config_default(mpr_config *cfg);
 
+/* ---- communicators ----------------------------------------------------------------
+ * NCCL (one process per GPU): rank 0 calls mpr_nccl_unique_id, the id (128 bytes) is sent
+ * to every rank out of band (e.g. a torch.distributed broadcast), and each rank calls
+ * mpr_nccl_comm_init with its device. libnccl.so.2 is resolved at run time (the copy the
+ * process already loaded, if any); without it these calls return MPR_ERR_NCCL. The
+ * communicator outlives every context that uses it; release with mpr_nccl_comm_destroy.
+ * In-process group: mpr_group_create(W) once, then W contexts with cfg.group = g and
+ * cfg.group_rank = 0..W-1, each driven by its own host thread (a rank blocks in a
+ * collective until all W have arrived; 600 s timeout, MPR_GROUP_TIMEOUT_S). Destroy the
+ * group after its contexts. */
+#define MPR_NCCL_UNIQUE_ID_BYTES 128
+mpr_status mpr_nccl_unique_id(void *id_out);
+mpr_status mpr_nccl_comm_init(int world, int rank, const void *id, int device, void **comm_out);
+mpr_status mpr_nccl_comm_destroy(void *comm);
+mpr_status mpr_group_create(int world, mpr_group **out);
+void mpr_group_destroy(mpr_group *g);
+
 /* Create a context on cfg->device. Validates cfg (INVALID_ARG) and copies the table.
  * Ownership of *out passes to the caller; release with mpr_destroy. */
 mpr_status mpr_init(const mpr_config *cfg, mpr_ctx **out);
@@ -93,7 +147,9 @@ void mpr_destroy(mpr_ctx *ctx);
 /* One-line description of the last failure on ctx ("" if none). Owned by ctx. */
 const char *mpr_last_error(const mpr_ctx *ctx);
 
-/* Stage a problem: grid (float32, Lx*Ly) and mask (uint8, Lx*Ly), host memory.
+/* Stage a problem: grid (float32, Lx*Ly) and mask (uint8, Lx*Ly), host memory: the WHOLE
+ * grid on every rank (SPMD); with MPR_SHARD_ROWS a rank copies only its own rows to the
+ * device and receives its ghost rows from the neighbouring ranks.
  * Computes z_min/z_max over the samples and the spin angles phi = 2pi(z - z_min)/
  * (z_max - z_min) at the samples (ARITH §D), and builds the gap-site
  * index. Errors: Lx < 2 or Ly < 2 or Lx*Ly > 2^30 (the bound under which every int64
@@ -104,9 +160,11 @@ const char *mpr_last_error(const mpr_ctx *ctx);
 mpr_status mpr_set_data(mpr_ctx *ctx, const float *grid, const uint8_t *mask, int64_t Lx, int64_t Ly);
 
 /* Same as mpr_set_data with device pointers (a device-to-device copy into the context).
- * Both calls return once the inputs are copied and the sample counts are known; the
- * gap-site index is still being built on the context stream (later calls are ordered
- * after it). */
+ * With MPR_SHARD_ROWS the pointers hold the rank's OWN rows only ((row_end - row_begin)
+ * x Lx, rows as in mpr_info), so no device ever holds the whole grid. Lx, Ly are the
+ * global sizes. Both calls return once the inputs are copied and the sample counts are
+ * known; the gap-site index may still be building on the context stream (later calls
+ * are ordered after it). */
 mpr_status mpr_set_data_device(mpr_ctx *ctx, const float *grid_dev, const uint8_t *mask_dev,
                                int64_t Lx, int64_t Ly);
 
@@ -114,7 +172,8 @@ mpr_status mpr_set_data_device(mpr_ctx *ctx, const float *grid_dev, const uint8_
  * block; a bond belongs to the block of its left/top end), block temperatures by
  * energy matching (table inversion), the lower-median fallback for blocks without
  * sample bonds, expansion to sites and n_s smoothing passes of radius r_s.
- * T_out (nullable, host, Lx*Ly floats) receives the per-site temperature field.
+ * T_out (nullable, host, Lx*Ly floats) receives the per-site temperature field (with
+ * MPR_SHARD_ROWS: the rank's own rows, written at their offsets; other rows untouched).
  * Errors: NO_SAMPLE_BONDS when no block has a sample-sample bond. */
 mpr_status mpr_estimate_local_params(mpr_ctx *ctx, float *T_out);
 
@@ -122,7 +181,8 @@ mpr_status mpr_estimate_local_params(mpr_ctx *ctx, float *T_out);
  * m = 0..M-1 (global ids), each initialised (BLOCK_MEAN or RANDOM) and swept
  * `sweeps` times (colour A = (r+c) even, then B) with the Philox stream keyed by
  * `seed`; the last n_avg sweeps of every realization are accumulated for the
- * conditional mean. Replaces any previous accumulation. Errors: M < 1, sweeps < 1,
+ * conditional mean. Replaces any previous accumulation. Multi-rank: see mpr_shard (the
+ * reduction over ranks happens inside this call). Errors: M < 1, sweeps < 1,
  * n_avg > sweeps -> INVALID_ARG. */
 mpr_status mpr_simulate(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed);
 
@@ -182,68 +242,18 @@ mpr_status mpr_accumulate_states(mpr_ctx *ctx);
  * pointer stays owned by ctx and valid until the next set_data/destroy. */
 mpr_status mpr_accumulator_device(mpr_ctx *ctx, double **acc_dev, int64_t *n);
 
-/* Row-slab decomposition (for grids split over GPUs by rows). Every
- * rank holds the whole problem (set_data + estimate_local_params are deterministic and
- * bit-exact, so each rank computes them itself) but updates only the gap sites of its
- * rows [row_begin, row_end). After each half-sweep the caller exchanges halo rows:
- * the colour-c states of the first and last own rows go to the neighbouring ranks,
- * whose ghost rows (row_begin-1, row_end) are overwritten in place through
- * mpr_slab_row_states. Because random numbers are keyed by global (site, sweep,
- * realization), the chains are bit-identical to a single-GPU mpr_simulate.
- *   mpr_slab_begin     : realizations [m_begin, m_end) (one batch, <= 1024), init of
- *                        every gap (a pure function of the ids: ghosts need no exchange)
- *   mpr_slab_half_sweep: sweep s (1-based), colour 0 = A ((r+c) even), 1 = B; own rows
- *   mpr_slab_row_states: device view of the colour-c gap states of one row: *count
- *                        floats, gap-site major, realization minor (send or receive in
- *                        place); valid until slab_end
- *   mpr_slab_end       : adds the own rows' realizations to the accumulator (others
- *                        stay 0, so an all-reduce of the accumulators completes it)
- * Not supported in slab mode: the energy trace (INVALID_ARG). Launches are stream
- * ordered; mpr_sync waits for the context stream. */
-mpr_status mpr_slab_begin(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed, int64_t m_begin,
-                          int64_t m_end, int64_t row_begin, int64_t row_end);
-mpr_status mpr_slab_half_sweep(mpr_ctx *ctx, int32_t sweep, int colour);
-mpr_status mpr_slab_row_states(mpr_ctx *ctx, int64_t row, int colour, float **dev_ptr, int64_t *count);
-
-/* Fused halo exchange over peer memory (the B200-native form of the exchange above).
- *
- * Every rank's state buffer has the same global layout (gap-site major, realization
- * minor, all gap ids of the grid). Between mpr_slab_begin and mpr_slab_end a rank may
- * register the state buffers of its neighbouring slabs. Its half-sweep kernel then also
- * stores every state it changes in its first own row into the upper neighbour's buffer,
- * and in its last own row into the lower neighbour's buffer, at the same offsets. Those
- * are exactly the neighbours' ghost rows, so no exchange call or copy is needed.
- *
- * The caller still orders half-sweeps across ranks: all kernels of half-sweep h must
- * complete before any rank starts h + 1 (for example mpr_sync followed by a
- * process-group barrier). States that are not accepted are not rewritten; the ghost
- * copies agree because initial states are a pure function of the global ids.
- *
- *   mpr_slab_state_ipc_handle: writes the MPR_IPC_HANDLE_BYTES-byte cudaIpcMemHandle_t
- *       of ctx's state buffer to handle_out, for a neighbour in another process.
- *   mpr_slab_state_device: the state buffer's device pointer, for a neighbour in this
- *       process.
- *   mpr_slab_set_peer: side 0 = upper neighbour (rows < row_begin), 1 = lower neighbour
- *       (rows >= row_end). Pass exactly one of:
- *         - ipc_handle: another process's buffer, opened with cudaIpcOpenMemHandle
- *           (lazy peer access over NVLink);
- *         - dev_ptr: device memory of this process. Peer access is enabled if it lives
- *           on another device; INVALID_ARG if that device is not P2P-reachable.
- *       Both NULL clears the side.
- * Registrations end at mpr_slab_end (IPC mappings are closed). A later mpr_slab_begin
- * may reallocate the buffer, so handles and pointers are exchanged again after each
- * mpr_slab_begin. */
-#define MPR_IPC_HANDLE_BYTES 64
-mpr_status mpr_slab_state_ipc_handle(mpr_ctx *ctx, void *handle_out);
-mpr_status mpr_slab_state_device(mpr_ctx *ctx, float **dev_ptr);
-mpr_status mpr_slab_set_peer(mpr_ctx *ctx, int side, const void *ipc_handle, float *dev_ptr);
-mpr_status mpr_slab_end(mpr_ctx *ctx);
+/* Wait for all work queued on the context stream. */
 mpr_status mpr_sync(mpr_ctx *ctx);
 
 /* Predictions (ARITH §I): known sites return the input bitwise, gaps
- * z_min + (z_max - z_min) * mean_phi / 2pi. out: host, Lx*Ly floats, caller-owned. */
+ * z_min + (z_max - z_min) * mean_phi / 2pi. out: host, Lx*Ly floats, caller-owned; every
+ * rank receives the whole grid (MPR_SHARD_ROWS: the slabs' rows are all-gathered).
+ * mpr_predict_device: the same into device memory (Lx*Ly floats). mpr_predict_rows: the
+ * rank's own rows only (MPR_SHARD_ROWS: (row_end - row_begin) x Lx floats, host; the
+ * whole grid otherwise): no rank ever holds the whole prediction. */
 mpr_status mpr_predict(mpr_ctx *ctx, float *out);
 mpr_status mpr_predict_device(mpr_ctx *ctx, float *out_dev);
+mpr_status mpr_predict_rows(mpr_ctx *ctx, float *out_rows);
 
 /* ---- diagnostics / test hooks -------------------------------------------- */
 typedef struct {
@@ -268,10 +278,19 @@ typedef struct {
                                                     (MPR_SWEEP_VARIANT; 28 default:
                                                     two realization pairs per thread,
                                                     13 for odd pair counts)         */
+  int32_t rank, world, shard;                    /* multi-rank layout                */
+  int64_t row_begin, row_end;                    /* own rows (whole grid unless
+                                                    MPR_SHARD_ROWS)                 */
+  int64_t m_begin, m_end;                        /* own realizations of the last
+                                                    simulate call                   */
+  int64_t n_gaps_local;                          /* gap sites held by this rank
+                                                    (own + ghost rows)              */
+  int64_t comm_calls;                            /* collectives issued since init    */
 } mpr_info;
 mpr_status mpr_get_info(mpr_ctx *ctx, mpr_info *info);
 
-/* Buffers for tests: */
+/* Buffers for tests (with MPR_SHARD_ROWS the Lx*Ly buffers get the rank's own rows at
+ * their offsets, other rows untouched; the block buffers and the energy are global): */
 typedef enum {
   MPR_BUF_PHI_KNOWN = 0,  /* float, Lx*Ly: angles at samples, 0 at gaps          */
   MPR_BUF_T = 1,          /* float, Lx*Ly: temperature field                      */

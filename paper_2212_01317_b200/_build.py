@@ -8,8 +8,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmpr.so")
-SOURCES = ["api.cu", "params.cu", "sweep.cu", "calib.cu"]
-HEADERS = ["device_math.cuh", "internal.cuh"]
+SOURCES = ["api.cu", "params.cu", "sweep.cu", "calib.cu", "comm.cu"]
+HEADERS = ["device_math.cuh", "internal.cuh", "comm.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
             logs = list(ex.map(_run, cmds))
         tmp = LIB + f".tmp{os.getpid()}"
-        logs.append(_run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]))
+        logs.append(_run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-ldl", "-lpthread"]))
     if verbose:
         print("\n".join(logs))
     os.replace(tmp, LIB)

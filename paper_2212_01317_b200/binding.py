@@ -17,10 +17,12 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MPR_LIB", os.path.join(_PKG, "libmpr.so"))
 
 MPR_OK, MPR_ERR_INVALID_ARG, MPR_ERR_STATE, MPR_ERR_TOO_FEW_SAMPLES, MPR_ERR_NO_SAMPLE_BONDS, \
-    MPR_ERR_CUDA, MPR_ERR_OOM = range(7)
+    MPR_ERR_CUDA, MPR_ERR_OOM, MPR_ERR_NCCL = range(8)
 STATUS_NAMES = {0: "MPR_OK", 1: "MPR_ERR_INVALID_ARG", 2: "MPR_ERR_STATE", 3: "MPR_ERR_TOO_FEW_SAMPLES",
-                4: "MPR_ERR_NO_SAMPLE_BONDS", 5: "MPR_ERR_CUDA", 6: "MPR_ERR_OOM"}
+                4: "MPR_ERR_NO_SAMPLE_BONDS", 5: "MPR_ERR_CUDA", 6: "MPR_ERR_OOM", 7: "MPR_ERR_NCCL"}
 MPR_INIT_BLOCK_MEAN, MPR_INIT_RANDOM = 0, 1
+MPR_SHARD_REALIZATIONS, MPR_SHARD_ROWS = 0, 1
+MPR_NCCL_UNIQUE_ID_BYTES = 128
 (MPR_BUF_PHI_KNOWN, MPR_BUF_T, MPR_BUF_BLOCK_T, MPR_BUF_BLOCK_STATS, MPR_BUF_STATE, MPR_BUF_ACC,
  MPR_BUF_ENERGY) = range(7)
 
@@ -29,10 +31,9 @@ EXPORTED = ["mpr_config_default", "mpr_init", "mpr_destroy", "mpr_last_error", "
             "mpr_set_data_device", "mpr_estimate_local_params", "mpr_simulate", "mpr_reset_accumulator",
             "mpr_simulate_range", "mpr_accumulator_device", "mpr_predict", "mpr_predict_device",
             "mpr_get_info", "mpr_debug_get", "mpr_set_energy_trace", "mpr_set_kernel_timing", "mpr_version",
-            "mpr_slab_begin", "mpr_slab_half_sweep", "mpr_slab_row_states", "mpr_slab_end", "mpr_sync",
-            "mpr_slab_state_ipc_handle", "mpr_slab_state_device", "mpr_slab_set_peer",
-            "mpr_set_deferred_reduce", "mpr_accumulate_states",
-            "mpr_simulate_adaptive", "mpr_build_calibration"]
+            "mpr_sync", "mpr_predict_rows", "mpr_set_deferred_reduce", "mpr_accumulate_states",
+            "mpr_simulate_adaptive", "mpr_build_calibration", "mpr_nccl_unique_id", "mpr_nccl_comm_init",
+            "mpr_nccl_comm_destroy", "mpr_group_create", "mpr_group_destroy"]
 
 
 class MprError(RuntimeError):
@@ -45,7 +46,9 @@ class mpr_config(C.Structure):
     _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("J", C.c_float), ("q", C.c_float),
                 ("l_b", C.c_int), ("r_s", C.c_int), ("n_s", C.c_int), ("init", C.c_int),
                 ("n_avg", C.c_int), ("calib_T", C.POINTER(C.c_float)), ("calib_e", C.POINTER(C.c_float)),
-                ("calib_n", C.c_int), ("max_batch", C.c_int64), ("order", C.c_int)]
+                ("calib_n", C.c_int), ("max_batch", C.c_int64), ("order", C.c_int),
+                ("nccl_comm", C.c_void_p), ("group", C.c_void_p), ("group_rank", C.c_int), ("shard", C.c_int),
+                ("ordered_reduce", C.c_int)]
 
 
 class mpr_info(C.Structure):
@@ -55,7 +58,9 @@ class mpr_info(C.Structure):
                 ("median_T", C.c_float), ("M", C.c_int64), ("sweeps", C.c_int64), ("batch", C.c_int64),
                 ("kernel_launches", C.c_int64), ("total_launches", C.c_int64), ("sweep_launches", C.c_int64),
                 ("sweep_ms", C.c_double), ("last_m_base", C.c_int64), ("last_batch", C.c_int64),
-                ("sweep_variant", C.c_int32)]
+                ("sweep_variant", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("shard", C.c_int32),
+                ("row_begin", C.c_int64), ("row_end", C.c_int64), ("m_begin", C.c_int64), ("m_end", C.c_int64),
+                ("n_gaps_local", C.c_int64), ("comm_calls", C.c_int64)]
 
 
 _lib = None
@@ -88,17 +93,16 @@ def load_library(path: str = LIB_PATH):
     L.mpr_debug_get.argtypes = [vp, C.c_int, i64, vp]; L.mpr_debug_get.restype = C.c_int
     L.mpr_set_energy_trace.argtypes = [vp, C.c_int]; L.mpr_set_energy_trace.restype = C.c_int
     L.mpr_set_kernel_timing.argtypes = [vp, C.c_int]; L.mpr_set_kernel_timing.restype = C.c_int
-    L.mpr_slab_begin.argtypes = [vp, i64, i32, u64, i64, i64, i64, i64]; L.mpr_slab_begin.restype = C.c_int
-    L.mpr_slab_half_sweep.argtypes = [vp, i32, C.c_int]; L.mpr_slab_half_sweep.restype = C.c_int
-    L.mpr_slab_row_states.argtypes = [vp, i64, C.c_int, C.POINTER(vp), C.POINTER(i64)]
-    L.mpr_slab_row_states.restype = C.c_int
-    L.mpr_slab_state_ipc_handle.argtypes = [vp, vp]; L.mpr_slab_state_ipc_handle.restype = C.c_int
-    L.mpr_slab_state_device.argtypes = [vp, C.POINTER(vp)]; L.mpr_slab_state_device.restype = C.c_int
-    L.mpr_slab_set_peer.argtypes = [vp, C.c_int, vp, vp]; L.mpr_slab_set_peer.restype = C.c_int
     L.mpr_set_deferred_reduce.argtypes = [vp, C.c_int]; L.mpr_set_deferred_reduce.restype = C.c_int
     L.mpr_accumulate_states.argtypes = [vp]; L.mpr_accumulate_states.restype = C.c_int
-    L.mpr_slab_end.argtypes = [vp]; L.mpr_slab_end.restype = C.c_int
     L.mpr_sync.argtypes = [vp]; L.mpr_sync.restype = C.c_int
+    L.mpr_predict_rows.argtypes = [vp, vp]; L.mpr_predict_rows.restype = C.c_int
+    L.mpr_nccl_unique_id.argtypes = [vp]; L.mpr_nccl_unique_id.restype = C.c_int
+    L.mpr_nccl_comm_init.argtypes = [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]
+    L.mpr_nccl_comm_init.restype = C.c_int
+    L.mpr_nccl_comm_destroy.argtypes = [vp]; L.mpr_nccl_comm_destroy.restype = C.c_int
+    L.mpr_group_create.argtypes = [C.c_int, C.POINTER(vp)]; L.mpr_group_create.restype = C.c_int
+    L.mpr_group_destroy.argtypes = [vp]; L.mpr_group_destroy.restype = None
     L.mpr_simulate_adaptive.argtypes = [vp, i64, u64, i32, i32, i32, C.c_double, vp]
     L.mpr_simulate_adaptive.restype = C.c_int
     L.mpr_build_calibration.argtypes = [vp, vp, i32, i32, C.c_float, i32, i32, i32, u64, vp, vp]
@@ -147,8 +151,8 @@ def mpr_set_data_device(ctx, grid_ptr: int, mask_ptr: int, Lx: int, Ly: int) -> 
 
 
 def mpr_estimate_local_params(ctx, want_T: bool = False, shape=None):
-    if want_T:
-        T = np.empty(shape, np.float32)
+    if want_T:  # row slabs write their own rows only: the rest stays NaN
+        T = np.full(shape, np.nan, np.float32)
         _check(ctx, load_library().mpr_estimate_local_params(ctx, T.ctypes.data))
         return T
     _check(ctx, load_library().mpr_estimate_local_params(ctx, None))
@@ -202,20 +206,6 @@ def mpr_set_kernel_timing(ctx, enable: bool) -> None:
     _check(ctx, load_library().mpr_set_kernel_timing(ctx, 1 if enable else 0))
 
 
-def mpr_slab_begin(ctx, M, sweeps, seed, m_begin, m_end, row_begin, row_end) -> None:
-    _check(ctx, load_library().mpr_slab_begin(ctx, M, sweeps, seed, m_begin, m_end, row_begin, row_end))
-
-
-def mpr_slab_half_sweep(ctx, sweep, colour) -> None:
-    _check(ctx, load_library().mpr_slab_half_sweep(ctx, sweep, colour))
-
-
-def mpr_slab_row_states(ctx, row, colour):
-    p, n = C.c_void_p(), C.c_int64()
-    _check(ctx, load_library().mpr_slab_row_states(ctx, row, colour, C.byref(p), C.byref(n)))
-    return p.value, n.value
-
-
 def mpr_set_deferred_reduce(ctx, enable: bool) -> None:
     _check(ctx, load_library().mpr_set_deferred_reduce(ctx, 1 if enable else 0))
 
@@ -224,32 +214,42 @@ def mpr_accumulate_states(ctx) -> None:
     _check(ctx, load_library().mpr_accumulate_states(ctx))
 
 
-MPR_IPC_HANDLE_BYTES = 64
+def mpr_sync(ctx) -> None:
+    _check(ctx, load_library().mpr_sync(ctx))
 
 
-def mpr_slab_state_ipc_handle(ctx) -> bytes:
-    buf = C.create_string_buffer(MPR_IPC_HANDLE_BYTES)
-    _check(ctx, load_library().mpr_slab_state_ipc_handle(ctx, buf))
+def mpr_predict_rows(ctx, rows: int, Lx: int) -> np.ndarray:
+    """The rank's own rows of the prediction ((row_end - row_begin) x Lx)."""
+    out = np.empty((rows, Lx), np.float32)
+    _check(ctx, load_library().mpr_predict_rows(ctx, out.ctypes.data))
+    return out
+
+
+def mpr_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(MPR_NCCL_UNIQUE_ID_BYTES)
+    _check(None, load_library().mpr_nccl_unique_id(buf))
     return buf.raw
 
 
-def mpr_slab_state_device(ctx) -> int:
-    p = C.c_void_p()
-    _check(ctx, load_library().mpr_slab_state_device(ctx, C.byref(p)))
-    return p.value
+def mpr_nccl_comm_init(world: int, rank: int, uid: bytes, device: int) -> int:
+    comm = C.c_void_p()
+    buf = C.create_string_buffer(uid, MPR_NCCL_UNIQUE_ID_BYTES)
+    _check(None, load_library().mpr_nccl_comm_init(world, rank, buf, device, C.byref(comm)))
+    return comm.value
 
 
-def mpr_slab_set_peer(ctx, side, ipc_handle: bytes | None = None, dev_ptr: int | None = None) -> None:
-    h = C.create_string_buffer(ipc_handle, MPR_IPC_HANDLE_BYTES) if ipc_handle is not None else None
-    _check(ctx, load_library().mpr_slab_set_peer(ctx, side, h, dev_ptr))
+def mpr_nccl_comm_destroy(comm: int) -> None:
+    _check(None, load_library().mpr_nccl_comm_destroy(comm))
 
 
-def mpr_slab_end(ctx) -> None:
-    _check(ctx, load_library().mpr_slab_end(ctx))
+def mpr_group_create(world: int) -> int:
+    g = C.c_void_p()
+    _check(None, load_library().mpr_group_create(world, C.byref(g)))
+    return g.value
 
 
-def mpr_sync(ctx) -> None:
-    _check(ctx, load_library().mpr_sync(ctx))
+def mpr_group_destroy(group: int) -> None:
+    load_library().mpr_group_destroy(group)
 
 
 def mpr_build_calibration(ctx, T, L=128, q=0.5, n_eq=400, n_meas=800, reps=2, seed=20221202):
@@ -302,6 +302,14 @@ class Config:
     device: int = 0
     max_batch: int = 0
     order: str = "sc"   # "sc" single checkerboard, "dc" double checkerboard (row f3)
+    # multi-rank (include/mpr.h mpr_shard): a communicator (NCCL comm handle from
+    # mpr_nccl_comm_init, or an in-process group from mpr_group_create + this rank) and
+    # the decomposition "realizations" or "rows"
+    nccl_comm: int | None = None
+    group: int | None = None
+    group_rank: int = 0
+    shard: str = "realizations"
+    ordered_reduce: bool = False
 
 
 class LeMpr:
@@ -318,6 +326,11 @@ class LeMpr:
         c.init = MPR_INIT_BLOCK_MEAN if cfg.init == "block_mean" else MPR_INIT_RANDOM
         c.n_avg, c.max_batch = cfg.n_avg, cfg.max_batch
         c.order = 1 if cfg.order == "dc" else 0
+        c.nccl_comm, c.group, c.group_rank = cfg.nccl_comm, cfg.group, cfg.group_rank
+        if cfg.shard not in ("realizations", "rows"):
+            raise ValueError("shard must be 'realizations' or 'rows'")
+        c.shard = MPR_SHARD_ROWS if cfg.shard == "rows" else MPR_SHARD_REALIZATIONS
+        c.ordered_reduce = 1 if cfg.ordered_reduce else 0
         c.stream = stream
         c.calib_T = self._T.ctypes.data_as(C.POINTER(C.c_float))
         c.calib_e = self._e.ctypes.data_as(C.POINTER(C.c_float))
@@ -368,10 +381,11 @@ class LeMpr:
     def debug(self, which, index=0):
         Ly, Lx = self.shape
         inf = self.info()
+        # Lx*Ly buffers: row slabs fill their own rows only, the rest stays NaN
         if which in (MPR_BUF_PHI_KNOWN, MPR_BUF_T, MPR_BUF_STATE):
-            out = np.empty((Ly, Lx), np.float32)
+            out = np.full((Ly, Lx), np.nan, np.float32)
         elif which == MPR_BUF_ACC:
-            out = np.empty((Ly, Lx), np.float64)
+            out = np.full((Ly, Lx), np.nan, np.float64)
         elif which == MPR_BUF_BLOCK_T:
             out = np.empty(inf["n_blocks"], np.float32)
         elif which == MPR_BUF_BLOCK_STATS:
@@ -409,24 +423,10 @@ class LeMpr:
     def predict_device(self, out_ptr):
         mpr_predict_device(self.ctx, out_ptr)
 
-    # ---- row-slab mode (include/mpr.h mpr_slab_*) ----
-    def slab_begin(self, M, sweeps, seed, m_begin, m_end, row_begin, row_end):
-        mpr_slab_begin(self.ctx, M, sweeps, seed, m_begin, m_end, row_begin, row_end)
-
-    def slab_half_sweep(self, sweep, colour):
-        mpr_slab_half_sweep(self.ctx, sweep, colour)
-
-    def row_view(self, row, colour):
-        """Zero-copy (cuda, float32) view of the colour-`colour` gap states of `row`; the
-        halo exchange sends from / receives into it in place."""
-        ptr, n = mpr_slab_row_states(self.ctx, row, colour)
-        if n == 0:
-            import torch
-            return torch.empty(0, dtype=torch.float32, device=torch.device("cuda", self.cfg.device))
-        return self._device_view(ptr, n, "<f4")
-
-    def commit_row(self, row, colour, tensor):
-        """Received halo rows land in place (row_view is zero-copy): nothing to do."""
+    def predict_rows(self):
+        """The own rows of the prediction (row slabs; the whole grid otherwise)."""
+        inf = self.info()
+        return mpr_predict_rows(self.ctx, inf["row_end"] - inf["row_begin"], self.shape[1])
 
     def set_deferred_reduce(self, enable=True):
         """simulate_range keeps its states; accumulate_states adds them later (ordered
@@ -435,22 +435,6 @@ class LeMpr:
 
     def accumulate_states(self):
         mpr_accumulate_states(self.ctx)
-
-    def state_ipc_handle(self) -> bytes:
-        """cudaIpcMemHandle_t of this slab's state buffer (for a neighbour process)."""
-        return mpr_slab_state_ipc_handle(self.ctx)
-
-    def state_device(self) -> int:
-        """Device pointer of this slab's state buffer (for a neighbour in this process)."""
-        return mpr_slab_state_device(self.ctx)
-
-    def set_peer(self, side, ipc_handle=None, dev_ptr=None):
-        """Register the upper (side 0) / lower (side 1) neighbour's state buffer: the
-        half-sweep kernel then writes the boundary rows into it (fused halo exchange)."""
-        mpr_slab_set_peer(self.ctx, side, ipc_handle, dev_ptr)
-
-    def slab_end(self):
-        mpr_slab_end(self.ctx)
 
     def sync(self):
         mpr_sync(self.ctx)

@@ -1,7 +1,9 @@
 // api.cu — the C-ABI of libmpr.so (include/mpr.h): context state machine, device
-// memory ownership, stage orchestration and the realization-batch loop of the
-// conditional simulation. All arithmetic happens in the kernels of params.cu and
-// sweep.cu; this file only allocates, launches and copies.
+// memory ownership, stage orchestration, the realization-batch loop of the conditional
+// simulation and the multi-rank decompositions of SURVEY §8(e) (realization shards and
+// row slabs, through the Comm transport of comm.cuh). All arithmetic happens in the
+// kernels of params.cu and sweep.cu; this file only allocates, launches, copies and
+// issues collectives.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -10,9 +12,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
+#include "comm.cuh"
 #include "internal.cuh"
 #include "mpr.h"
 
@@ -60,6 +64,8 @@ struct BatchKey {
   // P and PA can have other phase boundaries)
   void* dclist;
   int64_t dc_off[5];
+  // own gap-id ranges per colour (row slabs: a sub-range of the local ids)
+  int64_t own[2][2];
 };
 
 struct GraphEntry {
@@ -67,6 +73,21 @@ struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   int64_t launches = 0;
 };
+
+// Contiguous, pair-aligned realization range of `rank` (one Philox call serves ids 2k and
+// 2k + 1, ARITH §A); the ranges cover [0, M) once and differ by at most one pair.
+void shard_range(int64_t M, int world, int rank, int64_t* m0, int64_t* m1) {
+  const int64_t npairs = (M + 1) / 2;
+  const int64_t p0 = rank * npairs / world, p1 = (rank + 1) * npairs / world;
+  *m0 = std::min<int64_t>(2 * p0, M);
+  *m1 = std::min<int64_t>(2 * p1, M);
+}
+
+// Rows [r0, r1) of row slab `rank`.
+void row_range(int64_t Ly, int world, int rank, int64_t* r0, int64_t* r1) {
+  *r0 = rank * Ly / world;
+  *r1 = (rank + 1) * Ly / world;
+}
 
 }  // namespace
 
@@ -80,17 +101,33 @@ struct mpr_ctx {
   std::string err;
   int sweep_grid = 0;
   int sweep_variant = 28;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
-  // problem
-  int64_t Lx = 0, Ly = 0, n = 0;
-  int64_t P = 0, PA = 0, n_known = 0;
+  // multi-rank
+  std::unique_ptr<Comm> comm;
+  int rank = 0, world = 1;
+  bool rows = false;       // MPR_SHARD_ROWS with world > 1: slab-local layout + halos
+  bool shards = false;     // MPR_SHARD_REALIZATIONS with world > 1: id ranges + reduction
+  int64_t comm_calls = 0;
+  // problem (global)
+  int64_t Lx = 0, Ly = 0;
+  int64_t P_glob = 0, PA_glob = 0, n_known = 0;
   float zmin = 0, zmax = 0;
   int degenerate = 0;
   int64_t nbx = 0, nby = 0, nblocks = 0;
   int64_t n_fallback = 0;
   float median_T = 0;
   long long sum_SB_fx = 0;  // fixed-point bond sum of the known-known bonds (ARITH §J)
+  // this rank's rows: own [row0, row1); local z/mask/phi/gid rows [lrow0, lrow1) (own + one
+  // ghost row per side); local temperature rows [trow0, trow1) (own + the smoothing halo)
+  int64_t row0 = 0, row1 = 0, lrow0 = 0, lrow1 = 0, trow0 = 0, trow1 = 0;
+  int64_t n = 0;            // local sites (lrow1 - lrow0) * Lx
+  int64_t nT = 0;           // local temperature sites
+  // local gap ids: (colour, local row, column) order; P of them, PA of colour A
+  int64_t P = 0, PA = 0;
+  int64_t own[2][2] = {{0, 0}, {0, 0}};      // own gap ids of colour c: [own[c][0], own[c][1])
+  int64_t ghost[2][2][2] = {};               // ghost row side s (0 up, 1 down), colour c: [b, e)
+  int64_t bnd[2][2][2] = {};                 // own boundary row side s (0 first, 1 last), colour c
   // simulation bookkeeping
-  int64_t M_total = 0, sweeps = 0, batch = 0, last_m_base = 0, last_R = 0;
+  int64_t M_total = 0, sweeps = 0, batch = 0, last_m_base = 0, last_R = 0, m_begin = 0, m_end = 0;
   int64_t split_min_P = int64_t(1) << 21;  // choose_batch's 4k + 2 split threshold (MPR_SPLIT_MIN_P)
   int64_t batch_key_P = -1, batch_key_R = -1, batch_cached = 0;
   int64_t launches = 0, total_launches = 0;
@@ -98,9 +135,11 @@ struct mpr_ctx {
   int64_t sweep_launches = 0;
   double sweep_ms = 0.0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> ev_pool;  // row slabs: events around each half-sweep kernel
   cudaEvent_t ev_check = nullptr;  // adaptive protocol: status copy of the last device check
   // CUDA graphs of the per-batch launch sequence (replayed when the key repeats)
   int use_graphs = 1;
+  int slab_graphs = 0;  // MPR_SLAB_GRAPHS: also capture row-slab batches (NCCL halos inside)
   std::vector<GraphEntry> graphs = std::vector<GraphEntry>(8);
   size_t graph_next = 0;
   int energy_enabled = 0;
@@ -109,14 +148,7 @@ struct mpr_ctx {
   int defer_reduce = 0;
   int pending_reduce = 0, pending_Rb = 0, pending_r_lo = 0, pending_r_hi = 0;
   int64_t energy_M = 0, energy_S = 0;
-  // row-slab mode (mpr_slab_*)
-  int slab_active = 0;
-  int64_t slab_row0 = 0, slab_row1 = 0, slab_m0 = 0, slab_m1 = 0, slab_mb = 0;
-  int slab_R = 0, slab_S = 0;
-  uint32_t slab_k0 = 0, slab_k1 = 0;
-  float* slab_peer[2] = {nullptr, nullptr};   // neighbouring slabs' state buffers
-  bool slab_peer_ipc[2] = {false, false};     // opened with cudaIpcOpenMemHandle
-  std::vector<int> rowoff_h;  // host copy of the gap-id row offsets (2*Ly)
+  std::vector<int> rowoff_h, rowcnt_h;  // host copies of the gap-id row offsets (row slabs)
   // device memory
   DBuf z, mask, phiK, scal, calTd, caled, rowcnt, rowoff, gid, rec, bstats, Tb, T, T2, G, A, acc,
       energy, out, tmp, win, dclist, dccnt;
@@ -158,6 +190,14 @@ mpr_status check_launch(mpr_ctx* c, const char* where) {
     ++c->total_launches;                        \
   } while (0)
 
+// A collective through the context's communicator; errors carry the transport's message.
+#define CKC(expr, where)                                                        \
+  do {                                                                          \
+    mpr_status s_ = (expr);                                                     \
+    ++c->comm_calls;                                                            \
+    if (s_ != MPR_OK) return fail(c, s_, std::string(where) + ": " + c->comm->err); \
+  } while (0)
+
 // Makes the context's device current for the duration of a call and restores the caller's
 // current device afterwards (the library must not move e.g. torch's current device).
 struct DeviceGuard {
@@ -177,24 +217,23 @@ struct DeviceGuard {
   DeviceGuard dev_guard_((c)->device);                                   \
   if (dev_guard_.err != cudaSuccess) return cuda_fail(c, dev_guard_.err, "set device")
 
-// Forget a registered neighbour state buffer (row slabs), closing an IPC mapping.
-void clear_peer(mpr_ctx* c, int side) {
-  if (c->slab_peer_ipc[side] && c->slab_peer[side]) cudaIpcCloseMemHandle(c->slab_peer[side]);
-  c->slab_peer[side] = nullptr;
-  c->slab_peer_ipc[side] = false;
-}
-
 mpr_status validate_cfg(const mpr_config* cfg, std::string& why) {
   if (!cfg) { why = "cfg is NULL"; return MPR_ERR_INVALID_ARG; }
   if (!(cfg->J > 0.0f) || !std::isfinite(cfg->J)) { why = "J must be finite and > 0"; return MPR_ERR_INVALID_ARG; }
   if (!(cfg->q > 0.0f && cfg->q <= 0.5f)) { why = "q must be in (0, 1/2]"; return MPR_ERR_INVALID_ARG; }
   if (cfg->l_b < 2) { why = "l_b must be >= 2"; return MPR_ERR_INVALID_ARG; }
   if (cfg->r_s < 0 || cfg->r_s > 16) { why = "r_s must be in [0, 16]"; return MPR_ERR_INVALID_ARG; }
-  if (cfg->n_s < 0) { why = "n_s must be >= 0"; return MPR_ERR_INVALID_ARG; }
+  if (cfg->n_s < 0 || cfg->n_s > 1024) { why = "n_s must be in [0, 1024]"; return MPR_ERR_INVALID_ARG; }
   if (cfg->init != MPR_INIT_BLOCK_MEAN && cfg->init != MPR_INIT_RANDOM) { why = "init must be BLOCK_MEAN or RANDOM"; return MPR_ERR_INVALID_ARG; }
   if (cfg->n_avg < 1) { why = "n_avg must be >= 1"; return MPR_ERR_INVALID_ARG; }
   if (cfg->max_batch < 0) { why = "max_batch must be >= 0"; return MPR_ERR_INVALID_ARG; }
   if (cfg->order != MPR_ORDER_SC && cfg->order != MPR_ORDER_DC) { why = "order must be SC or DC"; return MPR_ERR_INVALID_ARG; }
+  if (cfg->shard != MPR_SHARD_REALIZATIONS && cfg->shard != MPR_SHARD_ROWS) { why = "shard must be REALIZATIONS or ROWS"; return MPR_ERR_INVALID_ARG; }
+  if (cfg->nccl_comm && cfg->group) { why = "nccl_comm and group are exclusive"; return MPR_ERR_INVALID_ARG; }
+  if (cfg->shard == MPR_SHARD_ROWS && cfg->order != MPR_ORDER_SC && (cfg->nccl_comm || cfg->group)) {
+    why = "row slabs need the SC order";
+    return MPR_ERR_INVALID_ARG;
+  }
   if (!cfg->calib_T || !cfg->calib_e || cfg->calib_n < 2 || cfg->calib_n > 256) {
     why = "calibration table must have 2..256 points";
     return MPR_ERR_INVALID_ARG;
@@ -243,7 +282,6 @@ double energy_from_fx(const mpr_ctx* c, long long E_fx) {
   return (-static_cast<double>(E_fx) * 0x1p-32) / nb;
 }
 
-
 // Forget every captured batch graph: their launches bake in buffer pointers and gap-id
 // segments of the problem they were captured for.
 void drop_graphs(mpr_ctx* c) {
@@ -254,35 +292,139 @@ void drop_graphs(mpr_ctx* c) {
   c->graph_next = 0;
 }
 
+// ---- row slabs: neighbour exchange of whole local rows (z / mask halos) -------------
+// Row `r` (global) of a row-major local array with local row 0 = lrow0.
+template <class T>
+T* local_row(const mpr_ctx* c, T* base, int64_t r) {
+  return base + (r - c->lrow0) * c->Lx;
+}
+
+// The first own row goes up (it is the upper neighbour's lower ghost row), the last own
+// row goes down; the ghost rows come back from the neighbours.
+template <class T>
+mpr_status exchange_rows(mpr_ctx* c, T* base, CommType t) {
+  std::vector<P2P> sends, recvs;
+  const size_t cnt = static_cast<size_t>(c->Lx);
+  if (c->rank > 0) {
+    sends.push_back({c->rank - 1, local_row(c, base, c->row0), cnt});
+    recvs.push_back({c->rank - 1, local_row(c, base, c->row0 - 1), cnt});
+  }
+  if (c->rank < c->world - 1) {
+    sends.push_back({c->rank + 1, local_row(c, base, c->row1 - 1), cnt});
+    recvs.push_back({c->rank + 1, local_row(c, base, c->row1), cnt});
+  }
+  CKC(c->comm->exchange(sends, recvs, t, c->stream), "halo rows");
+  return MPR_OK;
+}
+
+// After a colour-`col` half-sweep: the colour's states of the first and last own rows go
+// to the neighbours' ghost rows (gap-site major, realization minor: each row's colour-c
+// states are one contiguous run of R floats per gap). SURVEY §8(e) 2.
+mpr_status exchange_halo(mpr_ctx* c, int col, int R) {
+  std::vector<P2P> sends, recvs;
+  float* G = c->G.as<float>();
+  auto seg = [&](const int64_t (&r)[2]) { return static_cast<size_t>((r[1] - r[0]) * R); };
+  if (c->rank > 0) {
+    sends.push_back({c->rank - 1, G + c->bnd[0][col][0] * R, seg(c->bnd[0][col])});
+    recvs.push_back({c->rank - 1, G + c->ghost[0][col][0] * R, seg(c->ghost[0][col])});
+  }
+  if (c->rank < c->world - 1) {
+    sends.push_back({c->rank + 1, G + c->bnd[1][col][0] * R, seg(c->bnd[1][col])});
+    recvs.push_back({c->rank + 1, G + c->ghost[1][col][0] * R, seg(c->ghost[1][col])});
+  }
+  CKC(c->comm->exchange(sends, recvs, CT_F32, c->stream), "halo exchange");
+  return MPR_OK;
+}
+
+// Own, ghost and boundary gap-id ranges from the host copy of the per-row colour offsets.
+void slab_ranges(mpr_ctx* c) {
+  const int64_t nl = c->lrow1 - c->lrow0;
+  auto off = [&](int col, int64_t r) -> int64_t {  // first id of colour col in global row r
+    const int64_t lr = r - c->lrow0;
+    if (lr >= nl) return col == 0 ? c->PA : c->P;
+    return c->rowoff_h[static_cast<size_t>(col * nl + lr)];
+  };
+  for (int col = 0; col < 2; ++col) {
+    c->own[col][0] = off(col, c->row0);
+    c->own[col][1] = off(col, c->row1);
+    c->ghost[0][col][0] = off(col, c->lrow0);
+    c->ghost[0][col][1] = off(col, c->row0);  // empty when lrow0 == row0
+    c->ghost[1][col][0] = off(col, c->row1);
+    c->ghost[1][col][1] = off(col, c->lrow1);  // empty when lrow1 == row1
+    c->bnd[0][col][0] = off(col, c->row0);
+    c->bnd[0][col][1] = off(col, c->row0 + 1);
+    c->bnd[1][col][0] = off(col, c->row1 - 1);
+    c->bnd[1][col][1] = off(col, c->row1);
+  }
+}
+
 mpr_status stage_data(mpr_ctx* c) {
   cudaStream_t st = c->stream;
   drop_graphs(c);
-  const int64_t n = c->n;
+  if (c->rows) {  // ghost rows of z and mask from the neighbours (cross-slab bonds, sweep)
+    mpr_status s = exchange_rows(c, c->z.as<float>(), CT_F32);
+    if (s != MPR_OK) return s;
+    s = exchange_rows(c, c->mask.as<uint8_t>(), CT_U8);
+    if (s != MPR_OK) return s;
+  }
   set_scalars_init(c->hsc);
   CK(cudaMemcpyAsync(c->scal.p, c->hsc, sizeof(DevScalars), cudaMemcpyHostToDevice, st), "scalars upload");
-  launch_minmax_count(c->z.as<float>(), c->mask.as<uint8_t>(), c->Lx, c->Ly, c->scal.as<DevScalars>(), st);
+  // a1 over the OWN rows (each sample counted by exactly one rank)
+  launch_minmax_count(local_row(c, c->z.as<float>(), c->row0), local_row(c, c->mask.as<uint8_t>(), c->row0), c->Lx,
+                      c->row1 - c->row0, c->row0, c->scal.as<DevScalars>(), st);
   CKL("minmax_count");
+  if (c->rows) {  // global extrema and counts (exact: min/max of keys, integer sums)
+    DevScalars* d = c->scal.as<DevScalars>();
+    CKC(c->comm->allreduce(&d->zmin_key, 1, CT_I32, OP_MIN, st), "allreduce z_min");
+    CKC(c->comm->allreduce(&d->zmax_key, 1, CT_I32, OP_MAX, st), "allreduce z_max");
+    CKC(c->comm->allreduce(&d->bad_sample, 1, CT_I32, OP_MAX, st), "allreduce flags");
+    CKC(c->comm->allreduce(&d->n_known, 3, CT_U64, OP_SUM, st), "allreduce counts");
+  }
   CK(cudaMemcpyAsync(c->hsc, c->scal.p, sizeof(DevScalars), cudaMemcpyDeviceToHost, st), "scalars download");
   CK(cudaStreamSynchronize(st), "minmax_count sync");
   if (c->hsc->bad_sample) return fail(c, MPR_ERR_INVALID_ARG, "non-finite value at a known sample");
   c->n_known = static_cast<int64_t>(c->hsc->n_known);
   if (c->n_known < 2) return fail(c, MPR_ERR_TOO_FEW_SAMPLES, "fewer than 2 known samples");
-  c->PA = static_cast<int64_t>(c->hsc->n_gap[0]);
-  c->P = c->PA + static_cast<int64_t>(c->hsc->n_gap[1]);
+  c->PA_glob = static_cast<int64_t>(c->hsc->n_gap[0]);
+  c->P_glob = c->PA_glob + static_cast<int64_t>(c->hsc->n_gap[1]);
   c->zmin = key_to_float(c->hsc->zmin_key) + 0.0f;
   c->zmax = key_to_float(c->hsc->zmax_key) + 0.0f;
   c->degenerate = (c->zmin == c->zmax);
+  const int64_t n = c->n;
+  const int64_t nl = c->lrow1 - c->lrow0;
   CK(c->phiK.ensure(sizeof(float) * n), "alloc phi");
   launch_transform(c->z.as<float>(), c->mask.as<uint8_t>(), n, c->scal.as<DevScalars>(), c->phiK.as<float>(), st);
   CKL("transform");
   CK(c->gid.ensure(sizeof(int32_t) * n), "alloc gid");
+  CK(c->rowcnt.ensure(sizeof(int) * 2 * nl), "alloc rowcnt");
+  CK(c->rowoff.ensure(sizeof(int) * 2 * nl), "alloc rowoff");
+  if (!c->rows) {
+    c->PA = c->PA_glob;
+    c->P = c->P_glob;
+  } else {  // local ids cover the ghost rows too: count them first
+    launch_gap_rows(c->mask.as<uint8_t>(), c->Lx, nl, c->lrow0, c->rowcnt.as<int>(), c->rowoff.as<int>(), st);
+    c->total_launches += 2;
+    c->rowoff_h.resize(static_cast<size_t>(2 * nl));
+    c->rowcnt_h.resize(static_cast<size_t>(2 * nl));
+    CK(cudaMemcpyAsync(c->rowoff_h.data(), c->rowoff.p, sizeof(int) * 2 * nl, cudaMemcpyDeviceToHost, st), "D2H rowoff");
+    CK(cudaMemcpyAsync(c->rowcnt_h.data(), c->rowcnt.p, sizeof(int) * 2 * nl, cudaMemcpyDeviceToHost, st), "D2H rowcnt");
+    CK(cudaStreamSynchronize(st), "gap rows sync");
+    c->PA = c->rowoff_h[static_cast<size_t>(nl)];
+    c->P = c->rowoff_h[static_cast<size_t>(2 * nl - 1)] + c->rowcnt_h[static_cast<size_t>(2 * nl - 1)];
+  }
   CK(c->rec.ensure(sizeof(GapRec) * std::max<int64_t>(c->P, 1)), "alloc records");
-  CK(c->rowcnt.ensure(sizeof(int) * 2 * c->Ly), "alloc rowcnt");
-  CK(c->rowoff.ensure(sizeof(int) * 2 * c->Ly), "alloc rowoff");
-  launch_gap_index(c->mask.as<uint8_t>(), c->Lx, c->Ly, c->PA, c->rowcnt.as<int>(), c->rowoff.as<int>(),
-                   c->gid.as<int32_t>(), c->rec.as<GapRec>(), st);
-  CKL("gap_index");
-  c->total_launches += 2;  // row counts, scan, compaction
+  if (!c->rows) {
+    launch_gap_index(c->mask.as<uint8_t>(), c->Lx, nl, 0, c->rowcnt.as<int>(), c->rowoff.as<int>(), c->gid.as<int32_t>(),
+                     c->rec.as<GapRec>(), st);
+    c->total_launches += 3;
+    c->own[0][0] = 0; c->own[0][1] = c->PA;
+    c->own[1][0] = c->PA; c->own[1][1] = c->P;
+  } else {
+    launch_gap_compact(c->mask.as<uint8_t>(), c->Lx, nl, c->lrow0, c->rowoff.as<int>(), c->gid.as<int32_t>(),
+                       c->rec.as<GapRec>(), st);
+    CKL("gap_compact");
+    slab_ranges(c);
+  }
   // no final sync: the caller's buffers were copied before the min/max sync above, and
   // the gap-index kernels only touch context buffers (stream-ordered before later calls)
   c->stage = ST_DATA;
@@ -297,13 +439,29 @@ mpr_status check_dims(mpr_ctx* c, int64_t Lx, int64_t Ly) {
   // energy and a one-block SB have < 2^31 bonds of magnitude <= 2^32; SP < 2^30 * 2^31)
   if (Lx > (int64_t(1) << 30) || Ly > (int64_t(1) << 30) || Lx * Ly > (int64_t(1) << 30))
     return fail(c, MPR_ERR_INVALID_ARG, "Lx*Ly must be <= 2^30 (ARITH §E fixed-point bounds)");
+  if (c->rows && Ly < c->world) return fail(c, MPR_ERR_INVALID_ARG, "row slabs need Ly >= world");
   return MPR_OK;
 }
 
+// Geometry of this rank's slab and the local buffers (whole grid unless row slabs).
 mpr_status alloc_inputs(mpr_ctx* c, int64_t Lx, int64_t Ly) {
   c->Lx = Lx;
   c->Ly = Ly;
-  c->n = Lx * Ly;
+  if (c->rows) {
+    row_range(Ly, c->world, c->rank, &c->row0, &c->row1);
+    c->lrow0 = std::max<int64_t>(c->row0 - 1, 0);
+    c->lrow1 = std::min<int64_t>(c->row1 + 1, Ly);
+    // a temperature halo of r_s * n_s rows (at least the ghost row): after n_s passes the
+    // clipped-window error of the halo's inner edge has moved r_s * n_s rows, not into the slab
+    const int64_t H = std::max<int64_t>(static_cast<int64_t>(c->cfg.r_s) * c->cfg.n_s, 1);
+    c->trow0 = std::max<int64_t>(c->row0 - H, 0);
+    c->trow1 = std::min<int64_t>(c->row1 + H, Ly);
+  } else {
+    c->row0 = c->lrow0 = c->trow0 = 0;
+    c->row1 = c->lrow1 = c->trow1 = Ly;
+  }
+  c->n = (c->lrow1 - c->lrow0) * Lx;
+  c->nT = (c->trow1 - c->trow0) * Lx;
   c->stage = ST_INIT;
   CK(c->z.ensure(sizeof(float) * c->n), "alloc z");
   CK(c->mask.ensure(c->n), "alloc mask");
@@ -346,7 +504,7 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
 
 extern "C" {
 
-const char* mpr_version(void) { return "libmpr 0.1 (sm_100a, LE-MPR / SV-MPR arXiv 2212.01317)"; }
+const char* mpr_version(void) { return "libmpr 0.2 (sm_100a, LE-MPR / SV-MPR arXiv 2212.01317)"; }
 
 void mpr_config_default(mpr_config* cfg) {
   if (!cfg) return;
@@ -361,6 +519,7 @@ void mpr_config_default(mpr_config* cfg) {
   cfg->init = MPR_INIT_BLOCK_MEAN;
   cfg->n_avg = 1;
   cfg->max_batch = 0;
+  cfg->shard = MPR_SHARD_REALIZATIONS;
 }
 
 mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
@@ -409,8 +568,27 @@ mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
     mpr_destroy(c);
     return e == cudaErrorMemoryAllocation ? MPR_ERR_OOM : MPR_ERR_CUDA;
   }
+  if (cfg->nccl_comm || cfg->group) {
+    Comm* cm = cfg->nccl_comm ? make_nccl_comm(cfg->nccl_comm, c->device, why)
+                              : make_group_comm(cfg->group, cfg->group_rank, why);
+    if (!cm) {
+      std::fprintf(stderr, "mpr_init: %s\n", why.c_str());
+      mpr_destroy(c);
+      return cfg->nccl_comm ? MPR_ERR_NCCL : MPR_ERR_INVALID_ARG;
+    }
+    c->comm.reset(cm);
+    c->rank = cm->rank;
+    c->world = cm->world;
+  }
+  // MPR_FORCE_COMM=1 (tests): the multi-rank code paths even at world size 1, so that a
+  // single GPU runs the transport's collectives for real
+  const char* fc = std::getenv("MPR_FORCE_COMM");
+  const bool multi = c->comm && (c->world > 1 || (fc && std::atoi(fc)));
+  c->rows = multi && cfg->shard == MPR_SHARD_ROWS;
+  c->shards = multi && cfg->shard == MPR_SHARD_REALIZATIONS;
   if (const char* v = std::getenv("MPR_SWEEP_VARIANT")) c->sweep_variant = std::atoi(v);
   if (const char* v = std::getenv("MPR_NO_GRAPHS")) c->use_graphs = std::atoi(v) ? 0 : 1;
+  if (const char* v = std::getenv("MPR_SLAB_GRAPHS")) c->slab_graphs = std::atoi(v) ? 1 : 0;
   if (const char* v = std::getenv("MPR_SPLIT_MIN_P")) c->split_min_P = std::atoll(v);
   c->sweep_grid = sweep_grid_size(c->device, c->sweep_variant);
   *out = c;
@@ -421,8 +599,6 @@ void mpr_destroy(mpr_ctx* c) {
   if (!c) return;
   DeviceGuard dev_guard(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  clear_peer(c, 0);
-  clear_peer(c, 1);
   DBuf* bufs[] = {&c->z, &c->mask, &c->phiK, &c->scal, &c->calTd, &c->caled, &c->rowcnt, &c->rowoff,
                   &c->gid, &c->rec, &c->bstats, &c->Tb, &c->T, &c->T2, &c->G, &c->A, &c->acc,
                   &c->energy, &c->out, &c->tmp, &c->win, &c->dclist, &c->dccnt};
@@ -432,6 +608,7 @@ void mpr_destroy(mpr_ctx* c) {
     if (e.exec) cudaGraphExecDestroy(e.exec);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
   if (c->ev_check) cudaEventDestroy(c->ev_check);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -447,8 +624,12 @@ mpr_status mpr_set_data(mpr_ctx* c, const float* grid, const uint8_t* mask, int6
   SET_DEVICE(c);
   s = alloc_inputs(c, Lx, Ly);
   if (s != MPR_OK) return s;
-  CK(cudaMemcpyAsync(c->z.p, grid, sizeof(float) * c->n, cudaMemcpyHostToDevice, c->stream), "H2D grid");
-  CK(cudaMemcpyAsync(c->mask.p, mask, c->n, cudaMemcpyHostToDevice, c->stream), "H2D mask");
+  // the own rows only (the whole grid unless row slabs); ghost rows come from the neighbours
+  const int64_t off = c->row0 * Lx, cnt = (c->row1 - c->row0) * Lx;
+  CK(cudaMemcpyAsync(local_row(c, c->z.as<float>(), c->row0), grid + off, sizeof(float) * cnt, cudaMemcpyHostToDevice,
+                     c->stream), "H2D grid");
+  CK(cudaMemcpyAsync(local_row(c, c->mask.as<uint8_t>(), c->row0), mask + off, cnt, cudaMemcpyHostToDevice, c->stream),
+     "H2D mask");
   return stage_data(c);
 }
 
@@ -460,8 +641,12 @@ mpr_status mpr_set_data_device(mpr_ctx* c, const float* grid, const uint8_t* mas
   SET_DEVICE(c);
   s = alloc_inputs(c, Lx, Ly);
   if (s != MPR_OK) return s;
-  CK(cudaMemcpyAsync(c->z.p, grid, sizeof(float) * c->n, cudaMemcpyDeviceToDevice, c->stream), "D2D grid");
-  CK(cudaMemcpyAsync(c->mask.p, mask, c->n, cudaMemcpyDeviceToDevice, c->stream), "D2D mask");
+  // row slabs: the device pointers hold the own rows only
+  const int64_t cnt = (c->row1 - c->row0) * Lx;
+  CK(cudaMemcpyAsync(local_row(c, c->z.as<float>(), c->row0), grid, sizeof(float) * cnt, cudaMemcpyDeviceToDevice,
+                     c->stream), "D2D grid");
+  CK(cudaMemcpyAsync(local_row(c, c->mask.as<uint8_t>(), c->row0), mask, cnt, cudaMemcpyDeviceToDevice, c->stream),
+     "D2D mask");
   return stage_data(c);
 }
 
@@ -477,8 +662,8 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   c->nblocks = c->nbx * c->nby;
   CK(c->bstats.ensure(sizeof(long long) * 4 * c->nblocks), "alloc block stats");
   CK(c->Tb.ensure(sizeof(float) * c->nblocks), "alloc Tb");
-  CK(c->T.ensure(sizeof(float) * c->n), "alloc T");
-  if (c->cfg.n_s > 0) CK(c->T2.ensure(sizeof(float) * c->n), "alloc T2");
+  CK(c->T.ensure(sizeof(float) * c->nT), "alloc T");
+  if (c->cfg.n_s > 0) CK(c->T2.ensure(sizeof(float) * c->nT), "alloc T2");
   long long* SB = c->bstats.as<long long>();
   long long* NB = SB + c->nblocks;
   long long* SP = NB + c->nblocks;
@@ -487,26 +672,33 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   // reset the parameter-stage scalars (n_avail .. median_T)
   const size_t off = offsetof(DevScalars, n_avail);
   CK(cudaMemsetAsync(reinterpret_cast<char*>(dsc) + off, 0, sizeof(DevScalars) - off, st), "reset scalars");
-  launch_block_stats(c->phiK.as<float>(), c->mask.as<uint8_t>(), c->Lx, c->Ly, lb, c->cfg.q, SB, NB, SP, NK,
-                     c->nblocks, st);
+  // a3 over the own rows (a bond belongs to the block of its left/top end: the rank owning
+  // that end counts it; a down bond of the last own row reads the lower ghost row)
+  launch_block_stats(c->phiK.as<float>(), c->mask.as<uint8_t>(), c->Lx, c->Ly, c->lrow0, c->row0, c->row1, lb,
+                     c->cfg.q, SB, NB, SP, NK, c->nblocks, st);
   CKL("block_stats");
+  // row slabs: every rank's partial block sums -> the global ones on every rank (exact int64)
+  if (c->rows) CKC(c->comm->allreduce(SB, static_cast<size_t>(4 * c->nblocks), CT_I64, OP_SUM, st), "allreduce block sums");
   launch_block_T(SB, NB, SP, NK, c->nblocks, c->calTd.as<float>(), c->caled.as<float>(),
                  static_cast<int>(c->calT.size()), c->Tb.as<float>(), dsc, st);
   CKL("block_T");
   launch_median_fill(c->Tb.as<float>(), NB, c->nblocks, dsc, st);
   CKL("median_fill");
-  launch_expand(c->Tb.as<float>(), c->Lx, c->Ly, lb, c->T.as<float>(), st);
+  // a5 on the local temperature rows [trow0, trow1) (the whole grid unless row slabs)
+  launch_expand(c->Tb.as<float>(), c->Lx, c->trow0, c->trow1, lb, c->T.as<float>(), st);
   CKL("expand");
   for (int k = 0; k < c->cfg.n_s; ++k) {
-    launch_smooth(c->T.as<float>(), c->T2.as<float>(), c->Lx, c->Ly, c->cfg.r_s, st);
+    launch_smooth(c->T.as<float>(), c->T2.as<float>(), c->Lx, c->trow1 - c->trow0, c->trow0, c->Ly, c->cfg.r_s, st);
     CKL("smooth");
     std::swap(c->T, c->T2);
   }
-  launch_build_records(c->gid.as<int32_t>(), c->mask.as<uint8_t>(), c->phiK.as<float>(), c->T.as<float>(), SP,
-                       NK, dsc, c->Lx, c->Ly, lb, c->P, c->rec.as<GapRec>(), st);
+  launch_build_records(c->gid.as<int32_t>(), c->mask.as<uint8_t>(), c->phiK.as<float>(), c->T.as<float>(), SP, NK, dsc,
+                       c->Lx, c->Ly, c->lrow0, c->lrow1, c->trow0, c->trow1, lb, c->P, c->rec.as<GapRec>(), st);
   CKL("build_records");
   CK(cudaMemcpyAsync(c->hsc, c->scal.p, sizeof(DevScalars), cudaMemcpyDeviceToHost, st), "scalars download");
-  if (T_out) CK(cudaMemcpyAsync(T_out, c->T.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, st), "D2H T");
+  if (T_out)
+    CK(cudaMemcpyAsync(T_out + c->row0 * c->Lx, c->T.as<float>() + (c->row0 - c->trow0) * c->Lx,
+                       sizeof(float) * (c->row1 - c->row0) * c->Lx, cudaMemcpyDeviceToHost, st), "D2H T");
   CK(cudaStreamSynchronize(st), "estimate_local_params sync");
   c->n_fallback = static_cast<int64_t>(c->hsc->n_fallback);
   c->median_T = c->hsc->median_T;
@@ -564,14 +756,29 @@ mpr_status mpr_reset_accumulator(mpr_ctx* c) {
   return MPR_OK;
 }
 
-// One realization batch: init, 2*S half-sweeps (bracketed by the timing events), and the
-// realization sum into the accumulator. Issued directly or captured into a CUDA graph.
+// Row slabs: the half-sweep kernel's own device time (events around the launch; the
+// batch-level events would also include the halo collectives).
+static mpr_status slab_timing_event(mpr_ctx* c, size_t k, cudaEvent_t* ev) {
+  while (c->ev_pool.size() <= k) {
+    cudaEvent_t e = nullptr;
+    CK(cudaEventCreate(&e), "event");
+    c->ev_pool.push_back(e);
+  }
+  *ev = c->ev_pool[k];
+  return MPR_OK;
+}
+
+// One realization batch: init, 2*S half-sweeps (bracketed by the timing events; row slabs:
+// each followed by the halo exchange of its colour), and the realization sum into the
+// accumulator. Issued directly or captured into a CUDA graph.
 static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bool capturing) {
   // inside a stream capture the timing events must be external record nodes
   const unsigned ev_flags = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
   cudaStream_t st = c->stream;
   const bool avg = k.n_avg > 1;
   const int npairs = k.Rb / 2;
+  // every local gap (ghost rows too: initial states are a pure function of the global ids,
+  // so the ghost rows need no exchange before the first half-sweep)
   launch_init_states(c->rec.as<GapRec>(), c->G.as<float>(), avg ? c->A.as<float>() : nullptr, k.P, k.Rb, npairs,
                      k.pair_base, k.init == MPR_INIT_RANDOM, k.k0, k.k1, st);
   CKL("init_states");
@@ -592,7 +799,9 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
   a.r_valid_hi = k.r_hi;
   a.energy_stride = k.sweeps;
   *nsweep = 0;
-  if (k.timing) CK(cudaEventRecordWithFlags(c->ev0, st, ev_flags), "event record");
+  const bool per_launch_timing = k.timing && c->rows;
+  size_t evk = 0;
+  if (k.timing && !c->rows) CK(cudaEventRecordWithFlags(c->ev0, st, ev_flags), "event record");
   for (int32_t s = 1; s <= k.sweeps; ++s) {
     a.sweep = static_cast<uint32_t>(s);
     a.accumulate = avg && (s > k.sweeps - k.n_avg);
@@ -608,23 +817,45 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
         a.g_count = c->dc_off[ph + 1] - c->dc_off[ph];
       } else {
         a.glist = nullptr;
-        a.g_begin = colour ? k.PA : 0;
-        a.g_count = colour ? k.P - k.PA : k.PA;
+        a.g_begin = k.own[colour][0];
+        a.g_count = k.own[colour][1] - k.own[colour][0];
       }
       if (a.g_count > 0) {
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (per_launch_timing) {
+          mpr_status se = slab_timing_event(c, evk++, &e0);
+          if (se == MPR_OK) se = slab_timing_event(c, evk++, &e1);
+          if (se != MPR_OK) return se;
+          CK(cudaEventRecordWithFlags(e0, st, ev_flags), "event record");
+        }
         launch_sweep_half(a, c->sweep_grid, k.variant, st);
         CKL("sweep_half");
+        if (per_launch_timing) CK(cudaEventRecordWithFlags(e1, st, ev_flags), "event record");
         ++c->launches;
         ++*nsweep;
       }
+      if (c->rows) {
+        mpr_status sh = exchange_halo(c, colour, k.Rb);
+        if (sh != MPR_OK) return sh;
+      }
     }
   }
-  if (k.timing) CK(cudaEventRecordWithFlags(c->ev1, st, ev_flags), "event record");
+  if (k.timing && !c->rows) CK(cudaEventRecordWithFlags(c->ev1, st, ev_flags), "event record");
   if (!k.defer) {
-    launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), 0, k.P, k.Rb, k.r_lo, k.r_hi, c->acc.as<double>(),
-                      st);
-    CKL("acc_reduce");
-    ++c->launches;
+    // the realization sum over the own gap ids (one contiguous range unless row slabs)
+    const float* X = avg ? c->A.as<float>() : c->G.as<float>();
+    if (k.own[0][1] == k.own[1][0]) {
+      launch_acc_reduce(X, k.own[0][0], k.own[1][1] - k.own[0][0], k.Rb, k.r_lo, k.r_hi, c->acc.as<double>(), st);
+      CKL("acc_reduce");
+      ++c->launches;
+    } else {
+      for (int col = 0; col < 2; ++col) {
+        launch_acc_reduce(X, k.own[col][0], k.own[col][1] - k.own[col][0], k.Rb, k.r_lo, k.r_hi, c->acc.as<double>(),
+                          st);
+        CKL("acc_reduce");
+        ++c->launches;
+      }
+    }
   }
   return MPR_OK;
 }
@@ -637,6 +868,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
   if (c->cfg.n_avg > sweeps) return fail(c, MPR_ERR_INVALID_ARG, "n_avg must be <= sweeps");
   if (m_begin < 0 || m_end > M || m_begin > m_end) return fail(c, MPR_ERR_INVALID_ARG, "bad realization range");
   if (M >= (int64_t(1) << 32)) return fail(c, MPR_ERR_INVALID_ARG, "M too large");
+  if (c->rows && c->defer_reduce) return fail(c, MPR_ERR_INVALID_ARG, "row slabs do not defer the reduction");
   if (!c->acc.p) {
     mpr_status s = mpr_reset_accumulator(c);
     if (s != MPR_OK) return s;
@@ -646,6 +878,8 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
   c->M_total = M;
   c->sweeps = sweeps;
   c->launches = 0;
+  c->m_begin = m_begin;
+  c->m_end = m_end;
   const uint32_t k0 = static_cast<uint32_t>(seed & 0xffffffffu), k1 = static_cast<uint32_t>(seed >> 32);
   if (c->energy_enabled && c->cfg.order != MPR_ORDER_SC)
     return fail(c, MPR_ERR_INVALID_ARG, "the fused energy trace needs the SC order");
@@ -657,7 +891,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
       c->energy_S = sweeps;
     }
   }
-  if (c->degenerate || c->P == 0 || m_begin == m_end) {
+  if (c->degenerate || c->P_glob == 0 || m_begin == m_end) {
     c->stage = ST_SIM;
     return MPR_OK;
   }
@@ -668,8 +902,10 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
   if (c->pending_reduce) return fail(c, MPR_ERR_STATE, "deferred states not accumulated yet");
   c->batch = R;
   const bool avg = c->cfg.n_avg > 1;
-  CK(c->G.ensure(sizeof(float) * c->P * R), "alloc state");
-  if (avg) CK(c->A.ensure(sizeof(float) * c->P * R), "alloc accumulator state");
+  CK(c->G.ensure(sizeof(float) * std::max<int64_t>(c->P, 1) * R), "alloc state");
+  if (avg) CK(c->A.ensure(sizeof(float) * std::max<int64_t>(c->P, 1) * R), "alloc accumulator state");
+  // row slabs capture their batches only with a stream-ordered transport, on request
+  const bool graphs = c->use_graphs && (!c->rows || (c->comm->stream_ordered() && c->slab_graphs));
   for (int64_t mb = mb0; mb < m_end; mb += R) {
     const int64_t span = std::min<int64_t>(R, m_end - mb);
     const int Rb = static_cast<int>(span + (span & 1));
@@ -692,8 +928,10 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
       key.dclist = c->dclist.p;
       for (int k = 0; k < 5; ++k) key.dc_off[k] = c->dc_off[k];
     }
+    for (int col = 0; col < 2; ++col)
+      for (int e = 0; e < 2; ++e) key.own[col][e] = c->own[col][e];
     int64_t nsweep_launch = 0;
-    if (c->use_graphs) {
+    if (graphs) {
       cudaGraphExec_t exec = nullptr;
       for (auto& e : c->graphs)
         if (e.exec && std::memcmp(&e.key, &key, sizeof key) == 0) exec = e.exec;
@@ -720,17 +958,27 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
           if (e.exec == exec) nsweep_launch = e.launches;
       }
       CK(cudaGraphLaunch(exec, st), "graph launch");
-      c->launches += nsweep_launch + (key.defer ? 1 : 2);
-      c->total_launches += nsweep_launch + (key.defer ? 1 : 2);
+      const int64_t nacc = key.defer ? 0 : (key.own[0][1] == key.own[1][0] ? 1 : 2);
+      c->launches += nsweep_launch + 1 + nacc;
+      c->total_launches += nsweep_launch + 1 + nacc;
     } else {
       mpr_status sb = issue_batch(c, key, &nsweep_launch, false);
       if (sb != MPR_OK) return sb;
     }
     if (c->timing) {
-      CK(cudaEventSynchronize(c->ev1), "event sync");
-      float ms = 0.0f;
-      CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event elapsed");
-      c->sweep_ms += ms;
+      if (!c->rows) {
+        CK(cudaEventSynchronize(c->ev1), "event sync");
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event elapsed");
+        c->sweep_ms += ms;
+      } else {
+        CK(cudaStreamSynchronize(st), "timing sync");
+        for (int64_t k = 0; k < nsweep_launch; ++k) {
+          float ms = 0.0f;
+          CK(cudaEventElapsedTime(&ms, c->ev_pool[2 * k], c->ev_pool[2 * k + 1]), "event elapsed");
+          c->sweep_ms += ms;
+        }
+      }
       c->sweep_launches += nsweep_launch;
     }
     c->last_m_base = mb;
@@ -767,16 +1015,67 @@ mpr_status mpr_accumulate_states(mpr_ctx* c) {
   return MPR_OK;
 }
 
+// Realization shards: this rank's range, then the sum over ranks — one
+// all-reduce of the fp64 accumulator, or the rank-ordered chain (bit-identical to one GPU).
+static mpr_status simulate_realization_shards(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed) {
+  int64_t m0 = 0, m1 = 0;
+  shard_range(M, c->world, c->rank, &m0, &m1);
+  cudaStream_t st = c->stream;
+  const size_t nP = static_cast<size_t>(std::max<int64_t>(c->P, 1));
+  double* acc = c->acc.as<double>();
+  mpr_status s = MPR_OK;
+  if (c->cfg.ordered_reduce) {
+    const int prev = c->defer_reduce;
+    c->defer_reduce = 1;
+    s = mpr_simulate_range(c, M, sweeps, seed, m0, m1);
+    c->defer_reduce = prev;
+    if (s != MPR_OK) return s;
+    SET_DEVICE(c);
+    if (c->rank > 0) CKC(c->comm->exchange({}, {{c->rank - 1, acc, nP}}, CT_F64, st), "ordered reduce recv");
+    if (c->pending_reduce) {
+      s = mpr_accumulate_states(c);
+      if (s != MPR_OK) return s;
+    }
+    if (c->rank < c->world - 1) CKC(c->comm->exchange({{c->rank + 1, acc, nP}}, {}, CT_F64, st), "ordered reduce send");
+    CKC(c->comm->broadcast(acc, nP, CT_F64, c->world - 1, st), "ordered reduce broadcast");
+  } else {
+    s = mpr_simulate_range(c, M, sweeps, seed, m0, m1);
+    if (s != MPR_OK) return s;
+    SET_DEVICE(c);
+    CKC(c->comm->allreduce(acc, nP, CT_F64, OP_SUM, st), "allreduce accumulator");
+  }
+  CK(cudaStreamSynchronize(st), "shard reduce sync");
+  c->m_begin = m0;
+  c->m_end = m1;
+  c->M_total = M;
+  return MPR_OK;
+}
+
 mpr_status mpr_simulate(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed) {
   mpr_status s = mpr_reset_accumulator(c);
   if (s != MPR_OK) return s;
-  return mpr_simulate_range(c, M, sweeps, seed, 0, M);
+  if (c->shards) {
+    if (M < 1 || sweeps < 1) return fail(c, MPR_ERR_INVALID_ARG, "M and sweeps must be >= 1");
+    s = simulate_realization_shards(c, M, sweeps, seed);
+  } else {
+    s = mpr_simulate_range(c, M, sweeps, seed, 0, M);
+  }
+  if (s != MPR_OK) return s;
+  // the energy trace: every rank summed its own sites (row slabs) or realizations (shards)
+  if ((c->rows || c->shards) && c->energy_enabled && c->energy_M > 0) {
+    SET_DEVICE(c);
+    CKC(c->comm->allreduce(c->energy.p, static_cast<size_t>(c->energy_M * c->energy_S), CT_I64, OP_SUM, c->stream),
+        "allreduce energy");
+    CK(cudaStreamSynchronize(c->stream), "energy sync");
+  }
+  return MPR_OK;
 }
 
 // Row f1 (ARITH §K): every realization sweeps until its energy trace passes
 // the slope test at a check sweep, then averages n_avg more sweeps. The sweeps run on the
 // device for the whole batch; at check sweeps the host reads the fixed-point energies,
-// decides, and uploads the per-realization accumulation windows.
+// decides, and uploads the per-realization accumulation windows. Realization shards: each
+// rank runs its range; the accumulators and s_eq are summed over the ranks.
 mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n_fit, int32_t n_f,
                                  int32_t max_sweeps, double slope_tol, int32_t* s_eq_out) {
   if (!c) return MPR_ERR_INVALID_ARG;
@@ -787,6 +1086,7 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
     return fail(c, MPR_ERR_INVALID_ARG, "need M >= 1, n_fit >= 3, n_f >= 1, max_sweeps > n_avg");
   if (c->cfg.order != MPR_ORDER_SC)
     return fail(c, MPR_ERR_INVALID_ARG, "the adaptive protocol needs the SC order (fused energy)");
+  if (c->rows) return fail(c, MPR_ERR_INVALID_ARG, "the adaptive protocol runs with realization shards, not row slabs");
   mpr_status st0 = mpr_reset_accumulator(c);
   if (st0 != MPR_OK) return st0;
   SET_DEVICE(c);
@@ -794,14 +1094,20 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
   c->M_total = M;
   c->sweeps = max_sweeps;
   c->launches = 0;
+  int64_t m0 = 0, m1 = M;
+  const bool sharded = c->shards;
+  if (sharded) shard_range(M, c->world, c->rank, &m0, &m1);
+  c->m_begin = m0;
+  c->m_end = m1;
   if (c->degenerate || c->P == 0) {
     if (s_eq_out)
       for (int64_t m = 0; m < M; ++m) s_eq_out[m] = 0;
     c->stage = ST_SIM;
     return MPR_OK;
   }
+  std::vector<int32_t> s_eq_all(static_cast<size_t>(sharded ? M : 0), 0);
   const uint32_t k0 = static_cast<uint32_t>(seed & 0xffffffffu), k1 = static_cast<uint32_t>(seed >> 32);
-  const int64_t R = choose_batch(c, M);
+  const int64_t R = choose_batch(c, std::max<int64_t>(m1 - m0, 2));
   CK(c->G.ensure(sizeof(float) * c->P * R), "alloc state");
   CK(c->A.ensure(sizeof(float) * c->P * R), "alloc accumulator state");
   CK(c->energy.ensure(sizeof(long long) * R * max_sweeps), "alloc energy");
@@ -823,8 +1129,8 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
   volatile int* status_h = hbuf + 2 * R;
   int* eq_h = hbuf + 2 * R + 2;
   if (!c->ev_check) CK(cudaEventCreateWithFlags(&c->ev_check, cudaEventDisableTiming), "event");
-  for (int64_t mb = 0; mb < M; mb += R) {
-    const int64_t span = std::min<int64_t>(R, M - mb);
+  for (int64_t mb = m0; mb < m1; mb += R) {
+    const int64_t span = std::min<int64_t>(R, m1 - mb);
     const int Rb = static_cast<int>(span + (span & 1));
     const int r_hi = static_cast<int>(span);
     // windows: (lo, hi] accumulates; hi = INT_MAX while undecided; the pad realization
@@ -921,192 +1227,23 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
     CKL("acc_reduce");
     ++c->launches;
     CK(cudaStreamSynchronize(st), "adaptive sync");
-    if (s_eq_out)
-      for (int r = 0; r < r_hi; ++r) s_eq_out[mb + r] = eq_h[r];
+    for (int r = 0; r < r_hi; ++r) {
+      if (sharded) s_eq_all[static_cast<size_t>(mb + r)] = eq_h[r];
+      else if (s_eq_out) s_eq_out[mb + r] = eq_h[r];
+    }
     c->last_m_base = mb;
     c->last_R = Rb;
   }
+  if (sharded) {  // accumulators and decisions of every rank (zeros outside a rank's range)
+    CKC(c->comm->allreduce(c->acc.p, static_cast<size_t>(c->P), CT_F64, OP_SUM, st), "allreduce accumulator");
+    CK(c->tmp.ensure(sizeof(int32_t) * static_cast<size_t>(M)), "alloc s_eq");
+    CK(cudaMemcpyAsync(c->tmp.p, s_eq_all.data(), sizeof(int32_t) * M, cudaMemcpyHostToDevice, st), "H2D s_eq");
+    CKC(c->comm->allreduce(c->tmp.p, static_cast<size_t>(M), CT_I32, OP_SUM, st), "allreduce s_eq");
+    CK(cudaMemcpyAsync(s_eq_all.data(), c->tmp.p, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, st), "D2H s_eq");
+    CK(cudaStreamSynchronize(st), "adaptive reduce sync");
+    if (s_eq_out) std::memcpy(s_eq_out, s_eq_all.data(), sizeof(int32_t) * M);
+  }
   c->batch = R;
-  c->stage = ST_SIM;
-  return MPR_OK;
-}
-
-// ---- row-slab decomposition ------------------------------------
-namespace {
-// First gap id of colour `col` in row r (r == Ly: end of the colour range).
-int64_t gap_row_offset(const mpr_ctx* c, int col, int64_t r) {
-  if (r >= c->Ly) return col == 0 ? c->PA : c->P;
-  return c->rowoff_h[static_cast<size_t>(col * c->Ly + r)];
-}
-}  // namespace
-
-mpr_status mpr_slab_begin(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed, int64_t m_begin, int64_t m_end,
-                          int64_t row_begin, int64_t row_end) {
-  if (!c) return MPR_ERR_INVALID_ARG;
-  if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "slab_begin before estimate_local_params");
-  if (M < 1 || sweeps < 1 || c->cfg.n_avg > sweeps) return fail(c, MPR_ERR_INVALID_ARG, "bad M / sweeps / n_avg");
-  if (m_begin < 0 || m_end > M || m_begin >= m_end) return fail(c, MPR_ERR_INVALID_ARG, "bad realization range");
-  if (row_begin < 0 || row_end > c->Ly || row_begin >= row_end) return fail(c, MPR_ERR_INVALID_ARG, "bad row range");
-  if (c->energy_enabled) return fail(c, MPR_ERR_INVALID_ARG, "energy trace is not supported in slab mode");
-  if (c->cfg.order != MPR_ORDER_SC) return fail(c, MPR_ERR_INVALID_ARG, "slab mode needs the SC order");
-  if (!c->acc.p) {
-    mpr_status s = mpr_reset_accumulator(c);
-    if (s != MPR_OK) return s;
-  }
-  SET_DEVICE(c);
-  cudaStream_t st = c->stream;
-  c->rowoff_h.resize(static_cast<size_t>(2 * c->Ly));
-  CK(cudaMemcpyAsync(c->rowoff_h.data(), c->rowoff.p, sizeof(int) * 2 * c->Ly, cudaMemcpyDeviceToHost, st),
-     "D2H row offsets");
-  CK(cudaStreamSynchronize(st), "slab sync");
-  const int64_t mb = m_begin & ~int64_t(1);
-  const int64_t span = m_end - mb;
-  const int Rb = static_cast<int>(span + (span & 1));
-  if (Rb > 1024 || static_cast<int64_t>(Rb) * std::max<int64_t>(c->P, 1) >= (int64_t(1) << 31))
-    return fail(c, MPR_ERR_INVALID_ARG, "slab mode runs its realizations as one batch: range too large");
-  const bool avg = c->cfg.n_avg > 1;
-  CK(c->G.ensure(sizeof(float) * std::max<int64_t>(c->P, 1) * Rb), "alloc state");
-  if (avg) CK(c->A.ensure(sizeof(float) * std::max<int64_t>(c->P, 1) * Rb), "alloc accumulator state");
-  c->M_total = M;
-  c->sweeps = sweeps;
-  c->slab_active = 1;
-  c->slab_row0 = row_begin;
-  c->slab_row1 = row_end;
-  c->slab_m0 = m_begin;
-  c->slab_m1 = m_end;
-  c->slab_mb = mb;
-  c->slab_R = Rb;
-  c->slab_S = sweeps;
-  c->slab_k0 = static_cast<uint32_t>(seed & 0xffffffffu);
-  c->slab_k1 = static_cast<uint32_t>(seed >> 32);
-  c->batch = Rb;
-  c->last_m_base = mb;
-  c->last_R = Rb;
-  if (c->degenerate || c->P == 0) return MPR_OK;
-  // every gap (own rows and ghost rows alike) gets its initial state: the init is a pure
-  // function of the global ids, so ghost rows need no exchange before the first sweep
-  launch_init_states(c->rec.as<GapRec>(), c->G.as<float>(), avg ? c->A.as<float>() : nullptr, c->P, Rb, Rb / 2,
-                     static_cast<uint32_t>(mb / 2), c->cfg.init == MPR_INIT_RANDOM, c->slab_k0, c->slab_k1, st);
-  CKL("init_states");
-  return MPR_OK;
-}
-
-mpr_status mpr_slab_half_sweep(mpr_ctx* c, int32_t sweep, int colour) {
-  if (!c) return MPR_ERR_INVALID_ARG;
-  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_half_sweep outside slab_begin/slab_end");
-  if (sweep < 1 || sweep > c->slab_S || (colour != 0 && colour != 1))
-    return fail(c, MPR_ERR_INVALID_ARG, "bad sweep or colour");
-  if (c->degenerate || c->P == 0) return MPR_OK;
-  SET_DEVICE(c);
-  const int64_t g0 = gap_row_offset(c, colour, c->slab_row0);
-  const int64_t g1 = gap_row_offset(c, colour, c->slab_row1);
-  if (g1 <= g0) return MPR_OK;
-  const bool avg = c->cfg.n_avg > 1;
-  SweepArgs a{};
-  a.rec = c->rec.as<GapRec>();
-  a.G = c->G.as<float>();
-  a.P = c->P;
-  a.A = avg ? c->A.as<float>() : nullptr;
-  a.g_begin = g0;
-  a.g_count = g1 - g0;
-  a.R = c->slab_R;
-  a.npairs = c->slab_R / 2;
-  a.pair_base = static_cast<uint32_t>(c->slab_mb / 2);
-  a.sweep = static_cast<uint32_t>(sweep);
-  a.k0 = c->slab_k0;
-  a.k1 = c->slab_k1;
-  a.q = c->cfg.q;
-  a.J = c->cfg.J;
-  a.is_b = colour;
-  a.accumulate = avg && (sweep > c->slab_S - c->cfg.n_avg);
-  a.energy = nullptr;
-  // fused halo: the first own row goes to the upper neighbour, the last to the lower one
-  const int64_t brow[2] = {c->slab_row0, c->slab_row1 - 1};
-  for (int k = 0; k < 2; ++k) {
-    a.peer[k] = c->slab_peer[k];
-    a.peer_lo[k] = static_cast<uint32_t>(gap_row_offset(c, colour, brow[k]) * c->slab_R);
-    a.peer_hi[k] = static_cast<uint32_t>(gap_row_offset(c, colour, brow[k] + 1) * c->slab_R);
-  }
-  launch_sweep_half(a, c->sweep_grid, c->sweep_variant, c->stream);
-  CKL("sweep_half");
-  return MPR_OK;
-}
-
-mpr_status mpr_slab_row_states(mpr_ctx* c, int64_t row, int colour, float** dev_ptr, int64_t* count) {
-  if (!c || !dev_ptr || !count) return MPR_ERR_INVALID_ARG;
-  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_row_states outside slab_begin/slab_end");
-  if (row < 0 || row >= c->Ly || (colour != 0 && colour != 1)) return fail(c, MPR_ERR_INVALID_ARG, "bad row/colour");
-  const int64_t g0 = gap_row_offset(c, colour, row), g1 = gap_row_offset(c, colour, row + 1);
-  *dev_ptr = c->G.as<float>() + g0 * c->slab_R;
-  *count = (g1 - g0) * c->slab_R;
-  return MPR_OK;
-}
-
-mpr_status mpr_slab_state_ipc_handle(mpr_ctx* c, void* handle_out) {
-  if (!c || !handle_out) return MPR_ERR_INVALID_ARG;
-  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_state_ipc_handle outside slab_begin/slab_end");
-  SET_DEVICE(c);
-  cudaIpcMemHandle_t h;
-  CK(cudaIpcGetMemHandle(&h, c->G.p), "cudaIpcGetMemHandle");
-  static_assert(sizeof(cudaIpcMemHandle_t) == MPR_IPC_HANDLE_BYTES, "IPC handle size");
-  std::memcpy(handle_out, &h, sizeof h);
-  return MPR_OK;
-}
-
-mpr_status mpr_slab_state_device(mpr_ctx* c, float** dev_ptr) {
-  if (!c || !dev_ptr) return MPR_ERR_INVALID_ARG;
-  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_state_device outside slab_begin/slab_end");
-  *dev_ptr = c->G.as<float>();
-  return MPR_OK;
-}
-
-mpr_status mpr_slab_set_peer(mpr_ctx* c, int side, const void* ipc_handle, float* dev_ptr) {
-  if (!c || (side != 0 && side != 1) || (ipc_handle && dev_ptr)) return MPR_ERR_INVALID_ARG;
-  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_set_peer outside slab_begin/slab_end");
-  SET_DEVICE(c);
-  clear_peer(c, side);
-  if (ipc_handle) {
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, ipc_handle, sizeof h);
-    void* p = nullptr;
-    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-    c->slab_peer[side] = static_cast<float*>(p);
-    c->slab_peer_ipc[side] = true;
-  } else if (dev_ptr) {
-    cudaPointerAttributes at{};
-    CK(cudaPointerGetAttributes(&at, dev_ptr), "peer pointer attributes");
-    if (at.type != cudaMemoryTypeDevice) return fail(c, MPR_ERR_INVALID_ARG, "peer pointer is not device memory");
-    if (at.device != c->device) {
-      int ok = 0;
-      CK(cudaDeviceCanAccessPeer(&ok, c->device, at.device), "peer access query");
-      if (!ok) return fail(c, MPR_ERR_INVALID_ARG, "peer device not reachable (no P2P)");
-      cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
-      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-      else if (e != cudaSuccess) return cuda_fail(c, e, "enable peer access");
-    }
-    c->slab_peer[side] = dev_ptr;
-  }
-  return MPR_OK;
-}
-
-mpr_status mpr_slab_end(mpr_ctx* c) {
-  if (!c) return MPR_ERR_INVALID_ARG;
-  if (!c->slab_active) return fail(c, MPR_ERR_STATE, "slab_end without slab_begin");
-  SET_DEVICE(c);
-  c->slab_active = 0;
-  clear_peer(c, 0);
-  clear_peer(c, 1);
-  if (!(c->degenerate || c->P == 0)) {
-    const bool avg = c->cfg.n_avg > 1;
-    const int r_lo = static_cast<int>(c->slab_m0 - c->slab_mb), r_hi = static_cast<int>(c->slab_m1 - c->slab_mb);
-    for (int col = 0; col < 2; ++col) {
-      const int64_t g0 = gap_row_offset(c, col, c->slab_row0), g1 = gap_row_offset(c, col, c->slab_row1);
-      launch_acc_reduce(avg ? c->A.as<float>() : c->G.as<float>(), g0, g1 - g0, c->slab_R, r_lo, r_hi,
-                        c->acc.as<double>(), c->stream);
-      CKL("acc_reduce");
-    }
-  }
-  CK(cudaStreamSynchronize(c->stream), "slab_end sync");
   c->stage = ST_SIM;
   return MPR_OK;
 }
@@ -1183,12 +1320,30 @@ mpr_status mpr_accumulator_device(mpr_ctx* c, double** acc_dev, int64_t* n) {
   return MPR_OK;
 }
 
-static mpr_status predict_impl(mpr_ctx* c, float* out_dev) {
+// a11 over the own rows into out_rows_dev ((row1 - row0) x Lx floats).
+static mpr_status predict_own_rows(mpr_ctx* c, float* out_rows_dev) {
   if (c->stage < ST_SIM || c->M_total < 1) return fail(c, MPR_ERR_STATE, "predict before simulate");
   const double denom = static_cast<double>(c->M_total * static_cast<int64_t>(c->cfg.n_avg));
-  launch_predict(c->z.as<float>(), c->mask.as<uint8_t>(), c->gid.as<int32_t>(), c->acc.as<double>(), c->n, denom,
-                 c->scal.as<DevScalars>(), c->degenerate, out_dev, c->stream);
+  launch_predict(local_row(c, c->z.as<float>(), c->row0), local_row(c, c->mask.as<uint8_t>(), c->row0),
+                 local_row(c, c->gid.as<int32_t>(), c->row0), c->acc.as<double>(), (c->row1 - c->row0) * c->Lx, denom,
+                 c->scal.as<DevScalars>(), c->degenerate, out_rows_dev, c->stream);
   CKL("predict");
+  return MPR_OK;
+}
+
+// The whole prediction into out_dev (Lx*Ly floats): row slabs all-gather their rows.
+static mpr_status predict_all(mpr_ctx* c, float* out_dev) {
+  mpr_status s = predict_own_rows(c, out_dev + c->row0 * c->Lx);
+  if (s != MPR_OK || !c->rows) return s;
+  std::vector<size_t> counts(static_cast<size_t>(c->world)), displs(static_cast<size_t>(c->world));
+  for (int w = 0; w < c->world; ++w) {
+    int64_t r0 = 0, r1 = 0;
+    row_range(c->Ly, c->world, w, &r0, &r1);
+    counts[static_cast<size_t>(w)] = static_cast<size_t>((r1 - r0) * c->Lx);
+    displs[static_cast<size_t>(w)] = static_cast<size_t>(r0 * c->Lx);
+  }
+  CKC(c->comm->allgatherv(out_dev + c->row0 * c->Lx, out_dev, counts, displs, CT_F32, c->stream),
+      "allgather predictions");
   return MPR_OK;
 }
 
@@ -1196,10 +1351,11 @@ mpr_status mpr_predict(mpr_ctx* c, float* out) {
   if (!c) return MPR_ERR_INVALID_ARG;
   if (!out) return fail(c, MPR_ERR_INVALID_ARG, "out is NULL");
   SET_DEVICE(c);
-  CK(c->out.ensure(sizeof(float) * c->n), "alloc out");
-  mpr_status s = predict_impl(c, c->out.as<float>());
+  const int64_t total = c->Lx * c->Ly;
+  CK(c->out.ensure(sizeof(float) * total), "alloc out");
+  mpr_status s = predict_all(c, c->out.as<float>());
   if (s != MPR_OK) return s;
-  CK(cudaMemcpyAsync(out, c->out.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, c->stream), "D2H out");
+  CK(cudaMemcpyAsync(out, c->out.p, sizeof(float) * total, cudaMemcpyDeviceToHost, c->stream), "D2H out");
   CK(cudaStreamSynchronize(c->stream), "predict sync");
   return MPR_OK;
 }
@@ -1208,8 +1364,21 @@ mpr_status mpr_predict_device(mpr_ctx* c, float* out_dev) {
   if (!c) return MPR_ERR_INVALID_ARG;
   if (!out_dev) return fail(c, MPR_ERR_INVALID_ARG, "out is NULL");
   SET_DEVICE(c);
-  mpr_status s = predict_impl(c, out_dev);
+  mpr_status s = predict_all(c, out_dev);
   if (s != MPR_OK) return s;
+  CK(cudaStreamSynchronize(c->stream), "predict sync");
+  return MPR_OK;
+}
+
+mpr_status mpr_predict_rows(mpr_ctx* c, float* out_rows) {
+  if (!c) return MPR_ERR_INVALID_ARG;
+  if (!out_rows) return fail(c, MPR_ERR_INVALID_ARG, "out is NULL");
+  SET_DEVICE(c);
+  const int64_t cnt = (c->row1 - c->row0) * c->Lx;
+  CK(c->out.ensure(sizeof(float) * std::max<int64_t>(cnt, 1)), "alloc out");
+  mpr_status s = predict_own_rows(c, c->out.as<float>());
+  if (s != MPR_OK) return s;
+  CK(cudaMemcpyAsync(out_rows, c->out.p, sizeof(float) * cnt, cudaMemcpyDeviceToHost, c->stream), "D2H out");
   CK(cudaStreamSynchronize(c->stream), "predict sync");
   return MPR_OK;
 }
@@ -1220,8 +1389,8 @@ mpr_status mpr_get_info(mpr_ctx* c, mpr_info* info) {
   info->Lx = c->Lx;
   info->Ly = c->Ly;
   info->n_samples = c->n_known;
-  info->n_gaps = c->P;
-  info->n_gaps_a = c->PA;
+  info->n_gaps = c->P_glob;
+  info->n_gaps_a = c->PA_glob;
   info->z_min = c->zmin;
   info->z_max = c->zmax;
   info->degenerate_range = c->degenerate;
@@ -1238,6 +1407,15 @@ mpr_status mpr_get_info(mpr_ctx* c, mpr_info* info) {
   info->last_m_base = c->last_m_base;
   info->last_batch = c->last_R;
   info->sweep_variant = c->sweep_variant;
+  info->rank = c->rank;
+  info->world = c->world;
+  info->shard = c->cfg.shard;
+  info->row_begin = c->row0;
+  info->row_end = c->row1;
+  info->m_begin = c->m_begin;
+  info->m_end = c->m_end;
+  info->n_gaps_local = c->P;
+  info->comm_calls = c->comm_calls;
   return MPR_OK;
 }
 
@@ -1245,14 +1423,18 @@ mpr_status mpr_debug_get(mpr_ctx* c, mpr_buffer which, int64_t index, void* host
   if (!c || !host_out) return MPR_ERR_INVALID_ARG;
   SET_DEVICE(c);
   cudaStream_t st = c->stream;
+  // the Lx*Ly buffers: the own rows, at their offsets of the (whole-grid) host buffer
+  const int64_t own = (c->row1 - c->row0) * c->Lx, hoff = c->row0 * c->Lx;
   switch (which) {
     case MPR_BUF_PHI_KNOWN:
       if (c->stage < ST_DATA) return fail(c, MPR_ERR_STATE, "no data");
-      CK(cudaMemcpyAsync(host_out, c->phiK.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, st), "D2H");
+      CK(cudaMemcpyAsync(static_cast<float*>(host_out) + hoff, local_row(c, c->phiK.as<float>(), c->row0),
+                         sizeof(float) * own, cudaMemcpyDeviceToHost, st), "D2H");
       break;
     case MPR_BUF_T:
       if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "no parameters");
-      CK(cudaMemcpyAsync(host_out, c->T.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, st), "D2H");
+      CK(cudaMemcpyAsync(static_cast<float*>(host_out) + hoff, c->T.as<float>() + (c->row0 - c->trow0) * c->Lx,
+                         sizeof(float) * own, cudaMemcpyDeviceToHost, st), "D2H");
       break;
     case MPR_BUF_BLOCK_T:
       if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "no parameters");
@@ -1267,19 +1449,22 @@ mpr_status mpr_debug_get(mpr_ctx* c, mpr_buffer which, int64_t index, void* host
       if (c->stage < ST_SIM || !c->G.p || c->last_R == 0) return fail(c, MPR_ERR_STATE, "no state");
       const int64_t r = index - c->last_m_base;
       if (r < 0 || r >= c->last_R) return fail(c, MPR_ERR_INVALID_ARG, "realization not in the last batch");
-      CK(c->tmp.ensure(sizeof(double) * c->n), "alloc tmp");
-      launch_scatter_state(c->phiK.as<float>(), c->gid.as<int32_t>(), c->G.as<float>(), c->last_R, r, c->n,
-                           c->tmp.as<float>(), st);
+      CK(c->tmp.ensure(sizeof(double) * std::max<int64_t>(own, 1)), "alloc tmp");
+      launch_scatter_state(local_row(c, c->phiK.as<float>(), c->row0), local_row(c, c->gid.as<int32_t>(), c->row0),
+                           c->G.as<float>(), c->last_R, r, own, c->tmp.as<float>(), st);
       CKL("scatter_state");
-      CK(cudaMemcpyAsync(host_out, c->tmp.p, sizeof(float) * c->n, cudaMemcpyDeviceToHost, st), "D2H");
+      CK(cudaMemcpyAsync(static_cast<float*>(host_out) + hoff, c->tmp.p, sizeof(float) * own, cudaMemcpyDeviceToHost,
+                         st), "D2H");
       break;
     }
     case MPR_BUF_ACC:
       if (c->stage < ST_PARAMS || !c->acc.p) return fail(c, MPR_ERR_STATE, "no accumulator");
-      CK(c->tmp.ensure(sizeof(double) * c->n), "alloc tmp");
-      launch_scatter_acc(c->gid.as<int32_t>(), c->acc.as<double>(), c->n, c->tmp.as<double>(), st);
+      CK(c->tmp.ensure(sizeof(double) * std::max<int64_t>(own, 1)), "alloc tmp");
+      launch_scatter_acc(local_row(c, c->gid.as<int32_t>(), c->row0), c->acc.as<double>(), own, c->tmp.as<double>(),
+                         st);
       CKL("scatter_acc");
-      CK(cudaMemcpyAsync(host_out, c->tmp.p, sizeof(double) * c->n, cudaMemcpyDeviceToHost, st), "D2H");
+      CK(cudaMemcpyAsync(static_cast<double*>(host_out) + hoff, c->tmp.p, sizeof(double) * own,
+                         cudaMemcpyDeviceToHost, st), "D2H");
       break;
     case MPR_BUF_ENERGY: {
       if (!c->energy_enabled || c->energy_M == 0) return fail(c, MPR_ERR_STATE, "energy trace not enabled");

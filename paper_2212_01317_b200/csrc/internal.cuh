@@ -46,26 +46,37 @@ struct DevScalars {
 };
 
 // ---- launchers (params.cu) ----
-void launch_minmax_count(const float* z, const uint8_t* mask, int64_t Lx, int64_t Ly,
+// Row-slab convention: a local buffer of `Ly` rows whose row 0 is the global row `row_base`
+// (row_base = 0 and Ly = the grid's rows outside row-slab mode); colours and Philox site
+// counters are global.
+void launch_minmax_count(const float* z, const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base,
                          DevScalars* sc, cudaStream_t st);
 void launch_transform(const float* z, const uint8_t* mask, int64_t n, const DevScalars* sc,
                       float* phiK, cudaStream_t st);
-void launch_gap_index(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t PA, int* rowcnt,
+// gap ids in (colour, local row, column) order: per-row counts + exclusive scan, then the
+// compaction (gid per site, rec[g].site = global site index)
+void launch_gap_rows(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, int* rowcnt, int* rowoff,
+                     cudaStream_t st);
+void launch_gap_compact(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, const int* rowoff,
+                        int32_t* gid, GapRec* rec, cudaStream_t st);
+void launch_gap_index(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, int* rowcnt,
                       int* rowoff, int32_t* gid, GapRec* rec, cudaStream_t st);
-void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int64_t Ly, int lb,
-                        float q, long long* SB, long long* NB, long long* SP, long long* NK,
-                        int64_t nblocks, cudaStream_t st);
+// block sums of the own rows [row0, row1) (global) of a buffer starting at global row lrow0
+void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t lrow0,
+                        int64_t row0, int64_t row1, int lb, float q, long long* SB, long long* NB,
+                        long long* SP, long long* NK, int64_t nblocks, cudaStream_t st);
 void launch_block_T(const long long* SB, const long long* NB, const long long* SP,
                     const long long* NK, int64_t nblocks, const float* calT, const float* cale,
                     int K, float* Tb, DevScalars* sc, cudaStream_t st);
 void launch_median_fill(float* Tb, const long long* NB, int64_t nblocks, DevScalars* sc,
                         cudaStream_t st);
-void launch_expand(const float* Tb, int64_t Lx, int64_t Ly, int lb, float* T, cudaStream_t st);
-void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int rs, cudaStream_t st);
+void launch_expand(const float* Tb, int64_t Lx, int64_t trow0, int64_t trow1, int lb, float* T, cudaStream_t st);
+void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int64_t row_base, int64_t Ly_g, int rs,
+                   cudaStream_t st);
 void launch_build_records(const int32_t* gid, const uint8_t* mask, const float* phiK,
                           const float* T, const long long* SP, const long long* NK,
-                          const DevScalars* sc, int64_t Lx, int64_t Ly, int lb, int64_t P,
-                          GapRec* rec, cudaStream_t st);
+                          const DevScalars* sc, int64_t Lx, int64_t Ly, int64_t lrow0, int64_t lrow1,
+                          int64_t trow0, int64_t trow1, int lb, int64_t P, GapRec* rec, cudaStream_t st);
 void launch_predict(const float* z, const uint8_t* mask, const int32_t* gid, const double* acc,
                     int64_t n, double denom, const DevScalars* sc, int degenerate, float* out,
                     cudaStream_t st);

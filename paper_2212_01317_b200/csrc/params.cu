@@ -39,7 +39,8 @@ __device__ __forceinline__ unsigned long long warp_sum_ull(unsigned long long v)
 template <bool VEC>
 __global__ void __launch_bounds__(256) k_minmax_count(const float* __restrict__ z,
                                                       const uint8_t* __restrict__ mask,
-                                                      int64_t Lx, int64_t n, DevScalars* sc) {
+                                                      int64_t Lx, int64_t n, int64_t row_base,
+                                                      DevScalars* sc) {
   int kmin = 0x7fffffff, kmax = static_cast<int>(0x80000000u);
   unsigned long long nk = 0, ng0 = 0, ng1 = 0;
   int bad = 0;
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(256) k_minmax_count(const float* __restrict__ 
         zv[k] = (i < n && mv[k]) ? z[i] : 0.0f;
       }
     }
-    int64_t r = i0 / Lx, c = i0 - r * Lx;
+    int64_t r = i0 / Lx + row_base, c = i0 - (i0 / Lx) * Lx;  // r: global row (colour parity)
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const bool in = (i0 + k) < n;
@@ -150,12 +151,15 @@ __global__ void __launch_bounds__(256) k_transform(const float* __restrict__ z,
 
 // ------------------------------------------------------------ gap-site index
 // Gap ids: colour A ((r+c) even) first, then colour B; row-major within a colour.
+// Local rows r = 0 .. Ly-1 of a buffer whose row 0 is global row row_base (row slabs);
+// colours are global: (row_base + r + c) & 1.
 __global__ void __launch_bounds__(256) k_row_counts(const uint8_t* __restrict__ mask, int64_t Lx,
-                                                    int64_t Ly, int* __restrict__ rowcnt) {
+                                                    int64_t Ly, int64_t row_base,
+                                                    int* __restrict__ rowcnt) {
   const int64_t r = blockIdx.x;
   int cnt[2] = {0, 0};
   for (int64_t c = threadIdx.x; c < Lx; c += blockDim.x)
-    if (!mask[r * Lx + c]) ++cnt[(r + c) & 1];
+    if (!mask[r * Lx + c]) ++cnt[(row_base + r + c) & 1];
   __shared__ int s[2][8];
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
@@ -210,7 +214,8 @@ __global__ void __launch_bounds__(1024) k_scan_excl(const int* __restrict__ in, 
 }
 
 __global__ void __launch_bounds__(256) k_row_compact(const uint8_t* __restrict__ mask, int64_t Lx,
-                                                     int64_t Ly, const int* __restrict__ rowoff,
+                                                     int64_t Ly, int64_t row_base,
+                                                     const int* __restrict__ rowoff,
                                                      int32_t* __restrict__ gid,
                                                      GapRec* __restrict__ rec) {
   const int64_t r = blockIdx.x;
@@ -224,7 +229,7 @@ __global__ void __launch_bounds__(256) k_row_compact(const uint8_t* __restrict__
     const int64_t i = r * Lx + c;
     const bool in = c < Lx;
     const bool gap = in && !mask[i];
-    const int col = static_cast<int>((r + c) & 1);
+    const int col = static_cast<int>((row_base + r + c) & 1);
     const unsigned b0 = __ballot_sync(0xffffffffu, gap && col == 0);
     const unsigned b1 = __ballot_sync(0xffffffffu, gap && col == 1);
     if (lane == 0) { wcnt[0][wid] = __popc(b0); wcnt[1][wid] = __popc(b1); }
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(256) k_row_compact(const uint8_t* __restrict__
       if (gap) {
         const int g = base[col] + rank;
         gid[i] = g;
-        rec[g].site = static_cast<uint32_t>(i);
+        rec[g].site = static_cast<uint32_t>(i + row_base * Lx);  // global site (Philox counter)
       } else {
         gid[i] = -1;
       }
@@ -256,18 +261,23 @@ __global__ void __launch_bounds__(256) k_row_compact(const uint8_t* __restrict__
 constexpr int kTile = 32;            // 32 x 32 sites per CTA
 constexpr int kMaxSlots = 17 * 17;   // blocks a tile can touch when l_b >= 2
 
+// Rows [row0, row1) (global) of a local buffer whose row 0 is global row lrow0; the buffer
+// also holds row row1 when row1 < Ly (the down bonds of the last own row read it). Tiles are
+// aligned to global multiples of 32 rows, so a tile lies in one l_b block whenever l_b is a
+// multiple of 32, wherever the slab starts.
 __global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ phi,
                                                      const uint8_t* __restrict__ mask, int64_t Lx,
-                                                     int64_t Ly, int lb, float q,
+                                                     int64_t Ly, int64_t lrow0, int64_t row0,
+                                                     int64_t row1, int lb, float q,
                                                      long long* __restrict__ SB,
                                                      long long* __restrict__ NB,
                                                      long long* __restrict__ SP,
                                                      long long* __restrict__ NK) {
   __shared__ long long sSB[kMaxSlots], sNB[kMaxSlots], sSP[kMaxSlots], sNK[kMaxSlots];
-  const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (int64_t)blockIdx.y * kTile;
+  const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (row0 / kTile) * kTile + (int64_t)blockIdx.y * kTile;
   const int64_t nbx = (Lx + lb - 1) / lb;
-  const int64_t bc0 = c0 / lb, br0 = r0 / lb;
-  const int64_t cl = min(c0 + kTile, Lx) - 1, rl = min(r0 + kTile, Ly) - 1;
+  const int64_t bc0 = c0 / lb, br0 = max(r0, row0) / lb;
+  const int64_t cl = min(c0 + kTile, Lx) - 1, rl = min(r0 + kTile, row1) - 1;
   const int nbc = static_cast<int>(cl / lb - bc0 + 1), nbr = static_cast<int>(rl / lb - br0 + 1);
   const int nslots = nbc * nbr;
   for (int t = threadIdx.x; t < nslots; t += blockDim.x) { sSB[t] = 0; sNB[t] = 0; sSP[t] = 0; sNK[t] = 0; }
@@ -282,8 +292,8 @@ __global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ p
 #pragma unroll
     for (int k = 0; k < kTile / 8; ++k) {
       const int64_t r = r0 + ty + 8 * k, c = c0 + tx;
-      if (r < Ly && c < Lx) {
-        const int64_t i = r * Lx + c;
+      if (r >= row0 && r < row1 && c < Lx) {
+        const int64_t i = (r - lrow0) * Lx + c;
         if (mask[i]) {
           const float pi = phi[i];
           vsp += __float2ll_rn(__fmul_rn(pi, 0x1p28f));
@@ -321,11 +331,11 @@ __global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ p
     const int64_t r = r0 + ty + 8 * k, c = c0 + tx;
     long long vsb = 0, vnb = 0, vsp = 0, vnk = 0;
     int slot = 0;
-    const bool in = r < Ly && c < Lx;
+    const bool in = r >= row0 && r < row1 && c < Lx;
     if (in) {
       const int rbl = static_cast<int>(static_cast<uint32_t>(r) / static_cast<uint32_t>(lb) - br0);
       slot = rbl * nbc + cbl;
-      const int64_t i = r * Lx + c;
+      const int64_t i = (r - lrow0) * Lx + c;
       if (mask[i]) {
         const float pi = phi[i];
         vsp = __float2ll_rn(__fmul_rn(pi, 0x1p28f));
@@ -463,13 +473,15 @@ __global__ void __launch_bounds__(1024) k_median_fill(float* __restrict__ Tb,
 }
 
 // ---------------------------------------------------- a5: expand + SST smoothing
+// Local temperature rows [trow0, trow1) (global): T[(r - trow0) * Lx + c] = Tb(block(r, c)).
 __global__ void __launch_bounds__(256) k_expand(const float* __restrict__ Tb, int64_t Lx,
-                                                int64_t Ly, int lb, float* __restrict__ T) {
-  const int64_t n = Lx * Ly, nbx = (Lx + lb - 1) / lb;
+                                                int64_t trow0, int64_t trow1, int lb,
+                                                float* __restrict__ T) {
+  const int64_t n = Lx * (trow1 - trow0), nbx = (Lx + lb - 1) / lb;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / Lx, c = i - r * Lx;
-    T[i] = Tb[(r / lb) * nbx + c / lb];
+    const int64_t lr = i / Lx, c = i - lr * Lx;
+    T[i] = Tb[((lr + trow0) / lb) * nbx + c / lb];
   }
 }
 
@@ -481,10 +493,13 @@ __global__ void __launch_bounds__(256) k_expand(const float* __restrict__ Tb, in
 // the additions does not change a bit. A tall tile (TY = 64) amortises the vertical halo and
 // the two barriers on large grids; small grids keep TY = 32 for more CTAs. Interior tiles
 // use 32-bit offsets from the tile origin.
+// Row slabs: the buffer holds rows [row_base, row_base + Ly) of a grid of Ly_g rows. Windows
+// clip at the GRID edges (the counts); rows outside the buffer contribute 0, which only
+// corrupts the outermost r_s buffer rows per pass (the halo that the slab does not consume).
 template <int TY>
 __global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
                                                 float* __restrict__ Tout, int64_t Lx, int64_t Ly,
-                                                int rs) {
+                                                int64_t row_base, int64_t Ly_g, int rs) {
   extern __shared__ long long smem[];
   const int W = kTile + 2 * rs, HY = TY + 2 * rs, w = 2 * rs + 1;
   long long* Q = smem;             // HY rows x W cols
@@ -535,8 +550,9 @@ __global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
     if (k > 0) s += H[(yb + k + w - 1) * kTile + tx] - H[(yb + k - 1) * kTile + tx];
     if (r >= Ly) break;
     double cnt = full;
-    if (r - rs < 0 || r + rs > Ly - 1) {
-      const int64_t ra = r - rs > 0 ? r - rs : 0, rb = r + rs < Ly - 1 ? r + rs : Ly - 1;
+    const int64_t rg = r + row_base;
+    if (rg - rs < 0 || rg + rs > Ly_g - 1) {
+      const int64_t ra = rg - rs > 0 ? rg - rs : 0, rb = rg + rs < Ly_g - 1 ? rg + rs : Ly_g - 1;
       cnt = static_cast<double>(static_cast<int>(rb - ra + 1) * ncol);
     }
     out[static_cast<int64_t>(k) * Lx] = __double2float_rn(__ddiv_rn(__ll2double_rn(s) * 0x1p-40, cnt));
@@ -544,15 +560,19 @@ __global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
 }
 
 // -------------------------------------------------- per-gap records (sweep input)
+// Local gap ids of a buffer of rows [lrow0, lrow1) (global; the whole grid unless row slabs):
+// neighbours outside those rows are left out — only ghost-row gaps, which are never
+// updated, have any. T holds rows [trow0, trow1).
 __global__ void __launch_bounds__(256) k_build_records(
     const int32_t* __restrict__ gid, const uint8_t* __restrict__ mask,
     const float* __restrict__ phi, const float* __restrict__ T, const long long* __restrict__ SP,
     const long long* __restrict__ NK, const DevScalars* __restrict__ sc, int64_t Lx, int64_t Ly,
-    int lb, int64_t P, GapRec* __restrict__ rec) {
+    int64_t lrow0, int64_t lrow1, int64_t trow0, int64_t trow1, int lb, int64_t P,
+    GapRec* __restrict__ rec) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= P) return;
   GapRec R = rec[g];
-  const int64_t i = R.site, r = i / Lx, c = i - r * Lx;
+  const int64_t i = R.site, r = i / Lx, c = i - r * Lx;  // global row / column
   const int64_t nr[4] = {r - 1, r + 1, r, r};
   const int64_t nc[4] = {c, c, c - 1, c + 1};
   uint32_t flags = 0;
@@ -560,8 +580,8 @@ __global__ void __launch_bounds__(256) k_build_records(
   for (int k = 0; k < 4; ++k) {
     int32_t v = 0;
     uint32_t ty = NB_NONE;
-    if (nr[k] >= 0 && nr[k] < Ly && nc[k] >= 0 && nc[k] < Lx) {
-      const int64_t j = nr[k] * Lx + nc[k];
+    if (nr[k] >= lrow0 && nr[k] < lrow1 && nr[k] < Ly && nc[k] >= 0 && nc[k] < Lx) {
+      const int64_t j = (nr[k] - lrow0) * Lx + nc[k];
       if (mask[j]) { ty = NB_KNOWN; v = __float_as_int(phi[j]); }
       else         { ty = NB_GAP;   v = gid[j]; }
     }
@@ -569,7 +589,7 @@ __global__ void __launch_bounds__(256) k_build_records(
     R.nb[k] = v;
   }
   R.flags = flags;
-  R.beta = __fdiv_rn(1.0f, T[i]);
+  R.beta = (r >= trow0 && r < trow1) ? __fdiv_rn(1.0f, T[(r - trow0) * Lx + c]) : 0.0f;
   const int64_t nbx = (Lx + lb - 1) / lb;
   const int64_t b = (r / lb) * nbx + c / lb;
   const long long nk = NK[b];
@@ -630,14 +650,14 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 }  // namespace
 
-void launch_minmax_count(const float* z, const uint8_t* mask, int64_t Lx, int64_t Ly,
+void launch_minmax_count(const float* z, const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base,
                          DevScalars* sc, cudaStream_t st) {
   const int64_t n = Lx * Ly;
   const int g = grid_for((n + 15) / 16, 256);
   if (aligned16(z) && aligned16(mask))
-    k_minmax_count<true><<<g, 256, 0, st>>>(z, mask, Lx, n, sc);
+    k_minmax_count<true><<<g, 256, 0, st>>>(z, mask, Lx, n, row_base, sc);
   else
-    k_minmax_count<false><<<g, 256, 0, st>>>(z, mask, Lx, n, sc);
+    k_minmax_count<false><<<g, 256, 0, st>>>(z, mask, Lx, n, row_base, sc);
 }
 
 void launch_transform(const float* z, const uint8_t* mask, int64_t n, const DevScalars* sc,
@@ -649,22 +669,33 @@ void launch_transform(const float* z, const uint8_t* mask, int64_t n, const DevS
     k_transform<false><<<g, 256, 0, st>>>(z, mask, n, sc, phiK);
 }
 
-void launch_gap_index(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t /*PA*/, int* rowcnt,
-                      int* rowoff, int32_t* gid, GapRec* rec, cudaStream_t st) {
-  k_row_counts<<<static_cast<unsigned>(Ly), 256, 0, st>>>(mask, Lx, Ly, rowcnt);
+void launch_gap_rows(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, int* rowcnt, int* rowoff,
+                     cudaStream_t st) {
+  k_row_counts<<<static_cast<unsigned>(Ly), 256, 0, st>>>(mask, Lx, Ly, row_base, rowcnt);
   k_scan_excl<<<1, 1024, 0, st>>>(rowcnt, 2 * Ly, rowoff);
-  k_row_compact<<<static_cast<unsigned>(Ly), 256, 0, st>>>(mask, Lx, Ly, rowoff, gid, rec);
 }
 
-void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int64_t Ly, int lb,
-                        float q, long long* SB, long long* NB, long long* SP, long long* NK,
-                        int64_t nblocks, cudaStream_t st) {
+void launch_gap_compact(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, const int* rowoff,
+                        int32_t* gid, GapRec* rec, cudaStream_t st) {
+  k_row_compact<<<static_cast<unsigned>(Ly), 256, 0, st>>>(mask, Lx, Ly, row_base, rowoff, gid, rec);
+}
+
+void launch_gap_index(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, int* rowcnt,
+                      int* rowoff, int32_t* gid, GapRec* rec, cudaStream_t st) {
+  launch_gap_rows(mask, Lx, Ly, row_base, rowcnt, rowoff, st);
+  launch_gap_compact(mask, Lx, Ly, row_base, rowoff, gid, rec, st);
+}
+
+void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t lrow0,
+                        int64_t row0, int64_t row1, int lb, float q, long long* SB, long long* NB,
+                        long long* SP, long long* NK, int64_t nblocks, cudaStream_t st) {
   cudaMemsetAsync(SB, 0, sizeof(long long) * nblocks, st);
   cudaMemsetAsync(NB, 0, sizeof(long long) * nblocks, st);
   cudaMemsetAsync(SP, 0, sizeof(long long) * nblocks, st);
   cudaMemsetAsync(NK, 0, sizeof(long long) * nblocks, st);
-  dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((Ly + kTile - 1) / kTile));
-  k_block_stats<<<grid, 256, 0, st>>>(phiK, mask, Lx, Ly, lb, q, SB, NB, SP, NK);
+  const int64_t tile0 = (row0 / kTile) * kTile;
+  dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((row1 - tile0 + kTile - 1) / kTile));
+  k_block_stats<<<grid, 256, 0, st>>>(phiK, mask, Lx, Ly, lrow0, row0, row1, lb, q, SB, NB, SP, NK);
 }
 
 void launch_block_T(const long long* SB, const long long* NB, const long long* SP,
@@ -679,11 +710,11 @@ void launch_median_fill(float* Tb, const long long* NB, int64_t nblocks, DevScal
   k_median_fill<<<1, 1024, 0, st>>>(Tb, NB, nblocks, sc);
 }
 
-void launch_expand(const float* Tb, int64_t Lx, int64_t Ly, int lb, float* T, cudaStream_t st) {
-  k_expand<<<grid_for(Lx * Ly, 256), 256, 0, st>>>(Tb, Lx, Ly, lb, T);
+void launch_expand(const float* Tb, int64_t Lx, int64_t trow0, int64_t trow1, int lb, float* T, cudaStream_t st) {
+  k_expand<<<grid_for(Lx * (trow1 - trow0), 256), 256, 0, st>>>(Tb, Lx, trow0, trow1, lb, T);
 }
 
-void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int rs,
+void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int64_t row_base, int64_t Ly_g, int rs,
                    cudaStream_t st) {
   // 32 x 64 tiles once the grid has >= 16 waves of them on 148 SMs (C4 16384^2: 1.66 -> 1.16
   // ms per pass); 32 x 32 below, where more CTAs hide latency better (1024^2: 10.9 vs 13.6 us)
@@ -698,18 +729,18 @@ void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int rs
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((Ly + TY - 1) / TY));
   if (tall)
-    k_smooth<64><<<grid, 256, smem, st>>>(Tin, Tout, Lx, Ly, rs);
+    k_smooth<64><<<grid, 256, smem, st>>>(Tin, Tout, Lx, Ly, row_base, Ly_g, rs);
   else
-    k_smooth<32><<<grid, 256, smem, st>>>(Tin, Tout, Lx, Ly, rs);
+    k_smooth<32><<<grid, 256, smem, st>>>(Tin, Tout, Lx, Ly, row_base, Ly_g, rs);
 }
 
 void launch_build_records(const int32_t* gid, const uint8_t* mask, const float* phiK,
                           const float* T, const long long* SP, const long long* NK,
-                          const DevScalars* sc, int64_t Lx, int64_t Ly, int lb, int64_t P,
-                          GapRec* rec, cudaStream_t st) {
+                          const DevScalars* sc, int64_t Lx, int64_t Ly, int64_t lrow0, int64_t lrow1,
+                          int64_t trow0, int64_t trow1, int lb, int64_t P, GapRec* rec, cudaStream_t st) {
   if (P == 0) return;
-  k_build_records<<<static_cast<unsigned>((P + 255) / 256), 256, 0, st>>>(gid, mask, phiK, T, SP, NK,
-                                                                         sc, Lx, Ly, lb, P, rec);
+  k_build_records<<<static_cast<unsigned>((P + 255) / 256), 256, 0, st>>>(gid, mask, phiK, T, SP, NK, sc, Lx, Ly,
+                                                                         lrow0, lrow1, trow0, trow1, lb, P, rec);
 }
 
 void launch_predict(const float* z, const uint8_t* mask, const int32_t* gid, const double* acc,

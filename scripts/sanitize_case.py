@@ -27,15 +27,19 @@ def main():
             m.set_energy_trace(False)
             m.simulate_adaptive(3, 4, n_fit=5, n_f=2, max_sweeps=20)
             m.predict()
-            m.reset_accumulator()
-            m.slab_begin(4, 3, 1, 0, 4, 10, 30)
-            for s in range(1, 4):
-                for c in (0, 1):
-                    m.slab_half_sweep(s, c)
-            m.row_view(10, 0)
-            m.slab_end()
-            m.predict()
         m.close()
+    # row slabs: three contexts joined by the in-process communicator
+    from paper_2212_01317_b200.sharding import run_group
+
+    def slab(rank, g):
+        m = P.LeMpr(P.Config(l_b=8, n_s=2, r_s=1, group=g, group_rank=rank, shard="rows"), calib)
+        m.set_data(z, mask)
+        m.estimate_local_params()
+        m.simulate(4, 3, 1)
+        out = m.predict()
+        m.close()
+        return out
+    run_group(3, slab)
     m = P.LeMpr(P.Config(), calib)
     P.mpr_build_calibration(m.ctx, calib[0][:6], L=16, n_eq=5, n_meas=5, reps=2)
     m.close()

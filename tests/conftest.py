@@ -10,6 +10,10 @@ if ROOT not in sys.path:
 
 CALIB_PATH = os.path.join(ROOT, "paper_2212_01317_b200", "data", "calib_q0.5.txt")
 
+# a rank that never reaches a collective of libmpr's in-process communicator fails the
+# test after 2 minutes instead of the library's 10
+os.environ.setdefault("MPR_GROUP_TIMEOUT_S", "120")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libmpr.so")

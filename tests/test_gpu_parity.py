@@ -227,94 +227,181 @@ def test_c2_full_size_sampled(P, calib):
     m.close()
 
 
-def _emulated_slabs(P, z, mask, cfg, calib, M, S, seed, world, halo="copy"):
-    """Row slabs of `world` contexts on one GPU. halo="copy": halo rows exchanged by device
-    copies through the same zero-copy row views the NCCL path sends from and receives
-    into. halo="peer": each context registers its neighbours' state buffers and the
-    half-sweep kernels write the boundary rows into them (the fused exchange); the host
-    only finishes every context's half-sweep before the next one starts."""
+def group_run(P, z, mask, cfg_kw, calib, M, S, seed, world, shard="rows", ordered=False, energy=False,
+              device_input=False, states=True):
+    """`world` contexts on this GPU joined by libmpr's in-process communicator (one host
+    thread each), every one running the SPMD call sequence with shard="rows" or
+    "realizations"; returns each rank's results (own rows of the Lx*Ly debug buffers)."""
     import torch
+    from paper_2212_01317_b200.sharding import row_range, run_group
+    Ly, Lx = z.shape
+
+    def fn(rank, g):
+        cfg = P.Config(**cfg_kw, group=g, group_rank=rank, shard=shard, ordered_reduce=ordered)
+        m = P.LeMpr(cfg, calib)
+        try:
+            if device_input:  # row slabs: the device buffers hold the own rows only
+                r0, r1 = row_range(Ly, world, rank) if shard == "rows" else (0, Ly)
+                zd = torch.from_numpy(np.ascontiguousarray(np.nan_to_num(z[r0:r1]))).cuda()
+                md = torch.from_numpy(np.ascontiguousarray(mask[r0:r1])).cuda()
+                m.set_data_device(zd.data_ptr(), md.data_ptr(), Lx, Ly)
+            else:
+                m.set_data(z, mask)
+            m.set_energy_trace(energy)
+            T = m.estimate_local_params(want_T=True)
+            m.simulate(M, S, seed)
+            out = dict(T=T, pred=m.predict(), rows=m.predict_rows(), info=m.info(),
+                       stats=m.debug(P.binding.MPR_BUF_BLOCK_STATS), Tb=m.debug(P.binding.MPR_BUF_BLOCK_T),
+                       phiK=m.debug(P.binding.MPR_BUF_PHI_KNOWN))
+            inf = out["info"]
+            if states:
+                lo, hi = inf["last_m_base"], min(inf["last_m_base"] + inf["last_batch"], M)
+                out["states"] = {r: m.debug(P.binding.MPR_BUF_STATE, r) for r in range(lo, hi)}
+            if energy:
+                out["energy"] = m.debug(P.binding.MPR_BUF_ENERGY)
+            return out
+        finally:
+            m.close()
+
+    return run_group(world, fn)
+
+
+def check_row_slabs(P, z, mask, cfg_kw, calib, M, S, seed, world, energy=True, device_input=False):
+    """Every rank of a row-slab run against the oracle: block sums (global on every rank),
+    z_min / z_max, the own rows of phi, T and the last batch's states bitwise, the energy
+    trace bitwise, the all-gathered predictions bitwise (n_avg = 1), and slab-local memory
+    (a rank holds its own rows' gap sites plus one ghost row per side)."""
     from paper_2212_01317_b200.sharding import row_range
-    Ly = z.shape[0]
-    engs = [P.LeMpr(cfg, calib) for _ in range(world)]
-    ranges = [row_range(Ly, world, w) for w in range(world)]
-    from paper_2212_01317_b200.sharding import slab_realization_chunks
-    for e in engs:
-        e.set_data(z, mask); e.estimate_local_params(); e.reset_accumulator()
-    for c0, c1 in slab_realization_chunks(M):  # the same realization split as bench / sharding
-        for e, (r0, r1) in zip(engs, ranges):
-            e.slab_begin(M, S, seed, c0, c1, r0, r1)
-        if halo == "peer":
-            for w, e in enumerate(engs):
-                if w > 0:
-                    e.set_peer(0, dev_ptr=engs[w - 1].state_device())
-                if w < world - 1:
-                    e.set_peer(1, dev_ptr=engs[w + 1].state_device())
-        for s in range(1, S + 1):
-            for colour in (0, 1):
-                for e in engs:
-                    e.slab_half_sweep(s, colour)
-                for e in engs:
-                    e.sync()
-                for w in range(world - 1 if halo == "copy" else 0):  # boundary between slab w and w+1
-                    r = ranges[w][1]
-                    engs[w + 1].row_view(r - 1, colour).copy_(engs[w].row_view(r - 1, colour))  # w's last row
-                    engs[w].row_view(r, colour).copy_(engs[w + 1].row_view(r, colour))          # w+1's first row
-                torch.cuda.synchronize()
-        for e in engs:
-            e.slab_end()
-    total = sum(e.accumulator_tensor().clone() for e in engs)
-    engs[0].accumulator_tensor().copy_(total)
-    torch.cuda.synchronize()
-    pred = engs[0].predict()
-    for e in engs:
-        e.close()
-    return pred
+    cfg = P.Config(**cfg_kw)
+    Tk, ek = calib
+    o = O.fill(z, mask, ocfg(cfg), Tk, ek, M, S, seed, energy=energy, states=True)
+    p = o["params"]
+    SB, NB, SP, NK = O.block_stats(p.phi0, mask, cfg.l_b, cfg.q)
+    res = group_run(P, z, mask, cfg_kw, calib, M, S, seed, world, energy=energy, device_input=device_input)
+    Ly, Lx = z.shape
+    gaps = mask == 0
+    for rank, g in enumerate(res):
+        r0, r1 = row_range(Ly, world, rank)
+        inf = g["info"]
+        assert (inf["rank"], inf["world"], inf["row_begin"], inf["row_end"]) == (rank, world, r0, r1)
+        assert inf["n_gaps"] == int(gaps.sum()) and inf["z_min"] == p.zmin and inf["z_max"] == p.zmax
+        local = int(gaps[max(r0 - 1, 0):min(r1 + 1, Ly)].sum())
+        assert inf["n_gaps_local"] == local, "slab-local gap sites: own rows + ghost rows"
+        for k, ref in enumerate((SB, NB, SP, NK)):
+            assert np.array_equal(g["stats"][k], ref.ravel()), f"rank {rank}: block statistic {k}"
+        assert_bitwise(g["Tb"], p.Tb.ravel(), f"rank {rank}: block temperatures")
+        assert_bitwise(g["phiK"][r0:r1], p.phi0[r0:r1], f"rank {rank}: phi at samples")
+        assert_bitwise(g["T"][r0:r1], p.T[r0:r1], f"rank {rank}: temperature rows")
+        for r, st in g["states"].items():
+            assert_bitwise(st[r0:r1], o["sim"]["phi"][r][r0:r1], f"rank {rank}: state rows of realization {r}")
+        if cfg.n_avg == 1:
+            assert_bitwise(g["pred"], o["pred"], f"rank {rank}: predictions")
+            assert_bitwise(g["rows"], o["pred"][r0:r1], f"rank {rank}: own prediction rows")
+        else:
+            assert np.max(np.abs(g["pred"][gaps] - o["pred"][gaps])) <= 1e-3 * (p.zmax - p.zmin)
+        if energy:
+            assert_bitwise(g["energy"], o["sim"]["energy"], f"rank {rank}: energy trace")
+    return res
 
 
-@pytest.mark.parametrize("halo", ["copy", "peer"])
-@pytest.mark.parametrize("world", [2, 3, 5])
-def test_row_slabs_emulated_bit_exact(P, calib, world, halo):
-    """Row-slab mode: slabs with one-row halo exchanges (row copies, or
-    the kernels writing into the neighbours' buffers) reproduce the single-context
-    predictions bit for bit (and therefore the oracle's)."""
+@pytest.mark.parametrize("world", [2, 3, 5, 8])
+def test_row_slabs_distributed_bit_exact(P, calib, world):
+    """Row slabs inside libmpr (MPR_SHARD_ROWS) on `world` contexts: the
+    distributed parameter stage, the halo exchange after every colour half-sweep and the
+    all-gathered predictions reproduce the oracle bit for bit on every rank."""
     truth, z, mask = make_problem(61, 0.5, Lx=52, corr_len=6.0)
-    cfg = P.Config(l_b=8, n_s=2, r_s=1)
-    ref = gpu_run(P, z, mask, cfg, calib, 6, 10, 123)["pred"]
-    got = _emulated_slabs(P, z, mask, cfg, calib, 6, 10, 123, world, halo=halo)
-    assert_bitwise(got, ref, f"row slabs x{world} ({halo})")
+    check_row_slabs(P, z, mask, dict(l_b=8, n_s=2, r_s=1), calib, 6, 10, 123, world)
 
 
-def _ipc_slab_worker(rank, world, port, out):
-    import os
-    import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    import paper_2212_01317_b200 as P
-    from paper_2212_01317_b200.sharding import distributed_fill_slabs
-    truth, z, mask = make_problem(61, 0.5, Lx=52, corr_len=6.0)
-    eng = P.LeMpr(P.Config(l_b=8, n_s=2, r_s=1), P.load_calibration())
-    out[rank] = distributed_fill_slabs(eng, z, mask, M=6, sweeps=10, seed=123, halo="peer")
-    eng.close()
-    dist.destroy_process_group()
+def test_row_slabs_device_input_wide_halo_random_init(P, calib):
+    """Device-resident own-row inputs (mpr_set_data_device with the slab's rows only), an SST
+    halo r_s n_s = 6 wider than a slab, RANDOM init, cloud gaps, M = 4k + 2 realizations."""
+    truth, z, mask = make_problem(40, 0.6, Lx=33, gaps="cloud", corr_len=5.0)
+    check_row_slabs(P, z, mask, dict(l_b=4, n_s=3, r_s=2, init="random"), calib, 10, 7, 77, 4, device_input=True)
 
 
-def test_row_slabs_ipc_peer_halo_two_processes(P, calib):
-    """The multi-process form of the fused halo: two processes (one GPU here, so both map
-    each other's state buffer with cudaIpcOpenMemHandle), handles all-gathered over a gloo
-    group, boundary rows written by the kernels, sync + barrier per half-sweep. Both ranks'
-    predictions equal the single-context run bit for bit."""
-    import socket
-    import torch.multiprocessing as mp
-    with socket.socket() as sk:
-        sk.bind(("127.0.0.1", 0))
-        port = sk.getsockname()[1]
-    out = mp.get_context("spawn").Manager().dict()
-    mp.spawn(_ipc_slab_worker, args=(2, port, out), nprocs=2, join=True)
-    truth, z, mask = make_problem(61, 0.5, Lx=52, corr_len=6.0)
-    ref = gpu_run(P, z, mask, P.Config(l_b=8, n_s=2, r_s=1), calib, 6, 10, 123)["pred"]
-    for r in range(2):
-        assert_bitwise(out[r], ref, f"IPC peer-halo slabs, rank {r}")
+def test_row_slabs_mpr_one_block_and_n_avg(P, calib):
+    """Uniform MPR (one block spanning every slab: its sums come from all ranks) and n_avg > 1."""
+    truth, z, mask = make_problem(37, 0.5, Lx=29, corr_len=6.0)
+    check_row_slabs(P, z, mask, dict(l_b=64, n_s=0), calib, 4, 8, 5, 3)
+    check_row_slabs(P, z, mask, dict(l_b=8, n_s=1, r_s=1, n_avg=3), calib, 4, 8, 6, 2, energy=False)
+
+
+@pytest.mark.parametrize("ordered", [False, True])
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_realization_shards_distributed(P, calib, world, ordered):
+    """Realization shards inside libmpr (MPR_SHARD_REALIZATIONS): the rank's pair-aligned id
+    range (= sharding.shard_range), then the all-reduce (equal up to fp64 reassociation) or
+    the rank-ordered chain (bit-identical); the energy trace summed over the ranks."""
+    from paper_2212_01317_b200.sharding import shard_range
+    truth, z, mask = make_problem(48, 0.45, Lx=41, corr_len=6.0)
+    M, S, seed = 11, 9, 4242
+    Tk, ek = calib
+    cfg = P.Config()
+    o = O.fill(z, mask, ocfg(cfg), Tk, ek, M, S, seed, energy=True)
+    res = group_run(P, z, mask, {}, calib, M, S, seed, world, shard="realizations", ordered=ordered, energy=True,
+                    states=False)
+    rng = o["params"].zmax - o["params"].zmin
+    for rank, g in enumerate(res):
+        assert (g["info"]["m_begin"], g["info"]["m_end"]) == shard_range(M, world, rank)
+        if ordered:
+            assert_bitwise(g["pred"], o["pred"], f"rank {rank}: ordered-reduce predictions")
+        else:
+            assert np.max(np.abs(g["pred"] - o["pred"])) <= 1e-6 * rng
+        assert_bitwise(g["energy"], o["sim"]["energy"], f"rank {rank}: energy trace")
+        assert_bitwise(g["pred"], res[0]["pred"], "every rank holds the same predictions")
+
+
+def test_adaptive_realization_shards_distributed(P, calib):
+    """The adaptive protocol (row f1) with realization shards: each rank decides its own
+    realizations on the device; s_eq and the accumulators are summed over the ranks."""
+    from paper_2212_01317_b200.sharding import run_group
+    truth, z, mask = make_problem(40, 0.5, corr_len=6.0)
+    M, seed = 7, 13
+    Tk, ek = calib
+    cfg = P.Config(n_avg=2)
+    oc = ocfg(cfg)
+    p = O.parameters(z, mask, oc, Tk, ek)
+    r = O.simulate_adaptive(p, mask, oc, M, seed, n_fit=8, n_f=3, S_max=60, slope_tol=1e-4)
+    ref = O.predict(np.nan_to_num(z), mask, r["acc"], M, 2, p.zmin, p.zmax, 0)
+
+    def fn(rank, g):
+        m = P.LeMpr(P.Config(n_avg=2, group=g, group_rank=rank), calib)
+        m.set_data(z, mask); m.estimate_local_params()
+        s_eq = m.simulate_adaptive(M, seed, n_fit=8, n_f=3, max_sweeps=60, slope_tol=1e-4)
+        pred = m.predict()
+        m.close()
+        return s_eq, pred
+    for s_eq, pred in run_group(3, fn):
+        assert s_eq.tolist() == r["s_eq"].tolist()
+        assert np.max(np.abs(pred - ref)) <= 1e-3 * (p.zmax - p.zmin)
+
+
+def test_nccl_transport_world1(P, calib, monkeypatch):
+    """The NCCL transport on the device: a communicator made through libmpr
+    (mpr_nccl_unique_id / mpr_nccl_comm_init, libnccl resolved at run time) and, with
+    MPR_FORCE_COMM=1, the multi-rank code paths at world size 1 — every all-reduce,
+    broadcast and the predictions' all-gather run as real NCCL operations on the stream
+    (neighbour exchanges have no peers at world 1). Results equal the single context."""
+    monkeypatch.setenv("MPR_FORCE_COMM", "1")
+    truth, z, mask = make_problem(40, 0.5, corr_len=6.0)
+    ref = gpu_run(P, z, mask, P.Config(l_b=8), calib, 6, 8, 3)
+    uid = P.mpr_nccl_unique_id()
+    comm = P.mpr_nccl_comm_init(1, 0, uid, 0)
+    try:
+        for shard, ordered in (("rows", False), ("realizations", False), ("realizations", True)):
+            m = P.LeMpr(P.Config(l_b=8, nccl_comm=comm, shard=shard, ordered_reduce=ordered), calib)
+            m.set_data(z, mask)
+            T = m.estimate_local_params(want_T=True)
+            m.simulate(6, 8, 3)
+            pred = m.predict()
+            inf = m.info()
+            m.close()
+            assert inf["world"] == 1 and inf["comm_calls"] > 0, (shard, inf["comm_calls"])
+            assert_bitwise(T, ref["T"], f"T ({shard})")
+            assert_bitwise(pred, ref["pred"], f"predictions ({shard}, ordered={ordered})")
+    finally:
+        P.mpr_nccl_comm_destroy(comm)
 
 
 def _full_size_sampled(P, calib, L, p, gaps, nu, M, S, windows):
@@ -460,34 +547,6 @@ def test_dc_rejects_sc_only_features(P, calib):
     m.close()
 
 
-def test_nccl_allreduce_on_accumulator_view(P, calib):
-    """The bench's N>1 path in miniature: an NCCL process group (world size 1 here) reduces
-    the library-owned accumulator in place through the zero-copy torch view."""
-    import os
-    import socket
-    import torch
-    import torch.distributed as dist
-    from paper_2212_01317_b200.sharding import allreduce_accumulator, distributed_fill
-    s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
-    try:
-        truth, z, mask = make_problem(40, 0.5, corr_len=6.0)
-        m = P.LeMpr(P.Config(l_b=8), calib, stream=torch.cuda.current_stream().cuda_stream)
-        pred = distributed_fill(m, z, mask, M=6, sweeps=8, seed=3)
-        acc = m.accumulator_tensor()
-        before = acc.clone()
-        dist.all_reduce(acc)          # in place on the library's buffer
-        allreduce_accumulator(acc)    # world size 1: no-op
-        torch.cuda.synchronize()
-        assert torch.equal(acc, before)
-        ref = gpu_run(P, z, mask, P.Config(l_b=8), calib, 6, 8, 3)["pred"]
-        assert_bitwise(pred, ref, "distributed_fill at world size 1")
-        m.close()
-    finally:
-        dist.destroy_process_group()
-
-
 def test_adaptive_with_slope_tolerance(P, calib):
     """The relaxed test (slope_tol > 0) stops earlier and still agrees with the oracle."""
     Tk, ek = calib
@@ -579,7 +638,7 @@ def test_fuzz_small_problems_bit_exact(P, calib, k):
 
 
 def test_context_lifecycle_releases_device_memory(P, calib):
-    """20 full init -> fill -> destroy cycles (graphs, batches, energy buffers, slabs)
+    """20 full init -> fill -> destroy cycles (graphs, batches, energy buffers, row slabs)
     leave the device's free memory where it was: the context frees what it allocates."""
     import torch
     truth, z, mask = make_problem(96, 0.5, corr_len=8.0)
@@ -591,15 +650,9 @@ def test_context_lifecycle_releases_device_memory(P, calib):
         m.estimate_local_params()
         m.simulate(6, 5, k)
         m.predict()
-        if k % 4 == 1:
-            m.set_energy_trace(False)  # slab mode has no energy trace
-            m.reset_accumulator()
-            m.slab_begin(4, 3, k, 0, 4, 0, 48)
-            for s in range(1, 4):
-                for colour in (0, 1):
-                    m.slab_half_sweep(s, colour)
-            m.slab_end()
         m.close()
+        if k % 4 == 1:  # row slabs: two contexts joined by the in-process communicator
+            group_run(P, z, mask, {}, calib, 4, 3, k, 2, energy=True)
 
     cycle(0)  # first use: lazily created device state (CUDA context, module load)
     torch.cuda.synchronize()
@@ -708,30 +761,24 @@ def test_fuzz_adaptive_protocol_matches_oracle(P, calib, k):
 
 
 @pytest.mark.parametrize("k", range(int(__import__("os").environ.get("MPR_FUZZ_SLAB_CASES", "12"))))
-def test_fuzz_row_slabs_match_single_context(P, calib, k):
-    """Row slabs randomised: random grids, world sizes 2..5 (contexts on one GPU), halo by
-    row copies or by the kernels writing into the neighbours' buffers, n_avg, M (chunks of
-    4k + remainder): predictions equal the single-context run bit for bit (n_avg = 1) or
-    within the n_avg tolerance."""
+def test_fuzz_row_slabs_match_oracle(P, calib, k):
+    """Row slabs randomised: random grids, world sizes 2..8 (contexts on one GPU joined by the
+    in-process communicator), l_b, r_s, n_s, init, n_avg, M, S: every rank bit-exact against
+    the oracle (predictions within the n_avg tolerance when n_avg > 1)."""
     rng = np.random.default_rng(8000 + k)
     Ly, Lx = int(rng.integers(12, 70)), int(rng.integers(6, 60))
     truth, z, mask = make_problem(Ly, float(rng.uniform(0.2, 0.8)), Lx=Lx, corr_len=float(rng.uniform(2, 10)),
                                   seed_field=int(rng.integers(1 << 30)), seed_mask=int(rng.integers(1 << 30)))
     n_avg = int(rng.integers(1, 3))
-    cfg = P.Config(l_b=int(rng.integers(4, 24)), n_s=int(rng.integers(0, 3)), r_s=1, n_avg=n_avg,
-                   init="random" if rng.random() < 0.5 else "block_mean")
+    kw = dict(l_b=int(rng.integers(2, 24)), n_s=int(rng.integers(0, 4)), r_s=int(rng.integers(0, 4)), n_avg=n_avg,
+              init="random" if rng.random() < 0.5 else "block_mean")
     M, S = int(rng.integers(1, 11)), int(rng.integers(n_avg, 9))
-    world = int(rng.integers(2, min(5, Ly // 2) + 1))
-    halo = "peer" if rng.random() < 0.5 else "copy"
+    world = int(rng.integers(2, min(8, Ly) + 1))
     Tk, ek = calib
-    if O.parameters(z, mask, ocfg(cfg), Tk, ek).status < 0:
+    if O.parameters(z, mask, ocfg(P.Config(**kw)), Tk, ek).status < 0:
         pytest.skip("problem rejected by the oracle (covered by the fixed-S fuzz)")
-    ref = gpu_run(P, z, mask, cfg, calib, M, S, 99 + k)["pred"]
-    got = _emulated_slabs(P, z, mask, cfg, calib, M, S, 99 + k, world, halo=halo)
-    if n_avg == 1:
-        assert_bitwise(got, ref, f"row slabs x{world} ({halo})")
-    else:
-        assert np.max(np.abs(got - ref)) <= 1e-5 * (np.nanmax(z) - np.nanmin(z))
+    check_row_slabs(P, z, mask, kw, calib, M, S, 99 + k, world, energy=n_avg == 1,
+                    device_input=bool(rng.random() < 0.5))
 
 
 @pytest.mark.parametrize("world,M", [(2, 12), (3, 10), (4, 7), (2, 100)])
