@@ -58,8 +58,8 @@ def parse():
     ap.add_argument("--M", type=int, default=None, help="realizations (per rank for weak-scaling configs)")
     ap.add_argument("--sweeps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-realizations", type=int, default=8)
-    ap.add_argument("--ref-sample-realizations", type=int, default=8)
+    ap.add_argument("--cpu-sample-realizations", type=int, default=100)
+    ap.add_argument("--ref-sample-realizations", type=int, default=20)
     ap.add_argument("--cpu-threads", type=int, default=0, help="oracle threads (0 = all host cores)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")

@@ -197,8 +197,9 @@ mpr_status mpr_simulate(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed);
  * sweep. Replaces any previous accumulation; predict as after mpr_simulate. The test
  * runs on the device after each check sweep (fp64, ARITH §K operation order); the host
  * trails one check behind, so sweeps issued after the last realization finished are
- * no-ops. Errors: M < 1, n_fit < 3, n_f < 1, max_sweeps <= n_avg, slope_tol < 0 ->
- * INVALID_ARG. */
+ * no-ops. Realization shards: each rank runs its id range; the accumulators and s_eq are
+ * summed over the ranks (every rank gets all M decisions). Errors: M < 1, n_fit < 3,
+ * n_f < 1, max_sweeps <= n_avg, slope_tol < 0, MPR_SHARD_ROWS with W > 1 -> INVALID_ARG. */
 mpr_status mpr_simulate_adaptive(mpr_ctx *ctx, int64_t M, uint64_t seed, int32_t n_fit, int32_t n_f,
                                  int32_t max_sweeps, double slope_tol, int32_t *s_eq_out);
 
@@ -215,11 +216,13 @@ mpr_status mpr_simulate_adaptive(mpr_ctx *ctx, int64_t M, uint64_t seed, int32_t
 mpr_status mpr_build_calibration(mpr_ctx *ctx, const float *T, int32_t K, int32_t L, float q, int32_t n_eq,
                                  int32_t n_meas, int32_t reps, uint64_t seed, float *e_out, double *e_raw_out);
 
-/* Multi-rank building block (realization sharding): simulate global realization
- * ids [m_begin, m_end) of an M-realization run and ADD them to the accumulator
- * (reset it first with mpr_reset_accumulator). The result of mpr_predict after all
- * ranks' accumulators are summed (mpr_accumulator_device + an all-reduce) equals
- * the single-call mpr_simulate(M) up to fp64 summation order. */
+/* Building block below mpr_simulate (no collective of its own): simulate global
+ * realization ids [m_begin, m_end) of an M-realization run and ADD them to the
+ * accumulator (reset it first with mpr_reset_accumulator). Summing the accumulators of
+ * ranks that ran disjoint ranges (mpr_accumulator_device + an external all-reduce) equals
+ * the single-call mpr_simulate(M) up to fp64 summation order. With MPR_SHARD_ROWS every
+ * rank must call it with the same range (the halo exchanges run inside); the energy
+ * trace is then per-rank partial (mpr_simulate sums it). */
 mpr_status mpr_reset_accumulator(mpr_ctx *ctx);
 mpr_status mpr_simulate_range(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed,
                               int64_t m_begin, int64_t m_end);
@@ -231,8 +234,9 @@ mpr_status mpr_simulate_range(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t 
  * accumulator holds at that moment. Chaining the ranks in rank order is then bit-identical
  * to one GPU: each rank receives the accumulator of the ranks before it (for example
  * NCCL recv into mpr_accumulator_device), accumulates its own realizations, and sends the
- * result on; the last rank broadcasts it. The adaptive protocol and row slabs ignore the
- * setting. A pending deferred batch blocks further simulate calls (STATE) until it is
+ * result on; the last rank broadcasts it (mpr_config.ordered_reduce does exactly this
+ * inside mpr_simulate). The adaptive protocol ignores the setting; row slabs reject it.
+ * A pending deferred batch blocks further simulate calls (STATE) until it is
  * accumulated; set_data drops it. */
 mpr_status mpr_set_deferred_reduce(mpr_ctx *ctx, int enable);
 mpr_status mpr_accumulate_states(mpr_ctx *ctx);
