@@ -415,13 +415,12 @@ mpr_status stage_data(mpr_ctx* c) {
   CK(c->rec.ensure(sizeof(GapRec) * std::max<int64_t>(c->P, 1)), "alloc records");
   if (!c->rows) {
     launch_gap_index(c->mask.as<uint8_t>(), c->Lx, nl, 0, c->rowcnt.as<int>(), c->rowoff.as<int>(), c->gid.as<int32_t>(),
-                     c->rec.as<GapRec>(), st);
+                     st);
     c->total_launches += 3;
     c->own[0][0] = 0; c->own[0][1] = c->PA;
     c->own[1][0] = c->PA; c->own[1][1] = c->P;
   } else {
-    launch_gap_compact(c->mask.as<uint8_t>(), c->Lx, nl, c->lrow0, c->rowoff.as<int>(), c->gid.as<int32_t>(),
-                       c->rec.as<GapRec>(), st);
+    launch_gap_compact(c->mask.as<uint8_t>(), c->Lx, nl, c->lrow0, c->rowoff.as<int>(), c->gid.as<int32_t>(), st);
     CKL("gap_compact");
     slab_ranges(c);
   }
@@ -492,6 +491,8 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
   // the 2-realization batch runs the one-pair kernel). Only for large grids: a separate 2-realization batch costs a full launch sequence,
   // which small, latency-bound problems do not win back (256^2..1024^2, M = 10: measured
   // 0.36 -> 0.50 ms and 1.25 -> 1.39 ms when split; 16384^2: 3.85 -> 3.40 ms / half-sweep).
+  // (A 5-pair-per-thread kernel running R = 10 as one batch with float2 moves was measured
+  // slower at C4: 3.65 ms per half-sweep against 2.21 + 0.78 ms for 8 + 2; dropped.)
   if ((c->sweep_variant == 22 || c->sweep_variant == 28) && B % 4 == 2 && B > 2 && c->P >= c->split_min_P)
     B -= 2;
   c->batch_key_P = c->P;
@@ -684,11 +685,23 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   CKL("block_T");
   launch_median_fill(c->Tb.as<float>(), NB, c->nblocks, dsc, st);
   CKL("median_fill");
-  // a5 on the local temperature rows [trow0, trow1) (the whole grid unless row slabs)
-  launch_expand(c->Tb.as<float>(), c->Lx, c->trow0, c->trow1, lb, c->T.as<float>(), st);
-  CKL("expand");
-  for (int k = 0; k < c->cfg.n_s; ++k) {
-    launch_smooth(c->T.as<float>(), c->T2.as<float>(), c->Lx, c->trow1 - c->trow0, c->trow0, c->Ly, c->cfg.r_s, st);
+  // a5 on the local temperature rows [trow0, trow1) (the whole grid unless row slabs). With a
+  // specialised radius the first pass reads the block temperatures directly (no expanded
+  // field is written); otherwise expand, then the generic passes.
+  const int64_t nTr = c->trow1 - c->trow0;
+  int k0 = 0;
+  if (c->cfg.n_s > 0 && launch_smooth_specialised(nullptr, c->Tb.as<float>(), c->T.as<float>(), c->Lx, nTr, c->trow0,
+                                                  c->Ly, c->cfg.r_s, lb, st)) {
+    CKL("smooth (from T_b)");
+    k0 = 1;
+  } else {
+    launch_expand(c->Tb.as<float>(), c->Lx, c->trow0, c->trow1, lb, c->T.as<float>(), st);
+    CKL("expand");
+  }
+  for (int k = k0; k < c->cfg.n_s; ++k) {
+    if (!launch_smooth_specialised(c->T.as<float>(), nullptr, c->T2.as<float>(), c->Lx, nTr, c->trow0, c->Ly,
+                                   c->cfg.r_s, lb, st))
+      launch_smooth(c->T.as<float>(), c->T2.as<float>(), c->Lx, nTr, c->trow0, c->Ly, c->cfg.r_s, st);
     CKL("smooth");
     std::swap(c->T, c->T2);
   }

@@ -54,13 +54,14 @@ void launch_minmax_count(const float* z, const uint8_t* mask, int64_t Lx, int64_
 void launch_transform(const float* z, const uint8_t* mask, int64_t n, const DevScalars* sc,
                       float* phiK, cudaStream_t st);
 // gap ids in (colour, local row, column) order: per-row counts + exclusive scan, then the
-// compaction (gid per site, rec[g].site = global site index)
+// compaction (gid per site); the records (site, neighbours, beta, init) are written whole by
+// launch_build_records once the temperatures exist
 void launch_gap_rows(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, int* rowcnt, int* rowoff,
                      cudaStream_t st);
 void launch_gap_compact(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, const int* rowoff,
-                        int32_t* gid, GapRec* rec, cudaStream_t st);
+                        int32_t* gid, cudaStream_t st);
 void launch_gap_index(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, int* rowcnt,
-                      int* rowoff, int32_t* gid, GapRec* rec, cudaStream_t st);
+                      int* rowoff, int32_t* gid, cudaStream_t st);
 // block sums of the own rows [row0, row1) (global) of a buffer starting at global row lrow0
 void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t lrow0,
                         int64_t row0, int64_t row1, int lb, float q, long long* SB, long long* NB,
@@ -73,6 +74,10 @@ void launch_median_fill(float* Tb, const long long* NB, int64_t nblocks, DevScal
 void launch_expand(const float* Tb, int64_t Lx, int64_t trow0, int64_t trow1, int lb, float* T, cudaStream_t st);
 void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int64_t row_base, int64_t Ly_g, int rs,
                    cudaStream_t st);
+// The specialised pass for r_s = 1..8 (false: not specialised, use launch_smooth). Tb non-null:
+// the input is the expansion of the block temperatures (first pass, Tin unused).
+bool launch_smooth_specialised(const float* Tin, const float* Tb, float* Tout, int64_t Lx, int64_t Ly,
+                               int64_t row_base, int64_t Ly_g, int rs, int lb, cudaStream_t st);
 void launch_build_records(const int32_t* gid, const uint8_t* mask, const float* phiK,
                           const float* T, const long long* SP, const long long* NK,
                           const DevScalars* sc, int64_t Lx, int64_t Ly, int64_t lrow0, int64_t lrow1,

@@ -216,8 +216,7 @@ __global__ void __launch_bounds__(1024) k_scan_excl(const int* __restrict__ in, 
 __global__ void __launch_bounds__(256) k_row_compact(const uint8_t* __restrict__ mask, int64_t Lx,
                                                      int64_t Ly, int64_t row_base,
                                                      const int* __restrict__ rowoff,
-                                                     int32_t* __restrict__ gid,
-                                                     GapRec* __restrict__ rec) {
+                                                     int32_t* __restrict__ gid) {
   const int64_t r = blockIdx.x;
   __shared__ int wcnt[2][8];
   __shared__ int base[2];
@@ -242,7 +241,6 @@ __global__ void __launch_bounds__(256) k_row_compact(const uint8_t* __restrict__
       if (gap) {
         const int g = base[col] + rank;
         gid[i] = g;
-        rec[g].site = static_cast<uint32_t>(i + row_base * Lx);  // global site (Philox counter)
       } else {
         gid[i] = -1;
       }
@@ -377,6 +375,128 @@ __global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ p
     if (sNB[t]) atomicAdd(reinterpret_cast<unsigned long long*>(&NB[b]), static_cast<unsigned long long>(sNB[t]));
     if (sSP[t]) atomicAdd(reinterpret_cast<unsigned long long*>(&SP[b]), static_cast<unsigned long long>(sSP[t]));
     if (sNK[t]) atomicAdd(reinterpret_cast<unsigned long long*>(&NK[b]), static_cast<unsigned long long>(sNK[t]));
+  }
+}
+
+// Streaming form of a3 for l_b % 4 == 0 and Lx % 4 == 0 (16-byte aligned rows): a thread owns
+// 4 adjacent columns and walks kRowsPerWarp rows, loading phi (float4) and mask (4 bytes) of
+// each row ONCE — the row below of one step is the current row of the next — and the right
+// neighbour of its 4th column from the next lane (lane 31 loads it). Sums stay in registers
+// until the thread's block row changes, then go to per-CTA shared slots (one warp-reduction
+// per group of lanes sharing a block when l_b / 4 is a power of two) and once per CTA to
+// global memory. A CTA covers 128 columns x 8 warps x kRowsPerWarp rows, aligned to global
+// row multiples so that l_b = 32 tiles never straddle a block row. Integer sums: the result
+// is k_block_stats' bit for bit.
+constexpr int kRowsPerWarp = 8;
+constexpr int kBs4Cols = 128, kBs4Rows = 8 * kRowsPerWarp;
+constexpr int kBs4Slots = (kBs4Cols / 4 + 1) * (kBs4Rows / 4 + 1);  // l_b >= 4
+__global__ void __launch_bounds__(256) k_block_stats4(const float* __restrict__ phi,
+                                                      const uint8_t* __restrict__ mask, int64_t Lx,
+                                                      int64_t Ly, int64_t lrow0, int64_t row0,
+                                                      int64_t row1, int lb, float q,
+                                                      long long* __restrict__ SB,
+                                                      long long* __restrict__ NB,
+                                                      long long* __restrict__ SP,
+                                                      long long* __restrict__ NK) {
+  __shared__ unsigned long long sl[4][kBs4Slots];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int64_t cbase = (int64_t)blockIdx.x * kBs4Cols;
+  const int64_t rbase = (row0 / kBs4Rows) * kBs4Rows + (int64_t)blockIdx.y * kBs4Rows;
+  const int64_t nbx = (Lx + lb - 1) / lb;
+  const int64_t bc0 = cbase / lb, br0 = max(rbase, row0) / lb;
+  const int64_t clast = min(cbase + kBs4Cols, Lx) - 1, rlast = min(rbase + kBs4Rows, row1) - 1;
+  const int nbc = static_cast<int>(clast / lb - bc0 + 1);
+  const int nslots = nbc * static_cast<int>(rlast / lb - br0 + 1);
+  for (int t = threadIdx.x; t < 4 * kBs4Slots; t += blockDim.x) sl[t / kBs4Slots][t % kBs4Slots] = 0ull;
+  __syncthreads();
+  const int64_t c = cbase + 4 * lane;  // first of this thread's 4 columns
+  const bool cin = c < Lx;             // Lx % 4 == 0: all 4 or none
+  const int bcl = cin ? static_cast<int>(c / lb - bc0) : 0;
+  const int grp = lb / 4;                                      // lanes per block column
+  const bool pow2 = grp <= 32 && (grp & (grp - 1)) == 0 && (cbase % lb) == 0;
+  const int64_t ra = max(rbase + wp * kRowsPerWarp, row0), rz = min(rbase + (wp + 1) * kRowsPerWarp, row1);
+  long long sb = 0, sp = 0;
+  int nb = 0, nk = 0;
+  int64_t cur_br = ra < rz ? ra / lb : -1;
+  auto flush = [&](int64_t br) {
+    // every lane of the warp calls this together (warp-uniform row loop)
+    const int slot = static_cast<int>(br - br0) * nbc + bcl;
+    long long v[4] = {sb, static_cast<long long>(nb), sp, static_cast<long long>(nk)};
+    if (pow2) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        for (int o = 1; o < grp; o <<= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    if (cin && (!pow2 || (lane % grp) == 0)) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (v[k]) atomicAdd(&sl[k][slot], static_cast<unsigned long long>(v[k]));
+    }
+    sb = sp = 0;
+    nb = nk = 0;
+  };
+  float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t m = 0;
+  if (ra < rz && cin) {
+    const int64_t i = (ra - lrow0) * Lx + c;
+    p = *reinterpret_cast<const float4*>(phi + i);
+    m = *reinterpret_cast<const uint32_t*>(mask + i);
+  }
+  for (int64_t r = ra; r < rz; ++r) {
+    const int64_t br = r / lb;
+    if (br != cur_br) {
+      flush(cur_br);
+      cur_br = br;
+    }
+    const bool down = r + 1 < Ly;
+    float4 pn = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t mn = 0;
+    if (down && cin) {
+      const int64_t i = (r + 1 - lrow0) * Lx + c;
+      pn = *reinterpret_cast<const float4*>(phi + i);
+      mn = *reinterpret_cast<const uint32_t*>(mask + i);
+    }
+    // right neighbour of the 4th column: the next lane's first, lane 31 loads it
+    float pr = __shfl_down_sync(0xffffffffu, p.x, 1);
+    uint32_t mr = __shfl_down_sync(0xffffffffu, m, 1) & 0xffu;
+    if (lane == 31) {
+      pr = 0.f;
+      mr = 0;
+      if (cin && c + 4 < Lx) {
+        const int64_t i = (r - lrow0) * Lx + c + 4;
+        pr = phi[i];
+        mr = mask[i];
+      }
+    }
+    const float pv[5] = {p.x, p.y, p.z, p.w, pr};
+    const float pd[4] = {pn.x, pn.y, pn.z, pn.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool kj = (m >> (8 * j)) & 0xffu;
+      if (!kj) continue;
+      sp += __float2ll_rn(__fmul_rn(pv[j], 0x1p28f));
+      nk += 1;
+      const bool kr = j < 3 ? ((m >> (8 * (j + 1))) & 0xffu) != 0 : mr != 0;
+      if (kr) {  // right bond (c + j + 1 < Lx: a column past the edge has mask 0)
+        sb += __float2ll_rn(__fmul_rn(cos_spec(__fmul_rn(q, __fsub_rn(pv[j], pv[j + 1]))), 0x1p32f));
+        nb += 1;
+      }
+      if ((mn >> (8 * j)) & 0xffu) {  // down bond
+        sb += __float2ll_rn(__fmul_rn(cos_spec(__fmul_rn(q, __fsub_rn(pv[j], pd[j]))), 0x1p32f));
+        nb += 1;
+      }
+    }
+    p = pn;
+    m = mn;
+  }
+  if (cur_br >= 0) flush(cur_br);
+  __syncthreads();
+  for (int t = threadIdx.x; t < nslots; t += blockDim.x) {
+    const int64_t b = (br0 + t / nbc) * nbx + (bc0 + t % nbc);
+    if (sl[0][t]) atomicAdd(reinterpret_cast<unsigned long long*>(&SB[b]), sl[0][t]);
+    if (sl[1][t]) atomicAdd(reinterpret_cast<unsigned long long*>(&NB[b]), sl[1][t]);
+    if (sl[2][t]) atomicAdd(reinterpret_cast<unsigned long long*>(&SP[b]), sl[2][t]);
+    if (sl[3][t]) atomicAdd(reinterpret_cast<unsigned long long*>(&NK[b]), sl[3][t]);
   }
 }
 
@@ -559,29 +679,110 @@ __global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
   }
 }
 
+// One SST pass with a compile-time radius RS (1..8; the generic k_smooth above serves the
+// rest). Same exact integer window sums as k_smooth (ARITH §F), fewer instructions per site:
+// each warp converts its halo row to fixed point into a per-warp staging row and sums it
+// horizontally at once (no block barrier between the two), the w-term sums unroll, and the
+// vertical pass slides over TY / 8 rows per thread. FROM_TB: the input is the step field
+// T(r, c) = T_b(block(r, c)) itself, read from the block temperatures (the a5 expansion
+// fused into the first pass: the expanded field is never written). Buffer rows
+// [row_base, row_base + Ly) of a grid of Ly_g rows (row slabs; see k_smooth).
+template <int RS, int TY, bool FROM_TB>
+__global__ void __launch_bounds__(256) k_smooth_rs(const float* __restrict__ Tin, const float* __restrict__ Tb,
+                                                   float* __restrict__ Tout, int64_t Lx, int64_t Ly,
+                                                   int64_t row_base, int64_t Ly_g, int lb) {
+  constexpr int W = kTile + 2 * RS, HY = TY + 2 * RS, w = 2 * RS + 1;
+  __shared__ long long Qw[8][W];
+  __shared__ long long H[HY][kTile];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (int64_t)blockIdx.y * TY;
+  const int64_t ca = c0 - RS + tx, cb = c0 + kTile - RS + tx;  // this lane's one or two columns
+  const bool ina = ca >= 0 && ca < Lx, inb = tx < 2 * RS && cb < Lx;
+  const int64_t nbx = (Lx + lb - 1) / lb;
+  uint32_t bca = 0, bcb = 0;
+  if (FROM_TB) {
+    bca = ina ? static_cast<uint32_t>(ca) / static_cast<uint32_t>(lb) : 0u;
+    bcb = inb ? static_cast<uint32_t>(cb) / static_cast<uint32_t>(lb) : 0u;
+  }
+  for (int y = ty; y < HY; y += 8) {
+    const int64_t r = r0 - RS + y;
+    long long qa = 0, qb = 0;
+    if (r >= 0 && r < Ly) {
+      if (FROM_TB) {
+        const float* tb = Tb + static_cast<int64_t>(static_cast<uint32_t>(r + row_base) / static_cast<uint32_t>(lb)) * nbx;
+        if (ina) qa = __float2ll_rn(__fmul_rn(__ldg(tb + bca), 0x1p40f));
+        if (inb) qb = __float2ll_rn(__fmul_rn(__ldg(tb + bcb), 0x1p40f));
+      } else {
+        const float* row = Tin + r * Lx;
+        if (ina) qa = __float2ll_rn(__fmul_rn(__ldg(row + ca), 0x1p40f));
+        if (inb) qb = __float2ll_rn(__fmul_rn(__ldg(row + cb), 0x1p40f));
+      }
+    }
+    Qw[ty][tx] = qa;
+    if (tx < 2 * RS) Qw[ty][kTile + tx] = qb;
+    __syncwarp();
+    long long h = 0;
+#pragma unroll
+    for (int d = 0; d < w; ++d) h += Qw[ty][tx + d];
+    H[y][tx] = h;
+    __syncwarp();
+  }
+  __syncthreads();
+  const int64_t c = c0 + tx;
+  if (c >= Lx) return;
+  const int64_t cl = c - RS > 0 ? c - RS : 0, cr = c + RS < Lx - 1 ? c + RS : Lx - 1;
+  const int ncol = static_cast<int>(cr - cl + 1);
+  constexpr int kRows = TY / 8;
+  const int yb = ty * kRows;
+  float* out = Tout + (r0 + yb) * Lx + c;
+  long long sum = 0;
+#pragma unroll
+  for (int d = 0; d < w; ++d) sum += H[yb + d][tx];
+  const double full = static_cast<double>(w * ncol);
+#pragma unroll 4
+  for (int k = 0; k < kRows; ++k) {
+    if (k > 0) sum += H[yb + k + w - 1][tx] - H[yb + k - 1][tx];
+    const int64_t r = r0 + yb + k;
+    if (r >= Ly) break;
+    double cnt = full;
+    const int64_t rg = r + row_base;
+    if (rg - RS < 0 || rg + RS > Ly_g - 1) {
+      const int64_t ra = rg - RS > 0 ? rg - RS : 0, rb = rg + RS < Ly_g - 1 ? rg + RS : Ly_g - 1;
+      cnt = static_cast<double>(static_cast<int>(rb - ra + 1) * ncol);
+    }
+    out[static_cast<int64_t>(k) * Lx] = __double2float_rn(__ddiv_rn(__ll2double_rn(sum) * 0x1p-40, cnt));
+  }
+}
+
 // -------------------------------------------------- per-gap records (sweep input)
-// Local gap ids of a buffer of rows [lrow0, lrow1) (global; the whole grid unless row slabs):
-// neighbours outside those rows are left out — only ghost-row gaps, which are never
-// updated, have any. T holds rows [trow0, trow1).
+// Per-gap records in ONE pass over the local sites (row-major, coalesced reads of mask /
+// gid / phi / T): every gap site writes its whole 32-byte record at its id. The ids of a
+// row's same-colour gaps are consecutive, so a warp's record stores are two contiguous runs
+// of whole sectors (no read-modify-write). The buffer holds rows [lrow0, lrow0 + nrows)
+// (global; the whole grid unless row slabs); neighbours outside those rows are left out —
+// only ghost-row gaps, which are never updated, have any. T holds rows [trow0, trow1).
 __global__ void __launch_bounds__(256) k_build_records(
     const int32_t* __restrict__ gid, const uint8_t* __restrict__ mask,
     const float* __restrict__ phi, const float* __restrict__ T, const long long* __restrict__ SP,
     const long long* __restrict__ NK, const DevScalars* __restrict__ sc, int64_t Lx, int64_t Ly,
-    int64_t lrow0, int64_t lrow1, int64_t trow0, int64_t trow1, int lb, int64_t P,
-    GapRec* __restrict__ rec) {
-  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g >= P) return;
-  GapRec R = rec[g];
-  const int64_t i = R.site, r = i / Lx, c = i - r * Lx;  // global row / column
-  const int64_t nr[4] = {r - 1, r + 1, r, r};
-  const int64_t nc[4] = {c, c, c - 1, c + 1};
+    int64_t lrow0, int64_t nrows, int64_t trow0, int64_t trow1, int lb, GapRec* __restrict__ rec) {
+  const int64_t lr = blockIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= Lx) return;
+  const int64_t i = lr * Lx + c;
+  if (mask[i]) return;
+  const int64_t r = lr + lrow0;  // global row
+  GapRec R;
+  R.site = static_cast<uint32_t>(r * Lx + c);  // global site index (Philox counter)
+  const bool has[4] = {lr > 0, lr + 1 < nrows && r + 1 < Ly, c > 0, c + 1 < Lx};
+  const int64_t off[4] = {-Lx, Lx, -1, 1};
   uint32_t flags = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     int32_t v = 0;
     uint32_t ty = NB_NONE;
-    if (nr[k] >= lrow0 && nr[k] < lrow1 && nr[k] < Ly && nc[k] >= 0 && nc[k] < Lx) {
-      const int64_t j = (nr[k] - lrow0) * Lx + nc[k];
+    if (has[k]) {
+      const int64_t j = i + off[k];
       if (mask[j]) { ty = NB_KNOWN; v = __float_as_int(phi[j]); }
       else         { ty = NB_GAP;   v = gid[j]; }
     }
@@ -591,12 +792,16 @@ __global__ void __launch_bounds__(256) k_build_records(
   R.flags = flags;
   R.beta = (r >= trow0 && r < trow1) ? __fdiv_rn(1.0f, T[(r - trow0) * Lx + c]) : 0.0f;
   const int64_t nbx = (Lx + lb - 1) / lb;
-  const int64_t b = (r / lb) * nbx + c / lb;
+  const int64_t b = static_cast<int64_t>(static_cast<uint32_t>(r) / static_cast<uint32_t>(lb)) * nbx +
+                    static_cast<uint32_t>(c) / static_cast<uint32_t>(lb);
   const long long nk = NK[b];
   R.init = nk ? __double2float_rn(__ddiv_rn(__ll2double_rn(SP[b]) * 0x1p-28, __ll2double_rn(nk)))
               : __double2float_rn(__ddiv_rn(__ll2double_rn(sc->sum_SP) * 0x1p-28,
                                             __ll2double_rn(sc->sum_NK)));
-  rec[g] = R;
+  uint4* dst = reinterpret_cast<uint4*>(rec + gid[i]);
+  dst[0] = make_uint4(R.site, __float_as_uint(R.beta), R.flags, __float_as_uint(R.init));
+  dst[1] = make_uint4(static_cast<uint32_t>(R.nb[0]), static_cast<uint32_t>(R.nb[1]), static_cast<uint32_t>(R.nb[2]),
+                      static_cast<uint32_t>(R.nb[3]));
 }
 
 // ------------------------------------------------------------- a11: predict
@@ -676,14 +881,14 @@ void launch_gap_rows(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_ba
 }
 
 void launch_gap_compact(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, const int* rowoff,
-                        int32_t* gid, GapRec* rec, cudaStream_t st) {
-  k_row_compact<<<static_cast<unsigned>(Ly), 256, 0, st>>>(mask, Lx, Ly, row_base, rowoff, gid, rec);
+                        int32_t* gid, cudaStream_t st) {
+  k_row_compact<<<static_cast<unsigned>(Ly), 256, 0, st>>>(mask, Lx, Ly, row_base, rowoff, gid);
 }
 
 void launch_gap_index(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, int* rowcnt,
-                      int* rowoff, int32_t* gid, GapRec* rec, cudaStream_t st) {
+                      int* rowoff, int32_t* gid, cudaStream_t st) {
   launch_gap_rows(mask, Lx, Ly, row_base, rowcnt, rowoff, st);
-  launch_gap_compact(mask, Lx, Ly, row_base, rowoff, gid, rec, st);
+  launch_gap_compact(mask, Lx, Ly, row_base, rowoff, gid, st);
 }
 
 void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t lrow0,
@@ -693,6 +898,13 @@ void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int6
   cudaMemsetAsync(NB, 0, sizeof(long long) * nblocks, st);
   cudaMemsetAsync(SP, 0, sizeof(long long) * nblocks, st);
   cudaMemsetAsync(NK, 0, sizeof(long long) * nblocks, st);
+  if (lb % 4 == 0 && Lx % 4 == 0 && aligned16(phiK) && (reinterpret_cast<uintptr_t>(mask) & 3u) == 0) {
+    const int64_t tile0 = (row0 / kBs4Rows) * kBs4Rows;
+    dim3 grid(static_cast<unsigned>((Lx + kBs4Cols - 1) / kBs4Cols),
+              static_cast<unsigned>((row1 - tile0 + kBs4Rows - 1) / kBs4Rows));
+    k_block_stats4<<<grid, 256, 0, st>>>(phiK, mask, Lx, Ly, lrow0, row0, row1, lb, q, SB, NB, SP, NK);
+    return;
+  }
   const int64_t tile0 = (row0 / kTile) * kTile;
   dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((row1 - tile0 + kTile - 1) / kTile));
   k_block_stats<<<grid, 256, 0, st>>>(phiK, mask, Lx, Ly, lrow0, row0, row1, lb, q, SB, NB, SP, NK);
@@ -712,6 +924,41 @@ void launch_median_fill(float* Tb, const long long* NB, int64_t nblocks, DevScal
 
 void launch_expand(const float* Tb, int64_t Lx, int64_t trow0, int64_t trow1, int lb, float* T, cudaStream_t st) {
   k_expand<<<grid_for(Lx * (trow1 - trow0), 256), 256, 0, st>>>(Tb, Lx, trow0, trow1, lb, T);
+}
+
+template <int RS, int TY>
+static void smooth_rs(const float* Tin, const float* Tb, float* Tout, int64_t Lx, int64_t Ly, int64_t row_base,
+                      int64_t Ly_g, int lb, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((Ly + TY - 1) / TY));
+  if (Tb)
+    k_smooth_rs<RS, TY, true><<<grid, 256, 0, st>>>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb);
+  else
+    k_smooth_rs<RS, TY, false><<<grid, 256, 0, st>>>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb);
+}
+
+template <int RS>
+static void smooth_rs_ty(const float* Tin, const float* Tb, float* Tout, int64_t Lx, int64_t Ly, int64_t row_base,
+                         int64_t Ly_g, int lb, cudaStream_t st) {
+  // 32 x 64 tiles once the grid has >= 16 waves of them on 148 SMs, 32 x 32 below
+  if ((Lx + kTile - 1) / kTile * ((Ly + 63) / 64) >= 148 * 16)
+    smooth_rs<RS, 64>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st);
+  else
+    smooth_rs<RS, 32>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st);
+}
+
+bool launch_smooth_specialised(const float* Tin, const float* Tb, float* Tout, int64_t Lx, int64_t Ly,
+                               int64_t row_base, int64_t Ly_g, int rs, int lb, cudaStream_t st) {
+  switch (rs) {
+    case 1: smooth_rs_ty<1>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
+    case 2: smooth_rs_ty<2>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
+    case 3: smooth_rs_ty<3>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
+    case 4: smooth_rs_ty<4>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
+    case 5: smooth_rs_ty<5>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
+    case 6: smooth_rs_ty<6>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
+    case 7: smooth_rs_ty<7>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
+    case 8: smooth_rs_ty<8>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
+    default: return false;
+  }
 }
 
 void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int64_t row_base, int64_t Ly_g, int rs,
@@ -739,8 +986,9 @@ void launch_build_records(const int32_t* gid, const uint8_t* mask, const float* 
                           const DevScalars* sc, int64_t Lx, int64_t Ly, int64_t lrow0, int64_t lrow1,
                           int64_t trow0, int64_t trow1, int lb, int64_t P, GapRec* rec, cudaStream_t st) {
   if (P == 0) return;
-  k_build_records<<<static_cast<unsigned>((P + 255) / 256), 256, 0, st>>>(gid, mask, phiK, T, SP, NK, sc, Lx, Ly,
-                                                                         lrow0, lrow1, trow0, trow1, lb, P, rec);
+  dim3 grid(static_cast<unsigned>((Lx + 255) / 256), static_cast<unsigned>(lrow1 - lrow0));
+  k_build_records<<<grid, 256, 0, st>>>(gid, mask, phiK, T, SP, NK, sc, Lx, Ly, lrow0, lrow1 - lrow0, trow0, trow1,
+                                        lb, rec);
 }
 
 void launch_predict(const float* z, const uint8_t* mask, const int32_t* gid, const double* acc,
