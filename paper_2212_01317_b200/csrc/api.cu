@@ -151,7 +151,7 @@ struct mpr_ctx {
   std::vector<int> rowoff_h, rowcnt_h;  // host copies of the gap-id row offsets (row slabs)
   // device memory
   DBuf z, mask, phiK, scal, calTd, caled, rowcnt, rowoff, gid, rec, bstats, Tb, T, T2, G, A, acc,
-      energy, out, tmp, win, dclist, dccnt;
+      energy, out, tmp, win, dclist, dccnt, ginit;
   int64_t dc_off[5] = {0, 0, 0, 0, 0};  // DC phase segments of dclist (row f3)
   DevScalars* hsc = nullptr;  // pinned host mirror of the device scalars
 };
@@ -413,6 +413,7 @@ mpr_status stage_data(mpr_ctx* c) {
     c->P = c->rowoff_h[static_cast<size_t>(2 * nl - 1)] + c->rowcnt_h[static_cast<size_t>(2 * nl - 1)];
   }
   CK(c->rec.ensure(sizeof(GapRec) * std::max<int64_t>(c->P, 1)), "alloc records");
+  CK(c->ginit.ensure(sizeof(float) * std::max<int64_t>(c->P, 1)), "alloc init angles");
   if (!c->rows) {
     launch_gap_index(c->mask.as<uint8_t>(), c->Lx, nl, 0, c->rowcnt.as<int>(), c->rowoff.as<int>(), c->gid.as<int32_t>(),
                      st);
@@ -602,7 +603,7 @@ void mpr_destroy(mpr_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   DBuf* bufs[] = {&c->z, &c->mask, &c->phiK, &c->scal, &c->calTd, &c->caled, &c->rowcnt, &c->rowoff,
                   &c->gid, &c->rec, &c->bstats, &c->Tb, &c->T, &c->T2, &c->G, &c->A, &c->acc,
-                  &c->energy, &c->out, &c->tmp, &c->win, &c->dclist, &c->dccnt};
+                  &c->energy, &c->out, &c->tmp, &c->win, &c->dclist, &c->dccnt, &c->ginit};
   for (DBuf* b : bufs) b->release();
   if (c->hsc) cudaFreeHost(c->hsc);
   for (auto& e : c->graphs)
@@ -662,7 +663,7 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   c->nby = (c->Ly + lb - 1) / lb;
   c->nblocks = c->nbx * c->nby;
   CK(c->bstats.ensure(sizeof(long long) * 4 * c->nblocks), "alloc block stats");
-  CK(c->Tb.ensure(sizeof(float) * c->nblocks), "alloc Tb");
+  CK(c->Tb.ensure(sizeof(float) * 2 * c->nblocks), "alloc Tb");  // T_b, then the blocks' init angles
   CK(c->T.ensure(sizeof(float) * c->nT), "alloc T");
   if (c->cfg.n_s > 0) CK(c->T2.ensure(sizeof(float) * c->nT), "alloc T2");
   long long* SB = c->bstats.as<long long>();
@@ -685,13 +686,17 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   CKL("block_T");
   launch_median_fill(c->Tb.as<float>(), NB, c->nblocks, dsc, st);
   CKL("median_fill");
+  float* binit = c->Tb.as<float>() + c->nblocks;
+  launch_block_init(SP, NK, c->nblocks, dsc, binit, st);
+  CKL("block_init");
   // a5 on the local temperature rows [trow0, trow1) (the whole grid unless row slabs). With a
   // specialised radius the first pass reads the block temperatures directly (no expanded
   // field is written); otherwise expand, then the generic passes.
   const int64_t nTr = c->trow1 - c->trow0;
   int k0 = 0;
+  const float Tmin = c->calT.front(), Tmax = c->calT.back();
   if (c->cfg.n_s > 0 && launch_smooth_specialised(nullptr, c->Tb.as<float>(), c->T.as<float>(), c->Lx, nTr, c->trow0,
-                                                  c->Ly, c->cfg.r_s, lb, st)) {
+                                                  c->Ly, c->cfg.r_s, lb, Tmin, Tmax, st)) {
     CKL("smooth (from T_b)");
     k0 = 1;
   } else {
@@ -700,13 +705,14 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   }
   for (int k = k0; k < c->cfg.n_s; ++k) {
     if (!launch_smooth_specialised(c->T.as<float>(), nullptr, c->T2.as<float>(), c->Lx, nTr, c->trow0, c->Ly,
-                                   c->cfg.r_s, lb, st))
+                                   c->cfg.r_s, lb, Tmin, Tmax, st))
       launch_smooth(c->T.as<float>(), c->T2.as<float>(), c->Lx, nTr, c->trow0, c->Ly, c->cfg.r_s, st);
     CKL("smooth");
     std::swap(c->T, c->T2);
   }
-  launch_build_records(c->gid.as<int32_t>(), c->mask.as<uint8_t>(), c->phiK.as<float>(), c->T.as<float>(), SP, NK, dsc,
-                       c->Lx, c->Ly, c->lrow0, c->lrow1, c->trow0, c->trow1, lb, c->P, c->rec.as<GapRec>(), st);
+  launch_build_records(c->gid.as<int32_t>(), c->mask.as<uint8_t>(), c->phiK.as<float>(), c->T.as<float>(), binit,
+                       c->Lx, c->Ly, c->lrow0, c->lrow1, c->trow0, c->trow1, lb, c->P, c->rec.as<GapRec>(),
+                       c->ginit.as<float>(), st);
   CKL("build_records");
   CK(cudaMemcpyAsync(c->hsc, c->scal.p, sizeof(DevScalars), cudaMemcpyDeviceToHost, st), "scalars download");
   if (T_out)
@@ -792,7 +798,8 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
   const int npairs = k.Rb / 2;
   // every local gap (ghost rows too: initial states are a pure function of the global ids,
   // so the ghost rows need no exchange before the first half-sweep)
-  launch_init_states(c->rec.as<GapRec>(), c->G.as<float>(), avg ? c->A.as<float>() : nullptr, k.P, k.Rb, npairs,
+  launch_init_states(c->rec.as<GapRec>(), c->ginit.as<float>(), c->G.as<float>(), avg ? c->A.as<float>() : nullptr, k.P,
+                     k.Rb, npairs,
                      k.pair_base, k.init == MPR_INIT_RANDOM, k.k0, k.k1, st);
   CKL("init_states");
   ++c->launches;
@@ -1160,7 +1167,7 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
     CK(cudaMemsetAsync(eq_d, 0, sizeof(int) * Rb, st), "zero decisions");
     CK(cudaMemsetAsync(c->energy.p, 0, sizeof(long long) * Rb * max_sweeps, st), "zero energy");
     CK(cudaStreamSynchronize(st), "adaptive batch start");  // the pinned windows are reused below
-    launch_init_states(c->rec.as<GapRec>(), c->G.as<float>(), c->A.as<float>(), c->P, Rb, Rb / 2,
+    launch_init_states(c->rec.as<GapRec>(), c->ginit.as<float>(), c->G.as<float>(), c->A.as<float>(), c->P, Rb, Rb / 2,
                        static_cast<uint32_t>(mb / 2), c->cfg.init == MPR_INIT_RANDOM, k0, k1, st);
     CKL("init_states");
     ++c->launches;

@@ -76,12 +76,18 @@ void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int64_
                    cudaStream_t st);
 // The specialised pass for r_s = 1..8 (false: not specialised, use launch_smooth). Tb non-null:
 // the input is the expansion of the block temperatures (first pass, Tin unused).
+// Tmin / Tmax: the calibration table's range (every T of the field lies in it; they decide
+// whether the exact window sums can be formed in fp64).
 bool launch_smooth_specialised(const float* Tin, const float* Tb, float* Tout, int64_t Lx, int64_t Ly,
-                               int64_t row_base, int64_t Ly_g, int rs, int lb, cudaStream_t st);
+                               int64_t row_base, int64_t Ly_g, int rs, int lb, float Tmin, float Tmax,
+                               cudaStream_t st);
+// BLOCK_MEAN initial angle per block (ARITH §G), after launch_block_T (global sample sums)
+void launch_block_init(const long long* SP, const long long* NK, int64_t nblocks, const DevScalars* sc,
+                       float* binit, cudaStream_t st);
 void launch_build_records(const int32_t* gid, const uint8_t* mask, const float* phiK,
-                          const float* T, const long long* SP, const long long* NK,
-                          const DevScalars* sc, int64_t Lx, int64_t Ly, int64_t lrow0, int64_t lrow1,
-                          int64_t trow0, int64_t trow1, int lb, int64_t P, GapRec* rec, cudaStream_t st);
+                          const float* T, const float* binit, int64_t Lx, int64_t Ly, int64_t lrow0, int64_t lrow1,
+                          int64_t trow0, int64_t trow1, int lb, int64_t P, GapRec* rec, float* ginit,
+                          cudaStream_t st);
 void launch_predict(const float* z, const uint8_t* mask, const int32_t* gid, const double* acc,
                     int64_t n, double denom, const DevScalars* sc, int degenerate, float* out,
                     cudaStream_t st);
@@ -129,7 +135,7 @@ struct SweepArgs {
 };
 int sweep_grid_size(int device, int variant);
 void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st);
-void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,
+void launch_init_states(const GapRec* rec, const float* ginit, float* G, float* A, int64_t P, int R, int npairs,
                         uint32_t pair_base, int random_init, uint32_t k0, uint32_t k1,
                         cudaStream_t st);
 // Adaptive protocol (row f1, ARITH §K) decided on the device: after sweep s, every

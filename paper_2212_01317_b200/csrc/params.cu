@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "device_math.cuh"
 #include "internal.cuh"
@@ -255,6 +256,56 @@ __global__ void __launch_bounds__(256) k_row_compact(const uint8_t* __restrict__
   }
 }
 
+// The same compaction with one WARP per row and no block barriers (Lx % 4 == 0, 4-byte
+// aligned mask rows): each lane takes 4 columns (one 32-bit mask load) per step, the lanes'
+// per-colour gap counts are scanned with shuffles, and the ids go out as one int4 per lane
+// (512 contiguous bytes per warp step). The next step's mask word is loaded ahead.
+__global__ void __launch_bounds__(256) k_row_compact4(const uint8_t* __restrict__ mask, int64_t Lx,
+                                                      int64_t Ly, int64_t row_base,
+                                                      const int* __restrict__ rowoff,
+                                                      int32_t* __restrict__ gid) {
+  const int64_t r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= Ly) return;
+  const int lane = threadIdx.x & 31;
+  const uint8_t* mrow = mask + r * Lx;
+  int32_t* grow = gid + r * Lx;
+  int base0 = rowoff[r], base1 = rowoff[Ly + r];  // first id of colour 0 / 1 in this row
+  // colour of column c: (row_base + r + c) & 1; lane columns 4l .. 4l+3 alternate from par
+  const int par = static_cast<int>((row_base + r) & 1);
+  uint32_t w = 0;
+  if (4 * lane < Lx) w = *reinterpret_cast<const uint32_t*>(mrow + 4 * lane);
+  for (int64_t c0 = 0; c0 < Lx; c0 += 128) {
+    const int64_t c = c0 + 4 * lane;
+    const bool in = c < Lx;
+    const uint32_t cur = w;
+    if (c + 128 < Lx) w = *reinterpret_cast<const uint32_t*>(mrow + c + 128);
+    int gaps[4];
+    int n0 = 0, n1 = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      gaps[k] = in && ((cur >> (8 * k)) & 0xffu) == 0;
+      if (((par + k) & 1) == 0) n0 += gaps[k];  // c is a multiple of 4: (c + k) & 1 == k & 1
+      else n1 += gaps[k];
+    }
+    int x0 = n0, x1 = n1;  // inclusive scans over the lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
+      if (lane >= o) { x0 += y0; x1 += y1; }
+    }
+    int i0 = base0 + x0 - n0, i1 = base1 + x1 - n1;
+    int out[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool col0 = ((par + k) & 1) == 0;
+      out[k] = gaps[k] ? (col0 ? i0++ : i1++) : -1;
+    }
+    if (in) *reinterpret_cast<int4*>(grow + c) = make_int4(out[0], out[1], out[2], out[3]);
+    base0 += __shfl_sync(0xffffffffu, x0, 31);
+    base1 += __shfl_sync(0xffffffffu, x1, 31);
+  }
+}
+
 // ----------------------------------------------------- a3: block bond statistics
 constexpr int kTile = 32;            // 32 x 32 sites per CTA
 constexpr int kMaxSlots = 17 * 17;   // blocks a tile can touch when l_b >= 2
@@ -391,36 +442,39 @@ constexpr int kRowsPerWarp = 8;
 constexpr int kBs4Cols = 128, kBs4Rows = 8 * kRowsPerWarp;
 constexpr int kBs4Slots = (kBs4Cols / 4 + 1) * (kBs4Rows / 4 + 1);  // l_b >= 4
 __global__ void __launch_bounds__(256) k_block_stats4(const float* __restrict__ phi,
-                                                      const uint8_t* __restrict__ mask, int64_t Lx,
-                                                      int64_t Ly, int64_t lrow0, int64_t row0,
-                                                      int64_t row1, int lb, float q,
+                                                      const uint8_t* __restrict__ mask, int64_t Lx64,
+                                                      int64_t Ly64, int64_t lrow064, int64_t row064,
+                                                      int64_t row164, int lb, float q,
                                                       long long* __restrict__ SB,
                                                       long long* __restrict__ NB,
                                                       long long* __restrict__ SP,
                                                       long long* __restrict__ NK) {
   __shared__ unsigned long long sl[4][kBs4Slots];
+  // 32-bit index arithmetic (< 2^30 sites)
+  const int Lx = static_cast<int>(Lx64), Ly = static_cast<int>(Ly64), lrow0 = static_cast<int>(lrow064);
+  const int row0 = static_cast<int>(row064), row1 = static_cast<int>(row164);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int64_t cbase = (int64_t)blockIdx.x * kBs4Cols;
-  const int64_t rbase = (row0 / kBs4Rows) * kBs4Rows + (int64_t)blockIdx.y * kBs4Rows;
-  const int64_t nbx = (Lx + lb - 1) / lb;
-  const int64_t bc0 = cbase / lb, br0 = max(rbase, row0) / lb;
-  const int64_t clast = min(cbase + kBs4Cols, Lx) - 1, rlast = min(rbase + kBs4Rows, row1) - 1;
-  const int nbc = static_cast<int>(clast / lb - bc0 + 1);
-  const int nslots = nbc * static_cast<int>(rlast / lb - br0 + 1);
+  const int cbase = blockIdx.x * kBs4Cols;
+  const int rbase = (row0 / kBs4Rows) * kBs4Rows + blockIdx.y * kBs4Rows;
+  const int nbx = (Lx + lb - 1) / lb;
+  const int bc0 = cbase / lb, br0 = max(rbase, row0) / lb;
+  const int clast = min(cbase + kBs4Cols, Lx) - 1, rlast = min(rbase + kBs4Rows, row1) - 1;
+  const int nbc = clast / lb - bc0 + 1;
+  const int nslots = nbc * (rlast / lb - br0 + 1);
   for (int t = threadIdx.x; t < 4 * kBs4Slots; t += blockDim.x) sl[t / kBs4Slots][t % kBs4Slots] = 0ull;
   __syncthreads();
-  const int64_t c = cbase + 4 * lane;  // first of this thread's 4 columns
-  const bool cin = c < Lx;             // Lx % 4 == 0: all 4 or none
-  const int bcl = cin ? static_cast<int>(c / lb - bc0) : 0;
+  const int c = cbase + 4 * lane;  // first of this thread's 4 columns
+  const bool cin = c < Lx;         // Lx % 4 == 0: all 4 or none
+  const int bcl = cin ? c / lb - bc0 : 0;
   const int grp = lb / 4;                                      // lanes per block column
   const bool pow2 = grp <= 32 && (grp & (grp - 1)) == 0 && (cbase % lb) == 0;
-  const int64_t ra = max(rbase + wp * kRowsPerWarp, row0), rz = min(rbase + (wp + 1) * kRowsPerWarp, row1);
+  const int ra = max(rbase + wp * kRowsPerWarp, row0), rz = min(rbase + (wp + 1) * kRowsPerWarp, row1);
   long long sb = 0, sp = 0;
   int nb = 0, nk = 0;
-  int64_t cur_br = ra < rz ? ra / lb : -1;
-  auto flush = [&](int64_t br) {
+  int cur_br = ra < rz ? ra / lb : -1;
+  auto flush = [&](int br) {
     // every lane of the warp calls this together (warp-uniform row loop)
-    const int slot = static_cast<int>(br - br0) * nbc + bcl;
+    const int slot = (br - br0) * nbc + bcl;
     long long v[4] = {sb, static_cast<long long>(nb), sp, static_cast<long long>(nk)};
     if (pow2) {
 #pragma unroll
@@ -438,23 +492,23 @@ __global__ void __launch_bounds__(256) k_block_stats4(const float* __restrict__ 
   float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
   uint32_t m = 0;
   if (ra < rz && cin) {
-    const int64_t i = (ra - lrow0) * Lx + c;
+    const int i = (ra - lrow0) * Lx + c;
     p = *reinterpret_cast<const float4*>(phi + i);
     m = *reinterpret_cast<const uint32_t*>(mask + i);
   }
-  for (int64_t r = ra; r < rz; ++r) {
-    const int64_t br = r / lb;
+  for (int r = ra; r < rz; ++r) {
+    const int br = r / lb;
     if (br != cur_br) {
       flush(cur_br);
       cur_br = br;
     }
     const bool down = r + 1 < Ly;
+    const int i = (r - lrow0) * Lx + c;
     float4 pn = make_float4(0.f, 0.f, 0.f, 0.f);
     uint32_t mn = 0;
     if (down && cin) {
-      const int64_t i = (r + 1 - lrow0) * Lx + c;
-      pn = *reinterpret_cast<const float4*>(phi + i);
-      mn = *reinterpret_cast<const uint32_t*>(mask + i);
+      pn = *reinterpret_cast<const float4*>(phi + i + Lx);
+      mn = *reinterpret_cast<const uint32_t*>(mask + i + Lx);
     }
     // right neighbour of the 4th column: the next lane's first, lane 31 loads it
     float pr = __shfl_down_sync(0xffffffffu, p.x, 1);
@@ -463,9 +517,8 @@ __global__ void __launch_bounds__(256) k_block_stats4(const float* __restrict__ 
       pr = 0.f;
       mr = 0;
       if (cin && c + 4 < Lx) {
-        const int64_t i = (r - lrow0) * Lx + c + 4;
-        pr = phi[i];
-        mr = mask[i];
+        pr = phi[i + 4];
+        mr = mask[i + 4];
       }
     }
     const float pv[5] = {p.x, p.y, p.z, p.w, pr};
@@ -492,7 +545,7 @@ __global__ void __launch_bounds__(256) k_block_stats4(const float* __restrict__ 
   if (cur_br >= 0) flush(cur_br);
   __syncthreads();
   for (int t = threadIdx.x; t < nslots; t += blockDim.x) {
-    const int64_t b = (br0 + t / nbc) * nbx + (bc0 + t % nbc);
+    const int64_t b = static_cast<int64_t>(br0 + t / nbc) * nbx + (bc0 + t % nbc);
     if (sl[0][t]) atomicAdd(reinterpret_cast<unsigned long long*>(&SB[b]), sl[0][t]);
     if (sl[1][t]) atomicAdd(reinterpret_cast<unsigned long long*>(&NB[b]), sl[1][t]);
     if (sl[2][t]) atomicAdd(reinterpret_cast<unsigned long long*>(&SP[b]), sl[2][t]);
@@ -544,6 +597,20 @@ __global__ void __launch_bounds__(256) k_block_T(const long long* __restrict__ S
     if (sp) atomicAdd(reinterpret_cast<unsigned long long*>(&sc->sum_SP), static_cast<unsigned long long>(sp));
     if (nk) atomicAdd(reinterpret_cast<unsigned long long*>(&sc->sum_NK), static_cast<unsigned long long>(nk));
   }
+}
+
+// a6 BLOCK_MEAN initial angle of every block (ARITH §G): the block's mean known angle, or the
+// global sample mean for a block without samples — one fp64 division per block instead of
+// one per gap site in the record builder.
+__global__ void __launch_bounds__(256) k_block_init(const long long* __restrict__ SP,
+                                                    const long long* __restrict__ NK, int64_t nblocks,
+                                                    const DevScalars* __restrict__ sc,
+                                                    float* __restrict__ binit) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= nblocks) return;
+  const long long nk = NK[b];
+  binit[b] = nk ? __double2float_rn(__ddiv_rn(__ll2double_rn(SP[b]) * 0x1p-28, __ll2double_rn(nk)))
+                : __double2float_rn(__ddiv_rn(__ll2double_rn(sc->sum_SP) * 0x1p-28, __ll2double_rn(sc->sum_NK)));
 }
 
 // ------------------------------------------- a4: lower median + fallback (1 CTA)
@@ -687,74 +754,104 @@ __global__ void __launch_bounds__(256) k_smooth(const float* __restrict__ Tin,
 // T(r, c) = T_b(block(r, c)) itself, read from the block temperatures (the a5 expansion
 // fused into the first pass: the expanded field is never written). Buffer rows
 // [row_base, row_base + Ly) of a grid of Ly_g rows (row slabs; see k_smooth).
-template <int RS, int TY, bool FROM_TB>
+//
+// F64 (host-checked: every T in [2^-17, T_max] with (2 RS + 1)^2 T_max < 2^13): the terms
+// llrint(T 2^40) are the floats T 2^40 themselves (integer-valued from 2^23 up) and every
+// partial window sum stays below 2^53, so the sums are formed EXACTLY in fp64 — one DADD
+// per term instead of a 64-bit integer add (two heavy-pipe IMADs on sm_100a) and no F2I /
+// I2F conversions — and equal ARITH §F's int64 sums bit for bit.
+template <typename Acc>
+__device__ __forceinline__ Acc smooth_term(float v);
+template <>
+__device__ __forceinline__ long long smooth_term<long long>(float v) { return __float2ll_rn(__fmul_rn(v, 0x1p40f)); }
+template <>
+__device__ __forceinline__ double smooth_term<double>(float v) { return static_cast<double>(__fmul_rn(v, 0x1p40f)); }
+__device__ __forceinline__ double smooth_value(long long s) { return __ll2double_rn(s); }
+__device__ __forceinline__ double smooth_value(double s) { return s; }
+
+template <int RS, int TY, bool FROM_TB, bool F64>
 __global__ void __launch_bounds__(256) k_smooth_rs(const float* __restrict__ Tin, const float* __restrict__ Tb,
-                                                   float* __restrict__ Tout, int64_t Lx, int64_t Ly,
-                                                   int64_t row_base, int64_t Ly_g, int lb) {
+                                                   float* __restrict__ Tout, int64_t Lx64, int64_t Ly64,
+                                                   int64_t row_base64, int64_t Ly_g64, int lb) {
+  using Acc = typename std::conditional<F64, double, long long>::type;
   constexpr int W = kTile + 2 * RS, HY = TY + 2 * RS, w = 2 * RS + 1;
-  __shared__ long long Qw[8][W];
-  __shared__ long long H[HY][kTile];
+  __shared__ Acc Qw[8][W];
+  __shared__ Acc H[HY][kTile];
+  // 32-bit index arithmetic throughout: buffers hold < 2^30 sites (the API's Lx*Ly bound)
+  const int Lx = static_cast<int>(Lx64), Ly = static_cast<int>(Ly64);
+  const int row_base = static_cast<int>(row_base64), Ly_g = static_cast<int>(Ly_g64);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (int64_t)blockIdx.y * TY;
-  const int64_t ca = c0 - RS + tx, cb = c0 + kTile - RS + tx;  // this lane's one or two columns
+  const int c0 = blockIdx.x * kTile, r0 = blockIdx.y * TY;
+  const int ca = c0 - RS + tx, cb = c0 + kTile - RS + tx;  // this lane's one or two columns
   const bool ina = ca >= 0 && ca < Lx, inb = tx < 2 * RS && cb < Lx;
-  const int64_t nbx = (Lx + lb - 1) / lb;
-  uint32_t bca = 0, bcb = 0;
+  const int nbx = (Lx + lb - 1) / lb;
+  int bca = 0, bcb = 0;
   if (FROM_TB) {
-    bca = ina ? static_cast<uint32_t>(ca) / static_cast<uint32_t>(lb) : 0u;
-    bcb = inb ? static_cast<uint32_t>(cb) / static_cast<uint32_t>(lb) : 0u;
+    bca = ina ? ca / lb : 0;
+    bcb = inb ? cb / lb : 0;
   }
-  for (int y = ty; y < HY; y += 8) {
-    const int64_t r = r0 - RS + y;
-    long long qa = 0, qb = 0;
-    if (r >= 0 && r < Ly) {
+  // every load of this warp's halo rows is issued before the first is used (the rows'
+  // values sit in registers: the loads overlap instead of one round trip per row)
+  constexpr int NYW = (HY + 7) / 8;
+  float va[NYW], vb[NYW];
+#pragma unroll
+  for (int t = 0; t < NYW; ++t) {
+    const int y = ty + 8 * t;
+    const int r = r0 - RS + y;
+    va[t] = vb[t] = 0.0f;
+    if (y < HY && static_cast<unsigned>(r) < static_cast<unsigned>(Ly)) {
       if (FROM_TB) {
-        const float* tb = Tb + static_cast<int64_t>(static_cast<uint32_t>(r + row_base) / static_cast<uint32_t>(lb)) * nbx;
-        if (ina) qa = __float2ll_rn(__fmul_rn(__ldg(tb + bca), 0x1p40f));
-        if (inb) qb = __float2ll_rn(__fmul_rn(__ldg(tb + bcb), 0x1p40f));
+        const float* tb = Tb + ((r + row_base) / lb) * nbx;
+        if (ina) va[t] = __ldg(tb + bca);
+        if (inb) vb[t] = __ldg(tb + bcb);
       } else {
         const float* row = Tin + r * Lx;
-        if (ina) qa = __float2ll_rn(__fmul_rn(__ldg(row + ca), 0x1p40f));
-        if (inb) qb = __float2ll_rn(__fmul_rn(__ldg(row + cb), 0x1p40f));
+        if (ina) va[t] = __ldg(row + ca);
+        if (inb) vb[t] = __ldg(row + cb);
       }
     }
-    Qw[ty][tx] = qa;
-    if (tx < 2 * RS) Qw[ty][kTile + tx] = qb;
-    __syncwarp();
-    long long h = 0;
+  }
 #pragma unroll
-    for (int d = 0; d < w; ++d) h += Qw[ty][tx + d];
+  for (int t = 0; t < NYW; ++t) {
+    const int y = ty + 8 * t;
+    if (y >= HY) break;
+    // outside the grid (or the buffer) the value is 0 and so is its fixed-point term
+    Qw[ty][tx] = smooth_term<Acc>(va[t]);
+    if (tx < 2 * RS) Qw[ty][kTile + tx] = smooth_term<Acc>(vb[t]);
+    __syncwarp();
+    Acc h = Qw[ty][tx];
+#pragma unroll
+    for (int d = 1; d < w; ++d) h += Qw[ty][tx + d];
     H[y][tx] = h;
     __syncwarp();
   }
   __syncthreads();
-  const int64_t c = c0 + tx;
+  const int c = c0 + tx;
   if (c >= Lx) return;
-  const int64_t cl = c - RS > 0 ? c - RS : 0, cr = c + RS < Lx - 1 ? c + RS : Lx - 1;
-  const int ncol = static_cast<int>(cr - cl + 1);
+  const int cl = c - RS > 0 ? c - RS : 0, cr = c + RS < Lx - 1 ? c + RS : Lx - 1;
+  const int ncol = cr - cl + 1;
   constexpr int kRows = TY / 8;
   const int yb = ty * kRows;
   float* out = Tout + (r0 + yb) * Lx + c;
-  long long sum = 0;
+  Acc sum = H[yb][tx];
 #pragma unroll
-  for (int d = 0; d < w; ++d) sum += H[yb + d][tx];
+  for (int d = 1; d < w; ++d) sum += H[yb + d][tx];
   const double full = static_cast<double>(w * ncol);
 #pragma unroll 4
   for (int k = 0; k < kRows; ++k) {
     if (k > 0) sum += H[yb + k + w - 1][tx] - H[yb + k - 1][tx];
-    const int64_t r = r0 + yb + k;
+    const int r = r0 + yb + k;
     if (r >= Ly) break;
     double cnt = full;
-    const int64_t rg = r + row_base;
+    const int rg = r + row_base;
     if (rg - RS < 0 || rg + RS > Ly_g - 1) {
-      const int64_t ra = rg - RS > 0 ? rg - RS : 0, rb = rg + RS < Ly_g - 1 ? rg + RS : Ly_g - 1;
-      cnt = static_cast<double>(static_cast<int>(rb - ra + 1) * ncol);
+      const int ra = rg - RS > 0 ? rg - RS : 0, rb = rg + RS < Ly_g - 1 ? rg + RS : Ly_g - 1;
+      cnt = static_cast<double>((rb - ra + 1) * ncol);
     }
-    out[static_cast<int64_t>(k) * Lx] = __double2float_rn(__ddiv_rn(__ll2double_rn(sum) * 0x1p-40, cnt));
+    out[k * Lx] = __double2float_rn(__ddiv_rn(smooth_value(sum) * 0x1p-40, cnt));
   }
 }
 
-// -------------------------------------------------- per-gap records (sweep input)
 // Per-gap records in ONE pass over the local sites (row-major, coalesced reads of mask /
 // gid / phi / T): every gap site writes its whole 32-byte record at its id. The ids of a
 // row's same-colour gaps are consecutive, so a warp's record stores are two contiguous runs
@@ -763,9 +860,9 @@ __global__ void __launch_bounds__(256) k_smooth_rs(const float* __restrict__ Tin
 // only ghost-row gaps, which are never updated, have any. T holds rows [trow0, trow1).
 __global__ void __launch_bounds__(256) k_build_records(
     const int32_t* __restrict__ gid, const uint8_t* __restrict__ mask,
-    const float* __restrict__ phi, const float* __restrict__ T, const long long* __restrict__ SP,
-    const long long* __restrict__ NK, const DevScalars* __restrict__ sc, int64_t Lx, int64_t Ly,
-    int64_t lrow0, int64_t nrows, int64_t trow0, int64_t trow1, int lb, GapRec* __restrict__ rec) {
+    const float* __restrict__ phi, const float* __restrict__ T, const float* __restrict__ binit,
+    int64_t Lx, int64_t Ly, int64_t lrow0, int64_t nrows, int64_t trow0, int64_t trow1, int lb,
+    GapRec* __restrict__ rec, float* __restrict__ ginit) {
   const int64_t lr = blockIdx.y;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= Lx) return;
@@ -794,14 +891,108 @@ __global__ void __launch_bounds__(256) k_build_records(
   const int64_t nbx = (Lx + lb - 1) / lb;
   const int64_t b = static_cast<int64_t>(static_cast<uint32_t>(r) / static_cast<uint32_t>(lb)) * nbx +
                     static_cast<uint32_t>(c) / static_cast<uint32_t>(lb);
-  const long long nk = NK[b];
-  R.init = nk ? __double2float_rn(__ddiv_rn(__ll2double_rn(SP[b]) * 0x1p-28, __ll2double_rn(nk)))
-              : __double2float_rn(__ddiv_rn(__ll2double_rn(sc->sum_SP) * 0x1p-28,
-                                            __ll2double_rn(sc->sum_NK)));
-  uint4* dst = reinterpret_cast<uint4*>(rec + gid[i]);
+  R.init = binit[b];
+  const int32_t g = gid[i];
+  ginit[g] = R.init;
+  uint4* dst = reinterpret_cast<uint4*>(rec + g);
   dst[0] = make_uint4(R.site, __float_as_uint(R.beta), R.flags, __float_as_uint(R.init));
   dst[1] = make_uint4(static_cast<uint32_t>(R.nb[0]), static_cast<uint32_t>(R.nb[1]), static_cast<uint32_t>(R.nb[2]),
                       static_cast<uint32_t>(R.nb[3]));
+}
+
+// The record builder with streamed rows (Lx % 4 == 0, 16-byte aligned buffers): a thread
+// owns 4 adjacent columns and walks kRowsPerWarp rows, keeping the rows above, at and below
+// in registers (mask as 4 bytes, phi as float4, gid as int4) — every row is loaded once
+// per column strip, all loads of a step are independent, and the west / east neighbours
+// of the outer columns come from the adjacent lanes. Writes the same records as
+// k_build_records.
+__device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) { return (w >> (8 * k)) & 0xffu; }
+
+__global__ void __launch_bounds__(256) k_build_records4(
+    const int32_t* __restrict__ gid, const uint8_t* __restrict__ mask, const float* __restrict__ phi,
+    const float* __restrict__ T, const float* __restrict__ binit, int64_t Lx64, int64_t Ly64, int64_t lrow064,
+    int64_t nrows64, int64_t trow064, int64_t trow164, int lb, GapRec* __restrict__ rec, float* __restrict__ ginit) {
+  // 32-bit index arithmetic (< 2^30 sites)
+  const int Lx = static_cast<int>(Lx64), Ly = static_cast<int>(Ly64), lrow0 = static_cast<int>(lrow064);
+  const int nrows = static_cast<int>(nrows64), trow0 = static_cast<int>(trow064), trow1 = static_cast<int>(trow164);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 128 + 4 * lane;
+  const bool cin = c < Lx;
+  const int la = blockIdx.y * (8 * kRowsPerWarp) + wp * kRowsPerWarp;  // local rows
+  const int lz = min(la + kRowsPerWarp, nrows);
+  if (la >= nrows) return;  // warp-uniform
+  const int nbx = (Lx + lb - 1) / lb;
+  int bcol[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) bcol[j] = (c + j) / lb;
+  auto ld = [&](int lr, uint32_t& m, float4& p, int4& g) {
+    m = 0;
+    p = make_float4(0.f, 0.f, 0.f, 0.f);
+    g = make_int4(0, 0, 0, 0);
+    if (cin && lr >= 0 && lr < nrows) {
+      const int i = lr * Lx + c;
+      m = *reinterpret_cast<const uint32_t*>(mask + i);
+      p = *reinterpret_cast<const float4*>(phi + i);
+      g = *reinterpret_cast<const int4*>(gid + i);
+    }
+  };
+  uint32_t mu, mc, md;
+  float4 pu, pc, pd;
+  int4 gu, gc, gd;
+  ld(la - 1, mu, pu, gu);
+  ld(la, mc, pc, gc);
+  for (int lr = la; lr < lz; ++lr) {
+    const int r = lr + lrow0;  // global row
+    const bool has_up = lr > 0, has_dn = lr + 1 < nrows && r + 1 < Ly;
+    ld(has_dn ? lr + 1 : -1, md, pd, gd);
+    float4 tv = make_float4(1.f, 1.f, 1.f, 1.f);
+    const bool tin = cin && r >= trow0 && r < trow1;
+    if (tin) tv = *reinterpret_cast<const float4*>(T + (r - trow0) * Lx + c);
+    // west neighbour of column 0 (lane - 1's column 3), east neighbour of column 3 (lane + 1's 0)
+    uint32_t mw = __shfl_up_sync(0xffffffffu, mc >> 24, 1);
+    float pw = __shfl_up_sync(0xffffffffu, pc.w, 1);
+    int gw = __shfl_up_sync(0xffffffffu, gc.w, 1);
+    uint32_t me = __shfl_down_sync(0xffffffffu, mc & 0xffu, 1);
+    float pe = __shfl_down_sync(0xffffffffu, pc.x, 1);
+    int ge = __shfl_down_sync(0xffffffffu, gc.x, 1);
+    const int i = lr * Lx + c;
+    if (lane == 0 && cin && c > 0) { mw = mask[i - 1]; pw = phi[i - 1]; gw = gid[i - 1]; }
+    if (lane == 31 && cin && c + 4 < Lx) { me = mask[i + 4]; pe = phi[i + 4]; ge = gid[i + 4]; }
+    const int rb = r / lb;
+    const float pcv[4] = {pc.x, pc.y, pc.z, pc.w}, puv[4] = {pu.x, pu.y, pu.z, pu.w}, pdv[4] = {pd.x, pd.y, pd.z, pd.w};
+    const int gcv[4] = {gc.x, gc.y, gc.z, gc.w}, guv[4] = {gu.x, gu.y, gu.z, gu.w}, gdv[4] = {gd.x, gd.y, gd.z, gd.w};
+    const float tvv[4] = {tv.x, tv.y, tv.z, tv.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!cin || byte_of(mc, j)) continue;
+      // neighbours N, S, W, E: (present, known, phi, gid)
+      const bool has[4] = {has_up, has_dn, c + j > 0, c + j + 1 < Lx};
+      const uint32_t km[4] = {byte_of(mu, j), byte_of(md, j), j > 0 ? byte_of(mc, j - 1) : mw,
+                              j < 3 ? byte_of(mc, j + 1) : me};
+      const float kp[4] = {puv[j], pdv[j], j > 0 ? pcv[j - 1] : pw, j < 3 ? pcv[j + 1] : pe};
+      const int kg[4] = {guv[j], gdv[j], j > 0 ? gcv[j - 1] : gw, j < 3 ? gcv[j + 1] : ge};
+      uint32_t flags = 0, nb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t ty = NB_NONE, v = 0;
+        if (has[k]) {
+          if (km[k]) { ty = NB_KNOWN; v = __float_as_uint(kp[k]); }
+          else       { ty = NB_GAP;   v = static_cast<uint32_t>(kg[k]); }
+        }
+        flags |= ty << (2 * k);
+        nb[k] = v;
+      }
+      const float beta = tin ? __fdiv_rn(1.0f, tvv[j]) : 0.0f;
+      const float init = binit[rb * nbx + bcol[j]];
+      const int32_t g = gcv[j];
+      ginit[g] = init;
+      uint4* dst = reinterpret_cast<uint4*>(rec + g);
+      dst[0] = make_uint4(static_cast<uint32_t>(r * Lx + c + j), __float_as_uint(beta), flags, __float_as_uint(init));
+      dst[1] = make_uint4(nb[0], nb[1], nb[2], nb[3]);
+    }
+    mu = mc; pu = pc; gu = gc;
+    mc = md; pc = pd; gc = gd;
+  }
 }
 
 // ------------------------------------------------------------- a11: predict
@@ -822,6 +1013,39 @@ __global__ void __launch_bounds__(256) k_predict(const float* __restrict__ z,
     const double v = __dadd_rn(static_cast<double>(zmin),
                                __dmul_rn(dz, __ddiv_rn(mean, static_cast<double>(kTwoPiF))));
     out[i] = __double2float_rn(v);
+  }
+}
+
+// The same, 4 sites per thread with 16-byte loads and stores (n % 4 == 0, aligned buffers).
+__global__ void __launch_bounds__(256) k_predict4(const float* __restrict__ z,
+                                                  const uint8_t* __restrict__ mask,
+                                                  const int32_t* __restrict__ gid,
+                                                  const double* __restrict__ acc, int64_t n,
+                                                  double denom, const DevScalars* __restrict__ sc,
+                                                  int degenerate, float* __restrict__ out) {
+  float zmin, zmax, s;
+  range_params(sc, &zmin, &zmax, &s);
+  const double dz = __dsub_rn(static_cast<double>(zmax), static_cast<double>(zmin));
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n / 4; q += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t m = *reinterpret_cast<const uint32_t*>(mask + 4 * q);
+    const float4 zv = __ldg(reinterpret_cast<const float4*>(z + 4 * q));
+    const int4 gv = __ldg(reinterpret_cast<const int4*>(gid + 4 * q));
+    const float zz[4] = {zv.x, zv.y, zv.z, zv.w};
+    const int gg[4] = {gv.x, gv.y, gv.z, gv.w};
+    float o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if ((m >> (8 * k)) & 0xffu) {
+        o[k] = zz[k];
+      } else if (degenerate) {
+        o[k] = zmin;
+      } else {
+        const double mean = __ddiv_rn(acc[gg[k]], denom);
+        o[k] = __double2float_rn(__dadd_rn(static_cast<double>(zmin),
+                                           __dmul_rn(dz, __ddiv_rn(mean, static_cast<double>(kTwoPiF)))));
+      }
+    }
+    *reinterpret_cast<float4*>(out + 4 * q) = make_float4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -882,6 +1106,10 @@ void launch_gap_rows(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_ba
 
 void launch_gap_compact(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, const int* rowoff,
                         int32_t* gid, cudaStream_t st) {
+  if (Lx % 4 == 0 && aligned16(gid) && (reinterpret_cast<uintptr_t>(mask) & 3u) == 0) {
+    k_row_compact4<<<static_cast<unsigned>((Ly + 7) / 8), 256, 0, st>>>(mask, Lx, Ly, row_base, rowoff, gid);
+    return;
+  }
   k_row_compact<<<static_cast<unsigned>(Ly), 256, 0, st>>>(mask, Lx, Ly, row_base, rowoff, gid);
 }
 
@@ -926,37 +1154,44 @@ void launch_expand(const float* Tb, int64_t Lx, int64_t trow0, int64_t trow1, in
   k_expand<<<grid_for(Lx * (trow1 - trow0), 256), 256, 0, st>>>(Tb, Lx, trow0, trow1, lb, T);
 }
 
-template <int RS, int TY>
+template <int RS, int TY, bool F64>
 static void smooth_rs(const float* Tin, const float* Tb, float* Tout, int64_t Lx, int64_t Ly, int64_t row_base,
                       int64_t Ly_g, int lb, cudaStream_t st) {
   dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((Ly + TY - 1) / TY));
   if (Tb)
-    k_smooth_rs<RS, TY, true><<<grid, 256, 0, st>>>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb);
+    k_smooth_rs<RS, TY, true, F64><<<grid, 256, 0, st>>>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb);
   else
-    k_smooth_rs<RS, TY, false><<<grid, 256, 0, st>>>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb);
+    k_smooth_rs<RS, TY, false, F64><<<grid, 256, 0, st>>>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb);
 }
 
 template <int RS>
 static void smooth_rs_ty(const float* Tin, const float* Tb, float* Tout, int64_t Lx, int64_t Ly, int64_t row_base,
-                         int64_t Ly_g, int lb, cudaStream_t st) {
+                         int64_t Ly_g, int lb, bool f64, cudaStream_t st) {
   // 32 x 64 tiles once the grid has >= 16 waves of them on 148 SMs, 32 x 32 below
-  if ((Lx + kTile - 1) / kTile * ((Ly + 63) / 64) >= 148 * 16)
-    smooth_rs<RS, 64>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st);
-  else
-    smooth_rs<RS, 32>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st);
+  const bool tall = (Lx + kTile - 1) / kTile * ((Ly + 63) / 64) >= 148 * 16;
+  if (f64) {
+    if (tall) smooth_rs<RS, 64, true>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st);
+    else smooth_rs<RS, 32, true>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st);
+  } else {
+    if (tall) smooth_rs<RS, 64, false>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st);
+    else smooth_rs<RS, 32, false>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st);
+  }
 }
 
 bool launch_smooth_specialised(const float* Tin, const float* Tb, float* Tout, int64_t Lx, int64_t Ly,
-                               int64_t row_base, int64_t Ly_g, int rs, int lb, cudaStream_t st) {
+                               int64_t row_base, int64_t Ly_g, int rs, int lb, float Tmin, float Tmax, cudaStream_t st) {
+  // exact fp64 window sums when every term is an integer-valued float and every sum < 2^53
+  const double w = 2.0 * rs + 1.0;
+  const bool f64 = Tmin >= 0x1p-17f && w * w * static_cast<double>(Tmax) < 8192.0;
   switch (rs) {
-    case 1: smooth_rs_ty<1>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
-    case 2: smooth_rs_ty<2>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
-    case 3: smooth_rs_ty<3>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
-    case 4: smooth_rs_ty<4>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
-    case 5: smooth_rs_ty<5>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
-    case 6: smooth_rs_ty<6>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
-    case 7: smooth_rs_ty<7>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
-    case 8: smooth_rs_ty<8>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, st); return true;
+    case 1: smooth_rs_ty<1>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, f64, st); return true;
+    case 2: smooth_rs_ty<2>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, f64, st); return true;
+    case 3: smooth_rs_ty<3>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, f64, st); return true;
+    case 4: smooth_rs_ty<4>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, f64, st); return true;
+    case 5: smooth_rs_ty<5>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, f64, st); return true;
+    case 6: smooth_rs_ty<6>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, f64, st); return true;
+    case 7: smooth_rs_ty<7>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, f64, st); return true;
+    case 8: smooth_rs_ty<8>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb, f64, st); return true;
     default: return false;
   }
 }
@@ -981,19 +1216,34 @@ void launch_smooth(const float* Tin, float* Tout, int64_t Lx, int64_t Ly, int64_
     k_smooth<32><<<grid, 256, smem, st>>>(Tin, Tout, Lx, Ly, row_base, Ly_g, rs);
 }
 
+void launch_block_init(const long long* SP, const long long* NK, int64_t nblocks, const DevScalars* sc,
+                       float* binit, cudaStream_t st) {
+  k_block_init<<<static_cast<unsigned>((nblocks + 255) / 256), 256, 0, st>>>(SP, NK, nblocks, sc, binit);
+}
+
 void launch_build_records(const int32_t* gid, const uint8_t* mask, const float* phiK,
-                          const float* T, const long long* SP, const long long* NK,
-                          const DevScalars* sc, int64_t Lx, int64_t Ly, int64_t lrow0, int64_t lrow1,
-                          int64_t trow0, int64_t trow1, int lb, int64_t P, GapRec* rec, cudaStream_t st) {
+                          const float* T, const float* binit, int64_t Lx, int64_t Ly, int64_t lrow0, int64_t lrow1,
+                          int64_t trow0, int64_t trow1, int lb, int64_t P, GapRec* rec, float* ginit,
+                          cudaStream_t st) {
   if (P == 0) return;
-  dim3 grid(static_cast<unsigned>((Lx + 255) / 256), static_cast<unsigned>(lrow1 - lrow0));
-  k_build_records<<<grid, 256, 0, st>>>(gid, mask, phiK, T, SP, NK, sc, Lx, Ly, lrow0, lrow1 - lrow0, trow0, trow1,
-                                        lb, rec);
+  const int64_t nrows = lrow1 - lrow0;
+  if (Lx % 4 == 0 && aligned16(gid) && aligned16(phiK) && aligned16(T) && (reinterpret_cast<uintptr_t>(mask) & 3u) == 0) {
+    dim3 grid(static_cast<unsigned>((Lx + 127) / 128), static_cast<unsigned>((nrows + 8 * kRowsPerWarp - 1) / (8 * kRowsPerWarp)));
+    k_build_records4<<<grid, 256, 0, st>>>(gid, mask, phiK, T, binit, Lx, Ly, lrow0, nrows, trow0, trow1, lb, rec, ginit);
+    return;
+  }
+  dim3 grid(static_cast<unsigned>((Lx + 255) / 256), static_cast<unsigned>(nrows));
+  k_build_records<<<grid, 256, 0, st>>>(gid, mask, phiK, T, binit, Lx, Ly, lrow0, nrows, trow0, trow1, lb,
+                                        rec, ginit);
 }
 
 void launch_predict(const float* z, const uint8_t* mask, const int32_t* gid, const double* acc,
                     int64_t n, double denom, const DevScalars* sc, int degenerate, float* out,
                     cudaStream_t st) {
+  if (n % 4 == 0 && aligned16(z) && aligned16(gid) && aligned16(out) && (reinterpret_cast<uintptr_t>(mask) & 3u) == 0) {
+    k_predict4<<<grid_for(n / 4, 256), 256, 0, st>>>(z, mask, gid, acc, n, denom, sc, degenerate, out);
+    return;
+  }
   k_predict<<<grid_for(n, 256), 256, 0, st>>>(z, mask, gid, acc, n, denom, sc, degenerate, out);
 }
 

@@ -522,7 +522,10 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
 // Items t = g * nunits + u are visited with a grid stride; (g, u) advance incrementally, so
 // the loop has no integer division (items < 2^31: the host caps P * R).
 template <int U>
+// ginit: the BLOCK_MEAN angle of every gap as a compact array (4 bytes per gap instead of
+// the 32-byte record sector that holds it).
 __global__ void __launch_bounds__(256) k_init_states(const GapRec* __restrict__ rec,
+                                                     const float* __restrict__ ginit,
                                                      float* __restrict__ G, float* __restrict__ A,
                                                      int64_t P, int R, int npairs,
                                                      uint32_t pair_base, int random_init,
@@ -543,7 +546,7 @@ __global__ void __launch_bounds__(256) k_init_states(const GapRec* __restrict__ 
         v[2 * h + 1] = proposal_angle(w.w2);
       }
     } else {
-      const float f = rec[g].init;
+      const float f = ginit[g];
 #pragma unroll
       for (int h = 0; h < 2 * U; ++h) v[h] = f;
     }
@@ -789,7 +792,7 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   launch_pdl(fn, static_cast<unsigned>(g), static_cast<unsigned>(nt), args, sweep_smem(variant), st);
 }
 
-void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R, int npairs,
+void launch_init_states(const GapRec* rec, const float* ginit, float* G, float* A, int64_t P, int R, int npairs,
                         uint32_t pair_base, int random_init, uint32_t k0, uint32_t k1,
                         cudaStream_t st) {
   const bool quad = (npairs % 2) == 0;  // float4 items (R % 4 == 0: 16-byte aligned rows)
@@ -797,7 +800,8 @@ void launch_init_states(const GapRec* rec, float* G, float* A, int64_t P, int R,
   int64_t g = (items + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
   if (g < 1) g = 1;
-  void* args[] = {const_cast<GapRec**>(&rec), &G, &A, &P, &R, &npairs, &pair_base, &random_init, &k0, &k1};
+  void* args[] = {const_cast<GapRec**>(&rec), const_cast<float**>(&ginit), &G, &A, &P, &R, &npairs, &pair_base,
+                  &random_init, &k0, &k1};
   launch_pdl(quad ? reinterpret_cast<const void*>(k_init_states<2>) : reinterpret_cast<const void*>(k_init_states<1>),
              static_cast<unsigned>(g), 256, args, 0, st);
 }

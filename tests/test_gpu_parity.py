@@ -154,6 +154,25 @@ def test_sst_field_bit_exact_window_sizes(P, calib, rs, ns):
     assert_bitwise(T, p.T, f"T field r_s={rs} n_s={ns}")
 
 
+@pytest.mark.parametrize("scale,rs,ns", [(1.0, 2, 5), (100.0, 2, 3), (300.0, 3, 2), (1e-2, 1, 2), (1e-3, 2, 2)])
+def test_sst_fixed_point_paths_bit_exact(P, calib, scale, rs, ns):
+    """The specialised SST pass forms the exact window sums in fp64 when every term is an
+    integer-valued float below the 2^53 bound ((2 r_s + 1)^2 T_max < 2^13, T_min >= 2^-17),
+    else in int64 (tables scaled by 100 and 300: the int64 path; by 1e-3: T_min < 2^-17, the
+    int64 path with llrint rounding). Both give the oracle's T field bit for bit, from the
+    first (T_b-reading) pass on, on a grid with interior and edge tiles."""
+    Tk, ek = calib
+    Ts = (Tk.astype(np.float64) * scale).astype(np.float32)
+    truth, z, mask = make_problem(150, 0.45, Lx=203, corr_len=7.0)
+    cfg = P.Config(r_s=rs, n_s=ns, l_b=16)
+    m = P.LeMpr(cfg, (Ts, ek))
+    m.set_data(z, mask)
+    T = m.estimate_local_params(want_T=True)
+    m.close()
+    p = O.parameters(z, mask, ocfg(cfg), Ts, ek)
+    assert_bitwise(T, p.T, f"T field (table x{scale}, r_s={rs}, n_s={ns})")
+
+
 def test_sharded_ranges_equal_single_call(P, calib):
     """simulate_range over [0,4) then [4,10) == simulate(10) bit for bit (global realization ids)."""
     truth, z, mask = make_problem(40, 0.5, corr_len=6.0)
