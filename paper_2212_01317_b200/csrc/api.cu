@@ -64,6 +64,7 @@ struct BatchKey {
   // P and PA can have other phase boundaries)
   void* dclist;
   int64_t dc_off[5];
+  int dc_rc;  // DC with shared-memory tiles: realizations per tile CTA (0: the phase lists)
   // own gap-id ranges per colour (row slabs: a sub-range of the local ids)
   int64_t own[2][2];
 };
@@ -140,6 +141,10 @@ struct mpr_ctx {
   // CUDA graphs of the per-batch launch sequence (replayed when the key repeats)
   int use_graphs = 1;
   int slab_graphs = 0;  // MPR_SLAB_GRAPHS: also capture row-slab batches (NCCL halos inside)
+  // MPR_DC_TILED=1: DC order on the paper's shared-memory tiles (k_sweep_dc_tile) instead of
+  // the phase lists. Bit-identical; measured 2.6-4.5x slower at C2 (M = 100: 12.4-21.7 ms of
+  // sweeps against 4.8 ms; profiles/r02_summary.md), so the lists are the default DC path.
+  int dc_tiled = 0;
   std::vector<GraphEntry> graphs = std::vector<GraphEntry>(8);
   size_t graph_next = 0;
   int energy_enabled = 0;
@@ -591,6 +596,7 @@ mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
   if (const char* v = std::getenv("MPR_SWEEP_VARIANT")) c->sweep_variant = std::atoi(v);
   if (const char* v = std::getenv("MPR_NO_GRAPHS")) c->use_graphs = std::atoi(v) ? 0 : 1;
   if (const char* v = std::getenv("MPR_SLAB_GRAPHS")) c->slab_graphs = std::atoi(v) ? 1 : 0;
+  if (const char* v = std::getenv("MPR_DC_TILED")) c->dc_tiled = std::atoi(v) ? 1 : 0;
   if (const char* v = std::getenv("MPR_SPLIT_MIN_P")) c->split_min_P = std::atoll(v);
   c->sweep_grid = sweep_grid_size(c->device, c->sweep_variant);
   *out = c;
@@ -826,6 +832,16 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
     a.sweep = static_cast<uint32_t>(s);
     a.accumulate = avg && (s > k.sweeps - k.n_avg);
     a.energy = k.energy ? k.energy + (s - 1) : nullptr;
+    if (k.dc_rc > 0) {  // DC on shared-memory tiles: one launch per tile parity (both colours)
+      for (int tau = 0; tau < 2; ++tau) {
+        launch_sweep_dc_tiles(a, c->gid.as<int32_t>(), c->phiK.as<float>(), c->T.as<float>(), c->Lx, c->Ly,
+                              c->cfg.l_b, tau, k.dc_rc, st);
+        CKL("sweep_dc_tiles");
+        ++c->launches;
+        ++*nsweep;
+      }
+      continue;
+    }
     // SC: colour A then B (contiguous gap-id ranges); DC: (even tiles A, B), (odd tiles A, B)
     const int nphase = k.order == MPR_ORDER_DC ? 4 : 2;
     for (int ph = 0; ph < nphase; ++ph) {
@@ -947,6 +963,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
     if (c->cfg.order == MPR_ORDER_DC) {
       key.dclist = c->dclist.p;
       for (int k = 0; k < 5; ++k) key.dc_off[k] = c->dc_off[k];
+      key.dc_rc = c->dc_tiled ? dc_tile_chunk(c->cfg.l_b, Rb) : 0;
     }
     for (int col = 0; col < 2; ++col)
       for (int e = 0; e < 2; ++e) key.own[col][e] = c->own[col][e];

@@ -134,6 +134,12 @@ struct SweepArgs {
   uint32_t peer_lo[2], peer_hi[2];
 };
 int sweep_grid_size(int device, int variant);
+// Row f3 with shared-memory tiles: one launch updates every l_b tile of parity
+// tau, both colours inside the tile (= the DC phases (tau, A), (tau, B)). dc_tile_chunk: the
+// realizations per CTA for this l_b and batch (0: the tile does not fit shared memory).
+int dc_tile_chunk(int lb, int R);
+void launch_sweep_dc_tiles(const SweepArgs& s, const int32_t* gid, const float* phiK, const float* T, int64_t Lx,
+                           int64_t Ly, int lb, int tau, int Rc, cudaStream_t st);
 void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st);
 void launch_init_states(const GapRec* rec, const float* ginit, float* G, float* A, int64_t P, int R, int npairs,
                         uint32_t pair_base, int random_init, uint32_t k0, uint32_t k1,

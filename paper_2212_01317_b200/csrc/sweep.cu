@@ -19,7 +19,9 @@
 // step chose (evaluated only in the ENERGY kernels).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "device_math.cuh"
 #include "internal.cuh"
@@ -517,6 +519,133 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
   pdl_trigger();
 }
 
+// Row f3, the paper's DC scheme with shared-memory tiles ("Each tile can be
+// loaded into the block's shared memory ... looking up the neighboring spins uses shared
+// instead of global memory"). One CTA per (l_b x l_b tile of parity tau, chunk of Rc
+// realizations): the tile and its one-site halo are staged densely in shared memory (gap
+// states of the chunk, the frozen angles of the samples), the tile's colour-A gaps are
+// updated, then its colour-B gaps against the new A states, and the tile's gap states are
+// written back. During the tau phase the other parity's tiles do not change, so this is
+// exactly the phases (tau, A), (tau, B) of ARITH §H's DC order — and each update is the
+// same metropolis_pair with the same Philox words as the list kernels: bit-identical.
+// The halo ring holds only the neighbours of tile sites, so out-of-grid cells are never read.
+struct DcTileArgs {
+  const int32_t* gid;   // gap id per site (-1: sample)
+  const float* phiK;    // frozen angles of the samples
+  const float* T;       // temperature field (beta = 1 / T, as the records hold it)
+  float* G;             // state [P][R]
+  float* A;             // last-n_avg accumulator [P][R] (nullable)
+  int64_t Lx, Ly;
+  int lb, tau, R, Rc;   // tile side, parity; batch stride; realizations per CTA chunk (even)
+  int nchunks;          // chunks of Rc realizations covering the npairs * 2 of the batch
+  int npairs;
+  uint32_t pair_base, sweep;
+  uint32_t rk0[10], rk1[10];
+  float q, J;
+  int accumulate;
+};
+
+template <bool QHALF>
+__global__ void __launch_bounds__(256) k_sweep_dc_tile(const DcTileArgs a) {
+  extern __shared__ float ds[];
+  pdl_wait();
+  const int W = a.lb + 2;            // tile + halo width (cells)
+  const int chunk = blockIdx.z;
+  const int tr = blockIdx.y;
+  const int s0 = (a.tau + tr) & 1;   // first tile column of parity tau in this tile row
+  const int tc = s0 + 2 * blockIdx.x;
+  const int64_t r0 = static_cast<int64_t>(tr) * a.lb, c0 = static_cast<int64_t>(tc) * a.lb;
+  if (c0 >= a.Lx) return;
+  const int hr = static_cast<int>(min(static_cast<int64_t>(a.lb), a.Ly - r0)), hc = static_cast<int>(min(static_cast<int64_t>(a.lb), a.Lx - c0));
+  const int rc0 = chunk * a.Rc;                 // first realization of the chunk in the batch
+  const int nr = min(a.Rc, 2 * a.npairs - rc0);  // realizations of this chunk (even)
+  const int Rc = a.Rc;
+  // shared layout: [W * W cells][Rc] floats, then two lists of tile gap cells (A, B)
+  float* S = ds;
+  int* list = reinterpret_cast<int*>(ds + W * W * Rc);
+  __shared__ int ncol[2];
+  if (threadIdx.x < 2) ncol[threadIdx.x] = 0;
+  __syncthreads();
+  // stage: cells of the tile and its halo ring inside the grid (corners are never read)
+  for (int t = threadIdx.x; t < W * W; t += blockDim.x) {
+    const int y = t / W, x = t - y * W;
+    const int64_t r = r0 - 1 + y, c = c0 - 1 + x;
+    const bool intile = y >= 1 && y <= hr && x >= 1 && x <= hc;
+    const bool ring = !intile && (y >= 1 && y <= hr ? (x == 0 || x == hc + 1) : (x >= 1 && x <= hc && (y == 0 || y == hr + 1)));
+    if (!(intile || ring) || r < 0 || r >= a.Ly || c < 0 || c >= a.Lx) continue;
+    const int64_t i = r * a.Lx + c;
+    const int g = a.gid[i];
+    float* cell = S + t * Rc;
+    if (g < 0) {
+      const float v = a.phiK[i];
+      for (int k = 0; k < nr; ++k) cell[k] = v;
+    } else {
+      const float* src = a.G + static_cast<int64_t>(g) * a.R + rc0;
+      for (int k = 0; k < nr; k += 2) *reinterpret_cast<float2*>(cell + k) = *reinterpret_cast<const float2*>(src + k);
+      if (intile) {  // a tile gap: onto its colour's list
+        const int col = static_cast<int>((r + c) & 1);
+        const int pos = atomicAdd(&ncol[col], 1);
+        list[col * a.lb * a.lb + pos] = t;
+      }
+    }
+  }
+  __syncthreads();
+  const int npc = nr / 2;  // pairs of the chunk
+  const uint32_t pair0 = a.pair_base + static_cast<uint32_t>(rc0 / 2);
+  const float* gA = nullptr;
+  for (int col = 0; col < 2; ++col) {
+    const int n = ncol[col];
+    for (int it = threadIdx.x; it < n * npc; it += blockDim.x) {
+      const int li = it / npc, j = it - li * npc;
+      const int t = list[col * a.lb * a.lb + li];
+      const int y = t / W, x = t - y * W;
+      const int64_t r = r0 - 1 + y, c = c0 - 1 + x;
+      const uint32_t site = static_cast<uint32_t>(r * a.Lx + c);
+      const Words4 w = philox4x32_10_rk(site, a.sweep, pair0 + j, 2u, a.rk0, a.rk1);
+      const int nbc[4] = {t - W, t + W, t - 1, t + 1};
+      const bool has[4] = {r > 0, r + 1 < a.Ly, c > 0, c + 1 < a.Lx};
+      uint32_t flags = 0;
+      float2 nb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        flags |= (has[k] ? 1u : 0u) << (2 * k);
+        nb[k] = has[k] ? *reinterpret_cast<const float2*>(S + nbc[k] * Rc + 2 * j) : make_float2(0.f, 0.f);
+      }
+      float2* cp = reinterpret_cast<float2*>(S + t * Rc + 2 * j);
+      const float2 cur = *cp;
+      const float beta = __fdiv_rn(1.0f, a.T[r * a.Lx + c]);
+      bool acc0, acc1;
+      long long e0 = 0, e1 = 0;
+      const float2 nv = (flags == 0x55u)
+          ? metropolis_pair<QHALF, false, true>(cur, nb, flags, 0u, beta, a.q, a.J, w, acc0, acc1, e0, e1)
+          : metropolis_pair<QHALF, false, false>(cur, nb, flags, 0u, beta, a.q, a.J, w, acc0, acc1, e0, e1);
+      *cp = nv;
+    }
+    __syncthreads();  // colour B reads the new colour-A states
+  }
+  (void)gA;
+  // write back the tile's gap states (and the last-n_avg accumulation)
+  for (int col = 0; col < 2; ++col) {
+    const int n = ncol[col];
+    for (int it = threadIdx.x; it < n * npc; it += blockDim.x) {
+      const int li = it / npc, j = it - li * npc;
+      const int t = list[col * a.lb * a.lb + li];
+      const int y = t / W, x = t - y * W;
+      const int64_t i = (r0 - 1 + y) * a.Lx + (c0 - 1 + x);
+      const int64_t off = static_cast<int64_t>(a.gid[i]) * a.R + rc0 + 2 * j;
+      const float2 v = *reinterpret_cast<const float2*>(S + t * Rc + 2 * j);
+      *reinterpret_cast<float2*>(a.G + off) = v;
+      if (a.accumulate) {
+        float2 av = *reinterpret_cast<float2*>(a.A + off);
+        av.x = __fadd_rn(av.x, v.x);
+        av.y = __fadd_rn(av.y, v.y);
+        *reinterpret_cast<float2*>(a.A + off) = av;
+      }
+    }
+  }
+  pdl_trigger();
+}
+
 // a6: initial states of a batch (ARITH §G).
 // U realization pairs per work item (U = 2: float4 stores, needs an even pair count).
 // Items t = g * nunits + u are visited with a grid stride; (g, u) advance incrementally, so
@@ -790,6 +919,69 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   }
   void* args[] = {&b};
   launch_pdl(fn, static_cast<unsigned>(g), static_cast<unsigned>(nt), args, sweep_smem(variant), st);
+}
+
+// Shared memory of one DC tile CTA: (l_b + 2)^2 cells x Rc realizations + the two gap lists.
+static size_t dc_tile_smem(int lb, int Rc) {
+  return sizeof(float) * static_cast<size_t>(lb + 2) * (lb + 2) * Rc + sizeof(int) * 2 * static_cast<size_t>(lb) * lb;
+}
+
+int dc_tile_chunk(int lb, int R) {
+  // the largest even chunk (<= R, <= MPR_DC_RC, default 4) whose tile fits 200 KB of shared
+  // memory; 0: none fits
+  static const int cap = [] {
+    const char* v = std::getenv("MPR_DC_RC");
+    const int c = v ? std::atoi(v) : 4;
+    return c >= 2 ? c : 2;
+  }();
+  for (int rc = std::min(R, cap) & ~1; rc >= 2; rc -= 2)
+    if (dc_tile_smem(lb, rc) <= 200 * 1024) return rc;
+  return 0;
+}
+
+void launch_sweep_dc_tiles(const SweepArgs& s, const int32_t* gid, const float* phiK, const float* T, int64_t Lx,
+                           int64_t Ly, int lb, int tau, int Rc, cudaStream_t st) {
+  DcTileArgs a{};
+  a.gid = gid;
+  a.phiK = phiK;
+  a.T = T;
+  a.G = s.G;
+  a.A = s.A;
+  a.Lx = Lx;
+  a.Ly = Ly;
+  a.lb = lb;
+  a.tau = tau;
+  a.R = s.R;
+  a.Rc = Rc;
+  a.npairs = s.npairs;
+  a.nchunks = (2 * s.npairs + Rc - 1) / Rc;
+  a.pair_base = s.pair_base;
+  a.sweep = s.sweep;
+  for (int i = 0; i < 10; ++i) {
+    a.rk0[i] = s.k0 + static_cast<uint32_t>(i) * 0x9E3779B9u;
+    a.rk1[i] = s.k1 + static_cast<uint32_t>(i) * 0xBB67AE85u;
+  }
+  a.q = s.q;
+  a.J = s.J;
+  a.accumulate = s.accumulate;
+  const int nbx = static_cast<int>((Lx + lb - 1) / lb), nby = static_cast<int>((Ly + lb - 1) / lb);
+  const size_t smem = dc_tile_smem(lb, Rc);
+  const bool qhalf = (s.q == 0.5f);
+  const void* fn = qhalf ? reinterpret_cast<const void*>(k_sweep_dc_tile<true>)
+                         : reinterpret_cast<const void*>(k_sweep_dc_tile<false>);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>((nbx + 1) / 2), static_cast<unsigned>(nby), static_cast<unsigned>(a.nchunks));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  void* args[] = {&a};
+  cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 void launch_init_states(const GapRec* rec, const float* ginit, float* G, float* A, int64_t P, int R, int npairs,

@@ -553,6 +553,20 @@ def test_dc_order_bit_exact(P, calib, lb):
     compare(P, z, mask, truth, P.Config(l_b=lb, order="dc", n_s=1, r_s=1), calib, 6, 12, 31)
 
 
+@pytest.mark.parametrize("tiled", ["1", "0"])
+@pytest.mark.parametrize("lb,M,kw", [(32, 40, {}), (13, 10, dict(n_avg=3)), (64, 6, dict(q=0.3, J=1.5)),
+                                      (5, 34, dict(init="random")), (96, 4, {})])
+def test_dc_tiles_and_lists_bit_exact(P, calib, monkeypatch, tiled, lb, M, kw):
+    """Row f3 both ways (MPR_DC_TILED): the paper's shared-memory tiles (one CTA per tile of a
+    parity and realization chunk, both colours inside the tile; several chunks when M > 16)
+    and the phase-list launches: states and predictions equal the oracle's DC order, on
+    ragged grids whose edge tiles are partial, with n_avg > 1, generic q and RANDOM init."""
+    monkeypatch.setenv("MPR_DC_TILED", tiled)
+    truth, z, mask = make_problem(99, 0.55, Lx=131, corr_len=7.0)
+    cfg = P.Config(l_b=lb, order="dc", n_s=1, r_s=1, **kw)
+    compare(P, z, mask, truth, cfg, calib, M, 7, 41, exact_pred=cfg.n_avg == 1)
+
+
 def test_dc_rejects_sc_only_features(P, calib):
     truth, z, mask = make_problem(32, 0.5, corr_len=5.0)
     m = P.LeMpr(P.Config(order="dc", l_b=8), calib)
