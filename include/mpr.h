@@ -191,7 +191,10 @@ mpr_status mpr_simulate(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed);
  * realization sweeps until, at a check sweep s = n_fit + k*n_f, the least-squares slope
  * of its last n_fit whole-grid energies (ARITH §J, exact fixed point) is >=
  * -max(2 sigma / n_fit, slope_tol); it then averages the next n_avg sweeps and stops.
- * slope_tol (energy per sweep, >= 0; 0 = SPEC's rule) is SPEC's configurable tolerance.
+ * slope_tol (energy per sweep; 0 = SPEC's rule) is SPEC's configurable tolerance; a
+ * negative slope_tol asks for the tolerance derived from the data (reading R22):
+ * SE(e_s) / n_fit, the standard error of the sample specific energy of Eq.(2) over the sample
+ * bonds' cosines, spread over the fit window (mpr_info.slope_tol reports the value used).
  * No check passes before max_sweeps - n_avg => equilibrium is declared there (returned
  * negated). s_eq_out (nullable, host, M int32) receives each realization's equilibrium
  * sweep. Replaces any previous accumulation; predict as after mpr_simulate. The test
@@ -199,7 +202,8 @@ mpr_status mpr_simulate(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed);
  * trails one check behind, so sweeps issued after the last realization finished are
  * no-ops. Realization shards: each rank runs its id range; the accumulators and s_eq are
  * summed over the ranks (every rank gets all M decisions). Errors: M < 1, n_fit < 3,
- * n_f < 1, max_sweeps <= n_avg, slope_tol < 0, MPR_SHARD_ROWS with W > 1 -> INVALID_ARG. */
+ * n_f < 1, max_sweeps <= n_avg, non-finite slope_tol, MPR_SHARD_ROWS with W > 1 ->
+ * INVALID_ARG. */
 mpr_status mpr_simulate_adaptive(mpr_ctx *ctx, int64_t M, uint64_t seed, int32_t n_fit, int32_t n_f,
                                  int32_t max_sweeps, double slope_tol, int32_t *s_eq_out);
 
@@ -290,6 +294,9 @@ typedef struct {
   int64_t n_gaps_local;                          /* gap sites held by this rank
                                                     (own + ghost rows)              */
   int64_t comm_calls;                            /* collectives issued since init    */
+  double slope_tol;                              /* slope tolerance of the last
+                                                    adaptive run (derived: R22)     */
+  int64_t sample_bonds;                          /* N_SP: sample-sample bonds        */
 } mpr_info;
 mpr_status mpr_get_info(mpr_ctx *ctx, mpr_info *info);
 

@@ -56,6 +56,18 @@ def heterogeneous_field(L: int, nu: float = 1.5, corr_len: float = 16.0,
     return z.astype(np.float32)
 
 
+def domain_wall_field(L: int, tile: int = 64, low: float = 0.1, high: float = 10.0, nu: float = 1.5,
+                      corr_len: float = 8.0, seed: int = SEED_FIELD) -> np.ndarray:
+    """A field with SHARP variance domain walls: unit-variance Matern x scaled by `high` on
+    the tiles (tile x tile) of one checkerboard colour and by `low` on the others — the
+    "domains of almost constant values as well as domains with large spatial fluctuations"
+    of PAPER.md:100, with walls the smoothing of SST removes. float32."""
+    x = matern_field(L, L, nu=nu, corr_len=corr_len, seed=seed)
+    rr, cc = np.meshgrid(np.arange(L) // tile, np.arange(L) // tile, indexing="ij")
+    sigma = np.where(((rr + cc) & 1) == 1, high, low)
+    return (sigma * x).astype(np.float32)
+
+
 def random_mask(Ly: int, Lx: int, p: float, seed: int = SEED_MASK) -> np.ndarray:
     """uint8 mask, 1 = known sample; exactly round(p*Ly*Lx) gaps (P = pL^2)."""
     n = Ly * Lx

@@ -715,6 +715,37 @@ int oracle_equilibrium_test(const double *y, int n_fit, double slope_tol)
     return b >= -tau;
 }
 
+/* Reading R22: the slope tolerance derived from the data, tau = SE(e_s) / n_fit,
+ * the standard error of the sample specific energy of Eq.(2) spread over the fit
+ * window: SE^2 = var(b) / N_SP over the sample bonds' cosines b = cos_spec(q (phi_i - phi_j)),
+ * each unordered pair once; the sums are exact fixed point (S1 = sum llrint(b 2^32),
+ * S2 = sum llrint(fp32(b b) 2^32)), then fp64 in this order. Pinned against the fp64/libm
+ * sample standard deviation and hand lattices (test_derived_slope_tolerance_*). */
+double oracle_derived_slope_tol(const float *phi, const uint8_t *mask, int Lx, int Ly, float q, int n_fit)
+{
+    int64_t S1 = 0, S2 = 0, N = 0;
+    for (int r = 0; r < Ly; ++r)
+        for (int c = 0; c < Lx; ++c) {
+            int64_t i = (int64_t)r * Lx + c;
+            if (!mask[i]) continue;
+            if (c + 1 < Lx && mask[i + 1]) {
+                float b = oracle_cos_spec(q * (phi[i] - phi[i + 1]));
+                S1 += llrintf(b * 0x1p32f); S2 += llrintf((b * b) * 0x1p32f); ++N;
+            }
+            if (r + 1 < Ly && mask[i + Lx]) {
+                float b = oracle_cos_spec(q * (phi[i] - phi[i + Lx]));
+                S1 += llrintf(b * 0x1p32f); S2 += llrintf((b * b) * 0x1p32f); ++N;
+            }
+        }
+    if (N < 1) return 0.0;
+    double n = (double)N;
+    double mean = ((double)S1 * 0x1p-32) / n;
+    double m2 = ((double)S2 * 0x1p-32) / n;
+    double var = m2 - mean * mean;
+    if (var < 0.0) var = 0.0;
+    return sqrt(var / n) / (double)n_fit;
+}
+
 /* Adaptive protocol (row f1; ARITH §K): realization m sweeps until the energy
  * trace passes the equilibrium test at a check sweep (s = n_fit + k n_f), then runs
  * n_avg more sweeps accumulating each; capped at S_max. acc (fp64, Lx*Ly) is added to;
@@ -727,6 +758,8 @@ void oracle_simulate_adaptive(const float *phi0, const uint8_t *mask, const floa
                               double *acc, int32_t *s_eq, double *energy, float *phi_out)
 {
     int64_t n = (int64_t)Lx * Ly;
+    /* slope_tol < 0: the tolerance derived from the samples (R22) */
+    if (slope_tol < 0.0) slope_tol = oracle_derived_slope_tol(phi0, mask, Lx, Ly, cfg->q, n_fit);
     float *phi = (float *)malloc(sizeof(float) * (size_t)n);
     double *e = (double *)malloc(sizeof(double) * (size_t)(S_max + 1));
     for (int64_t m = m_begin; m < m_end; ++m) {

@@ -152,6 +152,8 @@ def _declare(L):
     L.oracle_grid_energy_fx.restype = C.c_int64
     L.oracle_energy_from_fx.argtypes = [C.c_int64, C.c_int, C.c_int]
     L.oracle_energy_from_fx.restype = C.c_double
+    L.oracle_derived_slope_tol.argtypes = [_f32p, _u8p, C.c_int, C.c_int, C.c_float, C.c_int]
+    L.oracle_derived_slope_tol.restype = C.c_double
     L.oracle_equilibrium_test.argtypes = [_f64p, C.c_int, C.c_double]
     L.oracle_equilibrium_test.restype = C.c_int
     L.oracle_simulate_adaptive.argtypes = [_f32p, _u8p, _f32p, C.c_int, C.c_int, C.POINTER(_Cfg), _i64p, _i64p,
@@ -358,10 +360,19 @@ def equilibrium_test(y, slope_tol=0.0) -> bool:
     return bool(lib().oracle_equilibrium_test(y, len(y), float(slope_tol)))
 
 
+def derived_slope_tol(phi, mask, q=0.5, n_fit=20) -> float:
+    """Reading R22: SE(e_s) / n_fit over the sample bonds (exact fixed-point sums, fp64)."""
+    phi = np.ascontiguousarray(phi, np.float32); mask = np.ascontiguousarray(mask, np.uint8)
+    return lib().oracle_derived_slope_tol(phi.ravel(), mask.ravel(), phi.shape[1], phi.shape[0], float(q), int(n_fit))
+
+
 def simulate_adaptive(params, mask, cfg, M, seed, n_fit=20, n_f=5, S_max=500, m_begin=0, m_end=None,
                       energy=False, states=False, slope_tol=0.0):
     """Row f1 protocol (ARITH §K) for realizations [m_begin, m_end): returns
-    dict(acc, s_eq (negative = forced by the cap), energy, phi)."""
+    dict(acc, s_eq (negative = forced by the cap), energy, phi). slope_tol="derived" (or < 0):
+    the R22 tolerance SE(e_s) / n_fit."""
+    if slope_tol == "derived":
+        slope_tol = -1.0
     m_end = M if m_end is None else m_end
     mask = np.ascontiguousarray(mask, np.uint8)
     Ly, Lx = mask.shape

@@ -60,7 +60,8 @@ class mpr_info(C.Structure):
                 ("sweep_ms", C.c_double), ("last_m_base", C.c_int64), ("last_batch", C.c_int64),
                 ("sweep_variant", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("shard", C.c_int32),
                 ("row_begin", C.c_int64), ("row_end", C.c_int64), ("m_begin", C.c_int64), ("m_end", C.c_int64),
-                ("n_gaps_local", C.c_int64), ("comm_calls", C.c_int64)]
+                ("n_gaps_local", C.c_int64), ("comm_calls", C.c_int64), ("slope_tol", C.c_double),
+                ("sample_bonds", C.c_int64)]
 
 
 _lib = None
@@ -264,7 +265,9 @@ def mpr_build_calibration(ctx, T, L=128, q=0.5, n_eq=400, n_meas=800, reps=2, se
 
 def mpr_simulate_adaptive(ctx, M, seed, n_fit=20, n_f=5, max_sweeps=500, slope_tol=0.0) -> np.ndarray:
     """Adaptive equilibration (ARITH §K); returns s_eq per realization
-    (negative = forced by max_sweeps)."""
+    (negative = forced by max_sweeps). slope_tol="derived" (or < 0): SE(e_s) / n_fit (R22)."""
+    if slope_tol == "derived":
+        slope_tol = -1.0
     s_eq = np.zeros(M, np.int32)
     _check(ctx, load_library().mpr_simulate_adaptive(ctx, M, seed, n_fit, n_f, max_sweeps, float(slope_tol),
                                                      s_eq.ctypes.data))

@@ -117,6 +117,8 @@ struct mpr_ctx {
   int64_t n_fallback = 0;
   float median_T = 0;
   long long sum_SB_fx = 0;  // fixed-point bond sum of the known-known bonds (ARITH §J)
+  long long sum_SB2_fx = 0; // fixed-point sum of their squared cosines (reading R22)
+  long long n_sample_bonds = 0;
   // this rank's rows: own [row0, row1); local z/mask/phi/gid rows [lrow0, lrow1) (own + one
   // ghost row per side); local temperature rows [trow0, trow1) (own + the smoothing halo)
   int64_t row0 = 0, row1 = 0, lrow0 = 0, lrow1 = 0, trow0 = 0, trow1 = 0;
@@ -153,6 +155,7 @@ struct mpr_ctx {
   int defer_reduce = 0;
   int pending_reduce = 0, pending_Rb = 0, pending_r_lo = 0, pending_r_hi = 0;
   int64_t energy_M = 0, energy_S = 0;
+  double last_slope_tol = 0.0;  // the slope tolerance the last adaptive run used
   std::vector<int> rowoff_h, rowcnt_h;  // host copies of the gap-id row offsets (row slabs)
   // device memory
   DBuf z, mask, phiK, scal, calTd, caled, rowcnt, rowoff, gid, rec, bstats, Tb, T, T2, G, A, acc,
@@ -285,6 +288,22 @@ float key_to_float(int k) {
 double energy_from_fx(const mpr_ctx* c, long long E_fx) {
   const double nb = static_cast<double>(2 * c->Lx * c->Ly - c->Lx - c->Ly);
   return (-static_cast<double>(E_fx) * 0x1p-32) / nb;
+}
+
+// Reading R22: the slope tolerance of the equilibrium test derived from the data —
+// the standard error of the sample specific energy e_s (Eq.(2)), spread over
+// the n_fit-sweep fit window: tau = SE(e_s) / n_fit with SE(e_s)^2 = var(b) / N_SP over the
+// sample bonds' cosines b (exact fixed-point sums S1 = sum llrint(b 2^32), S2 = sum llrint(b^2
+// 2^32)). A drift below it over the window is smaller than the uncertainty of the energy the
+// temperatures were matched to. fp64, in this order (the oracle's oracle_derived_slope_tol).
+double derived_slope_tol(long long S1, long long S2, long long N, int n_fit) {
+  if (N < 1) return 0.0;
+  const double n = static_cast<double>(N);
+  const double mean = (static_cast<double>(S1) * 0x1p-32) / n;
+  const double m2 = (static_cast<double>(S2) * 0x1p-32) / n;
+  double var = m2 - mean * mean;
+  if (var < 0.0) var = 0.0;
+  return std::sqrt(var / n) / static_cast<double>(n_fit);
 }
 
 // Forget every captured batch graph: their launches bake in buffer pointers and gap-id
@@ -683,10 +702,13 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   // a3 over the own rows (a bond belongs to the block of its left/top end: the rank owning
   // that end counts it; a down bond of the last own row reads the lower ghost row)
   launch_block_stats(c->phiK.as<float>(), c->mask.as<uint8_t>(), c->Lx, c->Ly, c->lrow0, c->row0, c->row1, lb,
-                     c->cfg.q, SB, NB, SP, NK, c->nblocks, st);
+                     c->cfg.q, SB, NB, SP, NK, c->nblocks, dsc, st);
   CKL("block_stats");
   // row slabs: every rank's partial block sums -> the global ones on every rank (exact int64)
-  if (c->rows) CKC(c->comm->allreduce(SB, static_cast<size_t>(4 * c->nblocks), CT_I64, OP_SUM, st), "allreduce block sums");
+  if (c->rows) {
+    CKC(c->comm->allreduce(SB, static_cast<size_t>(4 * c->nblocks), CT_I64, OP_SUM, st), "allreduce block sums");
+    CKC(c->comm->allreduce(&dsc->sum_SB2, 1, CT_I64, OP_SUM, st), "allreduce squared bond sum");
+  }
   launch_block_T(SB, NB, SP, NK, c->nblocks, c->calTd.as<float>(), c->caled.as<float>(),
                  static_cast<int>(c->calT.size()), c->Tb.as<float>(), dsc, st);
   CKL("block_T");
@@ -728,6 +750,8 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   c->n_fallback = static_cast<int64_t>(c->hsc->n_fallback);
   c->median_T = c->hsc->median_T;
   c->sum_SB_fx = c->hsc->sum_SB;
+  c->sum_SB2_fx = c->hsc->sum_SB2;
+  c->n_sample_bonds = c->hsc->sum_NB;
   if (c->hsc->n_avail == 0 && !c->degenerate)
     return fail(c, MPR_ERR_NO_SAMPLE_BONDS, "no block has a sample-sample bond (PAPER.md:108)");
   if (c->cfg.order == MPR_ORDER_DC && c->P > 0) {
@@ -1116,11 +1140,14 @@ mpr_status mpr_simulate(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t seed) {
 mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n_fit, int32_t n_f,
                                  int32_t max_sweeps, double slope_tol, int32_t* s_eq_out) {
   if (!c) return MPR_ERR_INVALID_ARG;
-  if (!(slope_tol >= 0.0) || !std::isfinite(slope_tol)) return fail(c, MPR_ERR_INVALID_ARG, "slope_tol must be >= 0");
+  if (!std::isfinite(slope_tol)) return fail(c, MPR_ERR_INVALID_ARG, "slope_tol must be finite");
   if (c->stage < ST_PARAMS) return fail(c, MPR_ERR_STATE, "simulate before estimate_local_params");
   const int n_avg = c->cfg.n_avg;
   if (M < 1 || n_fit < 3 || n_f < 1 || max_sweeps < n_avg + 1 || M >= (int64_t(1) << 32))
     return fail(c, MPR_ERR_INVALID_ARG, "need M >= 1, n_fit >= 3, n_f >= 1, max_sweeps > n_avg");
+  // slope_tol < 0: the tolerance derived from the sample energy's standard error (R22)
+  if (slope_tol < 0.0) slope_tol = derived_slope_tol(c->sum_SB_fx, c->sum_SB2_fx, c->n_sample_bonds, n_fit);
+  c->last_slope_tol = slope_tol;
   if (c->cfg.order != MPR_ORDER_SC)
     return fail(c, MPR_ERR_INVALID_ARG, "the adaptive protocol needs the SC order (fused energy)");
   if (c->rows) return fail(c, MPR_ERR_INVALID_ARG, "the adaptive protocol runs with realization shards, not row slabs");
@@ -1453,6 +1480,8 @@ mpr_status mpr_get_info(mpr_ctx* c, mpr_info* info) {
   info->m_end = c->m_end;
   info->n_gaps_local = c->P;
   info->comm_calls = c->comm_calls;
+  info->slope_tol = c->last_slope_tol;
+  info->sample_bonds = c->n_sample_bonds;
   return MPR_OK;
 }
 

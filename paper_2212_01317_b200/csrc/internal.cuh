@@ -41,6 +41,8 @@ struct DevScalars {
   long long sum_SB;              // sum over blocks of SB (known-known bond cos, 2^32)
   long long sum_SP;              // sum of llrint(phi*2^28) over samples
   long long sum_NK;              // samples (again, as int64 for the global mean)
+  long long sum_SB2;             // sum over sample bonds of llrint(fp32(b*b) * 2^32) (R22)
+  long long sum_NB;              // sample bonds (N_SP of Eq.(2) over the whole grid)
   float median_T;
   float pad1;
 };
@@ -63,9 +65,10 @@ void launch_gap_compact(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row
 void launch_gap_index(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_base, int* rowcnt,
                       int* rowoff, int32_t* gid, cudaStream_t st);
 // block sums of the own rows [row0, row1) (global) of a buffer starting at global row lrow0
+// (also adds the squared sample-bond cosines to sc->sum_SB2: the derived slope tolerance, R22)
 void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t lrow0,
                         int64_t row0, int64_t row1, int lb, float q, long long* SB, long long* NB,
-                        long long* SP, long long* NK, int64_t nblocks, cudaStream_t st);
+                        long long* SP, long long* NK, int64_t nblocks, DevScalars* sc, cudaStream_t st);
 void launch_block_T(const long long* SB, const long long* NB, const long long* SP,
                     const long long* NK, int64_t nblocks, const float* calT, const float* cale,
                     int K, float* Tb, DevScalars* sc, cudaStream_t st);

@@ -321,8 +321,9 @@ __global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ p
                                                      long long* __restrict__ SB,
                                                      long long* __restrict__ NB,
                                                      long long* __restrict__ SP,
-                                                     long long* __restrict__ NK) {
+                                                     long long* __restrict__ NK, DevScalars* sc) {
   __shared__ long long sSB[kMaxSlots], sNB[kMaxSlots], sSP[kMaxSlots], sNK[kMaxSlots];
+  long long tsb2 = 0;  // this thread's squared sample-bond cosines (fixed point, R22)
   const int64_t c0 = (int64_t)blockIdx.x * kTile, r0 = (row0 / kTile) * kTile + (int64_t)blockIdx.y * kTile;
   const int64_t nbx = (Lx + lb - 1) / lb;
   const int64_t bc0 = c0 / lb, br0 = max(r0, row0) / lb;
@@ -350,11 +351,13 @@ __global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ p
           if (c + 1 < Lx && mask[i + 1]) {
             const float bnd = cos_spec(__fmul_rn(q, __fsub_rn(pi, phi[i + 1])));
             vsb += __float2ll_rn(__fmul_rn(bnd, 0x1p32f));
+            tsb2 += __float2ll_rn(__fmul_rn(__fmul_rn(bnd, bnd), 0x1p32f));
             vnb += 1;
           }
           if (r + 1 < Ly && mask[i + Lx]) {
             const float bnd = cos_spec(__fmul_rn(q, __fsub_rn(pi, phi[i + Lx])));
             vsb += __float2ll_rn(__fmul_rn(bnd, 0x1p32f));
+            tsb2 += __float2ll_rn(__fmul_rn(__fmul_rn(bnd, bnd), 0x1p32f));
             vnb += 1;
           }
         }
@@ -392,11 +395,13 @@ __global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ p
         if (c + 1 < Lx && mask[i + 1]) {
           const float b = cos_spec(__fmul_rn(q, __fsub_rn(pi, phi[i + 1])));
           vsb += __float2ll_rn(__fmul_rn(b, 0x1p32f));
+          tsb2 += __float2ll_rn(__fmul_rn(__fmul_rn(b, b), 0x1p32f));
           vnb += 1;
         }
         if (r + 1 < Ly && mask[i + Lx]) {
           const float b = cos_spec(__fmul_rn(q, __fsub_rn(pi, phi[i + Lx])));
           vsb += __float2ll_rn(__fmul_rn(b, 0x1p32f));
+          tsb2 += __float2ll_rn(__fmul_rn(__fmul_rn(b, b), 0x1p32f));
           vnb += 1;
         }
       }
@@ -427,6 +432,9 @@ __global__ void __launch_bounds__(256) k_block_stats(const float* __restrict__ p
     if (sSP[t]) atomicAdd(reinterpret_cast<unsigned long long*>(&SP[b]), static_cast<unsigned long long>(sSP[t]));
     if (sNK[t]) atomicAdd(reinterpret_cast<unsigned long long*>(&NK[b]), static_cast<unsigned long long>(sNK[t]));
   }
+  tsb2 = warp_sum_ll(tsb2);
+  if ((threadIdx.x & 31) == 0 && tsb2)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&sc->sum_SB2), static_cast<unsigned long long>(tsb2));
 }
 
 // Streaming form of a3 for l_b % 4 == 0 and Lx % 4 == 0 (16-byte aligned rows): a thread owns
@@ -448,8 +456,9 @@ __global__ void __launch_bounds__(256) k_block_stats4(const float* __restrict__ 
                                                       long long* __restrict__ SB,
                                                       long long* __restrict__ NB,
                                                       long long* __restrict__ SP,
-                                                      long long* __restrict__ NK) {
+                                                      long long* __restrict__ NK, DevScalars* sc) {
   __shared__ unsigned long long sl[4][kBs4Slots];
+  long long tsb2 = 0;  // this thread's squared sample-bond cosines (fixed point, R22)
   // 32-bit index arithmetic (< 2^30 sites)
   const int Lx = static_cast<int>(Lx64), Ly = static_cast<int>(Ly64), lrow0 = static_cast<int>(lrow064);
   const int row0 = static_cast<int>(row064), row1 = static_cast<int>(row164);
@@ -531,11 +540,15 @@ __global__ void __launch_bounds__(256) k_block_stats4(const float* __restrict__ 
       nk += 1;
       const bool kr = j < 3 ? ((m >> (8 * (j + 1))) & 0xffu) != 0 : mr != 0;
       if (kr) {  // right bond (c + j + 1 < Lx: a column past the edge has mask 0)
-        sb += __float2ll_rn(__fmul_rn(cos_spec(__fmul_rn(q, __fsub_rn(pv[j], pv[j + 1]))), 0x1p32f));
+        const float b = cos_spec(__fmul_rn(q, __fsub_rn(pv[j], pv[j + 1])));
+        sb += __float2ll_rn(__fmul_rn(b, 0x1p32f));
+        tsb2 += __float2ll_rn(__fmul_rn(__fmul_rn(b, b), 0x1p32f));
         nb += 1;
       }
       if ((mn >> (8 * j)) & 0xffu) {  // down bond
-        sb += __float2ll_rn(__fmul_rn(cos_spec(__fmul_rn(q, __fsub_rn(pv[j], pd[j]))), 0x1p32f));
+        const float b = cos_spec(__fmul_rn(q, __fsub_rn(pv[j], pd[j])));
+        sb += __float2ll_rn(__fmul_rn(b, 0x1p32f));
+        tsb2 += __float2ll_rn(__fmul_rn(__fmul_rn(b, b), 0x1p32f));
         nb += 1;
       }
     }
@@ -551,6 +564,9 @@ __global__ void __launch_bounds__(256) k_block_stats4(const float* __restrict__ 
     if (sl[2][t]) atomicAdd(reinterpret_cast<unsigned long long*>(&SP[b]), sl[2][t]);
     if (sl[3][t]) atomicAdd(reinterpret_cast<unsigned long long*>(&NK[b]), sl[3][t]);
   }
+  tsb2 = warp_sum_ll(tsb2);
+  if ((threadIdx.x & 31) == 0 && tsb2)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&sc->sum_SB2), static_cast<unsigned long long>(tsb2));
 }
 
 // ------------------------------------------------- a4: e_b -> T_b (table inversion)
@@ -566,10 +582,10 @@ __global__ void __launch_bounds__(256) k_block_T(const long long* __restrict__ S
   __syncthreads();
   const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   unsigned long long avail = 0;
-  long long sb = 0, sp = 0, nk = 0;
+  long long sb = 0, sp = 0, nk = 0, nbs = 0;
   if (b < nblocks) {
     const long long nbv = NB[b];
-    sb = SB[b]; sp = SP[b]; nk = NK[b];
+    sb = SB[b]; sp = SP[b]; nk = NK[b]; nbs = nbv;
     float T = -1.0f;  // marker: no sample bond in this block
     if (nbv > 0) {
       const double a = -__ll2double_rn(sb) * 0x1p-32;
@@ -590,9 +606,10 @@ __global__ void __launch_bounds__(256) k_block_T(const long long* __restrict__ S
     Tb[b] = T;
   }
   avail = warp_sum_ull(avail);
-  sb = warp_sum_ll(sb); sp = warp_sum_ll(sp); nk = warp_sum_ll(nk);
+  sb = warp_sum_ll(sb); sp = warp_sum_ll(sp); nk = warp_sum_ll(nk); nbs = warp_sum_ll(nbs);
   if ((threadIdx.x & 31) == 0) {
     if (avail) atomicAdd(&sc->n_avail, avail);
+    if (nbs) atomicAdd(reinterpret_cast<unsigned long long*>(&sc->sum_NB), static_cast<unsigned long long>(nbs));
     if (sb) atomicAdd(reinterpret_cast<unsigned long long*>(&sc->sum_SB), static_cast<unsigned long long>(sb));
     if (sp) atomicAdd(reinterpret_cast<unsigned long long*>(&sc->sum_SP), static_cast<unsigned long long>(sp));
     if (nk) atomicAdd(reinterpret_cast<unsigned long long*>(&sc->sum_NK), static_cast<unsigned long long>(nk));
@@ -1121,7 +1138,7 @@ void launch_gap_index(const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t row_b
 
 void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int64_t Ly, int64_t lrow0,
                         int64_t row0, int64_t row1, int lb, float q, long long* SB, long long* NB,
-                        long long* SP, long long* NK, int64_t nblocks, cudaStream_t st) {
+                        long long* SP, long long* NK, int64_t nblocks, DevScalars* sc, cudaStream_t st) {
   cudaMemsetAsync(SB, 0, sizeof(long long) * nblocks, st);
   cudaMemsetAsync(NB, 0, sizeof(long long) * nblocks, st);
   cudaMemsetAsync(SP, 0, sizeof(long long) * nblocks, st);
@@ -1130,12 +1147,12 @@ void launch_block_stats(const float* phiK, const uint8_t* mask, int64_t Lx, int6
     const int64_t tile0 = (row0 / kBs4Rows) * kBs4Rows;
     dim3 grid(static_cast<unsigned>((Lx + kBs4Cols - 1) / kBs4Cols),
               static_cast<unsigned>((row1 - tile0 + kBs4Rows - 1) / kBs4Rows));
-    k_block_stats4<<<grid, 256, 0, st>>>(phiK, mask, Lx, Ly, lrow0, row0, row1, lb, q, SB, NB, SP, NK);
+    k_block_stats4<<<grid, 256, 0, st>>>(phiK, mask, Lx, Ly, lrow0, row0, row1, lb, q, SB, NB, SP, NK, sc);
     return;
   }
   const int64_t tile0 = (row0 / kTile) * kTile;
   dim3 grid(static_cast<unsigned>((Lx + kTile - 1) / kTile), static_cast<unsigned>((row1 - tile0 + kTile - 1) / kTile));
-  k_block_stats<<<grid, 256, 0, st>>>(phiK, mask, Lx, Ly, lrow0, row0, row1, lb, q, SB, NB, SP, NK);
+  k_block_stats<<<grid, 256, 0, st>>>(phiK, mask, Lx, Ly, lrow0, row0, row1, lb, q, SB, NB, SP, NK, sc);
 }
 
 void launch_block_T(const long long* SB, const long long* NB, const long long* SP,

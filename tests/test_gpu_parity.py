@@ -304,6 +304,7 @@ def check_row_slabs(P, z, mask, cfg_kw, calib, M, S, seed, world, energy=True, d
         inf = g["info"]
         assert (inf["rank"], inf["world"], inf["row_begin"], inf["row_end"]) == (rank, world, r0, r1)
         assert inf["n_gaps"] == int(gaps.sum()) and inf["z_min"] == p.zmin and inf["z_max"] == p.zmax
+        assert inf["sample_bonds"] == int(NB.sum())
         local = int(gaps[max(r0 - 1, 0):min(r1 + 1, Ly)].sum())
         assert inf["n_gaps_local"] == local, "slab-local gap sites: own rows + ghost rows"
         for k, ref in enumerate((SB, NB, SP, NK)):
@@ -578,6 +579,35 @@ def test_dc_rejects_sc_only_features(P, calib):
     with pytest.raises(P.MprError):
         m.simulate(2, 3, 1)
     m.close()
+
+
+@pytest.mark.parametrize("n_avg,init", [(1, "block_mean"), (2, "random")])
+def test_adaptive_with_derived_tolerance(P, calib, n_avg, init):
+    """slope_tol = "derived" (reading R22: SE(e_s) / n_fit from the exact sums of the sample
+    bonds' cosines and squared cosines): the library's tolerance equals the oracle's bit for
+    bit, and so do s_eq and the predictions."""
+    Tk, ek = calib
+    truth, z, mask = make_problem(56, 0.45, Lx=49, corr_len=6.0)
+    cfg = P.Config(n_avg=n_avg, init=init)
+    m = P.LeMpr(cfg, calib)
+    m.set_data(z, mask)
+    m.estimate_local_params()
+    s_eq = m.simulate_adaptive(6, 21, n_fit=10, n_f=4, max_sweeps=90, slope_tol="derived")
+    pred, inf = m.predict(), m.info()
+    m.close()
+    oc = ocfg(cfg)
+    p = O.parameters(z, mask, oc, Tk, ek)
+    tol = O.derived_slope_tol(p.phi0, mask, oc.q, 10)
+    assert inf["slope_tol"] == tol and tol > 0
+    SB, NB, SP, NK = O.block_stats(p.phi0, mask, oc.lb, oc.q)
+    assert inf["sample_bonds"] == int(NB.sum())
+    r = O.simulate_adaptive(p, mask, oc, 6, 21, n_fit=10, n_f=4, S_max=90, slope_tol="derived")
+    assert s_eq.tolist() == r["s_eq"].tolist()
+    ref = O.predict(np.nan_to_num(z), mask, r["acc"], 6, n_avg, p.zmin, p.zmax, 0)
+    if n_avg == 1:
+        assert_bitwise(pred, ref, "adaptive (derived tolerance) predictions")
+    else:
+        assert np.max(np.abs(pred - ref)) <= 1e-3 * (p.zmax - p.zmin)
 
 
 def test_adaptive_with_slope_tolerance(P, calib):

@@ -712,3 +712,54 @@ def test_equilibrium_slope_tolerance():
     assert not O.equilibrium_test(y)
     assert not O.equilibrium_test(y, slope_tol=5e-5)
     assert O.equilibrium_test(y, slope_tol=2e-4)
+
+
+# ------------------------------------------------ R22: the derived slope tolerance
+def test_derived_slope_tolerance_hand_values():
+    """A row [0, 0, 2pi] (q = 1/2): bond cosines 1 and cos(-pi) = -1, mean 0, variance 1,
+    N_SP = 2 -> SE = 1/sqrt(2), tau = SE / n_fit; a constant field (variance 0) -> 0 exactly;
+    no sample bond -> 0."""
+    phi = np.array([[0.0, 0.0, float(TWO_PI_F)]], np.float32)
+    mask = np.ones((1, 3), np.uint8)
+    assert abs(O.derived_slope_tol(phi, mask, 0.5, 20) - math.sqrt(0.5) / 20) < 1e-7
+    assert O.derived_slope_tol(np.full((5, 6), 1.3, np.float32), np.ones((5, 6), np.uint8), 0.5, 20) == 0.0
+    iso = np.zeros((4, 4), np.uint8)
+    iso[0, 0] = iso[2, 2] = 1
+    assert O.derived_slope_tol(np.ones((4, 4), np.float32), iso, 0.5, 20) == 0.0
+
+
+def test_derived_slope_tolerance_matches_libm_sample_sd():
+    """The fixed-point definition equals the fp64/libm one, sd(cos q(phi_i - phi_j)) /
+    sqrt(N_SP) / n_fit over every unordered sample pair once, to 1e-6 relative."""
+    rng = np.random.default_rng(11)
+    for p_gap, q, n_fit in ((0.3, 0.5, 20), (0.7, 0.37, 8)):
+        phi = (rng.random((40, 33)) * 2 * np.pi).astype(np.float32)
+        mask = (rng.random(phi.shape) > p_gap).astype(np.uint8)
+        b = []
+        for r in range(40):
+            for c in range(33):
+                if not mask[r, c]:
+                    continue
+                if c + 1 < 33 and mask[r, c + 1]:
+                    b.append(math.cos(q * (float(phi[r, c]) - float(phi[r, c + 1]))))
+                if r + 1 < 40 and mask[r + 1, c]:
+                    b.append(math.cos(q * (float(phi[r, c]) - float(phi[r + 1, c]))))
+        b = np.array(b)
+        ref = b.std() / math.sqrt(b.size) / n_fit
+        got = O.derived_slope_tol(phi, mask, q, n_fit)
+        assert abs(got - ref) <= 1e-6 * ref, (got, ref)
+
+
+def test_adaptive_with_derived_tolerance_uses_it(calib):
+    """slope_tol = "derived" in the oracle's adaptive protocol equals passing the derived
+    value explicitly."""
+    from inputs.synth import make_problem
+    truth, z, mask = make_problem(40, 0.4, corr_len=6.0)
+    cfg = O.OracleConfig(lb=8)
+    p = O.parameters(z, mask, cfg, *calib)
+    tol = O.derived_slope_tol(p.phi0, mask, cfg.q, 10)
+    assert tol > 0
+    a = O.simulate_adaptive(p, mask, cfg, 4, 5, n_fit=10, n_f=3, S_max=80, slope_tol="derived")
+    b = O.simulate_adaptive(p, mask, cfg, 4, 5, n_fit=10, n_f=3, S_max=80, slope_tol=tol)
+    assert a["s_eq"].tolist() == b["s_eq"].tolist()
+    assert np.array_equal(a["acc"], b["acc"])
