@@ -33,11 +33,14 @@ def main():
     ap.add_argument("--fields", default="hetero,walls")
     ap.add_argument("--M", type=int, default=10)
     ap.add_argument("--S", type=int, default=60)
+    ap.add_argument("--corr-len", type=float, default=2.0,
+                    help="Matern correlation length in sites (2: rough, sample T of the order of the paper's 0.07)")
     a = ap.parse_args()
     calib = P.load_calibration()
     for field in a.fields.split(","):
         for L in map(int, a.sizes.split(",")):
-            truth = heterogeneous_field(L, corr_len=max(2.0, L / 256)) if field == "hetero" else domain_wall_field(L)
+            truth = (heterogeneous_field(L, corr_len=a.corr_len) if field == "hetero"
+                     else domain_wall_field(L, corr_len=a.corr_len))
             for p in map(float, a.ps.split(",")):
                 mask = random_mask(L, L, p)
                 z = np.where(mask != 0, truth, np.float32(np.nan)).astype(np.float32)
@@ -64,7 +67,8 @@ def main():
                     dt = time.perf_counter() - t0
                     inf = m.info()
                     m.close()
-                    print(json.dumps(dict(field=field, L=L, p=p, method=name, M=a.M, S=a.S, e_s=e_s, e_eq=e_eq,
+                    print(json.dumps(dict(field=field, corr_len=a.corr_len, L=L, p=p, method=name, M=a.M, S=a.S,
+                                          e_s=e_s, e_eq=e_eq, median_T=inf["median_T"],
                                           e_first=float(curve[0]), e_eq_minus_e_s=e_eq - e_s,
                                           slope_tol_derived=inf["slope_tol"], s_eq=[int(x) for x in s_eq],
                                           s_eq_median=float(np.median(np.abs(s_eq))),
