@@ -70,6 +70,10 @@ def parse():
                          "ordered chain (bit-identical to one GPU)")
     ap.add_argument("--decomp", default=None, choices=["realizations", "rows"],
                     help="multi-GPU split of the headline line (default: rows for C4, realizations otherwise)")
+    ap.add_argument("--emulate", type=int, default=0,
+                    help="W > 1: run the multi-rank path with W contexts on this ONE GPU (libmpr's in-process "
+                         "transport, one host thread each) and check it against one context; a functional "
+                         "line, not a scaling measurement")
     return ap.parse_args()
 
 
@@ -479,10 +483,67 @@ def run_mpr(args):
     return 0
 
 
+def run_emulated(args):
+    """W ranks as W contexts in this process on one GPU (in-process transport): the same SPMD
+    calls as the NCCL path, timed per rank by wall clock around each whole fill (all ranks
+    share the GPU, so this is not a scaling number); the all-gathered predictions are
+    compared bit for bit with one context's."""
+    import torch
+
+    import paper_2212_01317_b200 as Pk
+    from paper_2212_01317_b200.sharding import run_group
+    W = args.emulate
+    name = args.config
+    decomp = args.decomp or ("rows" if name == "C4" else "realizations")
+    c, truth, z, mask = load_problem(name)
+    M = args.M or c["M"]
+    S = args.sweeps or c["sweeps"]
+    P_sites = int((mask == 0).sum())
+    calib = Pk.load_calibration()
+    ref = Pk.fill(z, mask, M, S, SEED_SIM, Pk.Config(), calib)
+
+    def fn(rank, g):
+        m = Pk.LeMpr(Pk.Config(group=g, group_rank=rank, shard=decomp), calib)
+        times = []
+        for k in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            m.set_data(z, mask)
+            m.estimate_local_params()
+            m.simulate(M, S, SEED_SIM)
+            m.predict_rows()
+            torch.cuda.synchronize()
+            if k >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        full = m.predict()
+        inf = m.info()
+        m.close()
+        return times, inf, full
+
+    res = run_group(W, fn)
+    per_step = max(sum(t) for t, _, _ in res) / args.steps
+    same = all(np.array_equal(f.view(np.uint32), ref.view(np.uint32)) for _, _, f in res)
+    line = {"metric": METRIC, "value": P_sites * S * M / per_step, "unit": UNIT, "n_gpus": 1, "emulated": True,
+            "n_contexts": W, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * per_step,
+            "higher_is_better": True, "scaling": "strong" if decomp == "rows" else "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": describe(name, c, M, S, False), "parallelism": f"{decomp} x{W} on one GPU "
+                       "(in-process transport)"},
+            "bit_identical_to_one_context": bool(same),
+            "per_rank": [{"rank": inf["rank"], "rows": [inf["row_begin"], inf["row_end"]],
+                          "realizations": [inf["m_begin"], inf["m_end"]], "gap_sites_local": inf["n_gaps_local"],
+                          "collectives": inf["comm_calls"]} for _, inf, _ in res],
+            "note": "W contexts share ONE GPU: wall time of the SPMD fill, not a multi-GPU scaling measurement"}
+    print(json.dumps(line), flush=True)
+    return 0 if same else 1
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.emulate > 1:
+        return run_emulated(args)
     return run_mpr(args)
 
 

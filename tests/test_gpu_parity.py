@@ -464,6 +464,93 @@ def _full_size_sampled(P, calib, L, p, gaps, nu, M, S, windows):
 
 
 @pytest.mark.slow
+def test_fixed_point_bound_32768_mpr_energy_trace(P, calib):
+    """The API's largest grid, Lx*Ly = 2^30 (32768^2), in uniform-MPR mode (one block: its
+    SB sums all 2^31 - 2^16 sample bonds) with the energy trace on: a field so smooth that
+    every bond cosine rounds to 1.0f puts SB and the grid energy's fixed-point sum at
+    (2^31 - 2^16) * 2^32 = 2^63 - 2^48, the int64 limit ARITH §E/§J guarantees. SB, e_s and
+    the traced energies must be exact / finite (an overflow would wrap them negative)."""
+    L = 32768
+    r = np.arange(L, dtype=np.float32)
+    z = (r[:, None] + r[None, :]) * np.float32(1e-6)
+    mask = np.ones((L, L), np.uint8)
+    gaps = [(0, 0), (1, 5), (L // 2, L // 2), (L - 1, L - 1), (L - 1, 17), (12345, 23456)]
+    for (a, b) in gaps:
+        mask[a, b] = 0
+        z[a, b] = np.nan
+    cfg = P.Config(l_b=L, n_s=0)
+    m = P.LeMpr(cfg, calib)
+    m.set_data(z, mask)
+    m.set_energy_trace(True)
+    m.estimate_local_params()
+    stats = m.debug(P.binding.MPR_BUF_BLOCK_STATS)
+    del z
+    n_bonds_all = 2 * L * L - 2 * L
+    # bonds touching a gap are not sample bonds
+    missing = sum((a > 0) + (a < L - 1) + (b > 0) + (b < L - 1) for (a, b) in gaps)
+    nsp = n_bonds_all - missing
+    assert int(stats[1][0]) == nsp
+    assert int(stats[0][0]) == nsp * (1 << 32), "SB must be exactly N_SP * 2^32 (no wrap-around)"
+    m.simulate(2, 3, 5)
+    E = m.debug(P.binding.MPR_BUF_ENERGY)
+    inf = m.info()
+    m.close()
+    assert np.all(np.isfinite(E)) and np.all(E <= -0.999999) and np.all(E >= -1.0), E
+    assert inf["n_gaps"] == len(gaps)
+
+
+@pytest.mark.slow
+def test_c4_row_slabs_windows_vs_oracle(P, calib):
+    """C4 (16384^2, 50% random gaps, M = 10, S = 30) split into 4 row slabs (contexts on this
+    GPU, in-process transport): windows straddling every slab boundary and the grid edges
+    are bit-exact against the oracle (oracle.WindowOracle), on every rank that owns rows of
+    them; each rank holds ~1/4 of the gap sites."""
+    from paper_2212_01317_b200.sharding import row_range, run_group
+    L, M, S, seed, W = 16384, 10, 30, 20221202, 4
+    Tk, ek = calib
+    truth, z, mask = make_problem(L, 0.5)
+    bounds = [row_range(L, W, w)[0] for w in range(1, W)]
+    wins = [(b - 6, b + 6, 8000, 8012) for b in bounds] + [(0, 8, 16376, 16384), (16376, 16384, 0, 8)]
+
+    def fn(rank, g):
+        m = P.LeMpr(P.Config(group=g, group_rank=rank, shard="rows"), calib)
+        m.set_data(z, mask)
+        T = m.estimate_local_params(want_T=True)
+        m.simulate(M, S, seed)
+        pred = m.predict_rows()
+        inf = m.info()
+        lo = inf["last_m_base"]
+        st = {rr: m.debug(P.binding.MPR_BUF_STATE, rr) for rr in (lo, min(lo + inf["last_batch"], M) - 1)}
+        r0, r1 = inf["row_begin"], inf["row_end"]
+        out = []
+        for (a, b, c0, c1) in wins:
+            ra, rb = max(a, r0), min(b, r1)
+            if ra < rb:
+                out.append(((a, b, c0, c1), ra, rb, T[ra:rb, c0:c1].copy(), pred[ra - r0:rb - r0, c0:c1].copy(),
+                            {k: v[ra:rb, c0:c1].copy() for k, v in st.items()}))
+        m.close()
+        return inf, out
+
+    res = run_group(W, fn)
+    Wo = O.WindowOracle(z, mask, ocfg(P.Config()), Tk, ek)
+    P_total = int((mask == 0).sum())
+    for rank, (inf, out) in enumerate(res):
+        assert inf["n_gaps_local"] < P_total / W * 1.01 + 2 * L
+        for (a, b, c0, c1), ra, rb, T, pred, st in out:
+            assert_bitwise(T, Wo.T_window(ra, rb, c0, c1), f"rank {rank} T window {(ra, c0)}")
+            ref = Wo.states(ra, rb, c0, c1, range(M), S, seed)
+            for rr, v in st.items():
+                assert_bitwise(v, ref[rr], f"rank {rank} state {rr} window {(ra, c0)}")
+            acc = np.zeros(ref.shape[1:])
+            for k in range(M):  # realization order, as the oracle accumulates
+                acc += ref[k].astype(np.float64)
+            zw = np.ascontiguousarray(np.nan_to_num(z[ra:rb, c0:c1]))
+            mw = np.ascontiguousarray(mask[ra:rb, c0:c1])
+            pw = O.predict(zw, mw, np.where(mw == 0, acc, 0.0), M, 1, Wo.zmin, Wo.zmax, 0)
+            assert_bitwise(pred, pw, f"rank {rank} predictions window {(ra, c0)}")
+
+
+@pytest.mark.slow
 def test_c3_full_size_sampled(P, calib):
     """BASELINE config 3 at full size: 4096^2, 70% cloud gaps, M = 8 (one GPU's shard of 64)."""
     L = 4096
