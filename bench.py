@@ -409,6 +409,12 @@ def run_mpr(args):
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
     comm = make_nccl_comm(local) if ws > 1 else None
+    if ws > 1:  # one rank generates (and caches) the large inputs, the others then read them
+        if rank == 0:
+            load_problem(args.config)
+            if not args.no_c4:
+                load_problem("C4")
+        dist.barrier()
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))

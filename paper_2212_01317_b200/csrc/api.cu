@@ -107,6 +107,10 @@ struct mpr_ctx {
   int rank = 0, world = 1;
   bool rows = false;       // MPR_SHARD_ROWS with world > 1: slab-local layout + halos
   bool shards = false;     // MPR_SHARD_REALIZATIONS with world > 1: id ranges + reduction
+  // row slabs: the halo exchange on its own stream, overlapped with the interior rows
+  int halo_overlap = 1;    // MPR_HALO_OVERLAP=0: exchange in line after each half-sweep
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
   int64_t comm_calls = 0;
   // problem (global)
   int64_t Lx = 0, Ly = 0;
@@ -344,7 +348,7 @@ mpr_status exchange_rows(mpr_ctx* c, T* base, CommType t) {
 // After a colour-`col` half-sweep: the colour's states of the first and last own rows go
 // to the neighbours' ghost rows (gap-site major, realization minor: each row's colour-c
 // states are one contiguous run of R floats per gap). SURVEY §8(e) 2.
-mpr_status exchange_halo(mpr_ctx* c, int col, int R) {
+mpr_status exchange_halo(mpr_ctx* c, int col, int R, cudaStream_t stream) {
   std::vector<P2P> sends, recvs;
   float* G = c->G.as<float>();
   auto seg = [&](const int64_t (&r)[2]) { return static_cast<size_t>((r[1] - r[0]) * R); };
@@ -356,7 +360,7 @@ mpr_status exchange_halo(mpr_ctx* c, int col, int R) {
     sends.push_back({c->rank + 1, G + c->bnd[1][col][0] * R, seg(c->bnd[1][col])});
     recvs.push_back({c->rank + 1, G + c->ghost[1][col][0] * R, seg(c->ghost[1][col])});
   }
-  CKC(c->comm->exchange(sends, recvs, CT_F32, c->stream), "halo exchange");
+  CKC(c->comm->exchange(sends, recvs, CT_F32, stream), "halo exchange");
   return MPR_OK;
 }
 
@@ -612,6 +616,17 @@ mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
   const bool multi = c->comm && (c->world > 1 || (fc && std::atoi(fc)));
   c->rows = multi && cfg->shard == MPR_SHARD_ROWS;
   c->shards = multi && cfg->shard == MPR_SHARD_REALIZATIONS;
+  if (const char* v = std::getenv("MPR_HALO_OVERLAP")) c->halo_overlap = std::atoi(v) ? 1 : 0;
+  if (c->rows) {
+    e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_bnd, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      std::fprintf(stderr, "mpr_init: %s\n", cudaGetErrorString(e));
+      mpr_destroy(c);
+      return MPR_ERR_CUDA;
+    }
+  }
   if (const char* v = std::getenv("MPR_SWEEP_VARIANT")) c->sweep_variant = std::atoi(v);
   if (const char* v = std::getenv("MPR_NO_GRAPHS")) c->use_graphs = std::atoi(v) ? 0 : 1;
   if (const char* v = std::getenv("MPR_SLAB_GRAPHS")) c->slab_graphs = std::atoi(v) ? 1 : 0;
@@ -637,6 +652,12 @@ void mpr_destroy(mpr_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (cudaEvent_t ev : c->ev_pool) cudaEventDestroy(ev);
   if (c->ev_check) cudaEventDestroy(c->ev_check);
+  if (c->ev_bnd) cudaEventDestroy(c->ev_bnd);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->comm_stream) {
+    cudaStreamSynchronize(c->comm_stream);
+    cudaStreamDestroy(c->comm_stream);
+  }
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -880,7 +901,11 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
         a.g_begin = k.own[colour][0];
         a.g_count = k.own[colour][1] - k.own[colour][0];
       }
-      if (a.g_count > 0) {
+      // one launch over [g0, g1) of this colour (row slabs time each launch: kernel time only)
+      auto sweep_range = [&](int64_t g0, int64_t g1) -> mpr_status {
+        if (g1 <= g0) return MPR_OK;
+        a.g_begin = g0;
+        a.g_count = g1 - g0;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (per_launch_timing) {
           mpr_status se = slab_timing_event(c, evk++, &e0);
@@ -893,10 +918,32 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
         if (per_launch_timing) CK(cudaEventRecordWithFlags(e1, st, ev_flags), "event record");
         ++c->launches;
         ++*nsweep;
-      }
-      if (c->rows) {
-        mpr_status sh = exchange_halo(c, colour, k.Rb);
+        return MPR_OK;
+      };
+      mpr_status sr = MPR_OK;
+      if (c->rows && c->halo_overlap && c->row1 - c->row0 >= 3) {
+        // Row slabs, overlapped: the two boundary rows first; their halo exchange runs on the
+        // comm stream while the interior rows update; the next half-sweep (which reads this
+        // colour's ghost rows) waits for it. The interior does not touch the ghost rows of
+        // this colour, and the exchange does not touch the other colour's states.
+        sr = sweep_range(c->bnd[0][colour][0], c->bnd[0][colour][1]);
+        if (sr == MPR_OK) sr = sweep_range(c->bnd[1][colour][0], c->bnd[1][colour][1]);
+        if (sr != MPR_OK) return sr;
+        CK(cudaEventRecord(c->ev_bnd, st), "event record");
+        sr = sweep_range(c->bnd[0][colour][1], c->bnd[1][colour][0]);
+        if (sr != MPR_OK) return sr;
+        CK(cudaStreamWaitEvent(c->comm_stream, c->ev_bnd, 0), "comm stream wait");
+        mpr_status sh = exchange_halo(c, colour, k.Rb, c->comm_stream);
         if (sh != MPR_OK) return sh;
+        CK(cudaEventRecord(c->ev_halo, c->comm_stream), "event record");
+        CK(cudaStreamWaitEvent(st, c->ev_halo, 0), "stream wait halo");
+      } else {
+        sr = sweep_range(a.g_begin, a.g_begin + a.g_count);
+        if (sr != MPR_OK) return sr;
+        if (c->rows) {
+          mpr_status sh = exchange_halo(c, colour, k.Rb, st);
+          if (sh != MPR_OK) return sh;
+        }
       }
     }
   }

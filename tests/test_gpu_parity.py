@@ -324,11 +324,14 @@ def check_row_slabs(P, z, mask, cfg_kw, calib, M, S, seed, world, energy=True, d
     return res
 
 
+@pytest.mark.parametrize("overlap", ["1", "0"])
 @pytest.mark.parametrize("world", [2, 3, 5, 8])
-def test_row_slabs_distributed_bit_exact(P, calib, world):
+def test_row_slabs_distributed_bit_exact(P, calib, monkeypatch, world, overlap):
     """Row slabs inside libmpr (MPR_SHARD_ROWS) on `world` contexts: the
-    distributed parameter stage, the halo exchange after every colour half-sweep and the
+    distributed parameter stage, the halo exchange after every colour half-sweep (overlapped
+    with the interior rows on the comm stream, or in line: MPR_HALO_OVERLAP) and the
     all-gathered predictions reproduce the oracle bit for bit on every rank."""
+    monkeypatch.setenv("MPR_HALO_OVERLAP", overlap)
     truth, z, mask = make_problem(61, 0.5, Lx=52, corr_len=6.0)
     check_row_slabs(P, z, mask, dict(l_b=8, n_s=2, r_s=1), calib, 6, 10, 123, world)
 
