@@ -65,6 +65,8 @@ struct BatchKey {
   void* dclist;
   int64_t dc_off[5];
   int dc_rc;  // DC with shared-memory tiles: realizations per tile CTA (0: the phase lists)
+  // the other buffers the captured launches read (a realloc can hand back an old address)
+  void *ginit, *gid, *phiK, *T;
   // own gap-id ranges per colour (row slabs: a sub-range of the local ids)
   int64_t own[2][2];
 };
@@ -310,13 +312,6 @@ double derived_slope_tol(long long S1, long long S2, long long N, int n_fit) {
   return std::sqrt(var / n) / static_cast<double>(n_fit);
 }
 
-// Forget every captured batch graph: their launches bake in buffer pointers and gap-id
-// segments of the problem they were captured for.
-void drop_graphs(mpr_ctx* c) {
-  for (auto& e : c->graphs) {
-    if (e.exec) cudaGraphExecDestroy(e.exec);
-    e.exec = nullptr;
-  }
   c->graph_next = 0;
 }
 
@@ -388,7 +383,6 @@ void slab_ranges(mpr_ctx* c) {
 
 mpr_status stage_data(mpr_ctx* c) {
   cudaStream_t st = c->stream;
-  drop_graphs(c);
   if (c->rows) {  // ghost rows of z and mask from the neighbours (cross-slab bonds, sweep)
     mpr_status s = exchange_rows(c, c->z.as<float>(), CT_F32);
     if (s != MPR_OK) return s;
@@ -704,7 +698,6 @@ mpr_status mpr_estimate_local_params(mpr_ctx* c, float* T_out) {
   SET_DEVICE(c);
   cudaStream_t st = c->stream;
   const int lb = c->cfg.l_b;
-  drop_graphs(c);
   c->nbx = (c->Lx + lb - 1) / lb;
   c->nby = (c->Ly + lb - 1) / lb;
   c->nblocks = c->nbx * c->nby;
@@ -1030,6 +1023,7 @@ mpr_status mpr_simulate_range(mpr_ctx* c, int64_t M, int32_t sweeps, uint64_t se
     key.order = c->cfg.order;
     key.defer = c->defer_reduce;
     key.G = c->G.p; key.A = c->A.p; key.rec = c->rec.p; key.acc = c->acc.p;
+    key.ginit = c->ginit.p; key.gid = c->gid.p; key.phiK = c->phiK.p; key.T = c->T.p;
     key.energy = c->energy_enabled ? c->energy.as<long long>() + mb * sweeps : nullptr;
     if (c->cfg.order == MPR_ORDER_DC) {
       key.dclist = c->dclist.p;

@@ -658,6 +658,30 @@ def test_dc_tiles_and_lists_bit_exact(P, calib, monkeypatch, tiled, lb, M, kw):
     compare(P, z, mask, truth, cfg, calib, M, 7, 41, exact_pred=cfg.n_avg == 1)
 
 
+def test_context_reuse_across_masks_with_equal_counts(P, calib):
+    """One context, two problems with the SAME numbers of gap sites of each colour but other
+    gap positions (so other DC phase segments, records and neighbour ids), in SC and DC order:
+    the cached CUDA graph of the first problem must not be replayed for the second (its key
+    holds every pointer, size and segment the launches bake in). Both fills equal fresh
+    single-use contexts bit for bit."""
+    truth, z, mask = make_problem(48, 0.5, Lx=40, corr_len=6.0)
+    # the same multiset of colour-A / colour-B gaps, shifted by two columns (colour kept)
+    mask2 = np.roll(mask, 2, axis=1)
+    z2 = np.roll(z, 2, axis=1)
+    assert ((mask == 0) & ((np.indices(mask.shape).sum(0) & 1) == 0)).sum() == \
+           ((mask2 == 0) & ((np.indices(mask.shape).sum(0) & 1) == 0)).sum()
+    for order in ("sc", "dc"):
+        cfg = P.Config(order=order, l_b=8, n_s=1, r_s=1)
+        refs = [P.fill(zz, mm, 6, 5, 9, cfg, calib) for zz, mm in ((z, mask), (z2, mask2))]
+        m = P.LeMpr(cfg, calib)
+        for zz, mm, ref in ((z, mask, refs[0]), (z2, mask2, refs[1]), (z, mask, refs[0])):
+            m.set_data(zz, mm)
+            m.estimate_local_params()
+            m.simulate(6, 5, 9)
+            assert_bitwise(m.predict(), ref, f"reused context ({order})")
+        m.close()
+
+
 def test_dc_rejects_sc_only_features(P, calib):
     truth, z, mask = make_problem(32, 0.5, corr_len=5.0)
     m = P.LeMpr(P.Config(order="dc", l_b=8), calib)
