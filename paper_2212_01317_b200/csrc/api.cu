@@ -312,9 +312,6 @@ double derived_slope_tol(long long S1, long long S2, long long N, int n_fit) {
   return std::sqrt(var / n) / static_cast<double>(n_fit);
 }
 
-  c->graph_next = 0;
-}
-
 // ---- row slabs: neighbour exchange of whole local rows (z / mask halos) -------------
 // Row `r` (global) of a row-major local array with local row 0 = lrow0.
 template <class T>
