@@ -201,9 +201,10 @@ mpr_status mpr_simulate(mpr_ctx *ctx, int64_t M, int32_t sweeps, uint64_t seed);
  * runs on the device after each check sweep (fp64, ARITH §K operation order); the host
  * trails one check behind, so sweeps issued after the last realization finished are
  * no-ops. Realization shards: each rank runs its id range; the accumulators and s_eq are
- * summed over the ranks (every rank gets all M decisions). Errors: M < 1, n_fit < 3,
- * n_f < 1, max_sweeps <= n_avg, non-finite slope_tol, MPR_SHARD_ROWS with W > 1 ->
- * INVALID_ARG. */
+ * summed over the ranks (every rank gets all M decisions). Row slabs: every rank sweeps
+ * its rows for all M; the per-rank partial energies are summed over the ranks before each
+ * device-side check, so every rank takes the same decisions. Errors: M < 1, n_fit < 3,
+ * n_f < 1, max_sweeps <= n_avg, non-finite slope_tol -> INVALID_ARG. */
 mpr_status mpr_simulate_adaptive(mpr_ctx *ctx, int64_t M, uint64_t seed, int32_t n_fit, int32_t n_f,
                                  int32_t max_sweeps, double slope_tol, int32_t *s_eq_out);
 

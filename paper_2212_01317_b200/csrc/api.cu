@@ -828,6 +828,57 @@ static mpr_status slab_timing_event(mpr_ctx* c, size_t k, cudaEvent_t* ev) {
   return MPR_OK;
 }
 
+// One SC colour half-sweep over this rank's gap sites of `colour` (a carries the batch, the
+// sweep and the accumulation flags): one launch over the colour's own id range, or — row
+// slabs — the update of the own rows followed by the halo exchange of this colour. With
+// halo_overlap (and >= 3 own rows) the two boundary rows go first, their exchange runs on
+// the comm stream while the interior rows update, and the context stream waits for it
+// before the next half-sweep (which reads this colour's ghost rows). The interior does not
+// touch this colour's ghost rows and the exchange does not touch the other colour, so the
+// overlap changes no bit. timing: CUDA events around every launch (kernel time only).
+static mpr_status sc_half_sweep(mpr_ctx* c, SweepArgs& a, int colour, int variant, bool timing, unsigned ev_flags,
+                                size_t* evk, int64_t* nsweep) {
+  cudaStream_t st = c->stream;
+  a.is_b = colour;
+  auto sweep_range = [&](int64_t g0, int64_t g1) -> mpr_status {
+    if (g1 <= g0) return MPR_OK;
+    a.g_begin = g0;
+    a.g_count = g1 - g0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing) {
+      mpr_status se = slab_timing_event(c, (*evk)++, &e0);
+      if (se == MPR_OK) se = slab_timing_event(c, (*evk)++, &e1);
+      if (se != MPR_OK) return se;
+      CK(cudaEventRecordWithFlags(e0, st, ev_flags), "event record");
+    }
+    launch_sweep_half(a, c->sweep_grid, variant, st);
+    CKL("sweep_half");
+    if (timing) CK(cudaEventRecordWithFlags(e1, st, ev_flags), "event record");
+    ++c->launches;
+    if (nsweep) ++*nsweep;
+    return MPR_OK;
+  };
+  mpr_status sr = MPR_OK;
+  if (c->rows && c->halo_overlap && c->row1 - c->row0 >= 3) {
+    sr = sweep_range(c->bnd[0][colour][0], c->bnd[0][colour][1]);
+    if (sr == MPR_OK) sr = sweep_range(c->bnd[1][colour][0], c->bnd[1][colour][1]);
+    if (sr != MPR_OK) return sr;
+    CK(cudaEventRecord(c->ev_bnd, st), "event record");
+    sr = sweep_range(c->bnd[0][colour][1], c->bnd[1][colour][0]);
+    if (sr != MPR_OK) return sr;
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_bnd, 0), "comm stream wait");
+    sr = exchange_halo(c, colour, a.R, c->comm_stream);
+    if (sr != MPR_OK) return sr;
+    CK(cudaEventRecord(c->ev_halo, c->comm_stream), "event record");
+    CK(cudaStreamWaitEvent(st, c->ev_halo, 0), "stream wait halo");
+    return MPR_OK;
+  }
+  sr = sweep_range(c->own[colour][0], c->own[colour][1]);
+  if (sr != MPR_OK) return sr;
+  if (c->rows) return exchange_halo(c, colour, a.R, st);
+  return MPR_OK;
+}
+
 // One realization batch: init, 2*S half-sweeps (bracketed by the timing events; row slabs:
 // each followed by the halo exchange of its colour), and the realization sum into the
 // accumulator. Issued directly or captured into a CUDA graph.
@@ -886,55 +937,17 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
         a.glist = c->dclist.as<uint32_t>() + c->dc_off[ph];
         a.g_begin = 0;
         a.g_count = c->dc_off[ph + 1] - c->dc_off[ph];
-      } else {
-        a.glist = nullptr;
-        a.g_begin = k.own[colour][0];
-        a.g_count = k.own[colour][1] - k.own[colour][0];
-      }
-      // one launch over [g0, g1) of this colour (row slabs time each launch: kernel time only)
-      auto sweep_range = [&](int64_t g0, int64_t g1) -> mpr_status {
-        if (g1 <= g0) return MPR_OK;
-        a.g_begin = g0;
-        a.g_count = g1 - g0;
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (per_launch_timing) {
-          mpr_status se = slab_timing_event(c, evk++, &e0);
-          if (se == MPR_OK) se = slab_timing_event(c, evk++, &e1);
-          if (se != MPR_OK) return se;
-          CK(cudaEventRecordWithFlags(e0, st, ev_flags), "event record");
+        if (a.g_count > 0) {
+          launch_sweep_half(a, c->sweep_grid, k.variant, st);
+          CKL("sweep_half");
+          ++c->launches;
+          ++*nsweep;
         }
-        launch_sweep_half(a, c->sweep_grid, k.variant, st);
-        CKL("sweep_half");
-        if (per_launch_timing) CK(cudaEventRecordWithFlags(e1, st, ev_flags), "event record");
-        ++c->launches;
-        ++*nsweep;
-        return MPR_OK;
-      };
-      mpr_status sr = MPR_OK;
-      if (c->rows && c->halo_overlap && c->row1 - c->row0 >= 3) {
-        // Row slabs, overlapped: the two boundary rows first; their halo exchange runs on the
-        // comm stream while the interior rows update; the next half-sweep (which reads this
-        // colour's ghost rows) waits for it. The interior does not touch the ghost rows of
-        // this colour, and the exchange does not touch the other colour's states.
-        sr = sweep_range(c->bnd[0][colour][0], c->bnd[0][colour][1]);
-        if (sr == MPR_OK) sr = sweep_range(c->bnd[1][colour][0], c->bnd[1][colour][1]);
-        if (sr != MPR_OK) return sr;
-        CK(cudaEventRecord(c->ev_bnd, st), "event record");
-        sr = sweep_range(c->bnd[0][colour][1], c->bnd[1][colour][0]);
-        if (sr != MPR_OK) return sr;
-        CK(cudaStreamWaitEvent(c->comm_stream, c->ev_bnd, 0), "comm stream wait");
-        mpr_status sh = exchange_halo(c, colour, k.Rb, c->comm_stream);
-        if (sh != MPR_OK) return sh;
-        CK(cudaEventRecord(c->ev_halo, c->comm_stream), "event record");
-        CK(cudaStreamWaitEvent(st, c->ev_halo, 0), "stream wait halo");
-      } else {
-        sr = sweep_range(a.g_begin, a.g_begin + a.g_count);
-        if (sr != MPR_OK) return sr;
-        if (c->rows) {
-          mpr_status sh = exchange_halo(c, colour, k.Rb, st);
-          if (sh != MPR_OK) return sh;
-        }
+        continue;
       }
+      a.glist = nullptr;
+      mpr_status sr = sc_half_sweep(c, a, colour, k.variant, per_launch_timing, ev_flags, &evk, nsweep);
+      if (sr != MPR_OK) return sr;
     }
   }
   if (k.timing && !c->rows) CK(cudaEventRecordWithFlags(c->ev1, st, ev_flags), "event record");
@@ -1188,7 +1201,6 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
   c->last_slope_tol = slope_tol;
   if (c->cfg.order != MPR_ORDER_SC)
     return fail(c, MPR_ERR_INVALID_ARG, "the adaptive protocol needs the SC order (fused energy)");
-  if (c->rows) return fail(c, MPR_ERR_INVALID_ARG, "the adaptive protocol runs with realization shards, not row slabs");
   mpr_status st0 = mpr_reset_accumulator(c);
   if (st0 != MPR_OK) return st0;
   SET_DEVICE(c);
@@ -1212,7 +1224,11 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
   const int64_t R = choose_batch(c, std::max<int64_t>(m1 - m0, 2));
   CK(c->G.ensure(sizeof(float) * c->P * R), "alloc state");
   CK(c->A.ensure(sizeof(float) * c->P * R), "alloc accumulator state");
-  CK(c->energy.ensure(sizeof(long long) * R * max_sweeps), "alloc energy");
+  // row slabs: every rank's kernels sum the bonds of its own sites (a partial energy); the
+  // check reads the sum over the ranks, re-formed from the partials before each check
+  CK(c->energy.ensure(sizeof(long long) * R * max_sweeps * (c->rows ? 2 : 1)), "alloc energy");
+  long long* e_part = c->energy.as<long long>();
+  long long* e_glob = c->rows ? e_part + R * max_sweeps : e_part;
   CK(c->win.ensure(sizeof(int) * 2 * R), "alloc windows");
   // Decisions are taken on the device (k_adaptive_check, ARITH §K bit for bit), so the host
   // never stalls the GPU for a check: it reads the device status (undecided count, last
@@ -1247,7 +1263,7 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
     CK(cudaMemcpyAsync(status_d, const_cast<int*>(status_h), sizeof(int) * 2, cudaMemcpyHostToDevice, st),
        "H2D status");
     CK(cudaMemsetAsync(eq_d, 0, sizeof(int) * Rb, st), "zero decisions");
-    CK(cudaMemsetAsync(c->energy.p, 0, sizeof(long long) * Rb * max_sweeps, st), "zero energy");
+    CK(cudaMemsetAsync(e_part, 0, sizeof(long long) * Rb * max_sweeps, st), "zero energy");
     CK(cudaStreamSynchronize(st), "adaptive batch start");  // the pinned windows are reused below
     launch_init_states(c->rec.as<GapRec>(), c->ginit.as<float>(), c->G.as<float>(), c->A.as<float>(), c->P, Rb, Rb / 2,
                        static_cast<uint32_t>(mb / 2), c->cfg.init == MPR_INIT_RANDOM, k0, k1, st);
@@ -1271,7 +1287,7 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
     a.r_valid_lo = 0;
     a.r_valid_hi = r_hi;
     AdaptiveCheckArgs ca{};
-    ca.energy = c->energy.as<long long>();
+    ca.energy = e_glob;
     ca.energy_stride = max_sweeps;
     ca.sum_known_fx = c->sum_SB_fx;
     ca.n_bonds = static_cast<double>(2 * c->Lx * c->Ly - c->Lx - c->Ly);
@@ -1287,16 +1303,11 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
     int stop_all = INT32_MAX;     // known once the device reports no undecided realization
     for (int32_t s = 1; s <= max_sweeps && s <= stop_all; ++s) {
       a.sweep = static_cast<uint32_t>(s);
-      a.energy = c->energy.as<long long>() + (s - 1);
+      a.energy = e_part + (s - 1);
       for (int colour = 0; colour < 2; ++colour) {
-        a.is_b = colour;
-        a.g_begin = colour ? c->PA : 0;
-        a.g_count = colour ? c->P - c->PA : c->PA;
-        if (a.g_count > 0) {
-          launch_sweep_half(a, c->sweep_grid, c->sweep_variant, st);
-          CKL("sweep_half");
-          ++c->launches;
-        }
+        size_t evk = 0;
+        mpr_status sr = sc_half_sweep(c, a, colour, c->sweep_variant, false, 0u, &evk, nullptr);
+        if (sr != MPR_OK) return sr;
       }
       const bool check = s >= n_fit + n_f && (s - n_fit) % n_f == 0 && s + n_avg <= max_sweeps;
       const bool forced = s == max_sweeps - n_avg;
@@ -1310,6 +1321,11 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
           if (status_h[0] == 0) stop_all = status_h[1];
         }
         if (stop_all != INT32_MAX) continue;
+        if (c->rows) {  // the whole-grid energies of every realization so far (exact int64 sums)
+          CK(cudaMemcpyAsync(e_glob, e_part, sizeof(long long) * Rb * max_sweeps, cudaMemcpyDeviceToDevice, st),
+             "copy energies");
+          CKC(c->comm->allreduce(e_glob, static_cast<size_t>(Rb) * max_sweeps, CT_I64, OP_SUM, st), "allreduce energies");
+        }
         ca.s = s;
         ca.check = check;
         ca.forced = forced;
@@ -1325,9 +1341,14 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
       }
     }
     CK(cudaMemcpyAsync(eq_h, eq_d, sizeof(int) * Rb, cudaMemcpyDeviceToHost, st), "D2H decisions");
-    launch_acc_reduce(c->A.as<float>(), 0, c->P, Rb, 0, r_hi, c->acc.as<double>(), st);
-    CKL("acc_reduce");
-    ++c->launches;
+    for (int col = 0; col < 2; ++col) {  // the own gap ids (one range unless row slabs)
+      const int64_t g0 = col == 0 ? c->own[0][0] : c->own[1][0];
+      const int64_t g1 = (col == 0 && c->own[0][1] == c->own[1][0]) ? c->own[1][1] : c->own[col][1];
+      launch_acc_reduce(c->A.as<float>(), g0, g1 - g0, Rb, 0, r_hi, c->acc.as<double>(), st);
+      CKL("acc_reduce");
+      ++c->launches;
+      if (c->own[0][1] == c->own[1][0]) break;
+    }
     CK(cudaStreamSynchronize(st), "adaptive sync");
     for (int r = 0; r < r_hi; ++r) {
       if (sharded) s_eq_all[static_cast<size_t>(mb + r)] = eq_h[r];

@@ -400,6 +400,40 @@ def test_adaptive_realization_shards_distributed(P, calib):
         assert np.max(np.abs(pred - ref)) <= 1e-3 * (p.zmax - p.zmin)
 
 
+@pytest.mark.parametrize("overlap", ["1", "0"])
+def test_adaptive_row_slabs_distributed(P, calib, monkeypatch, overlap):
+    """The adaptive protocol on row slabs (3 contexts): each rank sweeps its rows for every
+    realization, the partial whole-grid energies are summed over the ranks before each
+    device check, so every rank takes the oracle's decisions (s_eq) and predicts the
+    oracle's values (derived tolerance, n_avg = 2 within the tolerance)."""
+    from paper_2212_01317_b200.sharding import run_group
+    monkeypatch.setenv("MPR_HALO_OVERLAP", overlap)
+    truth, z, mask = make_problem(45, 0.5, Lx=38, corr_len=6.0)
+    M, seed = 6, 19
+    Tk, ek = calib
+    for n_avg in (1, 2):
+        cfg = P.Config(n_avg=n_avg, l_b=8, n_s=2, r_s=1)
+        oc = ocfg(cfg)
+        p = O.parameters(z, mask, oc, Tk, ek)
+        r = O.simulate_adaptive(p, mask, oc, M, seed, n_fit=8, n_f=3, S_max=70, slope_tol="derived")
+        ref = O.predict(np.nan_to_num(z), mask, r["acc"], M, n_avg, p.zmin, p.zmax, 0)
+
+        def fn(rank, g):
+            m = P.LeMpr(P.Config(n_avg=n_avg, l_b=8, n_s=2, r_s=1, group=g, group_rank=rank, shard="rows"), calib)
+            m.set_data(z, mask)
+            m.estimate_local_params()
+            s_eq = m.simulate_adaptive(M, seed, n_fit=8, n_f=3, max_sweeps=70, slope_tol="derived")
+            pred = m.predict()
+            m.close()
+            return s_eq, pred
+        for s_eq, pred in run_group(3, fn):
+            assert s_eq.tolist() == r["s_eq"].tolist()
+            if n_avg == 1:
+                assert_bitwise(pred, ref, "adaptive row-slab predictions")
+            else:
+                assert np.max(np.abs(pred - ref)) <= 1e-3 * (p.zmax - p.zmin)
+
+
 def test_nccl_transport_world1(P, calib, monkeypatch):
     """The NCCL transport on the device: a communicator made through libmpr
     (mpr_nccl_unique_id / mpr_nccl_comm_init, libnccl resolved at run time) and, with
