@@ -811,20 +811,35 @@ __global__ void __launch_bounds__(256) k_smooth_rs(const float* __restrict__ Tin
   // values sit in registers: the loads overlap instead of one round trip per row)
   constexpr int NYW = (HY + 7) / 8;
   float va[NYW], vb[NYW];
+  // interior tiles (the halo tile inside the buffer): unguarded loads
+  const bool interior = r0 - RS >= 0 && r0 + TY + RS <= Ly && c0 - RS >= 0 && c0 + kTile + RS <= Lx;
+  if (interior && !FROM_TB) {
+    const float* row = Tin + (r0 - RS + ty) * Lx;
 #pragma unroll
-  for (int t = 0; t < NYW; ++t) {
-    const int y = ty + 8 * t;
-    const int r = r0 - RS + y;
-    va[t] = vb[t] = 0.0f;
-    if (y < HY && static_cast<unsigned>(r) < static_cast<unsigned>(Ly)) {
-      if (FROM_TB) {
-        const float* tb = Tb + ((r + row_base) / lb) * nbx;
-        if (ina) va[t] = __ldg(tb + bca);
-        if (inb) vb[t] = __ldg(tb + bcb);
-      } else {
-        const float* row = Tin + r * Lx;
-        if (ina) va[t] = __ldg(row + ca);
-        if (inb) vb[t] = __ldg(row + cb);
+    for (int t = 0; t < NYW; ++t) {
+      vb[t] = 0.0f;
+      if (ty + 8 * t < HY) {
+        va[t] = __ldg(row + ca);
+        if (tx < 2 * RS) vb[t] = __ldg(row + cb);
+      }
+      row += 8 * Lx;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < NYW; ++t) {
+      const int y = ty + 8 * t;
+      const int r = r0 - RS + y;
+      va[t] = vb[t] = 0.0f;
+      if (y < HY && static_cast<unsigned>(r) < static_cast<unsigned>(Ly)) {
+        if (FROM_TB) {
+          const float* tb = Tb + ((r + row_base) / lb) * nbx;
+          if (ina) va[t] = __ldg(tb + bca);
+          if (inb) vb[t] = __ldg(tb + bcb);
+        } else {
+          const float* row = Tin + r * Lx;
+          if (ina) va[t] = __ldg(row + ca);
+          if (inb) vb[t] = __ldg(row + cb);
+        }
       }
     }
   }
@@ -854,18 +869,29 @@ __global__ void __launch_bounds__(256) k_smooth_rs(const float* __restrict__ Tin
 #pragma unroll
   for (int d = 1; d < w; ++d) sum += H[yb + d][tx];
   const double full = static_cast<double>(w * ncol);
+  // The window mean's IEEE division by the unclipped count, with the reciprocal hoisted:
+  // y = RN(1 / cnt), q0 = RN(a y), rem = a - cnt q0 (exact by fma), q = RN(q0 + rem y) is
+  // RN(a / cnt) (Markstein's theorem: y within half an ulp of 1 / cnt, q0 within one ulp of
+  // a / cnt, no over- / underflow — a is a window sum of temperatures times 2^-40, cnt an
+  // integer <= 1089). Clipped rows divide with __ddiv_rn. Bit-identical to ARITH §F.
+  const double yfull = __drcp_rn(full);
 #pragma unroll 4
   for (int k = 0; k < kRows; ++k) {
     if (k > 0) sum += H[yb + k + w - 1][tx] - H[yb + k - 1][tx];
     const int r = r0 + yb + k;
     if (r >= Ly) break;
-    double cnt = full;
     const int rg = r + row_base;
+    const double a = smooth_value(sum) * 0x1p-40;
+    double q;
     if (rg - RS < 0 || rg + RS > Ly_g - 1) {
       const int ra = rg - RS > 0 ? rg - RS : 0, rb = rg + RS < Ly_g - 1 ? rg + RS : Ly_g - 1;
-      cnt = static_cast<double>((rb - ra + 1) * ncol);
+      q = __ddiv_rn(a, static_cast<double>((rb - ra + 1) * ncol));
+    } else {
+      const double q0 = __dmul_rn(a, yfull);
+      const double rem = __fma_rn(-full, q0, a);
+      q = __fma_rn(rem, yfull, q0);
     }
-    out[k * Lx] = __double2float_rn(__ddiv_rn(smooth_value(sum) * 0x1p-40, cnt));
+    out[k * Lx] = __double2float_rn(q);
   }
 }
 

@@ -763,3 +763,16 @@ def test_adaptive_with_derived_tolerance_uses_it(calib):
     b = O.simulate_adaptive(p, mask, cfg, 4, 5, n_fit=10, n_f=3, S_max=80, slope_tol=tol)
     assert a["s_eq"].tolist() == b["s_eq"].tolist()
     assert np.array_equal(a["acc"], b["acc"])
+
+
+def test_sst_division_with_hoisted_reciprocal_is_ieee(tmp_path):
+    """The GPU's SST pass divides unclipped window sums by their count as q0 = a RN(1/b),
+    q = fma(a - b q0, RN(1/b), q0) (Markstein): equal to the IEEE quotient the oracle uses
+    (ARITH §F) for every window count of r_s <= 8 and 3M random sums per count."""
+    import subprocess
+    src = os.path.join(os.path.dirname(__file__), "native", "markstein_div.c")
+    exe = str(tmp_path / "markstein_div")
+    subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-o", exe, src, "-lm"])
+    out = subprocess.run([exe, "3000000"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout
+    assert out.stdout.strip().startswith("0 mismatches")
