@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "device_math.cuh"
@@ -895,6 +896,135 @@ __global__ void __launch_bounds__(256) k_smooth_rs(const float* __restrict__ Tin
   }
 }
 
+// SST pass with 4 columns per thread (RS <= 4, Lx % 4 == 0, 16-byte aligned buffers): the
+// thread's columns arrive as one float4, the RS halo values on each side come from the
+// adjacent lanes by shuffle (the warp's outer lanes load theirs), and the 4 horizontal window
+// sums slide in registers (2 adds per column after the first), so shared memory holds only
+// the horizontal sums. The vertical pass slides down 16 rows per thread. Same exact sums
+// (F64 or int64, see k_smooth_rs), same division, same clipping: bit-identical.
+constexpr int kWideCols = 128, kWideRows = 32;
+template <int RS, bool F64, bool FROM_TB>
+__global__ void __launch_bounds__(256) k_smooth_wide(const float* __restrict__ Tin, const float* __restrict__ Tb,
+                                                     float* __restrict__ Tout, int64_t Lx64, int64_t Ly64,
+                                                     int64_t row_base64, int64_t Ly_g64, int lb) {
+  using Acc = typename std::conditional<F64, double, long long>::type;
+  constexpr int HY = kWideRows + 2 * RS, w = 2 * RS + 1;
+  __shared__ __align__(16) Acc H[HY][kWideCols];
+  const int Lx = static_cast<int>(Lx64), Ly = static_cast<int>(Ly64);
+  const int row_base = static_cast<int>(row_base64), Ly_g = static_cast<int>(Ly_g64);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int c0 = blockIdx.x * kWideCols, r0 = blockIdx.y * kWideRows;
+  const int c = c0 + 4 * lane;
+  const bool cin = c < Lx;  // all 4 columns or none (Lx % 4 == 0)
+  // every load of the warp's halo rows first (they overlap instead of one round trip per
+  // row): the float4 of the thread's columns, and for the outer lanes their RS halo columns
+  constexpr int NIT = (HY + 7) / 8;
+  float4 vv[NIT];
+  float ho[NIT][RS];  // lane 0: columns c - RS .. c - 1; lane 31: c + 4 .. c + 3 + RS
+  const bool outer = lane == 0 || lane == 31;
+  const int hc0 = lane == 0 ? c - RS : c + 4;
+  // FROM_TB: T(r, c) = T_b(block(r, c)) read from the block temperatures (the expansion
+  // fused into the first pass); the thread's columns' block indices are fixed
+  const int nbx = (Lx + lb - 1) / lb;
+  int bc[4] = {0, 0, 0, 0}, bh[RS];
+  if (FROM_TB) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bc[j] = cin ? (c + j) / lb : 0;
+#pragma unroll
+    for (int j = 0; j < RS; ++j) {
+      const int cc = hc0 + j;
+      bh[j] = (cc >= 0 && cc < Lx) ? cc / lb : 0;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < NIT; ++t) {
+    const int y = wp + 8 * t;
+    const int r = r0 - RS + y;
+    const bool rin = y < HY && static_cast<unsigned>(r) < static_cast<unsigned>(Ly);
+    vv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (FROM_TB) {
+      const float* tb = Tb + (rin ? ((r + row_base) / lb) * nbx : 0);
+      if (rin && cin) vv[t] = make_float4(__ldg(tb + bc[0]), __ldg(tb + bc[1]), __ldg(tb + bc[2]), __ldg(tb + bc[3]));
+#pragma unroll
+      for (int j = 0; j < RS; ++j) {
+        const int cc = hc0 + j;
+        ho[t][j] = (outer && rin && cc >= 0 && cc < Lx) ? __ldg(tb + bh[j]) : 0.0f;
+      }
+    } else {
+      const float* row = Tin + r * Lx;
+      if (rin && cin) vv[t] = __ldg(reinterpret_cast<const float4*>(row + c));
+#pragma unroll
+      for (int j = 0; j < RS; ++j) {
+        const int cc = hc0 + j;
+        ho[t][j] = (outer && rin && cc >= 0 && cc < Lx) ? __ldg(row + cc) : 0.0f;
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < NIT; ++t) {
+    const int y = wp + 8 * t;
+    if (y >= HY) break;  // warp-uniform
+    const float4 v = vv[t];
+    const Acc q[4] = {smooth_term<Acc>(v.x), smooth_term<Acc>(v.y), smooth_term<Acc>(v.z), smooth_term<Acc>(v.w)};
+    Acc xl[RS], xr[RS];  // columns c - RS .. c - 1 and c + 4 .. c + 3 + RS
+#pragma unroll
+    for (int j = 0; j < RS; ++j) {
+      xl[j] = __shfl_up_sync(0xffffffffu, q[4 - RS + j], 1);
+      xr[j] = __shfl_down_sync(0xffffffffu, q[j], 1);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < RS; ++j) xl[j] = smooth_term<Acc>(ho[t][j]);
+    }
+    if (lane == 31) {
+#pragma unroll
+      for (int j = 0; j < RS; ++j) xr[j] = smooth_term<Acc>(ho[t][j]);
+    }
+    auto x = [&](int k) -> Acc { return k < 0 ? xl[k + RS] : (k < 4 ? q[k] : xr[k - 4]); };
+    Acc h[4];
+    h[0] = x(-RS);
+#pragma unroll
+    for (int k = -RS + 1; k <= RS; ++k) h[0] += x(k);
+#pragma unroll
+    for (int i = 1; i < 4; ++i) h[i] = h[i - 1] + x(i + RS) - x(i - 1 - RS);
+    Acc* hp = &H[y][4 * lane];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) hp[i] = h[i];
+  }
+  __syncthreads();
+  const int cc = threadIdx.x & (kWideCols - 1), hh = threadIdx.x >> 7;  // column, row half
+  const int col = c0 + cc;
+  if (col >= Lx) return;
+  const int cl = col - RS > 0 ? col - RS : 0, cr = col + RS < Lx - 1 ? col + RS : Lx - 1;
+  const int ncol = cr - cl + 1;
+  constexpr int kRows = kWideRows / 2;
+  const int yb = hh * kRows;
+  float* out = Tout + (r0 + yb) * Lx + col;
+  Acc sum = H[yb][cc];
+#pragma unroll
+  for (int d = 1; d < w; ++d) sum += H[yb + d][cc];
+  const double full = static_cast<double>(w * ncol);
+  const double yfull = __drcp_rn(full);  // the Markstein division of k_smooth_rs
+#pragma unroll 4
+  for (int k = 0; k < kRows; ++k) {
+    if (k > 0) sum += H[yb + k + w - 1][cc] - H[yb + k - 1][cc];
+    const int r = r0 + yb + k;
+    if (r >= Ly) break;
+    const int rg = r + row_base;
+    const double a = smooth_value(sum) * 0x1p-40;
+    double qd;
+    if (rg - RS < 0 || rg + RS > Ly_g - 1) {
+      const int ra = rg - RS > 0 ? rg - RS : 0, rb = rg + RS < Ly_g - 1 ? rg + RS : Ly_g - 1;
+      qd = __ddiv_rn(a, static_cast<double>((rb - ra + 1) * ncol));
+    } else {
+      const double q0 = __dmul_rn(a, yfull);
+      const double rem = __fma_rn(-full, q0, a);
+      qd = __fma_rn(rem, yfull, q0);
+    }
+    out[k * Lx] = __double2float_rn(qd);
+  }
+}
+
 // Per-gap records in ONE pass over the local sites (row-major, coalesced reads of mask /
 // gid / phi / T): every gap site writes its whole 32-byte record at its id. The ids of a
 // row's same-colour gaps are consecutive, so a warp's record stores are two contiguous runs
@@ -1210,6 +1340,18 @@ static void smooth_rs(const float* Tin, const float* Tb, float* Tout, int64_t Lx
 template <int RS>
 static void smooth_rs_ty(const float* Tin, const float* Tb, float* Tout, int64_t Lx, int64_t Ly, int64_t row_base,
                          int64_t Ly_g, int lb, bool f64, cudaStream_t st) {
+  if (RS <= 4 && Lx % 4 == 0 && (Tb || aligned16(Tin)) && aligned16(Tout) && !std::getenv("MPR_SST_NARROW")) {
+    dim3 grid(static_cast<unsigned>((Lx + kWideCols - 1) / kWideCols), static_cast<unsigned>((Ly + kWideRows - 1) / kWideRows));
+    constexpr int R4 = RS <= 4 ? RS : 4;
+    if (Tb) {
+      if (f64) k_smooth_wide<R4, true, true><<<grid, 256, 0, st>>>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb);
+      else k_smooth_wide<R4, false, true><<<grid, 256, 0, st>>>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb);
+    } else {
+      if (f64) k_smooth_wide<R4, true, false><<<grid, 256, 0, st>>>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb);
+      else k_smooth_wide<R4, false, false><<<grid, 256, 0, st>>>(Tin, Tb, Tout, Lx, Ly, row_base, Ly_g, lb);
+    }
+    return;
+  }
   // 32 x 64 tiles once the grid has >= 16 waves of them on 148 SMs, 32 x 32 below
   const bool tall = (Lx + kTile - 1) / kTile * ((Ly + 63) / 64) >= 148 * 16;
   if (f64) {

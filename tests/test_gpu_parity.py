@@ -173,6 +173,27 @@ def test_sst_fixed_point_paths_bit_exact(P, calib, scale, rs, ns):
     assert_bitwise(T, p.T, f"T field (table x{scale}, r_s={rs}, n_s={ns})")
 
 
+@pytest.mark.parametrize("narrow", ["", "1"])
+@pytest.mark.parametrize("rs,scale,Lx", [(1, 1.0, 200), (2, 1.0, 1024), (3, 100.0, 132), (4, 1.0, 260), (4, 300.0, 128)])
+def test_sst_wide_tile_bit_exact(P, calib, monkeypatch, narrow, rs, scale, Lx):
+    """The 4-columns-per-thread SST pass (r_s <= 4, Lx % 4 == 0: float4 loads, halo by lane
+    shuffles, register-sliding horizontal sums; fp64 or int64 sums by the table's range) and,
+    with MPR_SST_NARROW, the one-column pass: T equals the oracle's bit for bit on grids with
+    partial edge tiles in both directions."""
+    if narrow:
+        monkeypatch.setenv("MPR_SST_NARROW", narrow)
+    Tk, ek = calib
+    Ts = (Tk.astype(np.float64) * scale).astype(np.float32)
+    truth, z, mask = make_problem(77, 0.5, Lx=Lx, corr_len=5.0)
+    cfg = P.Config(r_s=rs, n_s=3, l_b=16)
+    m = P.LeMpr(cfg, (Ts, ek))
+    m.set_data(z, mask)
+    T = m.estimate_local_params(want_T=True)
+    m.close()
+    p = O.parameters(z, mask, ocfg(cfg), Ts, ek)
+    assert_bitwise(T, p.T, f"T field (r_s={rs}, table x{scale}, Lx={Lx}, narrow={bool(narrow)})")
+
+
 def test_sharded_ranges_equal_single_call(P, calib):
     """simulate_range over [0,4) then [4,10) == simulate(10) bit for bit (global realization ids)."""
     truth, z, mask = make_problem(40, 0.5, corr_len=6.0)
