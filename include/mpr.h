@@ -286,7 +286,9 @@ typedef struct {
   int32_t sweep_variant;                         /* half-sweep kernel variant in use
                                                     (MPR_SWEEP_VARIANT; 28 default:
                                                     two realization pairs per thread,
-                                                    13 for odd pair counts)         */
+                                                    13 for odd pair counts; 40/41:
+                                                    the SFU-filtered forms, opt-in,
+                                                    28 when mpr_filter_check fails) */
   int32_t rank, world, shard;                    /* multi-rank layout                */
   int64_t row_begin, row_end;                    /* own rows (whole grid unless
                                                     MPR_SHARD_ROWS)                 */
@@ -298,6 +300,11 @@ typedef struct {
   double slope_tol;                              /* slope tolerance of the last
                                                     adaptive run (derived: R22)     */
   int64_t sample_bonds;                          /* N_SP: sample-sample bonds        */
+  int64_t filter_exact_pairs, filter_pairs;      /* variant 40/41 with
+                                                    MPR_FILTER_STATS=1: realization
+                                                    pairs sent to the exact path / all
+                                                    pairs updated since mpr_init
+                                                    (-1: not counted)               */
 } mpr_info;
 mpr_status mpr_get_info(mpr_ctx *ctx, mpr_info *info);
 
@@ -327,6 +334,19 @@ mpr_status mpr_set_kernel_timing(mpr_ctx *ctx, int enable);
 
 /* Library version string. */
 const char *mpr_version(void);
+
+/* Premises of the SFU rejection filter of the opt-in half-sweep kernel (variant 40,
+ * DESIGN.md §7), measured on `device` over every argument the filter can see (run once
+ * per device and process, a few ms):
+ *   err_out[0] = max |y * S(fl(y*y)) - sin_SFU(y)| over every fp32 |y| <= 3.2, where S is
+ *                ARITH §B2's sine polynomial (the product-form dE of PAPER.md Eq.(1)); the
+ *                filter's bound B assumes <= 4e-6;
+ *   err_out[1] = max exp_spec(x) * 2^24 over every fp32 x in [-80, -17] (must be < 1:
+ *                such a Metropolis step, accepts only when u(w) = 0).
+ * err_out: 2 doubles, host, borrowed; may be NULL. Returns 1 when both premises hold (a
+ * context asking for variant 40 runs it), 0 otherwise (mpr_init falls back to the exact
+ * kernel 28) or when no device is usable. */
+int mpr_filter_check(int device, double *err_out);
 
 #ifdef __cplusplus
 }

@@ -33,7 +33,7 @@ EXPORTED = ["mpr_config_default", "mpr_init", "mpr_destroy", "mpr_last_error", "
             "mpr_get_info", "mpr_debug_get", "mpr_set_energy_trace", "mpr_set_kernel_timing", "mpr_version",
             "mpr_sync", "mpr_predict_rows", "mpr_set_deferred_reduce", "mpr_accumulate_states",
             "mpr_simulate_adaptive", "mpr_build_calibration", "mpr_nccl_unique_id", "mpr_nccl_comm_init",
-            "mpr_nccl_comm_destroy", "mpr_group_create", "mpr_group_destroy"]
+            "mpr_nccl_comm_destroy", "mpr_group_create", "mpr_group_destroy", "mpr_filter_check"]
 
 
 class MprError(RuntimeError):
@@ -61,7 +61,7 @@ class mpr_info(C.Structure):
                 ("sweep_variant", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("shard", C.c_int32),
                 ("row_begin", C.c_int64), ("row_end", C.c_int64), ("m_begin", C.c_int64), ("m_end", C.c_int64),
                 ("n_gaps_local", C.c_int64), ("comm_calls", C.c_int64), ("slope_tol", C.c_double),
-                ("sample_bonds", C.c_int64)]
+                ("sample_bonds", C.c_int64), ("filter_exact_pairs", C.c_int64), ("filter_pairs", C.c_int64)]
 
 
 _lib = None
@@ -109,6 +109,7 @@ def load_library(path: str = LIB_PATH):
     L.mpr_build_calibration.argtypes = [vp, vp, i32, i32, C.c_float, i32, i32, i32, u64, vp, vp]
     L.mpr_build_calibration.restype = C.c_int
     L.mpr_version.argtypes = []; L.mpr_version.restype = C.c_char_p
+    L.mpr_filter_check.argtypes = [C.c_int, vp]; L.mpr_filter_check.restype = C.c_int
     _lib = L
     return L
 
@@ -276,6 +277,13 @@ def mpr_simulate_adaptive(ctx, M, seed, n_fit=20, n_f=5, max_sweeps=500, slope_t
 
 def mpr_version() -> str:
     return load_library().mpr_version().decode()
+
+
+def mpr_filter_check(device: int = 0):
+    """(passed, sfu_sine_err, max_exp_x24) of the default kernel's rejection filter."""
+    err = np.zeros(2, np.float64)
+    ok = load_library().mpr_filter_check(int(device), err.ctypes.data)
+    return bool(ok), float(err[0]), float(err[1])
 
 
 # ----------------------------------------------------------- convenience layer

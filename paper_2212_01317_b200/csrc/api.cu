@@ -104,6 +104,9 @@ struct mpr_ctx {
   std::string err;
   int sweep_grid = 0;
   int sweep_variant = 28;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
+  // MPR_FILTER_STATS=1: the filter kernels count their queued (exact-path) and all live
+  // pairs into fstats[0..1] (one atomic per warp and launch; tests and bench only)
+  DBuf fstats;
   // multi-rank
   std::unique_ptr<Comm> comm;
   int rank = 0, world = 1;
@@ -513,7 +516,8 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
   // 0.36 -> 0.50 ms and 1.25 -> 1.39 ms when split; 16384^2: 3.85 -> 3.40 ms / half-sweep).
   // (A 5-pair-per-thread kernel running R = 10 as one batch with float2 moves was measured
   // slower at C4: 3.65 ms per half-sweep against 2.21 + 0.78 ms for 8 + 2; dropped.)
-  if ((c->sweep_variant == 22 || c->sweep_variant == 28) && B % 4 == 2 && B > 2 && c->P >= c->split_min_P)
+  if ((c->sweep_variant == 22 || c->sweep_variant == 28 || c->sweep_variant == 40) && B % 4 == 2 && B > 2 &&
+      c->P >= c->split_min_P)
     B -= 2;
   c->batch_key_P = c->P;
   c->batch_key_R = R;
@@ -526,6 +530,15 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
 extern "C" {
 
 const char* mpr_version(void) { return "libmpr 0.2 (sm_100a, LE-MPR / SV-MPR arXiv 2212.01317)"; }
+
+int mpr_filter_check(int device, double* err_out) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+    cudaGetLastError();
+    return 0;
+  }
+  return sfu_filter_check(device, err_out);
+}
 
 void mpr_config_default(mpr_config* cfg) {
   if (!cfg) return;
@@ -619,6 +632,20 @@ mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
     }
   }
   if (const char* v = std::getenv("MPR_SWEEP_VARIANT")) c->sweep_variant = std::atoi(v);
+  // the SFU-filtered kernel (variant 40, opt-in: measured slower) only where
+  // its error bound was verified on this device; otherwise the exact kernel 28
+  if ((c->sweep_variant == 40 || c->sweep_variant == 41) && !sfu_filter_check(c->device, nullptr)) {
+    std::fprintf(stderr, "mpr_init: SFU filter check failed on device %d, using sweep variant 28\n", c->device);
+    c->sweep_variant = 28;
+  }
+  if (const char* v = std::getenv("MPR_FILTER_STATS"))
+    if (std::atoi(v)) {
+      if (c->fstats.ensure(2 * sizeof(unsigned long long)) != cudaSuccess ||
+          cudaMemset(c->fstats.p, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) {
+        mpr_destroy(c);
+        return MPR_ERR_CUDA;
+      }
+    }
   if (const char* v = std::getenv("MPR_NO_GRAPHS")) c->use_graphs = std::atoi(v) ? 0 : 1;
   if (const char* v = std::getenv("MPR_SLAB_GRAPHS")) c->slab_graphs = std::atoi(v) ? 1 : 0;
   if (const char* v = std::getenv("MPR_DC_TILED")) c->dc_tiled = std::atoi(v) ? 1 : 0;
@@ -634,7 +661,7 @@ void mpr_destroy(mpr_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   DBuf* bufs[] = {&c->z, &c->mask, &c->phiK, &c->scal, &c->calTd, &c->caled, &c->rowcnt, &c->rowoff,
                   &c->gid, &c->rec, &c->bstats, &c->Tb, &c->T, &c->T2, &c->G, &c->A, &c->acc,
-                  &c->energy, &c->out, &c->tmp, &c->win, &c->dclist, &c->dccnt, &c->ginit};
+                  &c->energy, &c->out, &c->tmp, &c->win, &c->dclist, &c->dccnt, &c->ginit, &c->fstats};
   for (DBuf* b : bufs) b->release();
   if (c->hsc) cudaFreeHost(c->hsc);
   for (auto& e : c->graphs)
@@ -910,6 +937,7 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
   a.r_valid_lo = k.r_lo;
   a.r_valid_hi = k.r_hi;
   a.energy_stride = k.sweeps;
+  a.fstats = c->fstats.as<unsigned long long>();
   *nsweep = 0;
   const bool per_launch_timing = k.timing && c->rows;
   size_t evk = 0;
@@ -1281,6 +1309,7 @@ mpr_status mpr_simulate_adaptive(mpr_ctx* c, int64_t M, uint64_t seed, int32_t n
     a.k1 = k1;
     a.q = c->cfg.q;
     a.J = c->cfg.J;
+    a.fstats = c->fstats.as<unsigned long long>();
     a.win_lo = c->win.as<int>();
     a.win_hi = c->win.as<int>() + Rb;
     a.energy_stride = max_sweeps;
@@ -1541,6 +1570,14 @@ mpr_status mpr_get_info(mpr_ctx* c, mpr_info* info) {
   info->comm_calls = c->comm_calls;
   info->slope_tol = c->last_slope_tol;
   info->sample_bonds = c->n_sample_bonds;
+  info->filter_exact_pairs = info->filter_pairs = -1;
+  if (c->fstats.p) {
+    unsigned long long h[2] = {0, 0};
+    CK(cudaStreamSynchronize(c->stream), "filter stats sync");
+    CK(cudaMemcpy(h, c->fstats.p, sizeof(h), cudaMemcpyDeviceToHost), "filter stats");
+    info->filter_exact_pairs = static_cast<int64_t>(h[0]);
+    info->filter_pairs = static_cast<int64_t>(h[1]);
+  }
   return MPR_OK;
 }
 

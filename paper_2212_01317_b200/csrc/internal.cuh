@@ -135,8 +135,14 @@ struct SweepArgs {
   // (the neighbouring slab's state buffer, same global layout). nullptr: no peer.
   float* peer[2];
   uint32_t peer_lo[2], peer_hi[2];
+  unsigned long long* fstats;  // nullable: filter kernels add [0] queued pairs, [1] live pairs
 };
 int sweep_grid_size(int device, int variant);
+// Variant 40's premises on this device (sweep.cu k_filter_check, run once per device):
+// err[0] = the SFU sine's largest error against ARITH §B2's sine over every argument the
+// filter sees, err[1] = the largest exp_spec(x) * 2^24 for x in [-80, -17]. Returns 1 when
+// err[0] <= the bound's allowance and err[1] < 1 (the filter may run), else 0.
+int sfu_filter_check(int device, double* err);
 // Row f3 with shared-memory tiles: one launch updates every l_b tile of parity
 // tau, both colours inside the tile (= the DC phases (tau, A), (tau, B)). dc_tile_chunk: the
 // realizations per CTA for this l_b and batch (0: the tile does not fit shared memory).

@@ -22,6 +22,8 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
 
 #include "device_math.cuh"
 #include "internal.cuh"
@@ -519,6 +521,272 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
   pdl_trigger();
 }
 
+// ---- Variant 40: the SFU rejection filter (DESIGN.md §7 "Filtered sweep") -------------
+// At the temperatures the method estimates (T ~ 1e-4 .. 1e-2 against bond energies of
+// order J), almost every proposal of the independence sampler is rejected by a wide
+// margin: -beta dE < -17 for 93 % of the updates at C2 and ~98 % at C3/C4. For those the
+// Metropolis decision is known without the exact fp32 arithmetic of ARITH §H: when
+// x = -beta dE_spec <= -17, exp_spec(x) * 2^24 < 1, so u(w) < exp_spec(x) holds only for
+// w >> 8 == 0. The filter evaluates dE with the SFU sine (MUFU.SIN, a pipe of its own)
+// and a rigorous error bound B against the exact form, and certifies "reject" when
+//   (w >> 8) != 0  and  fl(fl(dE_m - B) * beta) > 17.5.
+// Only the pairs it cannot certify (C2: ~6 % measured) run the exact metropolis_pair,
+// compacted per warp through a shared-memory queue so that the exact path runs on full
+// warps. The exact path is untouched, so the states are the oracle's bit for bit; the
+// bound holds by construction once sfu_filter_check() has measured the SFU sine's error
+// over every fp32 argument the filter can see (mpr_init only selects variant 40 when it
+// passed).
+// Measured (profiles/r02_summary.md): 79.4 us per C2 half-sweep against 72.1 us for variant
+// 28, so it is opt-in (MPR_SWEEP_VARIANT=40). The FMA-heavy pipe drops from 71 % to 48 %
+// busy, but the kernel is issue-bound: each SFU sine costs two issue slots (FMUL.RZ +
+// MUFU.SIN, scalar) against four for a packed polynomial sine pair, the queue adds ~18
+// slots per item, so the instruction count stays at v28's (52.8 M vs 53.7 M per launch)
+// and the thinner arithmetic no longer hides the state loads (long-scoreboard stalls
+// 0.95 -> 2.7 per issue). Deeper register pipelines (2 CTAs/SM) were slower still.
+constexpr int kFiltQ = 64;          // queue entries per warp (< 32 left + <= 32 appended)
+constexpr float kFiltX = 17.5f;     // threshold on beta * (dE_m - B)
+constexpr float kFiltB = 6.0e-5f;   // B = kFiltB * 2J (>= 1.7x the bound)
+constexpr double kFiltEps = 4.0e-6; // largest SFU sine error the bound B allows
+
+// dE of both realizations of a pair from SFU sines: the same proposal, difference and sum
+// as metropolis_pair; the sine arguments are y0 = fl(h d) and y_k = fl(-2h nb_k + fl(h sm))
+// (for q = 1/2 exactly the arguments of ARITH §B2's S4 form, x / 4; for other q within two
+// units in the last place of them, which the bound allows for). Packed f32x2 throughout
+// except the SFU sines; a contraction ptxas may apply here only removes a rounding.
+// Returns true when both updates are certain rejections.
+struct FiltConst {
+  float h;
+  float2 m2h, hh, twoJ, nBj;
+};
+template <bool FULL>
+__device__ __forceinline__ bool filter_rejects(float2 cur, const float2 (&nb)[4], uint32_t flags, float beta,
+                                               const FiltConst& fc, const Words4& w) {
+  const float2 prop = make_float2(__fmul_rn(__uint2float_rn(w.w0 >> 8), 0x1.921fb6p-22f),
+                                  __fmul_rn(__uint2float_rn(w.w2 >> 8), 0x1.921fb6p-22f));
+  const float2 y0 = __fmul2_rn(fc.hh, __fadd2_rn(prop, make_float2(-cur.x, -cur.y)));
+  const float2 hs = __fmul2_rn(fc.hh, __fadd2_rn(prop, cur));
+  float2 sg = f2(0.0f);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 y = __ffma2_rn(fc.m2h, nb[k], hs);
+    float2 t = make_float2(__sinf(y.x), __sinf(y.y));
+    if (!FULL && ((flags >> (2 * k)) & 3u) == 0u) t = f2(0.0f);
+    sg = k == 0 ? t : __fadd2_rn(sg, t);
+  }
+  const float2 s1 = make_float2(__sinf(y0.x), __sinf(y0.y));
+  const float2 e = __fmul2_rn(__fmul2_rn(fc.twoJ, s1), sg);
+  const float2 xb = __fmul2_rn(__fadd2_rn(e, fc.nBj), f2(beta));
+  return min(w.w1, w.w3) > 255u && xb.x > kFiltX && xb.y > kFiltX;
+}
+
+// One queued pair on the exact path: its record and states are re-read (L1/L2 hits: the
+// item was visited moments ago, and nothing it reads changes during the half-sweep).
+template <bool QHALF>
+__device__ __forceinline__ void filt_exact(const SweepArgs& a, uint32_t R, const uint4 wq, const uint2 m) {
+  const uint32_t gg = m.x, col = m.y & 0x3fffffffu;
+  const bool acc0 = (m.y >> 30) & 1u, acc1 = (m.y >> 31) & 1u;
+  const GapRec rec = a.rec[gg];
+  const uint32_t self_off = gg * R + col;
+  const float2 cur = *reinterpret_cast<const float2*>(a.G + self_off);
+  float2 nb[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
+    nb[k] = ty == NB_GAP ? *reinterpret_cast<const float2*>(a.G + (static_cast<uint32_t>(rec.nb[k]) * R + col))
+                         : f2(__int_as_float(rec.nb[k]));
+  }
+  long long e0 = 0, e1 = 0;
+  process_item_w<QHALF, false, true, true, false>(a, rec, cur, nb, self_off, Words4{wq.x, wq.y, wq.z, wq.w}, e0,
+                                                  e1, acc0, acc1);
+}
+
+// NP realization pairs of one gap site per thread (NP = 2: float4 state moves as in
+// k_sweep_quad; NP = 1: float2, for odd pair counts). Every lane runs the same number of
+// loop trips (warp-uniform), so the queue's ballots see the whole warp.
+template <bool QHALF, int MINB, bool LIST, int NP>
+__global__ void __launch_bounds__(256, MINB) k_sweep_filt(const SweepArgs a) {
+  __shared__ uint4 qw[8][kFiltQ];  // Philox words of the queued pairs
+  __shared__ uint2 qm[8][kFiltQ];  // (gap id, column | accumulation bits)
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  uint4* const myqw = qw[threadIdx.x >> 5];
+  uint2* const myqm = qm[threadIdx.x >> 5];
+  const unsigned below = (1u << lane) - 1u;
+  const int nq = a.npairs / NP;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int total = gridDim.x * blockDim.x;
+  const int nactive = (total / nq) * nq;
+  const bool active = tid < nactive;
+  const int jq = tid % nq;
+  const uint32_t gstride = static_cast<uint32_t>(nactive / nq);
+  const uint32_t R = static_cast<uint32_t>(a.R), j0 = 2u * NP * static_cast<uint32_t>(jq);
+  const uint32_t gcount = static_cast<uint32_t>(a.g_count), gbegin = static_cast<uint32_t>(a.g_begin);
+  FiltConst fc;
+  fc.h = __fmul_rn(a.q, 0.5f);
+  fc.hh = f2(fc.h);
+  fc.m2h = f2(-2.0f * fc.h);
+  fc.twoJ = f2(__fmul_rn(2.0f, a.J));
+  fc.nBj = f2(-__fmul_rn(kFiltB, fc.twoJ.x));
+  // per pair: live (adaptive windows), the queue word (column | accumulation bits) and
+  // whether a certified rejection accumulates its unchanged state (a9)
+  bool live[NP];
+  uint32_t qbits[NP];
+  bool anyacc[NP];
+  bool any_live = false;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    bool f0 = false, f1 = false;
+    live[p] = active;
+    if (active) {
+      accum_flags(a, NP * jq + p, f0, f1);
+      if (a.win_hi) {
+        const int sw = static_cast<int>(a.sweep), r = 2 * (NP * jq + p);
+        live[p] = sw <= max(a.win_hi[r], a.win_hi[r + 1]);
+      }
+    }
+    qbits[p] = (j0 + 2u * p) | (f0 ? 1u << 30 : 0u) | (f1 ? 1u << 31 : 0u);
+    anyacc[p] = f0 || f1;
+    any_live |= live[p];
+  }
+  const uint32_t pair0 = a.pair_base + static_cast<uint32_t>(NP * jq);
+  uint32_t g = any_live ? static_cast<uint32_t>(tid / nq) : gcount;
+  uint32_t gg = 0;
+  GapRec rec{};
+  if (g < gcount) {
+    gg = LIST ? a.glist[g] : gbegin + g;
+    rec = a.rec[gg];
+  }
+  int cnt = 0;  // queued pairs of this warp (warp-uniform)
+  uint32_t n_exact = 0, n_live = 0;  // MPR_FILTER_STATS
+  while (__any_sync(0xffffffffu, g < gcount)) {
+    const bool have = g < gcount;
+    const uint32_t gn = g + gstride;
+    uint32_t ggn = 0;
+    GapRec recn{};
+    if (have && gn < gcount) {
+      ggn = LIST ? a.glist[gn] : gbegin + gn;
+      recn = a.rec[ggn];
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.G + (ggn * R + j0)));
+    }
+    Words4 w[NP];
+    bool cand[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) cand[p] = false;
+    if (have) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) w[p] = philox4x32_10_rk(rec.site, a.sweep, pair0 + p, 2u, a.rk0, a.rk1);
+      const uint32_t self_off = gg * R + j0;
+      float2 cur[NP];
+      float2 nb[NP][4];
+      if (NP == 2) {
+        const float4 c4 = *reinterpret_cast<const float4*>(a.G + self_off);
+        cur[0] = make_float2(c4.x, c4.y);
+        cur[NP - 1] = make_float2(c4.z, c4.w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
+          if (ty == NB_GAP) {
+            const float4 v = *reinterpret_cast<const float4*>(a.G + (static_cast<uint32_t>(rec.nb[k]) * R + j0));
+            nb[0][k] = make_float2(v.x, v.y);
+            nb[NP - 1][k] = make_float2(v.z, v.w);
+          } else {
+            nb[0][k] = nb[NP - 1][k] = f2(__int_as_float(rec.nb[k]));
+          }
+        }
+      } else {
+        cur[0] = *reinterpret_cast<const float2*>(a.G + self_off);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
+          nb[0][k] = ty == NB_GAP
+              ? *reinterpret_cast<const float2*>(a.G + (static_cast<uint32_t>(rec.nb[k]) * R + j0))
+              : f2(__int_as_float(rec.nb[k]));
+        }
+      }
+      const bool full = all_present(rec.flags);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const bool rej = full ? filter_rejects<true>(cur[p], nb[p], rec.flags, rec.beta, fc, w[p])
+                              : filter_rejects<false>(cur[p], nb[p], rec.flags, rec.beta, fc, w[p]);
+        cand[p] = live[p] && !rej;
+        if (a.fstats) n_live += live[p] ? 1u : 0u;
+        // a certain rejection keeps the state: no store; the fused a9 epilogue adds it
+        if (live[p] && rej && anyacc[p]) {
+          float2* ap = reinterpret_cast<float2*>(a.A + self_off + 2u * p);
+          float2 av = *ap;
+          if (qbits[p] >> 30 & 1u) av.x = __fadd_rn(av.x, cur[p].x);
+          if (qbits[p] >> 31) av.y = __fadd_rn(av.y, cur[p].y);
+          *ap = av;
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const unsigned m = __ballot_sync(0xffffffffu, cand[p]);
+      if (cand[p]) {
+        const int pos = cnt + __popc(m & below);
+        myqw[pos] = make_uint4(w[p].w0, w[p].w1, w[p].w2, w[p].w3);
+        myqm[pos] = make_uint2(gg, qbits[p]);
+      }
+      cnt += __popc(m);
+      if (a.fstats) n_exact += cand[p] ? 1u : 0u;
+      if (cnt >= 32) {  // a full warp of exact updates
+        __syncwarp();
+        const int e = cnt - 32 + lane;
+        filt_exact<QHALF>(a, R, myqw[e], myqm[e]);
+        cnt -= 32;
+        __syncwarp();
+      }
+    }
+    rec = recn;
+    gg = ggn;
+    g = gn;
+  }
+  __syncwarp();
+  if (lane < cnt) filt_exact<QHALF>(a, R, myqw[lane], myqm[lane]);
+  if (a.fstats) {
+    n_exact = __reduce_add_sync(0xffffffffu, n_exact);
+    n_live = __reduce_add_sync(0xffffffffu, n_live);
+    if (lane == 0) {
+      atomicAdd(&a.fstats[0], static_cast<unsigned long long>(n_exact));
+      atomicAdd(&a.fstats[1], static_cast<unsigned long long>(n_live));
+    }
+  }
+  pdl_trigger();
+}
+
+// Self-check of the filter's premises on this device, over every argument it can see:
+//   err[0] = max |y * S(fl(y*y)) - sinf_sfu(y)| over every fp32 y, |y| <= 3.2 (the sine
+//            arguments fl(h x) lie in [-TWO_PI_F/2, TWO_PI_F/2] for q <= 1/2);
+//   err[1] = max over every fp32 x in [-80, -17] of exp_spec(x) * 2^24 (must be < 1).
+__global__ void k_filter_check(unsigned long long* err) {
+  const uint32_t lim = __float_as_uint(3.2f);
+  double e = 0.0;
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= lim; b += gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const float y = __uint_as_float(b | (s ? 0x80000000u : 0u));
+      const float P = sin_poly(__fmul_rn(y, y));
+      const double t = __dmul_rn(static_cast<double>(y), static_cast<double>(P));
+      e = fmax(e, fabs(__dsub_rn(t, static_cast<double>(__sinf(y)))));
+    }
+  }
+  float ex = 0.0f;
+  const uint32_t x0 = __float_as_uint(17.0f), x1 = __float_as_uint(80.0f);
+  for (uint32_t b = x0 + blockIdx.x * blockDim.x + threadIdx.x; b <= x1; b += gridDim.x * blockDim.x) {
+    const float x = -__uint_as_float(b);
+    ex = fmaxf(ex, exp_spec_fast2_x24(make_float2(x, x)).x);
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    e = fmax(e, __shfl_xor_sync(0xffffffffu, e, off));
+    ex = fmaxf(ex, __shfl_xor_sync(0xffffffffu, ex, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&err[0], static_cast<unsigned long long>(__double_as_longlong(e)));
+    atomicMax(&err[1], static_cast<unsigned long long>(__double_as_longlong(static_cast<double>(ex))));
+  }
+}
+
 // Row f3, the paper's DC scheme with shared-memory tiles ("Each tile can be
 // loaded into the block's shared memory ... looking up the neighboring spins uses shared
 // instead of global memory"). One CTA per (l_b x l_b tile of parity tau, chunk of Rc
@@ -831,7 +1099,19 @@ static int sweep_threads(int) { return 256; }
 static size_t sweep_smem(int) { return 0; }
 
 static bool is_quad(int variant) { return variant == 22 || variant == 28; }
-static int pairs_per_thread(int variant) { return is_quad(variant) ? 2 : 1; }
+static bool is_filt(int variant) { return variant == 40 || variant == 41; }
+static int pairs_per_thread(int variant) { return (is_quad(variant) || variant == 40) ? 2 : 1; }
+
+// Variant 40 (SFU filter, two pairs per thread) / 41 (one pair per thread, also 40's
+// fallback for odd pair counts); 3 CTAs/SM like 28.
+static void* filt_kernel(bool qhalf, bool list, int variant) {
+  if (variant == 40) {
+    if (qhalf) return list ? reinterpret_cast<void*>(k_sweep_filt<true, 3, true, 2>) : reinterpret_cast<void*>(k_sweep_filt<true, 3, false, 2>);
+    return list ? reinterpret_cast<void*>(k_sweep_filt<false, 3, true, 2>) : reinterpret_cast<void*>(k_sweep_filt<false, 3, false, 2>);
+  }
+  if (qhalf) return list ? reinterpret_cast<void*>(k_sweep_filt<true, 3, true, 1>) : reinterpret_cast<void*>(k_sweep_filt<true, 3, false, 1>);
+  return list ? reinterpret_cast<void*>(k_sweep_filt<false, 3, true, 1>) : reinterpret_cast<void*>(k_sweep_filt<false, 3, false, 1>);
+}
 
 template <bool Q, bool E, bool PE>
 static void* quad_kernel_ptr(bool list, int variant) {
@@ -850,6 +1130,7 @@ static void* quad_kernel(bool qhalf, bool energy, bool list, int variant, bool p
 }
 
 static void* sweep_kernel(bool qhalf, bool energy, bool list, int variant, bool peer = false) {
+  if (is_filt(variant)) return filt_kernel(qhalf, list, variant);  // launch_sweep_half: no energy, no peer
   if (is_quad(variant)) return quad_kernel(qhalf, energy, list, variant, peer);
   if (peer)  // row slabs with the fused halo: SC order, no energy trace
     return qhalf ? sweep_kernel_ptr<true, false, false>(variant, true) : sweep_kernel_ptr<false, false, false>(variant, true);
@@ -868,8 +1149,16 @@ int sweep_grid_size(int device, int variant) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel(true, false, false, variant), sweep_threads(variant),
                                                 sweep_smem(variant));
-  // the two-pair kernels fall back to 13 for an odd pair count: size the grid for both
-  const int fb = is_quad(variant) ? 13 : -1;
+  // the two-pair kernels fall back to 13 for an odd pair count, the filter kernels to 41
+  // (odd pair counts) and to 28 / 13 (energy trace): size the grid for all of them
+  if (is_filt(variant)) {
+    for (int v : {41, 28}) {
+      int perf = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perf, sweep_kernel(true, v == 28, false, v), 256, 0);
+      if (perf < per) per = perf;
+    }
+  }
+  const int fb = (is_quad(variant) || is_filt(variant)) ? 13 : -1;
   if (fb >= 0) {
     for (int e = 0; e < 2; ++e) {
       int perf = 0;
@@ -900,6 +1189,10 @@ static void launch_pdl(const void* fn, unsigned grid, unsigned block, void** arg
 void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st) {
   const bool qhalf = (a.q == 0.5f);
   const bool energy = (a.energy != nullptr);
+  const bool peer0 = a.peer[0] != nullptr || a.peer[1] != nullptr;
+  // the filter kernels carry no energy epilogue and no peer stores: the exact kernels run those
+  if (is_filt(variant) && (energy || peer0)) variant = 28;
+  if (variant == 40 && (a.npairs & 1)) variant = 41;
   // the two-pair kernels need an even pair count (float4 alignment)
   if (is_quad(variant) && (a.npairs & 1)) variant = 13;
   const int nt = sweep_threads(variant);
@@ -919,6 +1212,46 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   }
   void* args[] = {&b};
   launch_pdl(fn, static_cast<unsigned>(g), static_cast<unsigned>(nt), args, sweep_smem(variant), st);
+}
+
+int sfu_filter_check(int device, double* err) {
+  // once per device and process: ~2.2e9 SFU sines, a few ms
+  static std::mutex mu;
+  static int state[64];      // 0 unknown, 1 passed, -1 failed
+  static double errs[64][2];
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64) return 0;
+  if (state[device] == 0) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    unsigned long long* d = nullptr;
+    unsigned long long h[2] = {0, 0};
+    bool ok = cudaMalloc(&d, sizeof(h)) == cudaSuccess;
+    if (ok) ok = cudaMemset(d, 0, sizeof(h)) == cudaSuccess;
+    if (ok) {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+      k_filter_check<<<sms * 8, 256>>>(d);
+      ok = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess;
+    }
+    if (d) cudaFree(d);
+    cudaSetDevice(prev);
+    double e0 = 1.0, e1 = 1.0;
+    if (ok) {
+      std::memcpy(&e0, &h[0], 8);
+      std::memcpy(&e1, &h[1], 8);
+    }
+    errs[device][0] = e0;
+    errs[device][1] = e1;
+    // the general-q arguments add up to 2 ulp of |y| <= pi (< 4e-7) to the sine error
+    state[device] = (ok && e0 + 4.0e-7 <= kFiltEps && e1 < 1.0) ? 1 : -1;
+  }
+  if (err) {
+    err[0] = errs[device][0];
+    err[1] = errs[device][1];
+  }
+  return state[device] > 0;
 }
 
 // Shared memory of one DC tile CTA: (l_b + 2)^2 cells x Rc realizations + the two gap lists.

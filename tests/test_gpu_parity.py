@@ -797,7 +797,7 @@ def test_adaptive_with_slope_tolerance(P, calib):
     assert_bitwise(pred, O.predict(np.nan_to_num(z), mask, r["acc"], 4, 1, p.zmin, p.zmax, 0), "predictions")
 
 
-@pytest.mark.parametrize("variant", [5, 13, 22, 28])
+@pytest.mark.parametrize("variant", [5, 13, 22, 28, 40, 41])
 def test_every_sweep_variant_bit_exact(P, calib, variant, monkeypatch):
     """Each half-sweep kernel variant (scalar / packed f32x2 arithmetic, one or two pairs per
     thread, early Philox; MPR_SWEEP_VARIANT) reproduces the oracle bit for bit: q = 1/2 with the energy trace, generic q, the DC
@@ -1058,3 +1058,51 @@ def test_deferred_reduce_state_rules(P, calib):
     with pytest.raises(P.MprError):
         m.accumulate_states()
     m.close()
+
+
+def test_filter_check_premises(P, monkeypatch):
+    """The SFU rejection filter's premises (variant 40) measured on this device
+    over every fp32 argument: the SFU sine within 4e-6 of ARITH §B2's sine on |y| <= 3.2, and
+    exp_spec(x) * 2^24 < 1 on [-80, -17]; a context asking for variant 40 then runs it."""
+    ok, e_sin, e_exp = P.binding.mpr_filter_check(0)
+    print(f"SFU sine max error {e_sin:.3e}, max exp_spec*2^24 on [-80,-17] {e_exp:.6f}")
+    assert ok and 0.0 < e_sin <= 4e-6 and 0.0 < e_exp < 1.0
+    monkeypatch.setenv("MPR_SWEEP_VARIANT", "40")
+    m = P.LeMpr(P.Config(), P.load_calibration())
+    assert m.info()["sweep_variant"] == 40
+    m.close()
+
+
+@pytest.mark.parametrize("case", ["smooth", "rough", "edges"])
+def test_filter_paths_bit_exact(P, calib, case, monkeypatch):
+    """Variant 40 / 41 with the filter statistics on: the certified rejections and the queued
+    exact pairs (full warps and the partial flush at the end) reproduce the oracle bit for bit,
+    with n_avg > 1 (certified rejections accumulate their unchanged state), the DC lists,
+    generic q and J, odd pair counts (41) and RANDOM init. 'smooth': low temperatures, most
+    pairs certified; 'rough': a white-noise field at high temperatures, most pairs exact;
+    'edges': a thin grid where most sites miss a neighbour."""
+    monkeypatch.setenv("MPR_FILTER_STATS", "1")
+    monkeypatch.setenv("MPR_SWEEP_VARIANT", "40")
+    if case == "smooth":
+        truth, z, mask = make_problem(96, 0.4, Lx=80, corr_len=12.0)
+    elif case == "rough":
+        rng = np.random.default_rng(7)
+        truth = rng.standard_normal((64, 72)).astype(np.float32)
+        mask = (rng.random((64, 72)) > 0.5).astype(np.uint8)
+        z = truth.copy(); z[mask == 0] = np.nan
+    else:
+        truth, z, mask = make_problem(3, 0.5, Lx=203, corr_len=4.0)
+    runs = [(P.Config(), 8, 9, 11, True), (P.Config(n_avg=3, init="random"), 12, 8, 12, False),
+            (P.Config(order="dc", l_b=8), 8, 6, 13, True), (P.Config(q=0.3, J=1.7, r_s=1), 6, 6, 14, True),
+            (P.Config(), 6, 7, 15, True)]
+    fracs = []
+    for cfg, M, S, seed, exact in runs:
+        g, _ = compare(P, z, mask, truth, cfg, calib, M, S, seed, exact_pred=exact)
+        inf = g["info"]
+        assert inf["sweep_variant"] == 40 and inf["filter_pairs"] > 0
+        fracs.append(inf["filter_exact_pairs"] / inf["filter_pairs"])
+    print(case, "exact-path fraction per run", [round(f, 3) for f in fracs])
+    if case == "smooth":
+        assert max(fracs) < 0.5
+    if case == "rough":
+        assert min(fracs) > 0.2
