@@ -1199,6 +1199,20 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   const int64_t units = a.npairs / pairs_per_thread(variant);  // threads per gap site
   const int64_t items = a.g_count * units;
   int64_t g = (items + nt - 1) / nt;
+  // Several resident waves of CTAs instead of one persistent wave: a CTA that finishes early
+  // is replaced by a fresh one, so the slowest warps no longer set the launch's tail. About
+  // 16 items per thread (C2: 3 waves, 72.1 -> 69.3 us; C3: 16 waves, 1505 -> 1365 us; C4:
+  // 32 waves, 1529 -> 1354 us per half-sweep; profiles/r02_summary.md). Energy launches
+  // keep one wave (their epilogue issues global atomics per CTA). MPR_SWEEP_WAVES overrides.
+  if (!energy) {
+    static const int forced = [] {
+      const char* v = std::getenv("MPR_SWEEP_WAVES");
+      return v ? std::atoi(v) : 0;
+    }();
+    const int64_t per_thread = items / (static_cast<int64_t>(grid) * nt);
+    int64_t waves = forced > 0 ? forced : std::min<int64_t>(32, std::max<int64_t>(1, (per_thread + 15) / 16));
+    grid = static_cast<int>(grid * waves);
+  }
   if (g > grid) g = grid;
   const int64_t need = (units + nt - 1) / nt;  // active threads >= units
   if (g < need) g = need;
