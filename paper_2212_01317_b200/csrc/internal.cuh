@@ -130,11 +130,6 @@ struct SweepArgs {
                      // this sweep, stride energy_stride
   int64_t energy_stride;
   int r_valid_lo, r_valid_hi;  // realizations [lo, hi) of the batch contribute energy
-  // Fused halo exchange over peer memory (row slabs): an accepted state whose element
-  // offset lies in [peer_lo[k], peer_hi[k]) is also stored at the same offset of peer[k]
-  // (the neighbouring slab's state buffer, same global layout). nullptr: no peer.
-  float* peer[2];
-  uint32_t peer_lo[2], peer_hi[2];
   unsigned long long* fstats;  // nullable: filter kernels add [0] queued pairs, [1] live pairs
 };
 int sweep_grid_size(int device, int variant);

@@ -172,24 +172,21 @@ __device__ __forceinline__ bool all_present(uint32_t f) {
 
 // One work item (gap site, realization pair) once its record and the states it reads
 // are in registers: Philox, two Metropolis updates, store, fused epilogues.
-// PEER: the launch may carry neighbour state buffers (row slabs, fused halo): checked at
-// run time in the PEER = true instantiations only (launch_sweep_half picks them when the
-// launch has peers); the default kernels carry no peer code.
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool PEER = false>
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK>
 __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec& rec, float2 cur,
                                                const float2 (&nb)[4], uint32_t self_off, const Words4& w,
                                                long long& e0, long long& e1, bool accum0, bool accum1);
 
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool PEER = false>
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK>
 __device__ __forceinline__ void process_item(const SweepArgs& a, const GapRec& rec, float2 cur,
                                              const float2 (&nb)[4], uint32_t self_off, uint32_t pair,
                                              long long& e0, long long& e1, bool accum0, bool accum1) {
   const Words4 w = philox4x32_10_rk(rec.site, a.sweep, pair, 2u, a.rk0, a.rk1);
-  process_item_w<QHALF, ENERGY, BFEXP, PK, PEER>(a, rec, cur, nb, self_off, w, e0, e1, accum0, accum1);
+  process_item_w<QHALF, ENERGY, BFEXP, PK>(a, rec, cur, nb, self_off, w, e0, e1, accum0, accum1);
 }
 
 // The item once its Philox words are known (the quad kernel may draw them early).
-template <bool QHALF, bool ENERGY, bool BFEXP, bool PK, bool PEER>
+template <bool QHALF, bool ENERGY, bool BFEXP, bool PK>
 __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec& rec, float2 cur,
                                                const float2 (&nb)[4], uint32_t self_off, const Words4& w,
                                                long long& e0, long long& e1, bool accum0, bool accum1) {
@@ -224,14 +221,6 @@ __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec&
   if (acc0 || acc1) {
     const float2 nv = make_float2(n0, n1);
     *gp = nv;
-    // row slabs: a changed state of a boundary row also lands in the neighbour's buffer
-    // (its ghost row), so the halo exchange is part of the half-sweep itself
-    if (PEER && (a.peer[0] != nullptr || a.peer[1] != nullptr)) {
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-        if (a.peer[k] != nullptr && self_off >= a.peer_lo[k] && self_off < a.peer_hi[k])
-          *reinterpret_cast<float2*>(a.peer[k] + self_off) = nv;
-    }
   }
   if (accum0 || accum1) {
     float2* ap = reinterpret_cast<float2*>(a.A + self_off);
@@ -311,7 +300,7 @@ __device__ __forceinline__ Split split_work(int npairs) {
 // One realization pair per thread. PF = 2: record, own and neighbour states loaded at the
 // start of each item, with a register-free L2 prefetch of the next item; PF = 3: the next
 // item's record is loaded one item ahead (below).
-template <bool QHALF, bool ENERGY, int MINB, int PF, int NT, bool BFEXP, bool LIST, bool PK, bool PEER = false>
+template <bool QHALF, bool ENERGY, int MINB, int PF, int NT, bool BFEXP, bool LIST, bool PK>
 __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   pdl_wait();
   const Split sp = split_work(a.npairs);
@@ -361,7 +350,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
           nb[k] = f2(__int_as_float(rec.nb[k]));
         }
       }
-      process_item<QHALF, ENERGY, BFEXP, PK, PEER>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
+      process_item<QHALF, ENERGY, BFEXP, PK>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
       rec = recn;
       gg = ggn;
     }
@@ -390,7 +379,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
           nb[k] = f2(__int_as_float(rec.nb[k]));
         }
       }
-      process_item<QHALF, ENERGY, BFEXP, PK, PEER>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
+      process_item<QHALF, ENERGY, BFEXP, PK>(a, rec, cur, nb, self_off, pair, e0, e1, accum0, accum1);
     }
   }
   if (ENERGY) {
@@ -406,8 +395,8 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
 // neighbour states move as float4 (two pairs each). Each pair still draws its own Philox
 // call and runs metropolis_pair, so the results are those of k_sweep_half bit for bit.
 // Requires npairs % NP == 0 (launch_sweep_half falls back). EARLY: every pair's Philox
-// words are drawn right after the record arrives; PEER: fused halo stores (row slabs).
-template <bool QHALF, bool ENERGY, int MINB, bool LIST, int NP = 2, bool EARLY = false, bool PEER = false>
+// words are drawn right after the record arrives.
+template <bool QHALF, bool ENERGY, int MINB, bool LIST, int NP = 2, bool EARLY = false>
 __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
   pdl_wait();
   constexpr int NQ = NP / 2;  // float4 quads per thread
@@ -490,18 +479,18 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
         const int pa = 2 * qd, pb = 2 * qd + 1;
         if (EARLY) {
           if (live[pa])
-            process_item_w<QHALF, ENERGY, true, true, PEER>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
+            process_item_w<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
                                                       wpre[pa], e[pa][0], e[pa][1], acc[pa][0], acc[pa][1]);
           if (live[pb])
-            process_item_w<QHALF, ENERGY, true, true, PEER>(a, rec, make_float2(cur.z, cur.w), nbB,
+            process_item_w<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.z, cur.w), nbB,
                                                       self_off + 4u * qd + 2u, wpre[pb], e[pb][0], e[pb][1],
                                                       acc[pb][0], acc[pb][1]);
         } else {
           if (live[pa])
-            process_item<QHALF, ENERGY, true, true, PEER>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
+            process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
                                                     pair0 + pa, e[pa][0], e[pa][1], acc[pa][0], acc[pa][1]);
           if (live[pb])
-            process_item<QHALF, ENERGY, true, true, PEER>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 4u * qd + 2u,
+            process_item<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.z, cur.w), nbB, self_off + 4u * qd + 2u,
                                                     pair0 + pb, e[pb][0], e[pb][1], acc[pb][0], acc[pb][1]);
         }
       }
@@ -596,7 +585,7 @@ __device__ __forceinline__ void filt_exact(const SweepArgs& a, uint32_t R, const
                          : f2(__int_as_float(rec.nb[k]));
   }
   long long e0 = 0, e1 = 0;
-  process_item_w<QHALF, false, true, true, false>(a, rec, cur, nb, self_off, Words4{wq.x, wq.y, wq.z, wq.w}, e0,
+  process_item_w<QHALF, false, true, true>(a, rec, cur, nb, self_off, Words4{wq.x, wq.y, wq.z, wq.w}, e0,
                                                   e1, acc0, acc1);
 }
 
@@ -1078,20 +1067,18 @@ void launch_adaptive_check(const AdaptiveCheckArgs& a, cudaStream_t st) {
 //        (the fallback of 22/28 for odd pair counts);
 //   22 = k_sweep_quad: two pairs per thread, float4 state moves, 4 CTAs/SM;
 //   28 = 22 with both pairs' Philox words drawn before the state loads are used,
-//        3 CTAs/SM (default).
-// Half-sweep, us (C2 / C3 / C4 at M = 10), product-form dE (ARITH §H):
-//   v5  92.6 (C2);  v13 89.7 / 1965 / 3525;  v28 72.2 / 1509 / 3082.
+//        3 CTAs/SM (default);
+//   40 / 41 = the SFU rejection filter (two / one pair per thread; opt-in, slower).
+// Half-sweep, us (C2 / C3 / C4 at M = 10), product-form dE (ARITH §H), one resident wave:
+//   v5  92.6 (C2);  v13 89.7 / 1965 / 3525;  v28 72.2 / 1509 / 3082
+//   (v28 with the resident waves of launch_sweep_half: 69.3 / 1367 / ~2707).
 // Direct form (8 cos per update), for comparison:
 //   v5  99.5 / 2229 / 4127;  v13 93.9 / 2071 / 3717;
 //   v22 87.1 / 1838 / 3402;  v28 84.5 / 1780 / 3351.
 template <bool Q, bool E, bool LIST>
-static void* sweep_kernel_ptr(int variant, bool peer) {
-  if (variant == 5)
-    return peer ? reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, false, true>)
-                : reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, false>);
-  // 13 (and 22/28's fallback)
-  return peer ? reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true, true>)
-              : reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);
+static void* sweep_kernel_ptr(int variant) {
+  if (variant == 5) return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, false>);
+  return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);  // 13 (and 22/28's fallback)
 }
 
 static int sweep_threads(int) { return 256; }
@@ -1113,35 +1100,25 @@ static void* filt_kernel(bool qhalf, bool list, int variant) {
   return list ? reinterpret_cast<void*>(k_sweep_filt<false, 3, true, 1>) : reinterpret_cast<void*>(k_sweep_filt<false, 3, false, 1>);
 }
 
-template <bool Q, bool E, bool PE>
+template <bool Q, bool E>
 static void* quad_kernel_ptr(bool list, int variant) {
   if (variant == 28)
-    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true, 2, true, PE>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false, 2, true, PE>);
-  return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true, 2, false, PE>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false, 2, false, PE>);  // 22
+    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true, 2, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false, 2, true>);
+  return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true, 2, false>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false, 2, false>);  // 22
 }
 
-// peer: the launch writes into neighbour state buffers (row slabs with the fused halo)
-static void* quad_kernel(bool qhalf, bool energy, bool list, int variant, bool peer) {
-  if (peer) {  // slab mode: no energy trace
-    return qhalf ? quad_kernel_ptr<true, false, true>(list, variant) : quad_kernel_ptr<false, false, true>(list, variant);
+static void* sweep_kernel(bool qhalf, bool energy, bool list, int variant) {
+  if (is_filt(variant)) return filt_kernel(qhalf, list, variant);  // launch_sweep_half: no energy
+  if (is_quad(variant)) {
+    if (qhalf) return energy ? quad_kernel_ptr<true, true>(list, variant) : quad_kernel_ptr<true, false>(list, variant);
+    return energy ? quad_kernel_ptr<false, true>(list, variant) : quad_kernel_ptr<false, false>(list, variant);
   }
-  if (qhalf) return energy ? quad_kernel_ptr<true, true, false>(list, variant) : quad_kernel_ptr<true, false, false>(list, variant);
-  return energy ? quad_kernel_ptr<false, true, false>(list, variant) : quad_kernel_ptr<false, false, false>(list, variant);
-}
-
-static void* sweep_kernel(bool qhalf, bool energy, bool list, int variant, bool peer = false) {
-  if (is_filt(variant)) return filt_kernel(qhalf, list, variant);  // launch_sweep_half: no energy, no peer
-  if (is_quad(variant)) return quad_kernel(qhalf, energy, list, variant, peer);
-  if (peer)  // row slabs with the fused halo: SC order, no energy trace
-    return qhalf ? sweep_kernel_ptr<true, false, false>(variant, true) : sweep_kernel_ptr<false, false, false>(variant, true);
   if (list) {
-    if (qhalf)
-      return energy ? sweep_kernel_ptr<true, true, true>(variant, false) : sweep_kernel_ptr<true, false, true>(variant, false);
-    return energy ? sweep_kernel_ptr<false, true, true>(variant, false) : sweep_kernel_ptr<false, false, true>(variant, false);
+    if (qhalf) return energy ? sweep_kernel_ptr<true, true, true>(variant) : sweep_kernel_ptr<true, false, true>(variant);
+    return energy ? sweep_kernel_ptr<false, true, true>(variant) : sweep_kernel_ptr<false, false, true>(variant);
   }
-  if (qhalf)
-    return energy ? sweep_kernel_ptr<true, true, false>(variant, false) : sweep_kernel_ptr<true, false, false>(variant, false);
-  return energy ? sweep_kernel_ptr<false, true, false>(variant, false) : sweep_kernel_ptr<false, false, false>(variant, false);
+  if (qhalf) return energy ? sweep_kernel_ptr<true, true, false>(variant) : sweep_kernel_ptr<true, false, false>(variant);
+  return energy ? sweep_kernel_ptr<false, true, false>(variant) : sweep_kernel_ptr<false, false, false>(variant);
 }
 
 int sweep_grid_size(int device, int variant) {
@@ -1189,9 +1166,8 @@ static void launch_pdl(const void* fn, unsigned grid, unsigned block, void** arg
 void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st) {
   const bool qhalf = (a.q == 0.5f);
   const bool energy = (a.energy != nullptr);
-  const bool peer0 = a.peer[0] != nullptr || a.peer[1] != nullptr;
-  // the filter kernels carry no energy epilogue and no peer stores: the exact kernels run those
-  if (is_filt(variant) && (energy || peer0)) variant = 28;
+  // the filter kernels carry no energy epilogue: the exact kernels run energy sweeps
+  if (is_filt(variant) && energy) variant = 28;
   if (variant == 40 && (a.npairs & 1)) variant = 41;
   // the two-pair kernels need an even pair count (float4 alignment)
   if (is_quad(variant) && (a.npairs & 1)) variant = 13;
@@ -1217,8 +1193,7 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   const int64_t need = (units + nt - 1) / nt;  // active threads >= units
   if (g < need) g = need;
   if (g < 1) g = 1;
-  const bool peer = a.peer[0] != nullptr || a.peer[1] != nullptr;
-  void* fn = sweep_kernel(qhalf, energy, a.glist != nullptr, variant, peer);
+  void* fn = sweep_kernel(qhalf, energy, a.glist != nullptr, variant);
   SweepArgs b = a;
   for (int i = 0; i < 10; ++i) {
     b.rk0[i] = a.k0 + static_cast<uint32_t>(i) * 0x9E3779B9u;

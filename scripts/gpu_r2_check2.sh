@@ -1,7 +1,8 @@
 #!/bin/bash
-# Full check of the current build: every GPU test, the default bench line, C3 and C4 lines.
+# Full check of the current build: smoke, every GPU test, the default bench line, a C3 line.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-( time timeout 2400 python -m pytest tests -m gpu -x -q ) > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+( time timeout 2400 python -m pytest tests -m gpu -x -q -rs --durations=15 ) > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
 timeout 900 python bench.py --config C3 --steps 3 --warmup 3 --no-cpu-baseline --no-c4 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo "rc=$?" >> gpurun_out/bench_c3.err

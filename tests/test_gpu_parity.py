@@ -267,6 +267,36 @@ def test_c2_full_size_sampled(P, calib):
     m.close()
 
 
+@pytest.mark.slow
+def test_c2_full_predictions_bit_exact(P, calib):
+    """BASELINE config 2 exactly as bench.py runs it (1024^2, p = 0.33, M = 100, S = 30, the
+    default kernels and launch configuration): the accumulator over all 100 realizations and
+    the whole prediction grid equal the oracle's bit for bit. The oracle runs its OpenMP
+    build on the host cores (~1e9 updates; the same C source, pinned bit-identical to the
+    single-thread parity build by test_openmp_build_bit_identical)."""
+    Tk, ek = calib
+    truth, z, mask = make_problem(1024, 0.33, nu=0.5)
+    cfg = P.Config()
+    m = P.LeMpr(cfg, calib)
+    m.set_data(z, mask)
+    m.estimate_local_params()
+    m.simulate(100, 30, 20221202)
+    pred = m.predict()
+    acc = m.debug(P.binding.MPR_BUF_ACC)
+    m.close()
+    oc = ocfg(cfg)
+    try:
+        O.set_threads(0)
+        p = O.parameters(z, mask, oc, Tk, ek)
+        sim = O.simulate(p, mask, oc, 100, 30, 20221202)
+        opred = O.predict(np.nan_to_num(z), mask, sim["acc"], 100, 1, p.zmin, p.zmax, 0)
+    finally:
+        O.set_threads(1)
+    gaps = mask == 0
+    assert_bitwise(acc[gaps], sim["acc"][gaps], "accumulator over 100 realizations (1024^2)")
+    assert_bitwise(pred, opred, "predictions (1024^2, M = 100)")
+
+
 def group_run(P, z, mask, cfg_kw, calib, M, S, seed, world, shard="rows", ordered=False, energy=False,
               device_input=False, states=True):
     """`world` contexts on this GPU joined by libmpr's in-process communicator (one host
