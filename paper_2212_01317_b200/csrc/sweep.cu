@@ -1178,9 +1178,10 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   // Several resident waves of CTAs instead of one persistent wave: a CTA that finishes early
   // is replaced by a fresh one, so the slowest warps no longer set the launch's tail. About
   // 16 items per thread (C2: 3 waves, 72.1 -> 69.3 us; C3: 16 waves, 1505 -> 1365 us; C4:
-  // 32 waves, 1529 -> 1354 us per half-sweep; profiles/r02_summary.md). Energy launches
-  // keep one wave (their epilogue issues global atomics per CTA). MPR_SWEEP_WAVES overrides.
-  if (!energy) {
+  // 32 waves, 1529 -> 1354 us per half-sweep; profiles/r02_summary.md). Energy launches too
+  // (their per-CTA global atomics cost less than the tail: the adaptive protocol at 2048^2,
+  // M = 100, 57.9 -> 54.5 ms). MPR_SWEEP_WAVES overrides.
+  {
     static const int forced = [] {
       const char* v = std::getenv("MPR_SWEEP_WAVES");
       return v ? std::atoi(v) : 0;
