@@ -104,6 +104,7 @@ struct mpr_ctx {
   std::string err;
   int sweep_grid = 0;
   int sweep_variant = 28;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
+  int sweep_waves = 0;     // resident waves per half-sweep launch (MPR_SWEEP_WAVES; 0 = auto)
   // MPR_FILTER_STATS=1: the filter kernels count their queued (exact-path) and all live
   // pairs into fstats[0..1] (one atomic per warp and launch; tests and bench only)
   DBuf fstats;
@@ -632,6 +633,7 @@ mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
     }
   }
   if (const char* v = std::getenv("MPR_SWEEP_VARIANT")) c->sweep_variant = std::atoi(v);
+  if (const char* v = std::getenv("MPR_SWEEP_WAVES")) c->sweep_waves = std::max(0, std::atoi(v));
   // the SFU-filtered kernel (variant 40, opt-in: measured slower) only where
   // its error bound was verified on this device; otherwise the exact kernel 28
   if ((c->sweep_variant == 40 || c->sweep_variant == 41) && !sfu_filter_check(c->device, nullptr)) {
@@ -878,7 +880,7 @@ static mpr_status sc_half_sweep(mpr_ctx* c, SweepArgs& a, int colour, int varian
       if (se != MPR_OK) return se;
       CK(cudaEventRecordWithFlags(e0, st, ev_flags), "event record");
     }
-    launch_sweep_half(a, c->sweep_grid, variant, st);
+    launch_sweep_half(a, c->sweep_grid, variant, st, c->sweep_waves);
     CKL("sweep_half");
     if (timing) CK(cudaEventRecordWithFlags(e1, st, ev_flags), "event record");
     ++c->launches;
@@ -966,7 +968,7 @@ static mpr_status issue_batch(mpr_ctx* c, const BatchKey& k, int64_t* nsweep, bo
         a.g_begin = 0;
         a.g_count = c->dc_off[ph + 1] - c->dc_off[ph];
         if (a.g_count > 0) {
-          launch_sweep_half(a, c->sweep_grid, k.variant, st);
+          launch_sweep_half(a, c->sweep_grid, k.variant, st, c->sweep_waves);
           CKL("sweep_half");
           ++c->launches;
           ++*nsweep;

@@ -144,7 +144,9 @@ int sfu_filter_check(int device, double* err);
 int dc_tile_chunk(int lb, int R);
 void launch_sweep_dc_tiles(const SweepArgs& s, const int32_t* gid, const float* phiK, const float* T, int64_t Lx,
                            int64_t Ly, int lb, int tau, int Rc, cudaStream_t st);
-void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st);
+// grid: CTAs of one resident wave (sweep_grid_size); waves_forced > 0 fixes the number of
+// resident waves per launch (else ~16 items per thread, 1-32 waves)
+void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st, int waves_forced = 0);
 void launch_init_states(const GapRec* rec, const float* ginit, float* G, float* A, int64_t P, int R, int npairs,
                         uint32_t pair_base, int random_init, uint32_t k0, uint32_t k1,
                         cudaStream_t st);

@@ -1163,7 +1163,7 @@ static void launch_pdl(const void* fn, unsigned grid, unsigned block, void** arg
   cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st) {
+void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t st, int waves_forced) {
   const bool qhalf = (a.q == 0.5f);
   const bool energy = (a.energy != nullptr);
   // the filter kernels carry no energy epilogue: the exact kernels run energy sweeps
@@ -1180,14 +1180,11 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   // 16 items per thread (C2: 3 waves, 72.1 -> 69.3 us; C3: 16 waves, 1505 -> 1365 us; C4:
   // 32 waves, 1529 -> 1354 us per half-sweep; profiles/r02_summary.md). Energy launches too
   // (their per-CTA global atomics cost less than the tail: the adaptive protocol at 2048^2,
-  // M = 100, 57.9 -> 54.5 ms). MPR_SWEEP_WAVES overrides.
+  // M = 100, 57.9 -> 54.5 ms). waves_forced > 0 (MPR_SWEEP_WAVES, read at mpr_init) overrides.
   {
-    static const int forced = [] {
-      const char* v = std::getenv("MPR_SWEEP_WAVES");
-      return v ? std::atoi(v) : 0;
-    }();
     const int64_t per_thread = items / (static_cast<int64_t>(grid) * nt);
-    int64_t waves = forced > 0 ? forced : std::min<int64_t>(32, std::max<int64_t>(1, (per_thread + 15) / 16));
+    const int64_t waves =
+        waves_forced > 0 ? waves_forced : std::min<int64_t>(32, std::max<int64_t>(1, (per_thread + 15) / 16));
     grid = static_cast<int>(grid * waves);
   }
   if (g > grid) g = grid;

@@ -1136,3 +1136,19 @@ def test_filter_paths_bit_exact(P, calib, case, monkeypatch):
         assert max(fracs) < 0.5
     if case == "rough":
         assert min(fracs) > 0.2
+
+
+def test_multiwave_launches_bit_exact(P, calib, monkeypatch):
+    """Half-sweep launches spanning several resident waves of CTAs (MPR_SWEEP_WAVES = 8 makes
+    every launch here larger than one wave): SC and DC order, n_avg > 1 with RANDOM init,
+    the energy-trace kernels (per-CTA atomics from every wave), generic q and an odd pair
+    count (the one-pair kernel) against the oracle."""
+    monkeypatch.setenv("MPR_SWEEP_WAVES", "8")
+    truth, z, mask = make_problem(256, 0.5, corr_len=12.0)
+    g, _ = compare(P, z, mask, truth, P.Config(), calib, 48, 4, 501)
+    assert g["info"]["kernel_launches"] > 0
+    compare(P, z, mask, truth, P.Config(n_avg=2, init="random"), calib, 40, 4, 502, exact_pred=False)
+    compare(P, z, mask, truth, P.Config(order="dc", l_b=16), calib, 48, 3, 503)
+    compare(P, z, mask, truth, P.Config(), calib, 48, 3, 504, energy=True)
+    compare(P, z, mask, truth, P.Config(q=0.4, J=1.2), calib, 48, 3, 505)
+    compare(P, z, mask, truth, P.Config(), calib, 46, 3, 506)
