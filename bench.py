@@ -368,10 +368,16 @@ def sweep_roofline(w: Workload, r, steps, peaks):
     alu = ALG_OPS_PER_UPDATE * upd / sweep_s / 1e9 if sweep_s > 0 else None
     hbm = b_upd * upd / sweep_s / 1e9 if sweep_s > 0 else None
     traffic = None
+    pipe = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "sweep_traffic.json")))
         if prof.get("config") == w.name:
             traffic = prof.get("dram_bytes_per_launch")
+            if "fmaheavy_busy_frac_of_elapsed" in prof:
+                # the bound pipe as ncu measures it on this config's launch (FFMA2 and Philox's
+                # IMAD.WIDE share it): how busy it is, not a lane-op count
+                pipe = {"pipe": "fma_heavy", "busy_frac": prof["fmaheavy_busy_frac_of_elapsed"],
+                        "issue_active_frac": prof.get("issue_active_frac"), "source": prof.get("pipe_source")}
     except Exception:
         pass
     batch = info.get("batch", 0)
@@ -386,6 +392,7 @@ def sweep_roofline(w: Workload, r, steps, peaks):
             "sweep_ms_per_launch": r["sweep_ms"] / max(r["sweep_launches"], 1),
             "sweep_share_of_step": r["sweep_ms"] / max(r["ms_per_step"] * steps, 1e-9),
             "sweep_updates_per_s": upd / sweep_s if sweep_s > 0 else None,
+            "pipe_view": pipe,
             "hbm_view": {"achieved": hbm, "peak": hbm_peak, "unit": "GB/s",
                          "frac": (hbm / hbm_peak) if hbm else None,
                          "frac_of_8TBps": (hbm / 8000.0) if hbm else None,
