@@ -99,3 +99,32 @@ def test_c_example_runs(tmp_path):
                          timeout=120)
     assert out.returncode == 0, out.stderr
     assert "0 sample mismatches" in out.stdout
+
+
+def _build_c_slab_example(tmp_path):
+    import subprocess
+    exe = str(tmp_path / "mpr_fill_slabs")
+    subprocess.check_call(["gcc", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "fill_slabs.c"), "-L", PKG, "-lmpr", "-lpthread",
+                           f"-Wl,-rpath,{PKG}", "-lm", "-o", exe])
+    return exe
+
+
+def test_c_multirank_example_compiles(tmp_path):
+    """The multi-rank path is reachable from plain C: row slabs over an in-process group of
+    contexts, one host thread per rank (examples/fill_slabs.c)."""
+    assert os.path.exists(_build_c_slab_example(tmp_path))
+
+
+@pytest.mark.gpu
+def test_c_multirank_example_runs(tmp_path):
+    """4 row-slab ranks driven from C threads return the single context's prediction bit for bit."""
+    import subprocess
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    exe = _build_c_slab_example(tmp_path)
+    out = subprocess.run([exe, os.path.join(PKG, "data", "calib_q0.5.txt"), "4", str(torch.cuda.device_count())],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert " 0 mismatches" in out.stdout
