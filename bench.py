@@ -383,7 +383,7 @@ def sweep_roofline(w: Workload, r, steps, peaks):
     batch = info.get("batch", 0)
     variant = info.get("sweep_variant", 0)
     kernel = (f"k_sweep_quad (variant {variant}: two realization pairs per thread)"
-              if variant in (22, 28) and batch % 4 == 0 else f"k_sweep_half (variant {13 if variant in (22, 28) else variant})")
+              if variant in (22, 28, 33) and batch % 4 == 0 else f"k_sweep_half (variant {13 if variant in (22, 28, 33) else variant})")
     return {"bound": "alu", "kernel": kernel, "achieved": alu, "peak": alu_peak, "unit": "Gop/s",
             "frac": (alu / alu_peak) if alu else None, "traffic": traffic,
             "algorithmic_ops_per_update": ALG_OPS_PER_UPDATE,

@@ -284,11 +284,13 @@ typedef struct {
                                                     last_m_base + last_batch) are in
                                                     the state buffer (MPR_BUF_STATE)*/
   int32_t sweep_variant;                         /* half-sweep kernel variant in use
-                                                    (MPR_SWEEP_VARIANT; 28 default:
+                                                    (MPR_SWEEP_VARIANT; 33 default:
                                                     two realization pairs per thread,
-                                                    13 for odd pair counts; 40/41:
-                                                    the SFU-filtered forms, opt-in,
-                                                    28 when mpr_filter_check fails) */
+                                                    interleaved (28 for energy
+                                                    sweeps, 13 for odd pair counts);
+                                                    40/41: the SFU-filtered forms,
+                                                    opt-in, 33 when mpr_filter_check
+                                                    fails)                          */
   int32_t rank, world, shard;                    /* multi-rank layout                */
   int64_t row_begin, row_end;                    /* own rows (whole grid unless
                                                     MPR_SHARD_ROWS)                 */
@@ -345,7 +347,7 @@ const char *mpr_version(void);
  *                such a Metropolis step, accepts only when u(w) = 0).
  * err_out: 2 doubles, host, borrowed; may be NULL. Returns 1 when both premises hold (a
  * context asking for variant 40 runs it), 0 otherwise (mpr_init falls back to the exact
- * kernel 28) or when no device is usable. */
+ * kernel 33) or when no device is usable. */
 int mpr_filter_check(int device, double *err_out);
 
 #ifdef __cplusplus

@@ -103,7 +103,7 @@ struct mpr_ctx {
   int stage = ST_INIT;
   std::string err;
   int sweep_grid = 0;
-  int sweep_variant = 28;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
+  int sweep_variant = 33;  // kernel variant (MPR_SWEEP_VARIANT, tuning only; sweep.cu)
   int sweep_waves = 0;     // resident waves per half-sweep launch (MPR_SWEEP_WAVES; 0 = auto)
   // MPR_FILTER_STATS=1: the filter kernels count their queued (exact-path) and all live
   // pairs into fstats[0..1] (one atomic per warp and launch; tests and bench only)
@@ -517,7 +517,7 @@ int64_t choose_batch(mpr_ctx* c, int64_t M_span) {
   // 0.36 -> 0.50 ms and 1.25 -> 1.39 ms when split; 16384^2: 3.85 -> 3.40 ms / half-sweep).
   // (A 5-pair-per-thread kernel running R = 10 as one batch with float2 moves was measured
   // slower at C4: 3.65 ms per half-sweep against 2.21 + 0.78 ms for 8 + 2; dropped.)
-  if ((c->sweep_variant == 22 || c->sweep_variant == 28 || c->sweep_variant == 40) && B % 4 == 2 && B > 2 &&
+  if ((c->sweep_variant == 22 || c->sweep_variant == 28 || c->sweep_variant == 33 || c->sweep_variant == 40) && B % 4 == 2 && B > 2 &&
       c->P >= c->split_min_P)
     B -= 2;
   c->batch_key_P = c->P;
@@ -637,8 +637,8 @@ mpr_status mpr_init(const mpr_config* cfg, mpr_ctx** out) {
   // the SFU-filtered kernel (variant 40, opt-in: measured slower) only where
   // its error bound was verified on this device; otherwise the exact kernel 28
   if ((c->sweep_variant == 40 || c->sweep_variant == 41) && !sfu_filter_check(c->device, nullptr)) {
-    std::fprintf(stderr, "mpr_init: SFU filter check failed on device %d, using sweep variant 28\n", c->device);
-    c->sweep_variant = 28;
+    std::fprintf(stderr, "mpr_init: SFU filter check failed on device %d, using sweep variant 33\n", c->device);
+    c->sweep_variant = 33;
   }
   if (const char* v = std::getenv("MPR_FILTER_STATS"))
     if (std::atoi(v)) {

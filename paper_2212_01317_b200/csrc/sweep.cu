@@ -231,6 +231,65 @@ __device__ __forceinline__ void process_item_w(const SweepArgs& a, const GapRec&
   }
 }
 
+// Both pairs of a two-pair item (variant 33) as one block of straight-line arithmetic, so
+// the serial steps of one pair (the neighbour sum, exp) overlap the other pair's instead of
+// running back to back behind the per-pair branches; then each pair's store and a9
+// accumulation as before. Each pair's arithmetic is metropolis_pair's: bit-identical.
+// (Merging the two stores into one float4 store was measured slower: 72.0 vs 69.5 us.)
+template <bool QHALF, bool ENERGY>
+__device__ __forceinline__ void process_quad_w2(const SweepArgs& a, const GapRec& rec, float4 cur, const float2 (&nbA)[4],
+                                                const float2 (&nbB)[4], uint32_t self_off, const Words4& wA,
+                                                const Words4& wB, bool liveA, bool liveB, long long (&e)[2][2],
+                                                const bool (&acc)[2][2]) {
+  uint32_t sel = 0;
+  if (ENERGY) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t ty = (rec.flags >> (2 * k)) & 3u;
+      sel |= (a.is_b ? (ty != NB_NONE) : (ty == NB_KNOWN)) ? (1u << k) : 0u;
+    }
+  }
+  const float2 cA = make_float2(cur.x, cur.y), cB = make_float2(cur.z, cur.w);
+  bool a0, a1, b0, b1;
+  long long eA0 = 0, eA1 = 0, eB0 = 0, eB1 = 0;
+  float2 nA, nB;
+  if (all_present(rec.flags)) {
+    nA = metropolis_pair<QHALF, ENERGY, true>(cA, nbA, rec.flags, sel, rec.beta, a.q, a.J, wA, a0, a1, eA0, eA1);
+    nB = metropolis_pair<QHALF, ENERGY, true>(cB, nbB, rec.flags, sel, rec.beta, a.q, a.J, wB, b0, b1, eB0, eB1);
+  } else {
+    nA = metropolis_pair<QHALF, ENERGY, false>(cA, nbA, rec.flags, sel, rec.beta, a.q, a.J, wA, a0, a1, eA0, eA1);
+    nB = metropolis_pair<QHALF, ENERGY, false>(cB, nbB, rec.flags, sel, rec.beta, a.q, a.J, wB, b0, b1, eB0, eB1);
+  }
+  if (liveA) {
+    if (ENERGY) {
+      e[0][0] += eA0;
+      e[0][1] += eA1;
+    }
+    if (a0 || a1) *reinterpret_cast<float2*>(a.G + self_off) = nA;
+    if (acc[0][0] || acc[0][1]) {
+      float2* ap = reinterpret_cast<float2*>(a.A + self_off);
+      float2 av = *ap;
+      if (acc[0][0]) av.x = __fadd_rn(av.x, nA.x);
+      if (acc[0][1]) av.y = __fadd_rn(av.y, nA.y);
+      *ap = av;
+    }
+  }
+  if (liveB) {
+    if (ENERGY) {
+      e[1][0] += eB0;
+      e[1][1] += eB1;
+    }
+    if (b0 || b1) *reinterpret_cast<float2*>(a.G + self_off + 2u) = nB;
+    if (acc[1][0] || acc[1][1]) {
+      float2* ap = reinterpret_cast<float2*>(a.A + self_off + 2u);
+      float2 av = *ap;
+      if (acc[1][0]) av.x = __fadd_rn(av.x, nB.x);
+      if (acc[1][1]) av.y = __fadd_rn(av.y, nB.y);
+      *ap = av;
+    }
+  }
+}
+
 // Accumulation flags of the realization pair j for this sweep: the fixed window of the
 // last n_avg sweeps, or (adaptive protocol, ARITH §K) each realization's own window
 // (win_lo, win_hi].
@@ -396,7 +455,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
 // call and runs metropolis_pair, so the results are those of k_sweep_half bit for bit.
 // Requires npairs % NP == 0 (launch_sweep_half falls back). EARLY: every pair's Philox
 // words are drawn right after the record arrives.
-template <bool QHALF, bool ENERGY, int MINB, bool LIST, int NP = 2, bool EARLY = false>
+template <bool QHALF, bool ENERGY, int MINB, bool LIST, int NP = 2, bool EARLY = false, bool IL = false>
 __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
   pdl_wait();
   constexpr int NQ = NP / 2;  // float4 quads per thread
@@ -477,7 +536,11 @@ __global__ void __launch_bounds__(256, MINB) k_sweep_quad(const SweepArgs a) {
           }
         }
         const int pa = 2 * qd, pb = 2 * qd + 1;
-        if (EARLY) {
+        if (EARLY && IL && NP == 2) {
+          process_quad_w2<QHALF, ENERGY>(a, rec, cur, nbA, nbB, self_off, wpre[0], wpre[NP - 1], live[0], live[NP - 1],
+                                         reinterpret_cast<long long(&)[2][2]>(e[0][0]),
+                                         reinterpret_cast<const bool(&)[2][2]>(acc[0][0]));
+        } else if (EARLY) {
           if (live[pa])
             process_item_w<QHALF, ENERGY, true, true>(a, rec, make_float2(cur.x, cur.y), nbA, self_off + 4u * qd,
                                                       wpre[pa], e[pa][0], e[pa][1], acc[pa][0], acc[pa][1]);
@@ -1067,7 +1130,9 @@ void launch_adaptive_check(const AdaptiveCheckArgs& a, cudaStream_t st) {
 //        (the fallback of 22/28 for odd pair counts);
 //   22 = k_sweep_quad: two pairs per thread, float4 state moves, 4 CTAs/SM;
 //   28 = 22 with both pairs' Philox words drawn before the state loads are used,
-//        3 CTAs/SM (default);
+//        3 CTAs/SM (the energy-trace sweeps of 33);
+//   33 = 28 with both pairs' arithmetic in one block (the two chains interleave), per-pair
+//        stores (default: C2 69.25 -> 67.98 us, C4 equal within noise);
 //   40 / 41 = the SFU rejection filter (two / one pair per thread; opt-in, slower).
 // Half-sweep, us (C2 / C3 / C4 at M = 10), product-form dE (ARITH §H), one resident wave:
 //   v5  92.6 (C2);  v13 89.7 / 1965 / 3525;  v28 72.2 / 1509 / 3082
@@ -1085,7 +1150,7 @@ static int sweep_threads(int) { return 256; }
 
 static size_t sweep_smem(int) { return 0; }
 
-static bool is_quad(int variant) { return variant == 22 || variant == 28; }
+static bool is_quad(int variant) { return variant == 22 || variant == 28 || variant == 33; }
 static bool is_filt(int variant) { return variant == 40 || variant == 41; }
 static int pairs_per_thread(int variant) { return (is_quad(variant) || variant == 40) ? 2 : 1; }
 
@@ -1104,6 +1169,8 @@ template <bool Q, bool E>
 static void* quad_kernel_ptr(bool list, int variant) {
   if (variant == 28)
     return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true, 2, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false, 2, true>);
+  if (variant == 33)
+    return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, true, 2, true, true>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 3, false, 2, true, true>);
   return list ? reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, true, 2, false>) : reinterpret_cast<void*>(k_sweep_quad<Q, E, 4, false, 2, false>);  // 22
 }
 
@@ -1168,6 +1235,8 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   const bool energy = (a.energy != nullptr);
   // the filter kernels carry no energy epilogue: the exact kernels run energy sweeps
   if (is_filt(variant) && energy) variant = 28;
+  // the interleaved form spills in its energy instantiations: energy sweeps run variant 28
+  if (variant == 33 && energy) variant = 28;
   if (variant == 40 && (a.npairs & 1)) variant = 41;
   // the two-pair kernels need an even pair count (float4 alignment)
   if (is_quad(variant) && (a.npairs & 1)) variant = 13;
