@@ -448,6 +448,101 @@ __global__ void __launch_bounds__(NT, MINB) k_sweep_half(const SweepArgs a) {
   pdl_trigger();
 }
 
+// Variant 14: the one-pair item of variant 13 two at a time. A thread takes its items g and
+// g + gstride per loop trip (the same items, in the same split, as variant 13), draws both
+// Philox calls, loads both, and runs both metropolis_pair in one block so that the two
+// chains interleave. The fallback of the two-pair kernels for an odd pair count (the C4
+// tail batch); no energy epilogue (energy sweeps keep variant 13).
+template <bool QHALF, bool LIST>
+__global__ void __launch_bounds__(256, 3) k_sweep_half2(const SweepArgs a) {
+  pdl_wait();
+  const Split sp = split_work(a.npairs);
+  const uint32_t R = static_cast<uint32_t>(a.R);
+  const uint32_t j2 = 2u * static_cast<uint32_t>(sp.j);
+  const uint32_t gcount = static_cast<uint32_t>(a.g_count);
+  const uint32_t gbegin = static_cast<uint32_t>(a.g_begin);
+  bool acc0 = false, acc1 = false;
+  bool live = sp.active;
+  if (live) {
+    accum_flags(a, sp.j, acc0, acc1);
+    if (a.win_hi) live = static_cast<int>(a.sweep) <= max(a.win_hi[2 * sp.j], a.win_hi[2 * sp.j + 1]);
+  }
+  if (live) {
+    const uint32_t pair = a.pair_base + static_cast<uint32_t>(sp.j);
+    const uint32_t gs = sp.gstride;
+    uint32_t g = sp.g0;
+    uint32_t ga = 0, gb = 0;
+    GapRec ra{}, rb{};
+    if (g < gcount) {
+      ga = LIST ? a.glist[g] : gbegin + g;
+      ra = a.rec[ga];
+    }
+    if (g + gs < gcount) {
+      gb = LIST ? a.glist[g + gs] : gbegin + g + gs;
+      rb = a.rec[gb];
+    }
+    for (; g < gcount; g += 2u * gs) {
+      const bool vb = g + gs < gcount;
+      const uint32_t g2 = g + 2u * gs, g3 = g + 3u * gs;
+      uint32_t ga2 = 0, gb2 = 0;
+      GapRec ra2{}, rb2{};
+      if (g2 < gcount) {
+        ga2 = LIST ? a.glist[g2] : gbegin + g2;
+        ra2 = a.rec[ga2];
+      }
+      if (g3 < gcount) {
+        gb2 = LIST ? a.glist[g3] : gbegin + g3;
+        rb2 = a.rec[gb2];
+      }
+      const Words4 wa = philox4x32_10_rk(ra.site, a.sweep, pair, 2u, a.rk0, a.rk1);
+      const Words4 wb = philox4x32_10_rk(rb.site, a.sweep, pair, 2u, a.rk0, a.rk1);
+      const uint32_t offa = ga * R + j2, offb = gb * R + j2;
+      const float2 ca = *reinterpret_cast<const float2*>(a.G + offa);
+      const float2 cb = vb ? *reinterpret_cast<const float2*>(a.G + offb) : f2(0.0f);
+      float2 na[4], nbv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t ta = (ra.flags >> (2 * k)) & 3u, tb = (rb.flags >> (2 * k)) & 3u;
+        na[k] = ta == NB_GAP ? *reinterpret_cast<const float2*>(a.G + (static_cast<uint32_t>(ra.nb[k]) * R + j2))
+                             : f2(__int_as_float(ra.nb[k]));
+        nbv[k] = (vb && tb == NB_GAP) ? *reinterpret_cast<const float2*>(a.G + (static_cast<uint32_t>(rb.nb[k]) * R + j2))
+                                      : f2(__int_as_float(rb.nb[k]));
+      }
+      bool a0, a1, b0, b1;
+      long long e = 0;
+      float2 xa, xb;
+      if (all_present(ra.flags) && all_present(rb.flags)) {
+        xa = metropolis_pair<QHALF, false, true>(ca, na, ra.flags, 0u, ra.beta, a.q, a.J, wa, a0, a1, e, e);
+        xb = metropolis_pair<QHALF, false, true>(cb, nbv, rb.flags, 0u, rb.beta, a.q, a.J, wb, b0, b1, e, e);
+      } else {
+        xa = metropolis_pair<QHALF, false, false>(ca, na, ra.flags, 0u, ra.beta, a.q, a.J, wa, a0, a1, e, e);
+        xb = metropolis_pair<QHALF, false, false>(cb, nbv, rb.flags, 0u, rb.beta, a.q, a.J, wb, b0, b1, e, e);
+      }
+      if (a0 || a1) *reinterpret_cast<float2*>(a.G + offa) = xa;
+      if (vb && (b0 || b1)) *reinterpret_cast<float2*>(a.G + offb) = xb;
+      if (acc0 || acc1) {
+        float2* pa = reinterpret_cast<float2*>(a.A + offa);
+        float2 av = *pa;
+        if (acc0) av.x = __fadd_rn(av.x, xa.x);
+        if (acc1) av.y = __fadd_rn(av.y, xa.y);
+        *pa = av;
+        if (vb) {
+          float2* pb = reinterpret_cast<float2*>(a.A + offb);
+          float2 bv = *pb;
+          if (acc0) bv.x = __fadd_rn(bv.x, xb.x);
+          if (acc1) bv.y = __fadd_rn(bv.y, xb.y);
+          *pb = bv;
+        }
+      }
+      ra = ra2;
+      rb = rb2;
+      ga = ga2;
+      gb = gb2;
+    }
+  }
+  pdl_trigger();
+}
+
 // NP realization pairs (2 NP realizations) of one gap site per thread (NP = 2 is built;
 // NP = 4 measured no faster, profiles/r01_summary.md). The record, the flag decoding, the
 // neighbour addresses and the loop overhead are shared by the NP pairs, and the own /
@@ -1127,7 +1222,9 @@ void launch_adaptive_check(const AdaptiveCheckArgs& a, cudaStream_t st) {
 //   5  = one pair per thread, scalar arithmetic, L2 prefetch of the next item
 //        (the first optimised kernel, kept as the scalar reference);
 //   13 = one pair per thread, packed f32x2, record one item ahead, 4 CTAs/SM
-//        (the fallback of 22/28 for odd pair counts);
+//        (the fallback of 22/28/33 for odd pair counts in energy sweeps);
+//   14 = 13 two items per loop trip, both chains in one block (the odd-pair fallback
+//        otherwise);
 //   22 = k_sweep_quad: two pairs per thread, float4 state moves, 4 CTAs/SM;
 //   28 = 22 with both pairs' Philox words drawn before the state loads are used,
 //        3 CTAs/SM (the energy-trace sweeps of 33);
@@ -1142,6 +1239,7 @@ void launch_adaptive_check(const AdaptiveCheckArgs& a, cudaStream_t st) {
 //   v22 87.1 / 1838 / 3402;  v28 84.5 / 1780 / 3351.
 template <bool Q, bool E, bool LIST>
 static void* sweep_kernel_ptr(int variant) {
+  if (variant == 14 && !E) return reinterpret_cast<void*>(k_sweep_half2<Q, LIST>);
   if (variant == 5) return reinterpret_cast<void*>(k_sweep_half<Q, E, 1, 2, 256, true, LIST, false>);
   return reinterpret_cast<void*>(k_sweep_half<Q, E, 4, 3, 256, true, LIST, true>);  // 13 (and 22/28's fallback)
 }
@@ -1239,7 +1337,13 @@ void launch_sweep_half(const SweepArgs& a, int grid, int variant, cudaStream_t s
   if (variant == 33 && energy) variant = 28;
   if (variant == 40 && (a.npairs & 1)) variant = 41;
   // the two-pair kernels need an even pair count (float4 alignment)
-  if (is_quad(variant) && (a.npairs & 1)) variant = 13;
+  // (variant 14, the two-items-per-trip form of 13: the C2 grid at M = 10, where the whole
+  // batch runs it, 11.9 -> 10.5 us per half-sweep; MPR_TAIL_VARIANT=13 selects the old one)
+  static const int tail_variant = [] {
+    const char* v = std::getenv("MPR_TAIL_VARIANT");
+    return v ? std::atoi(v) : 14;
+  }();
+  if (is_quad(variant) && (a.npairs & 1)) variant = (energy ? 13 : tail_variant);
   const int nt = sweep_threads(variant);
   const int64_t units = a.npairs / pairs_per_thread(variant);  // threads per gap site
   const int64_t items = a.g_count * units;

@@ -1,8 +1,11 @@
 #!/bin/bash
+# The odd-pair fallback (C4 tail batch; M = 4k + 2 on small grids): variant 13 vs 14.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -k "split_tail or every_sweep_variant or fuzz_small or c1_config or c4_full or row_slabs_distributed or adaptive" > gpurun_out/pytest_tail.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_tail.log
-B="python bench.py --config C4 --steps 3 --warmup 2 --no-c4 --no-cpu-baseline"
-timeout 600 $B > gpurun_out/c4_tail.json 2> gpurun_out/c4_tail.err
-B="python bench.py --config C4 --steps 1 --warmup 1 --no-c4 --no-e2e --no-cpu-baseline --no-clocks"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches_c4.csv $B > gpurun_out/ncu_c4.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_c4.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "every_sweep_variant or split_tail or multiwave or c1_config or ragged or fuzz_small" > gpurun_out/pytest_tail.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_tail.log
+for i in 1 2; do
+  for t in 13 14; do
+    MPR_TAIL_VARIANT=$t timeout 600 python bench.py --config C4 --steps 2 --warmup 1 --no-cpu-baseline --no-c4 --no-e2e --no-clocks > gpurun_out/tail_c4_t${t}_$i.json 2>/dev/null
+    MPR_TAIL_VARIANT=$t timeout 300 python bench.py --M 10 --steps 20 --warmup 3 --no-cpu-baseline --no-c4 --no-e2e --no-clocks > gpurun_out/tail_c2m10_t${t}_$i.json 2>/dev/null
+  done
+done

@@ -827,7 +827,7 @@ def test_adaptive_with_slope_tolerance(P, calib):
     assert_bitwise(pred, O.predict(np.nan_to_num(z), mask, r["acc"], 4, 1, p.zmin, p.zmax, 0), "predictions")
 
 
-@pytest.mark.parametrize("variant", [5, 13, 22, 28, 33, 40, 41])
+@pytest.mark.parametrize("variant", [5, 13, 14, 22, 28, 33, 40, 41])
 def test_every_sweep_variant_bit_exact(P, calib, variant, monkeypatch):
     """Each half-sweep kernel variant (scalar / packed f32x2 arithmetic, one or two pairs per
     thread, early Philox; MPR_SWEEP_VARIANT) reproduces the oracle bit for bit: q = 1/2 with the energy trace, generic q, the DC
