@@ -27,10 +27,20 @@ def errors(pred, truth, mask):
     return float(np.mean(np.abs(e))), float(np.sqrt(np.mean(e * e)))
 
 
-def run(L=256, K=20, M=20, S=30, ps=(0.3, 0.5, 0.7, 0.85), skew=True, seed_field=2212):
+def make_truth(L, field="heterogeneous", skew=True, seed_field=2212):
+    """The synthetic field: 'heterogeneous' (smooth variance variation, inputs.synth) or
+    'two-regime' (SPEC's validation generator: a low-variance (sigma 0.1) and a high-variance
+    (sigma 10) domain, here the 2x2 quadrant checkerboard of inputs.synth.domain_wall_field)."""
+    from inputs.synth import domain_wall_field, heterogeneous_field
+    if field == "two-regime":
+        return domain_wall_field(L, tile=L // 2, low=0.1, high=10.0, corr_len=max(L / 32, 4.0), seed=seed_field)
+    return heterogeneous_field(L, corr_len=max(L / 32, 4.0), skew=skew, seed=seed_field)
+
+
+def run(L=256, K=20, M=20, S=30, ps=(0.3, 0.5, 0.7, 0.85), skew=True, seed_field=2212, field="heterogeneous"):
     import paper_2212_01317_b200 as P
-    from inputs.synth import heterogeneous_field, random_mask
-    truth = heterogeneous_field(L, corr_len=max(L / 32, 4.0), skew=skew, seed=seed_field)
+    from inputs.synth import random_mask
+    truth = make_truth(L, field, skew, seed_field)
     calib = P.load_calibration()
     methods = {"MPR": P.Config(l_b=max(L, 2), n_s=0), "BST": P.Config(l_b=32, n_s=0),
                "SST": P.Config(l_b=32, n_s=5, r_s=2)}
@@ -46,7 +56,7 @@ def run(L=256, K=20, M=20, S=30, ps=(0.3, 0.5, 0.7, 0.85), skew=True, seed_field
                 eng.estimate_local_params()
                 eng.simulate(M, S, 20221202 + k)
                 errs[name].append(errors(eng.predict(), truth, mask))
-        rec = {"L": L, "p": p, "K": K, "M": M, "S": S}
+        rec = {"field": field, "L": L, "p": p, "K": K, "M": M, "S": S}
         for name in methods:
             a = np.array(errs[name])
             rec[f"MAAE_{name}"] = float(a[:, 0].mean())
@@ -112,12 +122,13 @@ def main():
     ap.add_argument("--S", type=int, default=30)
     ap.add_argument("--ps", default="0.3,0.5,0.7,0.85")
     ap.add_argument("--no-skew", action="store_true")
+    ap.add_argument("--field", default="heterogeneous", choices=["heterogeneous", "two-regime"])
     ap.add_argument("--sweep", default="p", choices=["p", "lb", "ns"],
                     help="p: MPR/BST/SST vs missing ratio; lb: SST vs block side; ns: vs smoothing passes")
     ap.add_argument("--values", default=None, help="comma list for --sweep lb / ns")
     a = ap.parse_args()
     if a.sweep == "p":
-        run(a.L, a.K, a.M, a.S, tuple(float(x) for x in a.ps.split(",")), skew=not a.no_skew)
+        run(a.L, a.K, a.M, a.S, tuple(float(x) for x in a.ps.split(",")), skew=not a.no_skew, field=a.field)
     else:
         vals = a.values or ("8,16,32,64,128" if a.sweep == "lb" else "0,1,2,5,10")
         run_param_sweep(a.sweep, [int(x) for x in vals.split(",")], L=a.L, K=a.K, M=a.M, S=a.S,

@@ -707,6 +707,20 @@ def test_sv_mpr_beats_mpr_on_heterogeneous_field(P):
 
 
 @pytest.mark.slow
+def test_sv_mpr_beats_mpr_two_regime_spec1(P):
+    """SPEC acceptance #1 on its two-regime field (sigma 0.1 and 10 domains, 256^2): for
+    p = 0.5 and 0.8, MRASE(BST)/MRASE(MPR) < 1 and MRASE(SST)/MRASE(MPR) < 1 on paired
+    thinnings (the full run, K = 20, M = 20, p = 0.5/0.7/0.8: ratios 0.70-0.85, every
+    thinning won; profiles/r02_validation_spec1_two_regime.jsonl)."""
+    import sys
+    sys.path.insert(0, "scripts")
+    from validate_methods import run
+    for r in run(L=256, K=4, M=10, S=30, ps=(0.5, 0.8), field="two-regime"):
+        for name in ("BST", "SST"):
+            assert r[f"ratio_RASE_{name}"] < 1.0 and r[f"win_rate_RASE_{name}"] == 1.0
+
+
+@pytest.mark.slow
 def test_gpu_calibration_table_equals_shipped(P, calib):
     """Row f2: the e(T) table built on the GPU with the recipe of scripts/make_calibration.py
     is bit-identical to the shipped table the oracle wrote (same chains, exact fixed-point
