@@ -101,16 +101,15 @@ float oracle_cos_spec(float x)
 }
 
 /* --------------------------------------------------------------- ARITH §B2 */
-/* sin_spec(x) = x * S(x*x) for x in [-pi_f, pi_f]: odd polynomial of degree 13 whose
+/* sin_spec(x) = x * S(x*x) for x in [-pi_f, pi_f]: odd polynomial of degree 11 whose
  * even part S is evaluated by Horner in fp32 fmaf (coefficients frozen in ARITH §B2). */
 float oracle_sin_poly(float t)
 {
-    float p = 0x1.27e614p-33f;
-    p = fmaf(p, t, -0x1.a7f884p-26f);
-    p = fmaf(p, t, 0x1.717f0cp-19f);
-    p = fmaf(p, t, -0x1.a01412p-13f);
-    p = fmaf(p, t, 0x1.1110ep-7f);
-    p = fmaf(p, t, -0x1.555552p-3f);
+    float p = -0x1.610f4ap-26f;
+    p = fmaf(p, t, 0x1.6b1478p-19f);
+    p = fmaf(p, t, -0x1.9f8a18p-13f);
+    p = fmaf(p, t, 0x1.110ba2p-7f);
+    p = fmaf(p, t, -0x1.55550cp-3f);
     p = fmaf(p, t, 1.0f);
     return p;
 }
@@ -124,12 +123,11 @@ float oracle_sin_spec(float x)
  * (x/4) * S((x/4)^2) with the power-of-two scalings folded in (ARITH §B2). */
 float oracle_sin_poly_quarter(float t)
 {
-    float p = 0x1.27e614p-59f;
-    p = fmaf(p, t, -0x1.a7f884p-48f);
-    p = fmaf(p, t, 0x1.717f0cp-37f);
-    p = fmaf(p, t, -0x1.a01412p-27f);
-    p = fmaf(p, t, 0x1.1110ep-17f);
-    p = fmaf(p, t, -0x1.555552p-9f);
+    float p = -0x1.610f4ap-48f;
+    p = fmaf(p, t, 0x1.6b1478p-37f);
+    p = fmaf(p, t, -0x1.9f8a18p-27f);
+    p = fmaf(p, t, 0x1.110ba2p-17f);
+    p = fmaf(p, t, -0x1.55550cp-9f);
     p = fmaf(p, t, 0x1p-2f);
     return p;
 }
