@@ -39,10 +39,10 @@ from inputs.synth import CONFIGS, SEED_SIM, make_problem  # noqa: E402
 
 METRIC = "gap-site spin updates/sec (LE-MPR conditional simulation, whole fill)"
 # FP32 lane-ops the arithmetic contract fixes per gap-site update (ARITH §H
-# product form: sin of the half difference 9, four neighbour sine terms of 9, the sum
-# phi' + phi 1, dE / beta 3, exp_spec 12, 4 conversions = 65) + half a Philox4x32-10 call
-# (10 rounds x 2 IMAD.WIDE + 2 LOP3 = 40 per pair) = 85.
-ALG_OPS_PER_UPDATE = 85
+# product form with the degree-11 sine of §B2: sin of the half difference 8, four
+# neighbour sine terms of 8, the sum phi' + phi 1, dE / beta 3, exp_spec 12, 4 conversions
+# = 60) + half a Philox4x32-10 call (10 rounds x 2 IMAD.WIDE + 2 LOP3 = 40 per pair) = 80.
+ALG_OPS_PER_UPDATE = 80
 UNIT = "updates/s"
 # how each config scales over ranks: weak (M per rank) or strong (M in total)
 SCALING = {"C1": "weak", "C2": "weak", "C3": "strong", "C4": "strong"}

@@ -54,27 +54,25 @@ __device__ __forceinline__ Words4 philox4x32_10_rk(uint32_t c0, uint32_t c1, uin
   return Words4{c0, c1, c2, c3};
 }
 
-// ARITH §B2 — the even part S of sin_spec(x) = x * S(x*x), and S4 for q = 1/2 (the
+// ARITH §B2 — the even part S of sin_spec(x) = x * S(x*x) (degree 5 in t), and S4 for q = 1/2 (the
 // products by h = 1/4 folded into the coefficients c_k * 2^-(4k+2): x * S4(x*x) is
 // (x/4) * S((x/4)^2) with the exact power-of-two scalings done in the constants).
 __device__ __forceinline__ float sin_poly(float t) {
-  float p = 0x1.27e614p-33f;
-  p = __fmaf_rn(p, t, -0x1.a7f884p-26f);
-  p = __fmaf_rn(p, t, 0x1.717f0cp-19f);
-  p = __fmaf_rn(p, t, -0x1.a01412p-13f);
-  p = __fmaf_rn(p, t, 0x1.1110ep-7f);
-  p = __fmaf_rn(p, t, -0x1.555552p-3f);
+  float p = -0x1.610f4ap-26f;
+  p = __fmaf_rn(p, t, 0x1.6b1478p-19f);
+  p = __fmaf_rn(p, t, -0x1.9f8a18p-13f);
+  p = __fmaf_rn(p, t, 0x1.110ba2p-7f);
+  p = __fmaf_rn(p, t, -0x1.55550cp-3f);
   p = __fmaf_rn(p, t, 1.0f);
   return p;
 }
 
 __device__ __forceinline__ float sin_poly_quarter(float t) {
-  float p = 0x1.27e614p-59f;
-  p = __fmaf_rn(p, t, -0x1.a7f884p-48f);
-  p = __fmaf_rn(p, t, 0x1.717f0cp-37f);
-  p = __fmaf_rn(p, t, -0x1.a01412p-27f);
-  p = __fmaf_rn(p, t, 0x1.1110ep-17f);
-  p = __fmaf_rn(p, t, -0x1.555552p-9f);
+  float p = -0x1.610f4ap-48f;
+  p = __fmaf_rn(p, t, 0x1.6b1478p-37f);
+  p = __fmaf_rn(p, t, -0x1.9f8a18p-27f);
+  p = __fmaf_rn(p, t, 0x1.110ba2p-17f);
+  p = __fmaf_rn(p, t, -0x1.55550cp-9f);
   p = __fmaf_rn(p, t, 0x1p-2f);
   return p;
 }
@@ -179,21 +177,19 @@ __device__ __forceinline__ float2 cos_half_spec2(float2 d) {
 
 // S and S4 of ARITH §B2 on both components.
 __device__ __forceinline__ float2 sin_poly2(float2 t) {
-  float2 p = __ffma2_rn(f2(0x1.27e614p-33f), t, f2(-0x1.a7f884p-26f));
-  p = __ffma2_rn(p, t, f2(0x1.717f0cp-19f));
-  p = __ffma2_rn(p, t, f2(-0x1.a01412p-13f));
-  p = __ffma2_rn(p, t, f2(0x1.1110ep-7f));
-  p = __ffma2_rn(p, t, f2(-0x1.555552p-3f));
+  float2 p = __ffma2_rn(f2(-0x1.610f4ap-26f), t, f2(0x1.6b1478p-19f));
+  p = __ffma2_rn(p, t, f2(-0x1.9f8a18p-13f));
+  p = __ffma2_rn(p, t, f2(0x1.110ba2p-7f));
+  p = __ffma2_rn(p, t, f2(-0x1.55550cp-3f));
   p = __ffma2_rn(p, t, f2(1.0f));
   return p;
 }
 
 __device__ __forceinline__ float2 sin_poly_quarter2(float2 t) {
-  float2 p = __ffma2_rn(f2(0x1.27e614p-59f), t, f2(-0x1.a7f884p-48f));
-  p = __ffma2_rn(p, t, f2(0x1.717f0cp-37f));
-  p = __ffma2_rn(p, t, f2(-0x1.a01412p-27f));
-  p = __ffma2_rn(p, t, f2(0x1.1110ep-17f));
-  p = __ffma2_rn(p, t, f2(-0x1.555552p-9f));
+  float2 p = __ffma2_rn(f2(-0x1.610f4ap-48f), t, f2(0x1.6b1478p-37f));
+  p = __ffma2_rn(p, t, f2(-0x1.9f8a18p-27f));
+  p = __ffma2_rn(p, t, f2(0x1.110ba2p-17f));
+  p = __ffma2_rn(p, t, f2(-0x1.55550cp-9f));
   p = __ffma2_rn(p, t, f2(0x1p-2f));
   return p;
 }
