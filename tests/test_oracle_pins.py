@@ -820,3 +820,19 @@ def test_checkerboard_chain_matches_sequential_random_order_metropolis(tmp_path)
         assert abs(cb - sq) < tol, f"T={T}: checkerboard {cb:.5f} +- {cb_se:.1e} vs sequential {sq:.5f} +- {sq_se:.1e}"
     # sensitivity (measured when the test was written): the sequential sampler at T = 0.36
     # instead of 0.35 lands 1.7 tolerances away, at 1.25 instead of 1.2 3.2 tolerances
+
+
+@pytest.mark.slow
+def test_sin_and_exp_spec_exhaustive_error_bounds(tmp_path):
+    """ARITH §B2 / §C accuracy statements over EVERY fp32 argument (not a sample): the
+    degree-11 sin_spec stays within 3.9e-7 of libm on [0, pi_f] (3.84e-7 when the contract
+    was frozen) and exp_spec within 1.1 ulp on [-80, 0] (1.05 ulp)."""
+    import subprocess
+    exe = str(tmp_path / "spec_exhaustive")
+    src = os.path.join(os.path.dirname(__file__), "native", "spec_exhaustive.c")
+    libdir = os.path.dirname(O.build())
+    subprocess.check_call(["gcc", "-O2", "-fopenmp", "-o", exe, src, "-L", libdir, "-l:liboracle.so",
+                           f"-Wl,-rpath,{libdir}", "-lm"])
+    es, ee = map(float, subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split())
+    assert es <= 3.9e-7, es
+    assert ee <= 1.1, ee
